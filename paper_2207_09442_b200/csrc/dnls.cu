@@ -1,0 +1,875 @@
+// libdnls: C-ABI implementation (include/dnls.h) and the sm_100a kernels.
+//
+// Kernel design: one CTA owns one batch element for the whole solve.
+// k_forward runs all K GN/LM iterations plus the final implicit linearisation+factorisation in
+// ONE launch: the per-element phases (phases.cuh) are separated by __syncthreads only, so no
+// grid-wide synchronisation and no per-iteration launches exist.  The stage-level entry points
+// launch thin kernels around the same device phases.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dnls.h"
+#include "phases.cuh"
+#include "symbolic.h"
+
+using namespace dnls;
+
+namespace {
+constexpr int NT = 256;   // threads per CTA (one batch element per CTA)
+thread_local std::string g_err;
+
+dnls_status fail(dnls_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+dnls_status cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DNLS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return DNLS_OK;
+}
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+}  // namespace
+
+struct dnls_graph {
+  Symbolic sym;
+  int device = 0;
+  int* dbuf = nullptr;
+  DevGraph dg{};
+  std::mutex mu;
+  const void* last_ws = nullptr;   // workspace holding the last implicit factor
+  int last_batch = -1;
+};
+
+// ----------------------------------------------------------------------------- workspace layout
+namespace {
+struct WsLayout {
+  size_t L, x, jac, cost, trial, S, Sprev, lam, maxd, st, it, total;
+};
+WsLayout ws_layout(const Symbolic& s, int B) {
+  const int D = s.D, PS = D == 6 ? 12 : 6, JS = 2 * D * D + D;
+  const size_t n = (size_t)s.N * D, slots = (size_t)s.E + s.P;
+  WsLayout w{};
+  size_t o = 0;
+  w.L = o;     o = align_up(o + sizeof(double) * (size_t)B * s.storage);
+  w.x = o;     o = align_up(o + sizeof(double) * (size_t)B * n);
+  w.jac = o;   o = align_up(o + sizeof(double) * (size_t)B * slots * JS);
+  w.cost = o;  o = align_up(o + sizeof(double) * (size_t)B * slots);
+  w.trial = o; o = align_up(o + sizeof(double) * (size_t)B * s.N * PS);
+  w.S = o;     o = align_up(o + sizeof(double) * B);
+  w.Sprev = o; o = align_up(o + sizeof(double) * B);
+  w.lam = o;   o = align_up(o + sizeof(double) * B);
+  w.maxd = o;  o = align_up(o + sizeof(double) * B);
+  w.st = o;    o = align_up(o + sizeof(int) * B);
+  w.it = o;    o = align_up(o + sizeof(int) * B);
+  w.total = o;
+  return w;
+}
+DevWs ws_views(const WsLayout& l, void* base) {
+  char* p = (char*)base;
+  DevWs w;
+  w.L = (double*)(p + l.L);
+  w.x = (double*)(p + l.x);
+  w.jac = (double*)(p + l.jac);
+  w.cost = (double*)(p + l.cost);
+  w.trial = (double*)(p + l.trial);
+  w.S = (double*)(p + l.S);
+  w.Sprev = (double*)(p + l.Sprev);
+  w.lam = (double*)(p + l.lam);
+  w.maxd = (double*)(p + l.maxd);
+  w.st = (int*)(p + l.st);
+  w.it = (int*)(p + l.it);
+  return w;
+}
+DevProb dev_prob(const dnls_problem* p) {
+  DevProb d;
+  d.poses = p->poses;
+  d.meas = p->meas;
+  d.prior_meas = p->prior_meas;
+  d.pm_bstride = p->prior_meas_bstride;
+  d.w_edge = p->w_edge;
+  d.we_bstride = p->w_edge_bstride;
+  d.w_prior = p->w_prior;
+  d.wp_bstride = p->w_prior_bstride;
+  return d;
+}
+}  // namespace
+
+// ============================================================================= kernels
+namespace {
+
+struct FwdParams {
+  int K;
+  int lm;
+  double alpha;
+  double lam0, lam_min, lam_max, lam_down, lam_up;
+  int damping;
+  int early_stop;
+  double abs_tol, rel_tol;
+  int implicit;
+  double* objective;
+  int* status;
+  int* iterations;
+};
+
+// CTA-wide: S = sum(cost), maxdiag = max over warps.  Returns via shared variables.
+template <int D>
+__device__ void finish_assembly(const DevGraph& g, const double* cost_b, double* s_red, double* sh_S,
+                                double* sh_max) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s = warp0_sum(cost_b, g.E + g.P);
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int i = 0; i < NT / 32; ++i) m = fmax(m, s_red[i]);
+      *sh_S = s;
+      *sh_max = m;
+    }
+  }
+  __syncthreads();
+}
+
+template <int D>
+__global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs ws, FwdParams fp) {
+  constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
+  const int b = blockIdx.x;
+  __shared__ double s_red[NT / 32];
+  __shared__ double sh_S, sh_max, sh_Stry;
+  __shared__ int sh_fail;
+  const size_t slots = (size_t)g.E + g.P;
+  double* Tb = pr.poses + (size_t)b * g.N * PS;
+  double* Ttr = ws.trial + (size_t)b * g.N * PS;
+  double* jac_b = ws.jac + (size_t)b * slots * JS;
+  double* cost_b = ws.cost + (size_t)b * slots;
+  double* x_b = ws.x + (size_t)b * g.n;
+  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
+
+  int status = DNLS_ST_OK, iters = 0;
+  double lam = fp.lam0, Sprev = 0.0;
+  bool have_prev = false;
+  for (int k = 0; k < fp.K; ++k) {
+    // a1 + a2 at theta_k
+    jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
+    __syncthreads();
+    assemble_phase<D, NT>(g, L, jac_b, x_b, fp.lm ? lam : -1.0, fp.damping, s_red);
+    finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+    const double S = sh_S;
+    if (fp.early_stop && have_prev && fabs(S - Sprev) < fp.abs_tol + fp.rel_tol * Sprev) {
+      status = DNLS_ST_CONVERGED;
+      break;
+    }
+    if (threadIdx.x == 0) sh_fail = 0;
+    __syncthreads();
+    factor_phase<D, NT>(g, L, 1e-13 * sh_max, &sh_fail);
+    const bool ok = sh_fail == 0;
+    __syncthreads();
+    if (!fp.lm) {
+      if (!ok) {
+        status = DNLS_ST_NOT_SPD;
+        break;
+      }
+      solve_phase<D, NT>(g, L, x_b);
+      retract_phase<D, NT>(g, Tb, Tb, x_b, fp.alpha);
+      __syncthreads();
+      ++iters;
+      Sprev = S;
+      have_prev = true;
+    } else {
+      ++iters;
+      bool accept = false;
+      if (ok) {
+        solve_phase<D, NT>(g, L, x_b);
+        retract_phase<D, NT>(g, Tb, Ttr, x_b, fp.alpha);
+        __syncthreads();
+        objective_phase<D, NT>(g, pr, Ttr, b, cost_b);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          double s = warp0_sum(cost_b, g.E + g.P);
+          if (threadIdx.x == 0) sh_Stry = s;
+        }
+        __syncthreads();
+        accept = sh_Stry < S;
+      }
+      if (accept) {
+        for (int i = threadIdx.x; i < g.N * PS; i += NT) Tb[i] = Ttr[i];
+        __syncthreads();
+        lam = fmax(lam / fp.lam_down, fp.lam_min);
+        Sprev = S;
+        have_prev = true;
+      } else {
+        if (lam >= fp.lam_max) {
+          status = DNLS_ST_SATURATED;
+          break;
+        }
+        lam = fmin(lam * fp.lam_up, fp.lam_max);
+      }
+    }
+  }
+  __syncthreads();
+  // final objective S(theta_K); implicit: undamped H(theta_K) and its factor stay in ws
+  if (fp.implicit) {
+    jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
+    __syncthreads();
+    assemble_phase<D, NT>(g, L, jac_b, x_b, -1.0, 0, s_red);
+    finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+    if (threadIdx.x == 0) sh_fail = 0;
+    __syncthreads();
+    factor_phase<D, NT>(g, L, 1e-13 * sh_max, &sh_fail);
+    __syncthreads();
+    if (sh_fail && status == DNLS_ST_OK) status = DNLS_ST_NOT_SPD;
+  } else {
+    objective_phase<D, NT>(g, pr, Tb, b, cost_b);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double s = warp0_sum(cost_b, g.E + g.P);
+      if (threadIdx.x == 0) sh_S = s;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (fp.objective) fp.objective[b] = sh_S;
+    if (fp.status) fp.status[b] = status;
+    if (fp.iterations) fp.iterations[b] = iters;
+    ws.S[b] = sh_S;
+    ws.lam[b] = lam;
+    ws.st[b] = status;
+    ws.it[b] = iters;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, DevWs ws, const double* lam,
+                                                      int damping, double* objective) {
+  constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
+  const int b = blockIdx.x;
+  __shared__ double s_red[NT / 32];
+  __shared__ double sh_S, sh_max;
+  const size_t slots = (size_t)g.E + g.P;
+  const double* Tb = pr.poses + (size_t)b * g.N * PS;
+  double* jac_b = ws.jac + (size_t)b * slots * JS;
+  double* cost_b = ws.cost + (size_t)b * slots;
+  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
+  jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
+  __syncthreads();
+  assemble_phase<D, NT>(g, L, jac_b, ws.x + (size_t)b * g.n, lam ? lam[b] : -1.0, damping, s_red);
+  finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+  if (threadIdx.x == 0) {
+    if (objective) objective[b] = sh_S;
+    ws.S[b] = sh_S;
+    ws.maxd[b] = sh_max;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* status) {
+  const int b = blockIdx.x;
+  __shared__ int sh_fail;
+  if (threadIdx.x == 0) sh_fail = 0;
+  __syncthreads();
+  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
+  factor_phase<D, NT>(g, L, 1e-13 * ws.maxd[b], &sh_fail);
+  __syncthreads();
+  if (threadIdx.x == 0 && status) status[b] = sh_fail ? DNLS_ST_NOT_SPD : DNLS_ST_OK;
+}
+
+// rhs/x in original order [B][N][D]
+template <int D>
+__global__ void __launch_bounds__(NT, 1) k_solve(DevGraph g, DevWs ws, const double* rhs, double* xout) {
+  const int b = blockIdx.x;
+  double* x_b = ws.x + (size_t)b * g.n;
+  for (int i = threadIdx.x; i < g.n; i += NT) {
+    const int o = i / D, a = i - o * D;
+    x_b[(size_t)g.iperm[o] * D + a] = rhs[(size_t)b * g.n + i];
+  }
+  __syncthreads();
+  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
+  solve_phase<D, NT>(g, L, x_b);
+  __syncthreads();
+  for (int i = threadIdx.x; i < g.n; i += NT) {
+    const int o = i / D, a = i - o * D;
+    xout[(size_t)b * g.n + i] = x_b[(size_t)g.iperm[o] * D + a];
+  }
+}
+
+// implicit backward, per element: v -> lambda = H^-1 v (cached factor) -> per-slot weight grads
+template <int D>
+__global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
+                                                     int grad_kind) {
+  constexpr int PS = GT<D>::PS;
+  const int b = blockIdx.x;
+  const size_t slots = (size_t)g.E + g.P;
+  const double* Tb = pr.poses + (size_t)b * g.N * PS;
+  double* x_b = ws.x + (size_t)b * g.n;
+  double* out_b = ws.cost + (size_t)b * slots;
+  if (ws.st[b] == DNLS_ST_NOT_SPD) {   // no valid factor: zero gradient contribution
+    for (int s = threadIdx.x; s < (int)slots; s += NT) out_b[s] = 0.0;
+    return;
+  }
+  // v (original order) -> permuted
+  for (int o = threadIdx.x; o < g.N; o += NT) {
+    double v[D];
+    if (grad_kind == DNLS_GRAD_TANGENT) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) v[a] = gpose[((size_t)b * g.N + o) * D + a];
+    } else {
+      // v_a = < dL/dT , T G_a >  (top rows), G_a the Lie-algebra generators
+      const double* G = gpose + ((size_t)b * g.N + o) * PS;
+      const double* T = Tb + (size_t)o * PS;
+      if (D == 6) {
+        // T G_a for translation generators: column 3 = R e_a ; rotation generators: R [e_a]x in the
+        // 3x3 block.   <G, R[e]x> = sum_ij G_ij (R[e]x)_ij
+#pragma unroll
+        for (int a = 0; a < 3; ++a) v[a] = G[0 * 4 + 3] * T[0 * 4 + a] + G[1 * 4 + 3] * T[1 * 4 + a] + G[2 * 4 + 3] * T[2 * 4 + a];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          double e[3] = {0.0, 0.0, 0.0};
+          e[a] = 1.0;
+          // [e]x columns: col0 = (0, e2, -e1), col1 = (-e2, 0, e0), col2 = (e1, -e0, 0)
+          double Ex[3][3] = {{0.0, -e[2], e[1]}, {e[2], 0.0, -e[0]}, {-e[1], e[0], 0.0}};
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              double rex = T[i * 4 + 0] * Ex[0][j] + T[i * 4 + 1] * Ex[1][j] + T[i * 4 + 2] * Ex[2][j];
+              acc += G[i * 4 + j] * rex;
+            }
+          v[3 + a] = acc;
+        }
+      } else {
+        v[0] = G[2] * T[0] + G[5] * T[3];
+        v[1] = G[2] * T[1] + G[5] * T[4];
+        // rotation generator [[0,-1],[1,0]]: R*Gen = [[R01, -R00], [R11, -R10]]
+        v[2] = G[0] * T[1] - G[1] * T[0] + G[3] * T[4] - G[4] * T[3];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) x_b[(size_t)g.iperm[o] * D + a] = v[a];
+  }
+  __syncthreads();
+  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
+  solve_phase<D, NT>(g, L, x_b);
+  __syncthreads();
+  // dL/dw = -2 w (C lambda) . c  (unweighted C, c at theta_K)
+  for (int slot = threadIdx.x; slot < (int)slots; slot += NT) {
+    double c[D], Ci[D * D], Cj[D * D];
+    eval_slot<D>(g, pr, Tb, b, slot, c, Ci, Cj, true);
+    const double w = slot_weight<D>(g, pr, b, slot);
+    double dot = 0.0;
+    if (slot < g.E) {
+      const double* li = x_b + (size_t)D * g.iperm[g.edges[2 * slot]];
+      const double* lj = x_b + (size_t)D * g.iperm[g.edges[2 * slot + 1]];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double cl = 0.0;
+#pragma unroll
+        for (int q = 0; q < D; ++q) cl += Ci[r * D + q] * li[q] + Cj[r * D + q] * lj[q];
+        dot += cl * c[r];
+      }
+    } else {
+      const double* lp = x_b + (size_t)D * g.iperm[g.prior_vars[slot - g.E]];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double cl = 0.0;
+#pragma unroll
+        for (int q = 0; q < D; ++q) cl += Ci[r * D + q] * lp[q];
+        dot += cl * c[r];
+      }
+    }
+    out_b[slot] = -2.0 * w * dot;
+  }
+}
+
+// fixed-order batch reduction (or per-element copy) of the per-slot weight gradients
+__global__ void k_reduce_wgrad(int B, int E, int P, const double* src, double* ge, double* gp,
+                               long long bstride) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slots = E + P;
+  if (slot >= slots) return;
+  double* dst = slot < E ? ge : gp;
+  const int idx = slot < E ? slot : slot - E;
+  if (!dst) return;
+  if (bstride == 0) {
+    double s = 0.0;
+    for (int b = 0; b < B; ++b) s += src[(size_t)b * slots + slot];
+    dst[idx] = s;
+  } else {
+    for (int b = 0; b < B; ++b) dst[(size_t)b * bstride + idx] = src[(size_t)b * slots + slot];
+  }
+}
+
+template <int D>
+__global__ void k_export_factor(DevGraph g, DevWs ws, double* dense) {
+  const int b = blockIdx.x;
+  const size_t n = g.n;
+  double* Db = dense + (size_t)b * n * n;
+  const double* Lb = ws.L + (size_t)b * g.storage;
+  for (size_t i = threadIdx.x; i < n * n; i += NT) Db[i] = 0.0;
+  __syncthreads();
+  // iterate storage panels: (row, col) scalar within panel -> permuted global indices
+  for (int s = 0; s < g.S; ++s) {
+    const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s], off = g.sn_off[s];
+    const int rb = g.snr_ptr[s];
+    for (int it = threadIdx.x; it < m * w; it += NT) {
+      const int c = it / m, r = it - c * m;
+      int gr;
+      if (r < w) {
+        if (r < c) continue;
+        gr = D * f + r;
+      } else {
+        const int rr = (r - w) / D, a = (r - w) % D;
+        gr = D * g.snr[rb + rr] + a;
+      }
+      Db[(size_t)gr * n + (size_t)D * f + c] = Lb[off + (size_t)c * m + r];
+    }
+  }
+}
+
+template <int D>
+__global__ void k_import_matrix(DevGraph g, DevWs ws, const double* dense) {
+  const int b = blockIdx.x;
+  const size_t n = g.n;
+  const double* Db = dense + (size_t)b * n * n;
+  double* Lb = ws.L + (size_t)b * g.storage;
+  __shared__ double s_red[NT / 32];
+  double mymax = 0.0;
+  for (int s = 0; s < g.S; ++s) {
+    const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s], off = g.sn_off[s];
+    const int rb = g.snr_ptr[s];
+    for (int it = threadIdx.x; it < m * w; it += NT) {
+      const int c = it / m, r = it - c * m;
+      double v = 0.0;
+      const int pc = f + c / D, ac = c % D;
+      if (r >= c) {
+        int pr_, ar;
+        if (r < w) {
+          pr_ = f + r / D;
+          ar = r % D;
+        } else {
+          pr_ = g.snr[rb + (r - w) / D];
+          ar = (r - w) % D;
+        }
+        v = Db[((size_t)g.perm[pr_] * D + ar) * n + (size_t)g.perm[pc] * D + ac];
+        if (r == c) mymax = fmax(mymax, v);
+      }
+      Lb[off + (size_t)c * m + r] = v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < NT / 32; ++i) m = fmax(m, s_red[i]);
+    ws.maxd[b] = m;
+  }
+}
+
+template <int D>
+__global__ void k_export_rhs(DevGraph g, DevWs ws, double* out) {
+  const int b = blockIdx.x;
+  const double* x_b = ws.x + (size_t)b * g.n;
+  for (int i = threadIdx.x; i < g.n; i += NT) {
+    const int o = i / D, a = i - o * D;
+    out[(size_t)b * g.n + i] = x_b[(size_t)g.iperm[o] * D + a];
+  }
+}
+
+}  // namespace
+
+// ============================================================================= C ABI
+extern "C" {
+
+DNLS_API const char* dnls_version_string(void) {
+  return "libdnls 1 (sm_100a, fp64; one CTA per batch element; supernodal Cholesky)";
+}
+
+DNLS_API const char* dnls_last_error(void) { return g_err.c_str(); }
+
+DNLS_API void dnls_options_default(dnls_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->optimizer = DNLS_GN;
+  o->max_iterations = 10;
+  o->step_size = 1.0;
+  o->lambda0 = 1e-3;
+  o->lambda_min = 1e-8;
+  o->lambda_max = 1e5;
+  o->lambda_down = 3.0;
+  o->lambda_up = 2.0;
+  o->damping = DNLS_DAMP_MARQUARDT;
+  o->early_stop = 0;
+  o->abs_tol = 1e-10;
+  o->rel_tol = 1e-8;
+  o->backward_mode = DNLS_BWD_NONE;
+}
+
+DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t num_edges,
+                                       const int32_t* edges_ij, int32_t num_priors,
+                                       const int32_t* prior_vars, int32_t device, dnls_graph** out) {
+  if (!out) return fail(DNLS_E_INVALID, "dnls_graph_create: out is NULL");
+  *out = nullptr;
+  dnls_graph* g = new dnls_graph();
+  int code = 0;
+  SymbolicOptions sopt;
+  if (const char* env = std::getenv("DNLS_RELAX")) {   // tuning override: "a,sc,sf,mc,mf,max,bf"
+    std::sscanf(env, "%d,%d,%lf,%d,%lf,%d,%lf", &sopt.relax_always_cols, &sopt.relax_small_cols,
+                &sopt.relax_small_frac, &sopt.relax_mid_cols, &sopt.relax_mid_frac, &sopt.relax_max_cols,
+                &sopt.relax_big_frac);
+  }
+  std::string msg = analyze(group, num_vars, num_edges, edges_ij, num_priors, prior_vars, sopt, g->sym, &code);
+  if (!msg.empty()) {
+    delete g;
+    return fail((dnls_status)code, msg);
+  }
+  const Symbolic& s = g->sym;
+  // pack all int32 arrays into one device buffer
+  std::vector<int32_t> buf;
+  std::vector<size_t> offs;
+  auto add = [&](const std::vector<int32_t>& v) {
+    offs.push_back(buf.size());
+    buf.insert(buf.end(), v.begin(), v.end());
+    buf.push_back(0);   // never empty
+  };
+  std::vector<int32_t> sn_off32(s.sn_off.begin(), s.sn_off.end());
+  add(s.perm); add(s.iperm); add(s.edges); add(s.prior_vars);
+  add(s.sn_first); add(s.sn_ncols); add(s.sn_m); add(s.sn_w); add(sn_off32);
+  add(s.level_ptr); add(s.level_sn);
+  add(s.ut_level_ptr); add(s.ut_off); add(s.ut_ld); add(s.ut_cptr); add(s.uc_a); add(s.uc_b); add(s.uc_ld); add(s.uc_w);
+  add(s.fc_ptr); add(s.fc_off); add(s.fc_ld); add(s.fc_w); add(s.fc_x);
+  add(s.snr_ptr); add(s.snr);
+  add(s.blk_off); add(s.blk_ld); add(s.blk_kind); add(s.blk_cptr); add(s.blk_con);
+  add(s.bc_ptr); add(s.bc);
+  g->device = device;
+  if (device < 0) {   // host-only symbolic analysis (no device arrays; compute calls refuse it)
+    *out = g;
+    return DNLS_OK;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    delete g;
+    return fail(DNLS_E_CUDA, "dnls_graph_create: cudaSetDevice(" + std::to_string(device) + ") failed");
+  }
+  g->device = device;
+  if (cudaMalloc(&g->dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
+      cudaMemcpy(g->dbuf, buf.data(), buf.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+    std::string e = cudaGetErrorString(cudaGetLastError());
+    if (g->dbuf) cudaFree(g->dbuf);
+    cudaSetDevice(prev);
+    delete g;
+    return fail(DNLS_E_CUDA, "dnls_graph_create: device upload failed: " + e);
+  }
+  cudaSetDevice(prev);
+  const int* d = g->dbuf;
+  int k = 0;
+  DevGraph& dg = g->dg;
+  dg.D = s.D; dg.N = s.N; dg.E = s.E; dg.P = s.P; dg.S = s.S; dg.L = s.num_levels;
+  dg.storage = (int)s.storage; dg.nblk = (int)s.blk_off.size(); dg.n = s.N * s.D;
+  dg.perm = d + offs[k++]; dg.iperm = d + offs[k++]; dg.edges = d + offs[k++]; dg.prior_vars = d + offs[k++];
+  dg.sn_first = d + offs[k++]; dg.sn_ncols = d + offs[k++]; dg.sn_m = d + offs[k++]; dg.sn_w = d + offs[k++];
+  dg.sn_off = d + offs[k++];
+  dg.level_ptr = d + offs[k++]; dg.level_sn = d + offs[k++];
+  dg.ut_level_ptr = d + offs[k++]; dg.ut_off = d + offs[k++]; dg.ut_ld = d + offs[k++]; dg.ut_cptr = d + offs[k++];
+  dg.uc_a = d + offs[k++]; dg.uc_b = d + offs[k++]; dg.uc_ld = d + offs[k++]; dg.uc_w = d + offs[k++];
+  dg.fc_ptr = d + offs[k++]; dg.fc_off = d + offs[k++]; dg.fc_ld = d + offs[k++]; dg.fc_w = d + offs[k++];
+  dg.fc_x = d + offs[k++];
+  dg.snr_ptr = d + offs[k++]; dg.snr = d + offs[k++];
+  dg.blk_off = d + offs[k++]; dg.blk_ld = d + offs[k++]; dg.blk_kind = d + offs[k++]; dg.blk_cptr = d + offs[k++];
+  dg.blk_con = d + offs[k++];
+  dg.bc_ptr = d + offs[k++]; dg.bc = d + offs[k++];
+  *out = g;
+  return DNLS_OK;
+}
+
+DNLS_API void dnls_graph_destroy(dnls_graph* g) {
+  if (!g) return;
+  if (g->dbuf) cudaFree(g->dbuf);
+  delete g;
+}
+
+DNLS_API dnls_status dnls_graph_stats(const dnls_graph* g, dnls_stats* o) {
+  if (!g || !o) return fail(DNLS_E_INVALID, "dnls_graph_stats: NULL argument");
+  const Symbolic& s = g->sym;
+  std::memset(o, 0, sizeof(*o));
+  o->group = s.D;
+  o->num_vars = s.N;
+  o->num_edges = s.E;
+  o->num_priors = s.P;
+  o->num_supernodes = s.S;
+  o->num_levels = s.num_levels;
+  o->etree_height = s.etree_height;
+  o->max_supernode_cols = s.max_sn_cols_sc;
+  o->max_panel_rows = s.max_panel_rows;
+  o->nnz_H_blocks = s.nnz_H_blocks;
+  o->nnz_L_blocks = s.nnz_L_blocks;
+  o->nnz_L = s.nnz_L;
+  o->storage_doubles = s.storage;
+  o->factor_flops = s.factor_flops;
+  o->solve_flops = 4.0 * (double)s.nnz_L;
+  const double pose_b = s.D == 6 ? 96.0 : 48.0;
+  const double nvec = 8.0 * s.N * s.D;
+  o->bytes_linearize = pose_b * (s.N + s.E + s.P) + 8.0 * s.nnz_L + nvec;
+  o->bytes_factor = 16.0 * s.nnz_L;
+  o->bytes_solve = 16.0 * s.nnz_L + 2.0 * nvec;
+  o->bytes_update = 2.0 * pose_b * s.N + nvec;
+  o->bytes_backward = 16.0 * s.nnz_L + pose_b * (s.N + s.E + s.P) + 2.0 * nvec;
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_graph_perm(const dnls_graph* g, int32_t* perm) {
+  if (!g || !perm) return fail(DNLS_E_INVALID, "dnls_graph_perm: NULL argument");
+  std::copy(g->sym.perm.begin(), g->sym.perm.end(), perm);
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_graph_etree(const dnls_graph* g, int32_t* parent) {
+  if (!g || !parent) return fail(DNLS_E_INVALID, "dnls_graph_etree: NULL argument");
+  std::copy(g->sym.parent.begin(), g->sym.parent.end(), parent);
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_graph_pattern(const dnls_graph* g, int32_t* colptr, int32_t* rowidx) {
+  if (!g || !colptr || !rowidx) return fail(DNLS_E_INVALID, "dnls_graph_pattern: NULL argument");
+  const Symbolic& s = g->sym;
+  int32_t k = 0;
+  for (int c = 0; c < s.N; ++c) {
+    colptr[c] = k;
+    rowidx[k++] = c;
+    for (int r : s.colstruct[c]) rowidx[k++] = r;
+  }
+  colptr[s.N] = k;
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_graph_supernodes(const dnls_graph* g, int32_t* first, int32_t* ncols, int32_t* level) {
+  if (!g) return fail(DNLS_E_INVALID, "dnls_graph_supernodes: NULL graph");
+  const Symbolic& s = g->sym;
+  if (first) std::copy(s.sn_first.begin(), s.sn_first.end(), first);
+  if (ncols) std::copy(s.sn_ncols.begin(), s.sn_ncols.end(), ncols);
+  if (level) std::copy(s.sn_level.begin(), s.sn_level.end(), level);
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_workspace_bytes(const dnls_graph* g, int32_t batch, const dnls_options* opt,
+                                          size_t* bytes) {
+  (void)opt;
+  if (!g || !bytes) return fail(DNLS_E_INVALID, "dnls_workspace_bytes: NULL argument");
+  if (batch < 0) return fail(DNLS_E_SHAPE, "dnls_workspace_bytes: batch < 0");
+  *bytes = ws_layout(g->sym, batch).total;
+  return DNLS_OK;
+}
+
+namespace {
+dnls_status check_common(const char* fn, const dnls_graph* g, int32_t batch, const void* ws, size_t ws_bytes) {
+  if (!g) return fail(DNLS_E_INVALID, std::string(fn) + ": graph is NULL");
+  if (!g->dbuf) return fail(DNLS_E_INVALID, std::string(fn) + ": graph was created host-only (device < 0)");
+  if (batch < 0) return fail(DNLS_E_SHAPE, std::string(fn) + ": batch < 0");
+  if (!ws && batch > 0) return fail(DNLS_E_INVALID, std::string(fn) + ": workspace is NULL");
+  if (((uintptr_t)ws) % 256) return fail(DNLS_E_INVALID, std::string(fn) + ": workspace not 256-byte aligned");
+  size_t need = ws_layout(g->sym, batch).total;
+  if (ws_bytes < need)
+    return fail(DNLS_E_WORKSPACE, std::string(fn) + ": workspace has " + std::to_string(ws_bytes) +
+                                      " bytes, needs " + std::to_string(need));
+  return DNLS_OK;
+}
+dnls_status check_problem(const char* fn, const dnls_graph* g, const dnls_problem* p) {
+  if (!p) return fail(DNLS_E_INVALID, std::string(fn) + ": problem is NULL");
+  if (!p->poses) return fail(DNLS_E_INVALID, std::string(fn) + ": problem.poses is NULL");
+  if (g->sym.E > 0 && (!p->meas || !p->w_edge))
+    return fail(DNLS_E_INVALID, std::string(fn) + ": problem.meas / w_edge is NULL with num_edges > 0");
+  if (g->sym.P > 0 && (!p->prior_meas || !p->w_prior))
+    return fail(DNLS_E_INVALID, std::string(fn) + ": problem.prior_meas / w_prior is NULL with num_priors > 0");
+  if (p->prior_meas_bstride < 0 || p->w_edge_bstride < 0 || p->w_prior_bstride < 0)
+    return fail(DNLS_E_INVALID, std::string(fn) + ": negative batch stride");
+  return DNLS_OK;
+}
+#define DISPATCH_D(D_, ...)            \
+  if ((D_) == 6) {                     \
+    constexpr int DD = 6;              \
+    __VA_ARGS__;                       \
+  } else {                             \
+    constexpr int DD = 3;              \
+    __VA_ARGS__;                       \
+  }
+}  // namespace
+
+DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls_options* opt,
+                                  const dnls_problem* prob, void* workspace, size_t ws_bytes, void* stream) {
+  dnls_status st = check_common("dnls_forward", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if (!opt) return fail(DNLS_E_INVALID, "dnls_forward: options is NULL");
+  if ((st = check_problem("dnls_forward", g, prob))) return st;
+  if (opt->optimizer != DNLS_GN && opt->optimizer != DNLS_LM)
+    return fail(DNLS_E_INVALID, "dnls_forward: unknown optimizer " + std::to_string(opt->optimizer));
+  if (opt->max_iterations < 0) return fail(DNLS_E_INVALID, "dnls_forward: max_iterations < 0");
+  if (!(opt->step_size > 0.0 && opt->step_size <= 1.0))
+    return fail(DNLS_E_INVALID, "dnls_forward: step_size must be in (0, 1]");
+  if (opt->backward_mode != DNLS_BWD_NONE && opt->backward_mode != DNLS_BWD_IMPLICIT)
+    return fail(DNLS_E_UNSUPPORTED, "dnls_forward: backward_mode " + std::to_string(opt->backward_mode) +
+                                        " not supported (NONE or IMPLICIT)");
+  if (opt->optimizer == DNLS_LM &&
+      !(opt->lambda0 > 0 && opt->lambda_min > 0 && opt->lambda_max >= opt->lambda_min && opt->lambda_down > 1 &&
+        opt->lambda_up > 1))
+    return fail(DNLS_E_INVALID, "dnls_forward: invalid LM damping schedule");
+  if (opt->damping != DNLS_DAMP_MARQUARDT && opt->damping != DNLS_DAMP_IDENTITY)
+    return fail(DNLS_E_INVALID, "dnls_forward: unknown damping");
+  dnls_graph* gm = const_cast<dnls_graph*>(g);
+  {
+    std::lock_guard<std::mutex> lk(gm->mu);
+    if (gm->last_ws == workspace) {
+      gm->last_ws = nullptr;
+      gm->last_batch = -1;
+    }
+  }
+  if (batch == 0) return DNLS_OK;
+  WsLayout l = ws_layout(g->sym, batch);
+  DevWs ws = ws_views(l, workspace);
+  FwdParams fp;
+  fp.K = opt->max_iterations;
+  fp.lm = opt->optimizer == DNLS_LM;
+  fp.alpha = opt->step_size;
+  fp.lam0 = opt->lambda0;
+  fp.lam_min = opt->lambda_min;
+  fp.lam_max = opt->lambda_max;
+  fp.lam_down = opt->lambda_down;
+  fp.lam_up = opt->lambda_up;
+  fp.damping = opt->damping;
+  fp.early_stop = opt->early_stop;
+  fp.abs_tol = opt->abs_tol;
+  fp.rel_tol = opt->rel_tol;
+  fp.implicit = opt->backward_mode == DNLS_BWD_IMPLICIT;
+  fp.objective = prob->objective;
+  fp.status = prob->status;
+  fp.iterations = prob->iterations;
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, (k_forward<DD><<<batch, NT, 0, s>>>(g->dg, dev_prob(prob), ws, fp)));
+  if ((st = cuda_check("dnls_forward: k_forward launch"))) return st;
+  if (fp.implicit) {
+    std::lock_guard<std::mutex> lk(gm->mu);
+    gm->last_ws = workspace;
+    gm->last_batch = batch;
+  }
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
+                                            const double* grad_poses, int32_t grad_kind, double* grad_w_edge,
+                                            double* grad_w_prior, int64_t grad_bstride, void* workspace,
+                                            size_t ws_bytes, void* stream) {
+  dnls_status st = check_common("dnls_backward_implicit", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if ((st = check_problem("dnls_backward_implicit", g, prob))) return st;
+  if (!grad_poses && batch > 0) return fail(DNLS_E_INVALID, "dnls_backward_implicit: grad_poses is NULL");
+  if (grad_kind != DNLS_GRAD_TANGENT && grad_kind != DNLS_GRAD_MATRIX)
+    return fail(DNLS_E_INVALID, "dnls_backward_implicit: unknown grad_kind");
+  if (grad_bstride < 0) return fail(DNLS_E_INVALID, "dnls_backward_implicit: grad_bstride < 0");
+  if (grad_bstride > 0 && grad_bstride < std::max(g->sym.E, g->sym.P))
+    return fail(DNLS_E_SHAPE, "dnls_backward_implicit: grad_bstride smaller than num_edges/num_priors");
+  {
+    dnls_graph* gm = const_cast<dnls_graph*>(g);
+    std::lock_guard<std::mutex> lk(gm->mu);
+    if (gm->last_ws != workspace || gm->last_batch != batch)
+      return fail(DNLS_E_STATE,
+                  "dnls_backward_implicit: no implicit-mode dnls_forward on this workspace/batch "
+                  "(factor cache missing or overwritten)");
+  }
+  if (batch == 0) return DNLS_OK;
+  WsLayout l = ws_layout(g->sym, batch);
+  DevWs ws = ws_views(l, workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, (k_backward<DD><<<batch, NT, 0, s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind)));
+  if ((st = cuda_check("dnls_backward_implicit: k_backward launch"))) return st;
+  const int slots = g->sym.E + g->sym.P;
+  if (slots > 0 && (grad_w_edge || grad_w_prior)) {
+    k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
+                                                        grad_w_prior, (long long)grad_bstride);
+    if ((st = cuda_check("dnls_backward_implicit: k_reduce_wgrad launch"))) return st;
+  }
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_linearize(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
+                                    const double* lambda, int32_t damping, void* workspace, size_t ws_bytes,
+                                    void* stream) {
+  dnls_status st = check_common("dnls_linearize", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if ((st = check_problem("dnls_linearize", g, prob))) return st;
+  if (damping != DNLS_DAMP_MARQUARDT && damping != DNLS_DAMP_IDENTITY)
+    return fail(DNLS_E_INVALID, "dnls_linearize: unknown damping");
+  if (batch == 0) return DNLS_OK;
+  DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D,
+             (k_linearize<DD><<<batch, NT, 0, s>>>(g->dg, dev_prob(prob), ws, lambda, damping, prob->objective)));
+  return cuda_check("dnls_linearize: launch");
+}
+
+DNLS_API dnls_status dnls_factorize(const dnls_graph* g, int32_t batch, void* workspace, size_t ws_bytes,
+                                    int32_t* status, void* stream) {
+  dnls_status st = check_common("dnls_factorize", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if (batch == 0) return DNLS_OK;
+  DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, (k_factorize<DD><<<batch, NT, 0, s>>>(g->dg, ws, status)));
+  return cuda_check("dnls_factorize: launch");
+}
+
+DNLS_API dnls_status dnls_solve_factored(const dnls_graph* g, int32_t batch, void* workspace, size_t ws_bytes,
+                                         const double* rhs, double* x, void* stream) {
+  dnls_status st = check_common("dnls_solve_factored", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if (batch > 0 && (!rhs || !x)) return fail(DNLS_E_INVALID, "dnls_solve_factored: rhs/x is NULL");
+  if (batch == 0) return DNLS_OK;
+  DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, (k_solve<DD><<<batch, NT, 0, s>>>(g->dg, ws, rhs, x)));
+  return cuda_check("dnls_solve_factored: launch");
+}
+
+DNLS_API dnls_status dnls_export_factor(const dnls_graph* g, int32_t batch, const void* workspace, size_t ws_bytes,
+                                        double* dense, void* stream) {
+  dnls_status st = check_common("dnls_export_factor", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if (batch > 0 && !dense) return fail(DNLS_E_INVALID, "dnls_export_factor: dense is NULL");
+  if (batch == 0) return DNLS_OK;
+  DevWs ws = ws_views(ws_layout(g->sym, batch), const_cast<void*>(workspace));
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, (k_export_factor<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
+  return cuda_check("dnls_export_factor: launch");
+}
+
+DNLS_API dnls_status dnls_import_matrix(const dnls_graph* g, int32_t batch, const double* dense, void* workspace,
+                                        size_t ws_bytes, void* stream) {
+  dnls_status st = check_common("dnls_import_matrix", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if (batch > 0 && !dense) return fail(DNLS_E_INVALID, "dnls_import_matrix: dense is NULL");
+  if (batch == 0) return DNLS_OK;
+  DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, (k_import_matrix<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
+  return cuda_check("dnls_import_matrix: launch");
+}
+
+DNLS_API dnls_status dnls_export_rhs(const dnls_graph* g, int32_t batch, const void* workspace, size_t ws_bytes,
+                                     double* b, void* stream) {
+  dnls_status st = check_common("dnls_export_rhs", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if (batch > 0 && !b) return fail(DNLS_E_INVALID, "dnls_export_rhs: b is NULL");
+  if (batch == 0) return DNLS_OK;
+  DevWs ws = ws_views(ws_layout(g->sym, batch), const_cast<void*>(workspace));
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, (k_export_rhs<DD><<<batch, NT, 0, s>>>(g->dg, ws, b)));
+  return cuda_check("dnls_export_rhs: launch");
+}
+
+}  // extern "C"

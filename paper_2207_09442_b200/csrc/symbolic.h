@@ -1,0 +1,74 @@
+// Host symbolic analysis of a pose graph ("symbolic analysis ... as a separate
+// step", :221 "building an elimination tree and then clustering column blocks with similar
+// sparsity patterns", :584 App. F).  Pure C++17, no CUDA.  All indices are pose ("block")
+// indices unless named *_sc (scalar); D is the tangent dimension (3 or 6).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dnls {
+
+struct SymbolicOptions {
+  // relaxed supernode amalgamation (App. F: trade fragmentation against explicit zeros).
+  // A child supernode is merged into its parent when the merged width (pose columns) and the
+  // fraction of explicit zero blocks stay under these limits.
+  int relax_always_cols = 1;      // merged width <= this: always merge
+  int relax_small_cols = 4;       // ... <= this: merge if zero fraction <= relax_small_frac
+  double relax_small_frac = 0.3;
+  int relax_mid_cols = 16;
+  double relax_mid_frac = 0.1;
+  int relax_max_cols = 64;        // hard cap on supernode width (pose columns)
+  double relax_big_frac = 0.05;
+};
+
+struct Symbolic {
+  int D = 0, N = 0, E = 0, P = 0;
+  std::vector<int32_t> edges;       // [E][2] original indices
+  std::vector<int32_t> prior_vars;  // [P]
+  std::vector<int32_t> perm, iperm; // perm[k] = original var at position k
+  std::vector<int32_t> parent;      // pose-level elimination tree (permuted), -1 root
+  std::vector<std::vector<int32_t>> colstruct;  // below-diagonal block rows per pose column
+  int etree_height = 0;
+
+  // supernodes (contiguous pose-column ranges in the postordered numbering)
+  int S = 0;
+  std::vector<int32_t> sn_first, sn_ncols, sn_level, sn_parent, sn_m, sn_w, col_sn;
+  std::vector<int64_t> sn_off;                  // panel offset (doubles) in per-element storage
+  std::vector<std::vector<int32_t>> sn_rows;    // below rows (permuted pose indices, sorted)
+  int64_t storage = 0;
+  int num_levels = 0;
+  std::vector<int32_t> level_ptr, level_sn;     // supernodes grouped by level (height from leaves)
+
+  // numeric factorisation: gather-form update tasks grouped by level of the target
+  //   task t: target block at ut_off (storage offset of entry (0,0)), leading dim ut_ld,
+  //           contributions [ut_cptr[t], ut_cptr[t+1])
+  //   contribution c: source rows at uc_a (entry (row_p, k=0)), uc_b (row_q), ld uc_ld, width uc_w
+  std::vector<int32_t> ut_level_ptr, ut_off, ut_ld, ut_cptr;
+  std::vector<int32_t> uc_a, uc_b, uc_ld, uc_w;
+
+  // forward substitution gather per permuted pose row p: sum over source panels holding row p
+  std::vector<int32_t> fc_ptr, fc_off, fc_ld, fc_w, fc_x;
+  // backward substitution: below rows of each supernode (flattened sn_rows)
+  std::vector<int32_t> snr_ptr, snr;
+
+  // scatter-free assembly: every d x d block of the storage exactly once
+  //   block k: storage offset blk_off[k], leading dim blk_ld[k], kind blk_kind[k]
+  //   (0 = structural zero / upper part, 1 = diagonal, 2 = off-diagonal),
+  //   contributions blk_con[blk_cptr[k] .. blk_cptr[k+1]): slot*4 + rowside*2 + colside
+  //   (slot = edge e, or E + prior k; side 0 = first Jacobian J_i, 1 = J_j)
+  std::vector<int32_t> blk_off, blk_ld, blk_kind, blk_cptr, blk_con;
+  // b = J^T r per permuted pose: bc[bc_ptr[p] .. bc_ptr[p+1]) = slot*2 + side
+  std::vector<int32_t> bc_ptr, bc;
+
+  // stats
+  int64_t nnz_H_blocks = 0, nnz_L_blocks = 0, nnz_L = 0;
+  double factor_flops = 0;
+  int max_sn_cols_sc = 0, max_panel_rows = 0;
+};
+
+// Returns "" on success, else an error message; *code receives the dnls_status value.
+std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int32_t* priors,
+                    const SymbolicOptions& opt, Symbolic& out, int* code);
+
+}  // namespace dnls

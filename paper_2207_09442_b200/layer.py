@@ -1,0 +1,109 @@
+"""TheseusLayer-style differentiable pose-graph layer over libdnls (PAPER.md:147-151
+TheseusLayer "dict in -> dict out", Listing 1 :104-131, backward_mode "implicit").
+
+``PoseGraphSolver`` owns a dnls_graph (one-time symbolic analysis) and a device workspace.
+``pose_graph_layer(...)`` is a torch.autograd.Function: forward runs ``dnls_forward`` (K GN/LM
+iterations, implicit mode keeps the factor of H(theta_K)); backward runs
+``dnls_backward_implicit`` and returns gradients for the learnable cost weights.  Gradients
+w.r.t. the initial poses are refused in implicit mode (Table 6 :726 "Cannot be used
+for learning theta_init").
+"""
+from __future__ import annotations
+
+import torch
+
+from . import dnls as D
+
+
+class PoseGraphSolver:
+    def __init__(self, group: int, num_vars: int, edges, prior_vars, device: int | None = None, **options):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.graph = D.dnls_graph_create(group, num_vars, edges, prior_vars, device)
+        self.device = torch.device("cuda", device)
+        self.options = D.dnls_options_default(**options)
+        self.stats = D.dnls_graph_stats(self.graph)
+        self._ws = None
+        self._ws_batch = -1
+        self.generation = 0
+
+    @property
+    def group(self):
+        return self.graph.group
+
+    def workspace(self, batch: int) -> torch.Tensor:
+        if self._ws is None or self._ws_batch != batch:
+            self._ws = D.alloc_workspace(self.graph, batch, self.options, self.device)
+            self._ws_batch = batch
+        return self._ws
+
+    def forward(self, poses, meas, prior_meas, w_edge, w_prior, implicit: bool = False, options=None):
+        """Solve in place on a copy of ``poses``.  Returns (poses_K, objective, status, iterations)."""
+        opt = options if options is not None else self.options
+        opt.backward_mode = D.BWD_IMPLICIT if implicit else D.BWD_NONE
+        B = poses.shape[0]
+        out = poses.detach().clone().contiguous()
+        obj = torch.empty(B, dtype=torch.float64, device=poses.device)
+        st = torch.empty(B, dtype=torch.int32, device=poses.device)
+        it = torch.empty(B, dtype=torch.int32, device=poses.device)
+        ws = self.workspace(B)
+        prob = D.make_problem(out, meas.contiguous(), prior_meas.contiguous(), w_edge.detach().contiguous(),
+                              w_prior.detach().contiguous(), obj, st, it)
+        D.dnls_forward(self.graph, B, opt, prob, ws)
+        self.generation += 1
+        return out, obj, st, it
+
+    def backward(self, poses_K, meas, prior_meas, w_edge, w_prior, grad_poses, grad_kind=D.GRAD_MATRIX,
+                 per_element: bool = False):
+        B = poses_K.shape[0]
+        ws = self.workspace(B)
+        E, P = self.graph.E, self.graph.P
+        if per_element:
+            ge = torch.zeros(B, max(E, P), dtype=torch.float64, device=poses_K.device)
+            gp = torch.zeros(B, max(E, P), dtype=torch.float64, device=poses_K.device)
+            stride = max(E, P)
+        else:
+            ge = torch.zeros(E, dtype=torch.float64, device=poses_K.device)
+            gp = torch.zeros(P, dtype=torch.float64, device=poses_K.device)
+            stride = 0
+        prob = D.make_problem(poses_K, meas.contiguous(), prior_meas.contiguous(), w_edge.detach().contiguous(),
+                              w_prior.detach().contiguous())
+        D.dnls_backward_implicit(self.graph, B, prob, grad_poses.contiguous(), grad_kind,
+                                 ge if E else None, gp if P else None, stride, ws)
+        if per_element:
+            return ge[:, :E], gp[:, :P]
+        return ge, gp
+
+
+class _PoseGraphFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, solver, poses0, meas, prior_meas, w_edge, w_prior):
+        poses, obj, st, it = solver.forward(poses0, meas, prior_meas, w_edge, w_prior, implicit=True)
+        ctx.solver = solver
+        ctx.gen = solver.generation
+        ctx.save_for_backward(poses, meas, prior_meas, w_edge, w_prior)
+        ctx.mark_non_differentiable(obj, st, it)
+        return poses, obj, st, it
+
+    @staticmethod
+    def backward(ctx, g_poses, g_obj, g_st, g_it):
+        solver = ctx.solver
+        if solver.generation != ctx.gen:
+            raise RuntimeError("pose_graph_layer: the solver ran another forward since this one; its cached "
+                               "factor is gone (DNLS_E_STATE)")
+        poses, meas, prior_meas, w_edge, w_prior = ctx.saved_tensors
+        if g_poses is None:
+            g_poses = torch.zeros_like(poses)
+        ge, gp = solver.backward(poses, meas, prior_meas, w_edge, w_prior, g_poses, D.GRAD_MATRIX,
+                                 per_element=(w_edge.dim() == 2))
+        ge = ge if ctx.needs_input_grad[4] else None
+        gp = gp if ctx.needs_input_grad[5] else None
+        return None, None, None, None, ge, gp
+
+
+def pose_graph_layer(solver: PoseGraphSolver, poses0, meas, prior_meas, w_edge, w_prior):
+    """Differentiable solve (implicit backward).  Returns (poses*, objective, status, iterations)."""
+    if poses0.requires_grad or meas.requires_grad or prior_meas.requires_grad:
+        raise ValueError("implicit backward gives no gradient for theta_init or measurements "
+                         "(PAPER.md Table 6 :726); only w_edge / w_prior may require grad")
+    return _PoseGraphFn.apply(solver, poses0, meas, prior_meas, w_edge, w_prior)
