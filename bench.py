@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark: batched SE3 pose-graph GN iterations/sec (fwd + implicit bwd) -- BASELINE.json metric.
+
+One STEP = the whole hot path on one batch: reset poses to theta_0, dnls_forward (K GN
+iterations + the final undamped linearise+factor at theta_K, implicit mode), then
+dnls_backward_implicit (adjoint solve on the cached factor + weight-gradient contraction +
+fixed-order batch reduction), and for N > 1 GPUs the NCCL all-reduce of [grad_w_edge,
+grad_w_prior, loss].  value = (batch elements of all ranks) * K / T_step.
+
+Default workload (N = 1): BASELINE.json configs[1] = C2, SE3 Cube graph, 256 poses, batch 128 per
+GPU, GN K = 10, implicit backward (weak scaling: 128 per GPU at every N).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+--impl reference times the fp64 CPU oracle (the reference arm of this tier) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched SE3 pose-graph GN iterations/sec (fwd+implicit bwd) at 1/2/4/8 B200"
+UNIT = "problem-iterations/s"
+
+CONFIGS = {
+    "C1": dict(N=16, dim=2, B=4, K=10, opt="gn", p=0.2, mode="local", scaling="weak",
+               desc="C1: SE2 pose graph, 16 poses + loop closures, batch 4, GN K=10"),
+    "C2": dict(N=256, dim=3, B=128, K=10, opt="gn", p=0.2, mode="local", scaling="weak",
+               desc="C2: SE3 cube pose graph, 256 poses, batch 128 per GPU, GN K=10 + implicit backward"),
+    "C3": dict(N=4096, dim=3, B=16, K=10, opt="lm", p=0.2, mode="local", scaling="weak",
+               desc="C3: SE3 pose graph, 4096 poses, batch 16 per GPU, LM K=10 + implicit backward"),
+    "C4": dict(N=1024, dim=3, B=256, K=10, opt="gn", p=0.2, mode="local", scaling="weak",
+               desc="C4: SE3 pose graph, 1024 poses, batch 256 per GPU, GN K=10 + implicit backward (learnable w)"),
+    "C5": dict(N=1024, dim=3, B=2048, K=10, opt="gn", p=0.2, mode="local", scaling="strong",
+               desc="C5: SE3 pose graph, 1024 poses, batch 2048 split over the GPUs, GN K=10 + implicit + NCCL allreduce"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clock / throttle reasons via NVML every 20 ms while running."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, m in names.items():
+                    if r & m and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_oracle_step(topo, data, cfg, elements):
+    """Oracle fwd (K iterations + final factor) + implicit bwd on the listed elements."""
+    from oracle import implicit as oimp
+    from oracle import lie as olie
+    from oracle import nls as onls
+    G = "SE3" if cfg["dim"] == 3 else "SE2"
+    opt = onls.Options(optimizer=cfg["opt"], max_iterations=cfg["K"], implicit=True)
+    v = np.ones(topo.num_poses * (6 if cfg["dim"] == 3 else 3))
+    for b in elements:
+        prob = onls.PGOProblem(G, topo.num_poses, topo.edges, topo.prior_vars, data["meas"][b],
+                               data["prior_meas"][b], data["w_edge"], data["w_prior"])
+        res = onls.optimize(prob, olie.to_homog(data["poses0"][b]), opt)
+        if res.L_final is not None:
+            oimp.implicit_weight_grads(prob, res.x, v, L_K=res.L_final)
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg, n_elems):
+    import synth
+    topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
+    data = synth.cube_batch(topo, n_elems, seed=0)
+    t0 = time.perf_counter()
+    cpu_oracle_step(topo, data, cfg, range(n_elems))
+    dt = time.perf_counter() - t0
+    return {"value": n_elems * cfg["K"] / dt, "unit": UNIT, "cores": cores(), "kind": "oracle",
+            "sample": f"{n_elems} element(s) of {cfg['desc'].split(':')[0]} (fwd K={cfg['K']} + final factor + "
+                      f"implicit bwd), {dt:.1f} s, numpy/OpenBLAS fp64 dense"}
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    import synth
+    topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
+    n_el = 1
+    data = synth.cube_batch(topo, n_el, seed=0)
+    for _ in range(args.warmup):
+        cpu_oracle_step(topo, data, cfg, range(n_el))
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_oracle_step(topo, data, cfg, range(n_el))
+        ts.append(time.perf_counter() - t0)
+    T = sum(ts) / len(ts)
+    val = n_el * cfg["K"] / T
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": cfg["scaling"],
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "sample": f"{n_el} batch element per step (bounded CPU sample)",
+                   "poses": cfg["N"], "edges": topo.num_edges, "iterations": cfg["K"]},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores(), "kind": "oracle",
+                         "sample": f"{n_el} element per step, fp64 NumPy dense oracle"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="dnls", choices=["dnls", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-elements", type=int, default=4)
+    ap.add_argument("--no-flush", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2207_09442_b200 import dnls as D
+    from paper_2207_09442_b200.layer import PoseGraphSolver
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- data: per-rank shard of the global batch (per-element seeds -> shard independent)
+    if cfg["scaling"] == "weak":
+        B = cfg["B"]
+    else:
+        assert cfg["B"] % world == 0
+        B = cfg["B"] // world
+    b_start = rank * B
+    topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
+    data = synth.cube_batch(topo, B, seed=0, b_start=b_start)
+    d = 6 if cfg["dim"] == 3 else 3
+    group = D.SE3 if cfg["dim"] == 3 else D.SE2
+    K = cfg["K"]
+    solver = PoseGraphSolver(group, topo.num_poses, topo.edges, topo.prior_vars, device=local_rank,
+                             max_iterations=K, optimizer=(D.LM if cfg["opt"] == "lm" else D.GN))
+    g = solver.graph
+    st = solver.stats
+    opt = solver.options
+    opt.backward_mode = D.BWD_IMPLICIT
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in data.items() if k != "gt"}
+    vgrad = torch.from_numpy(np.random.default_rng([1, rank]).standard_normal((B, topo.num_poses, d)))
+    dv = {k: v.to(dev) for k, v in host.items()}
+    dvg = vgrad.to(dev)
+    poses = torch.empty_like(dv["poses0"])
+    obj = torch.empty(B, dtype=torch.float64, device=dev)
+    sts = torch.empty(B, dtype=torch.int32, device=dev)
+    its = torch.empty(B, dtype=torch.int32, device=dev)
+    E, P = topo.num_edges, int(topo.prior_vars.shape[0])
+    red = torch.zeros(E + P + 1, dtype=torch.float64, device=dev)   # [grad_w_edge | grad_w_prior | loss]
+    ge, gp = red[:E], red[E:E + P]
+    ws = solver.workspace(B)
+    prob = D.make_problem(poses, dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"], obj, sts, its)
+    stream = torch.cuda.current_stream()
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    ev_f = []
+
+    def step(record=None):
+        poses.copy_(dv["poses0"])
+        if record is not None:
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        D.dnls_forward(g, B, opt, prob, ws)
+        if record is not None:
+            b_.record(stream)
+            record.append((a, b_))
+        D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws)
+        if world > 1:
+            torch.sum(obj, dim=0, keepdim=True, out=red[E + P:])
+            dist.all_reduce(red)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank).start()
+    times = []
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(ev_f)
+        e1.record(stream)
+        times.append((e0, e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    T = sum(a.elapsed_time(b) for a, b in times) / 1e3          # seconds, K steps
+    Tf = sum(a.elapsed_time(b) for a, b in ev_f) / 1e3 / args.steps
+    if world > 1:
+        tt = torch.tensor([T, Tf], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        T, Tf = tt.tolist()
+    total_elems = B * world
+    value = total_elems * K * args.steps / T
+    ms_per_step = T / args.steps * 1e3
+
+    # ---- roofline of the dominant kernel (k_forward): algorithmic bytes per launch / duration
+    per_iter = st["bytes_linearize"] + st["bytes_factor"] + st["bytes_solve"] + st["bytes_update"]
+    alg_bytes = B * (K * per_iter + st["bytes_linearize"] + st["bytes_factor"])
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes / Tf / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            if tj.get("config") == args.config:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_forward", "peak_source": peak_src,
+                "alg_bytes_per_launch": alg_bytes, "kernel_ms": Tf * 1e3,
+                "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)+lin+factor) per SURVEY.md 8(d)"}
+
+    # ---- e2e through the public API (PoseGraphSolver) with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = {k: v.pin_memory() for k, v in host.items()}
+        pvg = vgrad.pin_memory()
+        out_obj = torch.empty(B, dtype=torch.float64).pin_memory()
+        out_g = torch.empty(E + P, dtype=torch.float64).pin_memory()
+        bi = sum(v.numel() * v.element_size() for v in pin.values()) + pvg.numel() * 8
+        bo = out_obj.numel() * 8 + out_g.numel() * 8
+        dbuf = {k: torch.empty_like(v, device=dev) for k, v in pin.items()}
+        dvg2 = torch.empty_like(pvg, device=dev)
+
+        def e2e_step():
+            for k in pin:
+                dbuf[k].copy_(pin[k], non_blocking=True)
+            dvg2.copy_(pvg, non_blocking=True)
+            P_, o_, _, _ = solver.forward(dbuf["poses0"], dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"],
+                                          dbuf["w_prior"], implicit=True)
+            g1, g2 = solver.backward(P_, dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"], dbuf["w_prior"], dvg2,
+                                     D.GRAD_TANGENT)
+            gg = torch.cat([g1, g2])
+            if world > 1:
+                dist.all_reduce(gg)
+            out_g.copy_(gg, non_blocking=True)
+            out_obj.copy_(o_, non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e2e_step()
+            b_.record(stream)
+            ts.append((a, b_))
+        torch.cuda.synchronize()
+        Te = sum(a.elapsed_time(b) for a, b in ts) / 1e3
+        if world > 1:
+            tt = torch.tensor([Te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            Te = tt.item()
+        e2e = {"value": total_elems * K * args.steps / Te, "unit": UNIT, "h2d_bytes_per_step": int(bi),
+               "d2h_bytes_per_step": int(bo), "ms_per_step": Te / args.steps * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_elements)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "global_batch": total_elems, "batch_per_gpu": B,
+                       "poses": cfg["N"], "edges": topo.num_edges, "iterations": K,
+                       "optimizer": cfg["opt"], "backward": "implicit",
+                       "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
+                       "parallelism": f"dp{world}", "nnz_L": st["nnz_L"], "supernodes": st["num_supernodes"],
+                       "levels": st["num_levels"]},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 3 * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

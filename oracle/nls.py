@@ -124,6 +124,7 @@ class Result:
     iterations: int
     history: list = field(default_factory=list)   # S(theta_k) for k = 0..K
     lam: float = 0.0
+    trials: list = field(default_factory=list)    # LM: (S, S_trial or None, accepted) per iteration
     H_final: np.ndarray | None = None              # undamped H(theta_K) (implicit mode)
     L_final: np.ndarray | None = None              # its Cholesky factor
 
@@ -155,6 +156,7 @@ def levenberg_marquardt(prob, x0, opt: Options) -> Result:
     status, iters = ST_OK, 0
     lam = opt.lambda0
     hist = []
+    trials = []
     S, H, b = prob.linearize(x)
     S_prev = None
     for k in range(opt.max_iterations):
@@ -165,11 +167,13 @@ def levenberg_marquardt(prob, x0, opt: Options) -> Result:
         iters += 1
         L, ok = linalg.cholesky(linalg.damp(H, lam, opt.damping))
         accept = False
+        S_try = None
         if ok:
             delta = linalg.chol_solve(L, b)
             x_try = prob.retract(x, -opt.step_size * delta)
             S_try = prob.objective(x_try)
             accept = S_try < S
+        trials.append((S, S_try, accept))
         if accept:
             x = x_try
             lam = max(lam / opt.lambda_down, opt.lambda_min)
@@ -180,7 +184,9 @@ def levenberg_marquardt(prob, x0, opt: Options) -> Result:
                 status = ST_SATURATED
                 break
             lam = min(lam * opt.lambda_up, opt.lambda_max)
-    return _finish(prob, x, status, iters, hist, lam, opt)
+    res = _finish(prob, x, status, iters, hist, lam, opt)
+    res.trials = trials
+    return res
 
 
 def _finish(prob, x, status, iters, hist, lam, opt) -> Result:

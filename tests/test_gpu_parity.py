@@ -144,16 +144,31 @@ def test_forward_gn_matches_oracle(N, dim, B, K, p, mode):
         assert st[b].item() == r.status and it[b].item() == r.iterations
 
 
-def test_forward_lm_matches_oracle():
-    topo, data = make_case(32, dim=3, p=0.4, seed=3, B=4, init_sigma_t=0.6, init_sigma_r=0.4)
-    opts = dict(optimizer=D.LM, max_iterations=10, lambda0=1e-4)
+def lm_has_tie(r, rel=1e-10):
+    # DESIGN.md reading A13: an accept/reject decision whose trial objective equals the current one
+    # to rounding can flip between two correct implementations; those runs are compared on the
+    # converged iterate (objective 1e-9, poses 1e-7) instead of iterate-wise.
+    return any(st is not None and abs(st - s) <= rel * s for s, st, _ in r.trials)
+
+
+@pytest.mark.parametrize("K,seed", [(6, 3), (10, 3), (8, 4)])
+def test_forward_lm_matches_oracle(K, seed):
+    topo, data = make_case(32, dim=3, p=0.4, seed=seed, B=4, init_sigma_t=0.6, init_sigma_r=0.4)
+    opts = dict(optimizer=D.LM, max_iterations=K, lambda0=1e-4)
     _, _, poses, obj, st, it = run_forward(topo, data, **opts)
-    res = oracle_results(topo, data, optimizer="lm", max_iterations=10, lambda0=1e-4)
+    res = oracle_results(topo, data, optimizer="lm", max_iterations=K, lambda0=1e-4)
     P = poses.cpu().numpy()
+    n_strict = 0
     for b, r in enumerate(res):
-        assert pose_err(P[b], r.x) <= TOL_POSE
         assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
-        assert st[b].item() == r.status and it[b].item() == r.iterations
+        if lm_has_tie(r):
+            assert pose_err(P[b], r.x) <= 1e-7
+        else:
+            n_strict += 1
+            assert pose_err(P[b], r.x) <= TOL_POSE
+            assert st[b].item() == r.status and it[b].item() == r.iterations
+    if K <= 6:
+        assert n_strict == len(res)      # far from convergence no ties occur: strict iterate parity
 
 
 def test_forward_step_size_and_early_stop():
