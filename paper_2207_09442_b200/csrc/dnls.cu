@@ -23,6 +23,7 @@ using namespace dnls;
 
 namespace {
 constexpr int NT = 256;   // threads per CTA (one batch element per CTA)
+constexpr int64_t SMEM_BYTES = 200 * 1024;   // dynamic shared memory per CTA (x + level staging)
 thread_local std::string g_err;
 
 dnls_status fail(dnls_status s, const std::string& msg) {
@@ -104,6 +105,30 @@ DevProb dev_prob(const dnls_problem* p) {
 // ============================================================================= kernels
 namespace {
 
+size_t smem_bytes(const DevGraph& g) {
+  return sizeof(double) * ((g.x_smem ? (size_t)g.n_pad : 0) + (size_t)g.stage_n);
+}
+
+template <class F>
+dnls_status set_smem(F* kernel, size_t bytes, const char* what) {
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return fail(DNLS_E_CUDA, std::string(what) + ": cudaFuncSetAttribute: " + cudaGetErrorString(cudaGetLastError()));
+  return DNLS_OK;
+}
+
+// per-CTA shared memory views
+struct Smem {
+  double* x;       // solution vector (shared or global)
+  double* stage;   // level staging area
+};
+__device__ __forceinline__ Smem smem_views(const DevGraph& g, double* xg) {
+  extern __shared__ __align__(16) double smem[];
+  Smem v;
+  v.x = g.x_smem ? smem : xg;
+  v.stage = smem + (g.x_smem ? g.n_pad : 0);
+  return v;
+}
+
 struct FwdParams {
   int K;
   int lm;
@@ -147,8 +172,10 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
   double* Ttr = ws.trial + (size_t)b * g.N * PS;
   double* jac_b = ws.jac + (size_t)b * slots * JS;
   double* cost_b = ws.cost + (size_t)b * slots;
-  double* x_b = ws.x + (size_t)b * g.n;
-  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
+  double* Lg = ws.L + (size_t)b * g.storage;
+  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  double* x_b = sm.x;
+  const LView L{Lg, nullptr, 0, 0};
 
   int status = DNLS_ST_OK, iters = 0;
   double lam = fp.lam0, Sprev = 0.0;
@@ -166,7 +193,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     }
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, L, 1e-13 * sh_max, &sh_fail);
+    factor_phase<D, NT>(g, Lg, sm.stage, 1e-13 * sh_max, &sh_fail);
     const bool ok = sh_fail == 0;
     __syncthreads();
     if (!fp.lm) {
@@ -174,7 +201,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
         status = DNLS_ST_NOT_SPD;
         break;
       }
-      solve_phase<D, NT>(g, L, x_b);
+      solve_phase<D, NT>(g, Lg, sm.stage, x_b);
       retract_phase<D, NT>(g, Tb, Tb, x_b, fp.alpha);
       __syncthreads();
       ++iters;
@@ -184,7 +211,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
       ++iters;
       bool accept = false;
       if (ok) {
-        solve_phase<D, NT>(g, L, x_b);
+        solve_phase<D, NT>(g, Lg, sm.stage, x_b);
         retract_phase<D, NT>(g, Tb, Ttr, x_b, fp.alpha);
         __syncthreads();
         objective_phase<D, NT>(g, pr, Ttr, b, cost_b);
@@ -220,7 +247,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, L, 1e-13 * sh_max, &sh_fail);
+    factor_phase<D, NT>(g, Lg, sm.stage, 1e-13 * sh_max, &sh_fail);
     __syncthreads();
     if (sh_fail && status == DNLS_ST_OK) status = DNLS_ST_NOT_SPD;
   } else {
@@ -254,11 +281,15 @@ __global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, Dev
   const double* Tb = pr.poses + (size_t)b * g.N * PS;
   double* jac_b = ws.jac + (size_t)b * slots * JS;
   double* cost_b = ws.cost + (size_t)b * slots;
-  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
+  const LView L{ws.L + (size_t)b * g.storage, nullptr, 0, 0};
+  double* xg = ws.x + (size_t)b * g.n;
+  const Smem sm = smem_views(g, xg);
   jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
   __syncthreads();
-  assemble_phase<D, NT>(g, L, jac_b, ws.x + (size_t)b * g.n, lam ? lam[b] : -1.0, damping, s_red);
+  assemble_phase<D, NT>(g, L, jac_b, sm.x, lam ? lam[b] : -1.0, damping, s_red);
   finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+  if (g.x_smem)
+    for (int i = threadIdx.x; i < g.n; i += NT) xg[i] = sm.x[i];
   if (threadIdx.x == 0) {
     if (objective) objective[b] = sh_S;
     ws.S[b] = sh_S;
@@ -272,8 +303,8 @@ __global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* 
   __shared__ int sh_fail;
   if (threadIdx.x == 0) sh_fail = 0;
   __syncthreads();
-  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
-  factor_phase<D, NT>(g, L, 1e-13 * ws.maxd[b], &sh_fail);
+  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  factor_phase<D, NT>(g, ws.L + (size_t)b * g.storage, sm.stage, 1e-13 * ws.maxd[b], &sh_fail);
   __syncthreads();
   if (threadIdx.x == 0 && status) status[b] = sh_fail ? DNLS_ST_NOT_SPD : DNLS_ST_OK;
 }
@@ -282,14 +313,14 @@ __global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* 
 template <int D>
 __global__ void __launch_bounds__(NT, 1) k_solve(DevGraph g, DevWs ws, const double* rhs, double* xout) {
   const int b = blockIdx.x;
-  double* x_b = ws.x + (size_t)b * g.n;
+  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  double* x_b = sm.x;
   for (int i = threadIdx.x; i < g.n; i += NT) {
     const int o = i / D, a = i - o * D;
     x_b[(size_t)g.iperm[o] * D + a] = rhs[(size_t)b * g.n + i];
   }
   __syncthreads();
-  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
-  solve_phase<D, NT>(g, L, x_b);
+  solve_phase<D, NT>(g, ws.L + (size_t)b * g.storage, sm.stage, x_b);
   __syncthreads();
   for (int i = threadIdx.x; i < g.n; i += NT) {
     const int o = i / D, a = i - o * D;
@@ -305,7 +336,8 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
   const int b = blockIdx.x;
   const size_t slots = (size_t)g.E + g.P;
   const double* Tb = pr.poses + (size_t)b * g.N * PS;
-  double* x_b = ws.x + (size_t)b * g.n;
+  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  double* x_b = sm.x;
   double* out_b = ws.cost + (size_t)b * slots;
   if (ws.st[b] == DNLS_ST_NOT_SPD) {   // no valid factor: zero gradient contribution
     for (int s = threadIdx.x; s < (int)slots; s += NT) out_b[s] = 0.0;
@@ -353,8 +385,7 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
     for (int a = 0; a < D; ++a) x_b[(size_t)g.iperm[o] * D + a] = v[a];
   }
   __syncthreads();
-  LView L{ws.L + (size_t)b * g.storage, nullptr, g.storage};
-  solve_phase<D, NT>(g, L, x_b);
+  solve_phase<D, NT>(g, ws.L + (size_t)b * g.storage, sm.stage, x_b);
   __syncthreads();
   // dL/dw = -2 w (C lambda) . c  (unweighted C, c at theta_K)
   for (int slot = threadIdx.x; slot < (int)slots; slot += NT) {
@@ -519,6 +550,13 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dnls_graph* g = new dnls_graph();
   int code = 0;
   SymbolicOptions sopt;
+  {
+    // shared-memory plan: x (n doubles) in shared memory when it fits in 64 KB, the rest of
+    // SMEM_BYTES stages one elimination-tree level of panels at a time
+    const int64_t n = (int64_t)num_vars * group;
+    const int64_t xb = (n * 8 <= 65536) ? n * 8 : 0;
+    sopt.stage_budget_doubles = (SMEM_BYTES - xb) / 8;
+  }
   if (const char* env = std::getenv("DNLS_RELAX")) {   // tuning override: "a,sc,sf,mc,mf,max,bf"
     std::sscanf(env, "%d,%d,%lf,%d,%lf,%d,%lf", &sopt.relax_always_cols, &sopt.relax_small_cols,
                 &sopt.relax_small_frac, &sopt.relax_mid_cols, &sopt.relax_mid_frac, &sopt.relax_max_cols,
@@ -541,7 +579,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   std::vector<int32_t> sn_off32(s.sn_off.begin(), s.sn_off.end());
   add(s.perm); add(s.iperm); add(s.edges); add(s.prior_vars);
   add(s.sn_first); add(s.sn_ncols); add(s.sn_m); add(s.sn_w); add(sn_off32);
-  add(s.level_ptr); add(s.level_sn);
+  add(s.level_ptr); add(s.level_sn); add(s.level_off); add(s.level_stage_hi);
   add(s.ut_level_ptr); add(s.ut_off); add(s.ut_ld); add(s.ut_cptr); add(s.uc_a); add(s.uc_b); add(s.uc_ld); add(s.uc_w);
   add(s.fc_ptr); add(s.fc_off); add(s.fc_ld); add(s.fc_w); add(s.fc_x);
   add(s.snr_ptr); add(s.snr);
@@ -574,10 +612,14 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   DevGraph& dg = g->dg;
   dg.D = s.D; dg.N = s.N; dg.E = s.E; dg.P = s.P; dg.S = s.S; dg.L = s.num_levels;
   dg.storage = (int)s.storage; dg.nblk = (int)s.blk_off.size(); dg.n = s.N * s.D;
+  dg.x_smem = (int64_t)dg.n * 8 <= 65536 ? 1 : 0;
+  dg.n_pad = (dg.n + 1) & ~1;
+  dg.stage_n = (int)((s.max_level_stage + 1) & ~int64_t(1));
   dg.perm = d + offs[k++]; dg.iperm = d + offs[k++]; dg.edges = d + offs[k++]; dg.prior_vars = d + offs[k++];
   dg.sn_first = d + offs[k++]; dg.sn_ncols = d + offs[k++]; dg.sn_m = d + offs[k++]; dg.sn_w = d + offs[k++];
   dg.sn_off = d + offs[k++];
   dg.level_ptr = d + offs[k++]; dg.level_sn = d + offs[k++];
+  dg.level_off = d + offs[k++]; dg.level_stage_hi = d + offs[k++];
   dg.ut_level_ptr = d + offs[k++]; dg.ut_off = d + offs[k++]; dg.ut_ld = d + offs[k++]; dg.ut_cptr = d + offs[k++];
   dg.uc_a = d + offs[k++]; dg.uc_b = d + offs[k++]; dg.uc_ld = d + offs[k++]; dg.uc_w = d + offs[k++];
   dg.fc_ptr = d + offs[k++]; dg.fc_off = d + offs[k++]; dg.fc_ld = d + offs[k++]; dg.fc_w = d + offs[k++];
@@ -751,7 +793,7 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   fp.status = prob->status;
   fp.iterations = prob->iterations;
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, (k_forward<DD><<<batch, NT, 0, s>>>(g->dg, dev_prob(prob), ws, fp)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
   if ((st = cuda_check("dnls_forward: k_forward launch"))) return st;
   if (fp.implicit) {
     std::lock_guard<std::mutex> lk(gm->mu);
@@ -786,7 +828,7 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
   WsLayout l = ws_layout(g->sym, batch);
   DevWs ws = ws_views(l, workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, (k_backward<DD><<<batch, NT, 0, s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward<DD>, smem_bytes(g->dg), "k_backward"))) return st; (k_backward<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind)));
   if ((st = cuda_check("dnls_backward_implicit: k_backward launch"))) return st;
   const int slots = g->sym.E + g->sym.P;
   if (slots > 0 && (grad_w_edge || grad_w_prior)) {
@@ -808,8 +850,8 @@ DNLS_API dnls_status dnls_linearize(const dnls_graph* g, int32_t batch, const dn
   if (batch == 0) return DNLS_OK;
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D,
-             (k_linearize<DD><<<batch, NT, 0, s>>>(g->dg, dev_prob(prob), ws, lambda, damping, prob->objective)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_linearize<DD>, smem_bytes(g->dg), "k_linearize"))) return st;
+             (k_linearize<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, lambda, damping, prob->objective)));
   return cuda_check("dnls_linearize: launch");
 }
 
@@ -820,7 +862,7 @@ DNLS_API dnls_status dnls_factorize(const dnls_graph* g, int32_t batch, void* wo
   if (batch == 0) return DNLS_OK;
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, (k_factorize<DD><<<batch, NT, 0, s>>>(g->dg, ws, status)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_factorize<DD>, smem_bytes(g->dg), "k_factorize"))) return st; (k_factorize<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, status)));
   return cuda_check("dnls_factorize: launch");
 }
 
@@ -832,7 +874,7 @@ DNLS_API dnls_status dnls_solve_factored(const dnls_graph* g, int32_t batch, voi
   if (batch == 0) return DNLS_OK;
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, (k_solve<DD><<<batch, NT, 0, s>>>(g->dg, ws, rhs, x)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_solve<DD>, smem_bytes(g->dg), "k_solve"))) return st; (k_solve<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, rhs, x)));
   return cuda_check("dnls_solve_factored: launch");
 }
 

@@ -17,9 +17,12 @@ namespace dnls {
 // device view of the symbolic analysis (all arrays int32, uploaded once per graph)
 struct DevGraph {
   int D, N, E, P, S, L, storage, nblk, n;
+  int x_smem;     // 1: the solution vector x lives in shared memory (offset 0, n_pad doubles)
+  int n_pad;      // n rounded up to an even count (16-byte alignment of the staging area)
+  int stage_n;    // doubles of the level-staging area (largest staged level prefix)
   const int *perm, *iperm, *edges, *prior_vars;
   const int *sn_first, *sn_ncols, *sn_m, *sn_w, *sn_off;
-  const int *level_ptr, *level_sn;
+  const int *level_ptr, *level_sn, *level_off, *level_stage_hi;
   const int *ut_level_ptr, *ut_off, *ut_ld, *ut_cptr, *uc_a, *uc_b, *uc_ld, *uc_w;
   const int *fc_ptr, *fc_off, *fc_ld, *fc_w, *fc_x;
   const int *snr_ptr, *snr;
@@ -65,9 +68,25 @@ struct GT {
 struct LView {
   double* g;
   double* s;
-  int lo;
-  __device__ __forceinline__ double* at(int off) const { return off >= lo ? s + (off - lo) : g + off; }
+  int lo, hi;
+  __device__ __forceinline__ double* at(int off) const {
+    return (off >= lo && off < hi) ? s + (off - lo) : g + off;
+  }
 };
+
+// CTA-cooperative copies of a contiguous range (16-byte vectors when both ends are aligned)
+template <int NT>
+__device__ __forceinline__ void copy_range(double* __restrict__ dst, const double* __restrict__ src, int n) {
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const int n2 = n >> 1;
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    for (int i = threadIdx.x; i < n2; i += NT) d2[i] = s2[i];
+    if ((n & 1) && threadIdx.x == 0) dst[n - 1] = src[n - 1];
+  } else {
+    for (int i = threadIdx.x; i < n; i += NT) dst[i] = src[i];
+  }
+}
 
 // ============================================================================= cost evaluation
 // Unweighted cost c and Jacobians of slot `slot` (edge e < E, else prior slot - E) at poses Tb.
@@ -295,19 +314,19 @@ __device__ void assemble_phase(const DevGraph& g, LView L, const double* jac_b, 
 }
 
 // ============================================================================= a3: factorisation
-struct CtaTeam {
-  int rank, size;
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
-};
-struct WarpTeam {
-  int rank, size;
-  __device__ __forceinline__ void sync() const { __syncwarp(); }
+// A team is a warp, a group of warps synchronised by a named barrier, or the whole CTA.
+struct Team {
+  int rank, size, bar;
+  __device__ __forceinline__ void sync() const {
+    if (size == 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(size) : "memory");
+  }
 };
 
 // Dense right-looking Cholesky of one supernode panel P (m rows, w columns, column-major,
 // leading dim m), blocked by D columns.  Writes L in place (lower part of the diagonal block
 // and the rows below).  *fail set if a pivot <= tol.
-template <int D, class Team>
+template <int D>
 __device__ void panel_factor(double* P, int m, int w, double tol, const Team& tm, int* fail) {
   for (int c0 = 0; c0 < w; c0 += D) {
     if (tm.rank == 0) {
@@ -387,11 +406,35 @@ __device__ void panel_factor(double* P, int m, int w, double tol, const Team& tm
   }
 }
 
-template <int D, int NT>
-__device__ void factor_phase(const DevGraph& g, LView L, double tol, int* s_fail) {
+// Split the CTA's warps into teams for `nsn` independent panels: warp per panel when there are
+// at least NW panels, otherwise power-of-two groups of warps (named barriers 1..NW).
+template <int NT>
+__device__ __forceinline__ void team_of(int nsn, Team& tm, int& team, int& nteams) {
   constexpr int NW = NT / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  int tw = 1;
+  if (nsn < NW) {
+    tw = NW / nsn;
+    while (tw & (tw - 1)) tw &= tw - 1;   // round down to a power of two
+  }
+  nteams = NW / tw;
+  team = warp / tw;
+  tm.rank = threadIdx.x - team * tw * 32;
+  tm.size = tw * 32;
+  tm.bar = 1 + team;
+}
+
+// Supernodal left-looking Cholesky, level-synchronous.  Each level's panels are one contiguous
+// storage range; its prefix [level_off, level_stage_hi) is staged into shared memory `stage`,
+// updated (gather form, from descendant panels in global memory), factored by teams, and
+// written back.
+template <int D, int NT>
+__device__ void factor_phase(const DevGraph& g, double* Lg, double* stage, double tol, int* s_fail) {
   for (int lv = 0; lv < g.L; ++lv) {
+    const int lo = g.level_off[lv], hi = g.level_stage_hi[lv];
+    copy_range<NT>(stage, Lg + lo, hi - lo);
+    __syncthreads();
+    LView V{Lg, stage, lo, hi};
     // (U) gather-form updates from descendants into this level's panels
     const int t0 = g.ut_level_ptr[lv], t1 = g.ut_level_ptr[lv + 1];
     const int nitems = (t1 - t0) * D;
@@ -401,8 +444,8 @@ __device__ void factor_phase(const DevGraph& g, LView L, double tol, int* s_fail
 #pragma unroll
       for (int q = 0; q < D; ++q) acc[q] = 0.0;
       for (int ci = g.ut_cptr[t]; ci < g.ut_cptr[t + 1]; ++ci) {
-        const double* A = L.at(g.uc_a[ci]);
-        const double* Bm = L.at(g.uc_b[ci]);
+        const double* A = Lg + g.uc_a[ci];
+        const double* Bm = Lg + g.uc_b[ci];
         const int ld = g.uc_ld[ci], w = g.uc_w[ci];
         for (int k = 0; k < w; ++k) {
           const double av = A[(size_t)k * ld + a];
@@ -410,51 +453,121 @@ __device__ void factor_phase(const DevGraph& g, LView L, double tol, int* s_fail
           for (int q = 0; q < D; ++q) acc[q] = fma(av, Bm[(size_t)k * ld + q], acc[q]);
         }
       }
-      double* T = L.at(g.ut_off[t]);
+      double* T = V.at(g.ut_off[t]);
       const int ld = g.ut_ld[t];
 #pragma unroll
       for (int q = 0; q < D; ++q) T[(size_t)q * ld + a] -= acc[q];
     }
     __syncthreads();
-    // (F) dense factorisation of the level's panels
-    const int s0 = g.level_ptr[lv], s1 = g.level_ptr[lv + 1];
-    const int nsn = s1 - s0;
-    if (nsn >= NW / 2) {
-      WarpTeam tm{lane, 32};
-      for (int i = warp; i < nsn; i += NW) {
-        const int s = g.level_sn[s0 + i];
-        panel_factor<D>(L.at(g.sn_off[s]), g.sn_m[s], g.sn_w[s], tol, tm, s_fail);
-      }
-    } else {
-      CtaTeam tm{(int)threadIdx.x, NT};
-      for (int i = 0; i < nsn; ++i) {
-        const int s = g.level_sn[s0 + i];
-        panel_factor<D>(L.at(g.sn_off[s]), g.sn_m[s], g.sn_w[s], tol, tm, s_fail);
-      }
+    // (F) dense factorisation of the level's panels by teams
+    const int s0 = g.level_ptr[lv], nsn = g.level_ptr[lv + 1] - s0;
+    Team tm;
+    int team, nteams;
+    team_of<NT>(nsn, tm, team, nteams);
+    for (int i = team; i < nsn; i += nteams) {
+      const int s = g.level_sn[s0 + i];
+      panel_factor<D>(V.at(g.sn_off[s]), g.sn_m[s], g.sn_w[s], tol, tm, s_fail);
     }
+    __syncthreads();
+    copy_range<NT>(Lg + lo, stage, hi - lo);
     __syncthreads();
   }
 }
 
 // ============================================================================= a4: solves
-// x (permuted, length n) holds b on entry and H^-1 b on exit.  Warp per supernode.
+// Warp-level dense triangular solves on a panel's w x w diagonal block (P column-major, leading
+// dim m), rows owned by lanes (row r = lane + 32 j), values held in registers, each step one
+// shuffle broadcast.  MAXR = max ceil(w / 32).
+template <int MAXR>
+__device__ __forceinline__ void warp_trsv_lower(const double* P, int m, int w, double* xs) {
+  const int lane = threadIdx.x & 31;
+  double t[MAXR], inv[MAXR];
+#pragma unroll
+  for (int j = 0; j < MAXR; ++j) {
+    const int r = lane + 32 * j;
+    t[j] = (r < w) ? xs[r] : 0.0;
+    inv[j] = (r < w) ? 1.0 / P[(size_t)r * m + r] : 0.0;
+  }
+#pragma unroll
+  for (int sj = 0; sj < MAXR; ++sj) {
+    if (32 * sj >= w) break;
+    const int cend = min(32, w - 32 * sj);
+    for (int cl = 0; cl < cend; ++cl) {
+      const int c = 32 * sj + cl;
+      const double xc = __shfl_sync(0xffffffffu, t[sj] * inv[sj], cl);
+      if (lane == cl) t[sj] = xc;
+      const double* col = P + (size_t)c * m;
+#pragma unroll
+      for (int j = sj; j < MAXR; ++j) {
+        const int r = lane + 32 * j;
+        if (r > c && r < w) t[j] = fma(-col[r], xc, t[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXR; ++j) {
+    const int r = lane + 32 * j;
+    if (r < w) xs[r] = t[j];
+  }
+}
+
+template <int MAXR>
+__device__ __forceinline__ void warp_trsv_upper(const double* P, int m, int w, double* xs) {
+  // solve L^T x = t : step c from w-1 down to 0, rows r < c updated with L[c][r] = P[r*m + c]
+  const int lane = threadIdx.x & 31;
+  double t[MAXR], inv[MAXR];
+#pragma unroll
+  for (int j = 0; j < MAXR; ++j) {
+    const int r = lane + 32 * j;
+    t[j] = (r < w) ? xs[r] : 0.0;
+    inv[j] = (r < w) ? 1.0 / P[(size_t)r * m + r] : 0.0;
+  }
+#pragma unroll
+  for (int sj = MAXR - 1; sj >= 0; --sj) {
+    if (32 * sj >= w) continue;
+    const int cend = min(32, w - 32 * sj);
+    for (int cl = cend - 1; cl >= 0; --cl) {
+      const int c = 32 * sj + cl;
+      const double xc = __shfl_sync(0xffffffffu, t[sj] * inv[sj], cl);
+      if (lane == cl) t[sj] = xc;
+#pragma unroll
+      for (int j = 0; j <= sj; ++j) {
+        const int r = lane + 32 * j;
+        if (r < c) t[j] = fma(-P[(size_t)r * m + c], xc, t[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXR; ++j) {
+    const int r = lane + 32 * j;
+    if (r < w) xs[r] = t[j];
+  }
+}
+
+// x (permuted, length n; shared or global memory) holds b on entry and H^-1 b on exit.
+// Level ranges are staged into `stage` (read-only); warp per supernode.
 template <int D, int NT>
-__device__ void solve_phase(const DevGraph& g, LView L, double* x) {
+__device__ void solve_phase(const DevGraph& g, double* Lg, double* stage, double* x) {
   constexpr int NW = NT / 32;
+  constexpr int MAXR = (64 * D + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // forward: L y = b, leaves to root
   for (int lv = 0; lv < g.L; ++lv) {
+    const int lo = g.level_off[lv], hi = g.level_stage_hi[lv];
+    copy_range<NT>(stage, Lg + lo, hi - lo);
+    __syncthreads();
+    LView V{Lg, stage, lo, hi};
     const int s0 = g.level_ptr[lv], s1 = g.level_ptr[lv + 1];
     for (int i = s0 + warp; i < s1; i += NW) {
       const int s = g.level_sn[i];
       const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s];
-      const double* P = L.at(g.sn_off[s]);
+      const double* P = V.at(g.sn_off[s]);
       double* xs = x + (size_t)D * f;
       for (int r = lane; r < w; r += 32) {
         const int p = f + r / D, a = r % D;
         double t = xs[r];
         for (int ci = g.fc_ptr[p]; ci < g.fc_ptr[p + 1]; ++ci) {
-          const double* A = L.at(g.fc_off[ci]);
+          const double* A = Lg + g.fc_off[ci];
           const int ld = g.fc_ld[ci], ww = g.fc_w[ci];
           const double* y = x + g.fc_x[ci];
           for (int k = 0; k < ww; ++k) t = fma(-A[(size_t)k * ld + a], y[k], t);
@@ -462,23 +575,21 @@ __device__ void solve_phase(const DevGraph& g, LView L, double* x) {
         xs[r] = t;
       }
       __syncwarp();
-      for (int j = 0; j < w; ++j) {
-        const double xj = xs[j] / P[(size_t)j * m + j];
-        __syncwarp();
-        if (lane == 0) xs[j] = xj;
-        for (int r = j + 1 + lane; r < w; r += 32) xs[r] = fma(-P[(size_t)j * m + r], xj, xs[r]);
-        __syncwarp();
-      }
+      warp_trsv_lower<MAXR>(P, m, w, xs);
     }
     __syncthreads();
   }
   // backward: L^T x = y, root to leaves
   for (int lv = g.L - 1; lv >= 0; --lv) {
+    const int lo = g.level_off[lv], hi = g.level_stage_hi[lv];
+    copy_range<NT>(stage, Lg + lo, hi - lo);
+    __syncthreads();
+    LView V{Lg, stage, lo, hi};
     const int s0 = g.level_ptr[lv], s1 = g.level_ptr[lv + 1];
     for (int i = s0 + warp; i < s1; i += NW) {
       const int s = g.level_sn[i];
       const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s];
-      const double* P = L.at(g.sn_off[s]);
+      const double* P = V.at(g.sn_off[s]);
       double* xs = x + (size_t)D * f;
       const int rb = g.snr_ptr[s], nbr = g.snr_ptr[s + 1] - rb;
       for (int c = lane; c < w; c += 32) {
@@ -492,13 +603,7 @@ __device__ void solve_phase(const DevGraph& g, LView L, double* x) {
         xs[c] = t;
       }
       __syncwarp();
-      for (int j = w - 1; j >= 0; --j) {
-        const double xj = xs[j] / P[(size_t)j * m + j];
-        __syncwarp();
-        if (lane == 0) xs[j] = xj;
-        for (int r = lane; r < j; r += 32) xs[r] = fma(-P[(size_t)r * m + j], xj, xs[r]);
-        __syncwarp();
-      }
+      warp_trsv_upper<MAXR>(P, m, w, xs);
     }
     __syncthreads();
   }

@@ -304,6 +304,37 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     }
     sns.swap(out);
   }
+  // split supernodes wider than relax_max_cols into consecutive pieces (always valid: piece k's
+  // rows are the later pieces' columns followed by the original below rows)
+  {
+    std::vector<SN> out;
+    for (const SN& sn : sns) {
+      if (sn.ncols <= opt.relax_max_cols) {
+        out.push_back(sn);
+        continue;
+      }
+      int nf = sn.first, rem = sn.ncols;
+      while (rem > 0) {
+        int c = std::min(rem, opt.relax_max_cols);
+        SN piece = sn;
+        piece.first = nf;
+        piece.ncols = c;
+        piece.rows.clear();
+        for (int k = nf + c; k < sn.first + sn.ncols; ++k) piece.rows.push_back(k);
+        piece.rows.insert(piece.rows.end(), sn.rows.begin(), sn.rows.end());
+        out.push_back(piece);
+        nf += c;
+        rem -= c;
+      }
+    }
+    for (size_t s = 0; s < out.size(); ++s)
+      for (int k = out[s].first; k < out[s].first + out[s].ncols; ++k) col_sn[k] = (int)s;
+    for (size_t s = 0; s < out.size(); ++s) {
+      int last = out[s].first + out[s].ncols - 1;
+      out[s].parent = parent[last] >= 0 ? col_sn[parent[last]] : -1;
+    }
+    sns.swap(out);
+  }
   const int NS = (int)sns.size();
   S.S = NS;
   S.col_sn = col_sn;
@@ -323,7 +354,6 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     S.sn_rows[s] = sns[s].rows;
     S.sn_w[s] = D * sns[s].ncols;
     S.sn_m[s] = D * (sns[s].ncols + (int)sns[s].rows.size());
-    S.sn_off[s] = S.storage;
     S.storage += (int64_t)S.sn_m[s] * S.sn_w[s];
     S.max_sn_cols_sc = std::max(S.max_sn_cols_sc, S.sn_w[s]);
     S.max_panel_rows = std::max(S.max_panel_rows, S.sn_m[s]);
@@ -344,6 +374,28 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
   {
     VI fill(S.level_ptr.begin(), S.level_ptr.end() - 1);
     for (int s = 0; s < NS; ++s) S.level_sn[fill[S.sn_level[s]]++] = s;
+  }
+  // panel storage in LEVEL order: every level is one contiguous range [level_off[l], level_off[l+1])
+  // so a level can be staged into shared memory with one contiguous copy.  level_stage_hi[l] is
+  // the end of the prefix of that range (whole panels) that fits the staging budget.
+  {
+    int64_t o = 0;
+    S.level_off.assign(S.num_levels + 1, 0);
+    S.level_stage_hi.assign(S.num_levels, 0);
+    for (int l = 0; l < S.num_levels; ++l) {
+      S.level_off[l] = (int32_t)o;
+      int64_t lo = o;
+      int64_t shi = o;
+      for (int i = S.level_ptr[l]; i < S.level_ptr[l + 1]; ++i) {
+        int sn = S.level_sn[i];
+        S.sn_off[sn] = o;
+        o += (int64_t)S.sn_m[sn] * S.sn_w[sn];
+        if (o - lo <= opt.stage_budget_doubles && shi == o - (int64_t)S.sn_m[sn] * S.sn_w[sn]) shi = o;
+      }
+      S.level_stage_hi[l] = (int32_t)shi;
+      S.max_level_stage = std::max<int64_t>(S.max_level_stage, shi - lo);
+    }
+    S.level_off[S.num_levels] = (int32_t)o;
   }
 
   // row position of pose p inside panel s (scalar), -1 if absent

@@ -20,6 +20,8 @@ struct SymbolicOptions {
   double relax_mid_frac = 0.1;
   int relax_max_cols = 64;        // hard cap on supernode width (pose columns)
   double relax_big_frac = 0.05;
+  // shared-memory staging budget (doubles) for one elimination-tree level of panels
+  int64_t stage_budget_doubles = 0;
 };
 
 struct Symbolic {
@@ -39,6 +41,9 @@ struct Symbolic {
   int64_t storage = 0;
   int num_levels = 0;
   std::vector<int32_t> level_ptr, level_sn;     // supernodes grouped by level (height from leaves)
+  std::vector<int32_t> level_off;               // [L+1] storage range of each level (level-ordered panels)
+  std::vector<int32_t> level_stage_hi;          // [L] end of the staged (shared-memory) prefix of the level
+  int64_t max_level_stage = 0;                  // largest staged prefix (doubles)
 
   // numeric factorisation: gather-form update tasks grouped by level of the target
   //   task t: target block at ut_off (storage offset of entry (0,0)), leading dim ut_ld,
