@@ -125,6 +125,9 @@ typedef struct dnls_stats {
   double bytes_solve;          /* 16 nnz_L + vectors */
   double bytes_update;         /* retraction: read/write poses, read delta */
   double bytes_backward;       /* adjoint solve + weight-gradient recompute */
+  int64_t index_bytes;         /* device bytes of the symbolic index arrays */
+  int64_t smem_bytes;          /* dynamic shared memory per CTA of the numeric kernels */
+  int64_t resident_doubles;    /* factor storage held in shared memory for the whole solve */
 } dnls_stats;
 
 typedef struct dnls_graph dnls_graph;
@@ -229,6 +232,11 @@ DNLS_API dnls_status dnls_import_matrix(const dnls_graph* g, int32_t batch, cons
                                         void* workspace, size_t ws_bytes, void* stream);
 DNLS_API dnls_status dnls_export_rhs(const dnls_graph* g, int32_t batch, const void* workspace,
                                      size_t ws_bytes, double* b, void* stream);
+
+/* Debug: (tag, clock64) pairs recorded by CTA 0 of the last kernels in a -DDNLS_TRACE build
+ * (pairs written to out[2*i], out[2*i+1]; at most `capacity` pairs; the buffer is reset).
+ * Host-synchronous.  Returns DNLS_E_UNSUPPORTED in the production build. */
+DNLS_API dnls_status dnls_debug_trace(int64_t* out, int32_t capacity, int32_t* count);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdnls.so")
+LIB_PATH = os.path.join(HERE, "lib", "libdnls_trace.so" if os.environ.get("DNLS_LIB") == "trace" else "libdnls.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "dnls.h")
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
@@ -75,6 +75,9 @@ class DnlsStats(ctypes.Structure):
         ("bytes_solve", ctypes.c_double),
         ("bytes_update", ctypes.c_double),
         ("bytes_backward", ctypes.c_double),
+        ("index_bytes", ctypes.c_int64),
+        ("smem_bytes", ctypes.c_int64),
+        ("resident_doubles", ctypes.c_int64),
     ]
 
 
@@ -107,6 +110,7 @@ _SIGS = {
                                           ctypes.c_void_p, ctypes.c_void_p]),
     "dnls_import_matrix": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p]),
+    "dnls_debug_trace": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
     "dnls_export_rhs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p, ctypes.c_void_p]),
 }

@@ -10,33 +10,36 @@ SRC = [os.path.join(HERE, "csrc", "dnls.cu"), os.path.join(HERE, "csrc", "symbol
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("phases.cuh", "lie.cuh", "symbolic.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "dnls.h")]
 OUT = os.path.join(HERE, "lib", "libdnls.so")
+OUT_TRACE = os.path.join(HERE, "lib", "libdnls_trace.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC,-fvisibility=hidden,-O2", "-shared", "-cudart", "static"]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(OUT):
+def up_to_date(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return False
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return all(os.path.getmtime(p) <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    tmp = OUT + ".tmp"
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """Compile libdnls.so (or, trace=True, the -DDNLS_TRACE debug variant libdnls_trace.so)."""
+    out = OUT_TRACE if trace else OUT
+    if not force and up_to_date(out):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    tmp = out + ".tmp"
+    cmd = [NVCC] + FLAGS + (["-DDNLS_TRACE"] if trace else []) + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libdnls.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -22,8 +22,8 @@
 using namespace dnls;
 
 namespace {
-constexpr int NT = 256;   // threads per CTA (one batch element per CTA)
-constexpr int64_t SMEM_BYTES = 200 * 1024;   // dynamic shared memory per CTA (x + level staging)
+constexpr int NT = 512;   // threads per CTA (one batch element per CTA)
+constexpr int64_t SMEM_BYTES = 218 * 1024;   // dynamic shared memory per CTA (x + resident + staging)
 thread_local std::string g_err;
 
 dnls_status fail(dnls_status s, const std::string& msg) {
@@ -42,6 +42,7 @@ struct dnls_graph {
   Symbolic sym;
   int device = 0;
   int* dbuf = nullptr;
+  size_t dbuf_bytes = 0;
   DevGraph dg{};
   std::mutex mu;
   const void* last_ws = nullptr;   // workspace holding the last implicit factor
@@ -105,8 +106,10 @@ DevProb dev_prob(const dnls_problem* p) {
 // ============================================================================= kernels
 namespace {
 
+size_t sched_ints(const DevGraph& g) { return (size_t)g.S + (size_t)g.n_forest + 2; }
 size_t smem_bytes(const DevGraph& g) {
-  return sizeof(double) * ((g.x_smem ? (size_t)g.n_pad : 0) + (size_t)g.stage_n);
+  return sizeof(double) * ((g.x_smem ? (size_t)g.n_pad : 0) + (size_t)g.res_n + (size_t)g.stage_n) +
+         sizeof(int) * sched_ints(g);
 }
 
 template <class F>
@@ -118,15 +121,36 @@ dnls_status set_smem(F* kernel, size_t bytes, const char* what) {
 
 // per-CTA shared memory views
 struct Smem {
-  double* x;       // solution vector (shared or global)
-  double* stage;   // level staging area
+  double* x;        // solution vector (shared or global)
+  double* res;      // resident top levels of the factor storage
+  double* stage;    // level staging area / per-warp forest slices
+  double* xinv;     // per-team D x D scratch (inverse diagonal of the current diagonal block)
+  int* sq;          // dataflow scheduler ints
+  uint64_t* mbar;   // mbarrier of the bulk (TMA) loads
+  uint32_t phase;
 };
+// must be called by every thread at kernel start (initialises the mbarrier, one barrier)
 __device__ __forceinline__ Smem smem_views(const DevGraph& g, double* xg) {
   extern __shared__ __align__(16) double smem[];
+  __shared__ uint64_t s_mbar;
+  __shared__ double s_xinv[(NT / 32) * 36];
   Smem v;
   v.x = g.x_smem ? smem : xg;
-  v.stage = smem + (g.x_smem ? g.n_pad : 0);
+  v.res = smem + (g.x_smem ? g.n_pad : 0);
+  v.stage = v.res + g.res_n;
+  v.sq = reinterpret_cast<int*>(v.stage + g.stage_n);
+  v.xinv = s_xinv;
+  v.mbar = &s_mbar;
+  v.phase = 0;
+  if (threadIdx.x == 0) mbar_init(&s_mbar);
+  __syncthreads();
   return v;
+}
+__device__ __forceinline__ LView full_view(const DevGraph& g, double* Lg, const Smem& sm) {
+  return LView{Lg, sm.res, g.res_lo, nullptr, 0, 0};
+}
+__device__ __forceinline__ LView global_view(const DevGraph& g, double* Lg) {
+  return LView{Lg, nullptr, g.storage, nullptr, 0, 0};
 }
 
 struct FwdParams {
@@ -173,19 +197,22 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
   double* jac_b = ws.jac + (size_t)b * slots * JS;
   double* cost_b = ws.cost + (size_t)b * slots;
   double* Lg = ws.L + (size_t)b * g.storage;
-  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
   double* x_b = sm.x;
-  const LView L{Lg, nullptr, 0, 0};
+  const LView L = full_view(g, Lg, sm);
 
   int status = DNLS_ST_OK, iters = 0;
   double lam = fp.lam0, Sprev = 0.0;
   bool have_prev = false;
   for (int k = 0; k < fp.K; ++k) {
     // a1 + a2 at theta_k
+    DNLS_TRACE_POINT(100);
     jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
     __syncthreads();
+    DNLS_TRACE_POINT(200);
     assemble_phase<D, NT>(g, L, jac_b, x_b, fp.lm ? lam : -1.0, fp.damping, s_red);
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+    DNLS_TRACE_POINT(300);
     const double S = sh_S;
     if (fp.early_stop && have_prev && fabs(S - Sprev) < fp.abs_tol + fp.rel_tol * Sprev) {
       status = DNLS_ST_CONVERGED;
@@ -193,7 +220,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     }
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, Lg, sm.stage, 1e-13 * sh_max, &sh_fail);
+    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, x_b, sm.sq);
     const bool ok = sh_fail == 0;
     __syncthreads();
     if (!fp.lm) {
@@ -201,9 +228,11 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
         status = DNLS_ST_NOT_SPD;
         break;
       }
-      solve_phase<D, NT>(g, Lg, sm.stage, x_b);
+      solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.sq, false);
+      DNLS_TRACE_POINT(400);
       retract_phase<D, NT>(g, Tb, Tb, x_b, fp.alpha);
       __syncthreads();
+      DNLS_TRACE_POINT(500);
       ++iters;
       Sprev = S;
       have_prev = true;
@@ -211,7 +240,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
       ++iters;
       bool accept = false;
       if (ok) {
-        solve_phase<D, NT>(g, Lg, sm.stage, x_b);
+        solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.sq, false);
         retract_phase<D, NT>(g, Tb, Ttr, x_b, fp.alpha);
         __syncthreads();
         objective_phase<D, NT>(g, pr, Ttr, b, cost_b);
@@ -247,9 +276,11 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, Lg, sm.stage, 1e-13 * sh_max, &sh_fail);
+    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, nullptr, sm.sq);
     __syncthreads();
     if (sh_fail && status == DNLS_ST_OK) status = DNLS_ST_NOT_SPD;
+    // the cached factor must be complete in global memory for dnls_backward_implicit
+    copy_range<NT>(Lg + g.res_lo, sm.res, g.storage - g.res_lo);
   } else {
     objective_phase<D, NT>(g, pr, Tb, b, cost_b);
     __syncthreads();
@@ -281,9 +312,9 @@ __global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, Dev
   const double* Tb = pr.poses + (size_t)b * g.N * PS;
   double* jac_b = ws.jac + (size_t)b * slots * JS;
   double* cost_b = ws.cost + (size_t)b * slots;
-  const LView L{ws.L + (size_t)b * g.storage, nullptr, 0, 0};
+  const LView L = global_view(g, ws.L + (size_t)b * g.storage);
   double* xg = ws.x + (size_t)b * g.n;
-  const Smem sm = smem_views(g, xg);
+  Smem sm = smem_views(g, xg);
   jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
   __syncthreads();
   assemble_phase<D, NT>(g, L, jac_b, sm.x, lam ? lam[b] : -1.0, damping, s_red);
@@ -303,8 +334,12 @@ __global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* 
   __shared__ int sh_fail;
   if (threadIdx.x == 0) sh_fail = 0;
   __syncthreads();
-  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
-  factor_phase<D, NT>(g, ws.L + (size_t)b * g.storage, sm.stage, 1e-13 * ws.maxd[b], &sh_fail);
+  Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  double* Lg = ws.L + (size_t)b * g.storage;
+  bulk_load<NT>(sm.res, Lg + g.res_lo, g.storage - g.res_lo, sm.mbar, sm.phase);
+  factor_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, 1e-13 * ws.maxd[b], &sh_fail, sm.mbar, sm.phase, sm.xinv,
+                      nullptr, sm.sq);
+  copy_range<NT>(Lg + g.res_lo, sm.res, g.storage - g.res_lo);
   __syncthreads();
   if (threadIdx.x == 0 && status) status[b] = sh_fail ? DNLS_ST_NOT_SPD : DNLS_ST_OK;
 }
@@ -313,14 +348,15 @@ __global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* 
 template <int D>
 __global__ void __launch_bounds__(NT, 1) k_solve(DevGraph g, DevWs ws, const double* rhs, double* xout) {
   const int b = blockIdx.x;
-  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
   double* x_b = sm.x;
   for (int i = threadIdx.x; i < g.n; i += NT) {
     const int o = i / D, a = i - o * D;
     x_b[(size_t)g.iperm[o] * D + a] = rhs[(size_t)b * g.n + i];
   }
-  __syncthreads();
-  solve_phase<D, NT>(g, ws.L + (size_t)b * g.storage, sm.stage, x_b);
+  double* Lg = ws.L + (size_t)b * g.storage;
+  bulk_load<NT>(sm.res, Lg + g.res_lo, g.storage - g.res_lo, sm.mbar, sm.phase);
+  solve_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, x_b, sm.mbar, sm.phase, sm.sq);
   __syncthreads();
   for (int i = threadIdx.x; i < g.n; i += NT) {
     const int o = i / D, a = i - o * D;
@@ -336,7 +372,7 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
   const int b = blockIdx.x;
   const size_t slots = (size_t)g.E + g.P;
   const double* Tb = pr.poses + (size_t)b * g.N * PS;
-  const Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
   double* x_b = sm.x;
   double* out_b = ws.cost + (size_t)b * slots;
   if (ws.st[b] == DNLS_ST_NOT_SPD) {   // no valid factor: zero gradient contribution
@@ -384,8 +420,9 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
 #pragma unroll
     for (int a = 0; a < D; ++a) x_b[(size_t)g.iperm[o] * D + a] = v[a];
   }
-  __syncthreads();
-  solve_phase<D, NT>(g, ws.L + (size_t)b * g.storage, sm.stage, x_b);
+  double* Lg = ws.L + (size_t)b * g.storage;
+  bulk_load<NT>(sm.res, Lg + g.res_lo, g.storage - g.res_lo, sm.mbar, sm.phase);
+  solve_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, x_b, sm.mbar, sm.phase, sm.sq);
   __syncthreads();
   // dL/dw = -2 w (C lambda) . c  (unweighted C, c at theta_K)
   for (int slot = threadIdx.x; slot < (int)slots; slot += NT) {
@@ -445,7 +482,7 @@ __global__ void k_export_factor(DevGraph g, DevWs ws, double* dense) {
   __syncthreads();
   // iterate storage panels: (row, col) scalar within panel -> permuted global indices
   for (int s = 0; s < g.S; ++s) {
-    const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s], off = g.sn_off[s];
+    const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s], ld = g.sn_ld[s], off = g.sn_off[s];
     const int rb = g.snr_ptr[s];
     for (int it = threadIdx.x; it < m * w; it += NT) {
       const int c = it / m, r = it - c * m;
@@ -457,7 +494,7 @@ __global__ void k_export_factor(DevGraph g, DevWs ws, double* dense) {
         const int rr = (r - w) / D, a = (r - w) % D;
         gr = D * g.snr[rb + rr] + a;
       }
-      Db[(size_t)gr * n + (size_t)D * f + c] = Lb[off + (size_t)c * m + r];
+      Db[(size_t)gr * n + (size_t)D * f + c] = Lb[off + (size_t)c * ld + r];
     }
   }
 }
@@ -471,7 +508,7 @@ __global__ void k_import_matrix(DevGraph g, DevWs ws, const double* dense) {
   __shared__ double s_red[NT / 32];
   double mymax = 0.0;
   for (int s = 0; s < g.S; ++s) {
-    const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s], off = g.sn_off[s];
+    const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s], ld = g.sn_ld[s], off = g.sn_off[s];
     const int rb = g.snr_ptr[s];
     for (int it = threadIdx.x; it < m * w; it += NT) {
       const int c = it / m, r = it - c * m;
@@ -489,7 +526,7 @@ __global__ void k_import_matrix(DevGraph g, DevWs ws, const double* dense) {
         v = Db[((size_t)g.perm[pr_] * D + ar) * n + (size_t)g.perm[pc] * D + ac];
         if (r == c) mymax = fmax(mymax, v);
       }
-      Lb[off + (size_t)c * m + r] = v;
+      Lb[off + (size_t)c * ld + r] = v;
     }
   }
 #pragma unroll
@@ -524,6 +561,25 @@ DNLS_API const char* dnls_version_string(void) {
 
 DNLS_API const char* dnls_last_error(void) { return g_err.c_str(); }
 
+DNLS_API dnls_status dnls_debug_trace(int64_t* out, int32_t capacity, int32_t* count) {
+#ifdef DNLS_TRACE
+  if (!out || !count) return fail(DNLS_E_INVALID, "dnls_debug_trace: NULL argument");
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(int));
+  n = std::min(n, (int)capacity);
+  if (n > 0) cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * 2 * n);
+  *count = n;
+  int zero = 0;
+  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(int));
+  return cuda_check("dnls_debug_trace");
+#else
+  (void)out;
+  (void)capacity;
+  if (count) *count = 0;
+  return fail(DNLS_E_UNSUPPORTED, "dnls_debug_trace: library built without -DDNLS_TRACE");
+#endif
+}
+
 DNLS_API void dnls_options_default(dnls_options* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
@@ -552,10 +608,15 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   SymbolicOptions sopt;
   {
     // shared-memory plan: x (n doubles) in shared memory when it fits in 64 KB, the rest of
-    // SMEM_BYTES stages one elimination-tree level of panels at a time
+    // SMEM_BYTES holds the resident top levels + the staging buffer of the lower levels
     const int64_t n = (int64_t)num_vars * group;
-    const int64_t xb = (n * 8 <= 65536) ? n * 8 : 0;
-    sopt.stage_budget_doubles = (SMEM_BYTES - xb) / 8;
+    const int64_t xb = (n * 8 <= 65536) ? ((n + 1) & ~int64_t(1)) * 8 : 0;
+    int64_t smem = SMEM_BYTES;
+    if (const char* env = std::getenv("DNLS_SMEM_KB")) smem = std::min<int64_t>(SMEM_BYTES, std::atoll(env) * 1024);
+    // reserve the scheduler ints (<= 2 per pose column + 2)
+    smem -= 8 * (int64_t)num_vars + 64;
+    sopt.smem_cap_doubles = std::max<int64_t>(0, smem - xb) / 8;
+    sopt.cta_threads = NT;
   }
   if (const char* env = std::getenv("DNLS_RELAX")) {   // tuning override: "a,sc,sf,mc,mf,max,bf"
     std::sscanf(env, "%d,%d,%lf,%d,%lf,%d,%lf", &sopt.relax_always_cols, &sopt.relax_small_cols,
@@ -572,20 +633,39 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   std::vector<int32_t> buf;
   std::vector<size_t> offs;
   auto add = [&](const std::vector<int32_t>& v) {
+    while (buf.size() % 4) buf.push_back(0);   // 16-byte aligned arrays (int4 loads)
     offs.push_back(buf.size());
     buf.insert(buf.end(), v.begin(), v.end());
     buf.push_back(0);   // never empty
   };
+  // packed 16-byte descriptors
+  std::vector<int32_t> task4, con4, fcon4;
+  for (size_t t = 0; t < s.ut_off.size(); ++t) {
+    task4.push_back(s.ut_off[t]); task4.push_back(s.ut_ld[t]);
+    task4.push_back(s.ut_cptr[t]); task4.push_back(s.ut_cptr[t + 1]);
+  }
+  for (size_t c = 0; c < s.uc_a.size(); ++c) {
+    con4.push_back(s.uc_a[c]); con4.push_back(s.uc_b[c]); con4.push_back(s.uc_ld[c]); con4.push_back(s.uc_w[c]);
+  }
+  for (size_t c = 0; c < s.fc_off.size(); ++c) {
+    fcon4.push_back(s.fc_off[c]); fcon4.push_back(s.fc_ld[c]); fcon4.push_back(s.fc_w[c]); fcon4.push_back(s.fc_x[c]);
+  }
   std::vector<int32_t> sn_off32(s.sn_off.begin(), s.sn_off.end());
   add(s.perm); add(s.iperm); add(s.edges); add(s.prior_vars);
-  add(s.sn_first); add(s.sn_ncols); add(s.sn_m); add(s.sn_w); add(sn_off32);
+  add(s.sn_first); add(s.sn_ncols); add(s.sn_m); add(s.sn_ld); add(s.sn_w); add(sn_off32);
   add(s.level_ptr); add(s.level_sn); add(s.level_off); add(s.level_stage_hi);
   add(s.ut_level_ptr); add(s.ut_off); add(s.ut_ld); add(s.ut_cptr); add(s.uc_a); add(s.uc_b); add(s.uc_ld); add(s.uc_w);
+  add(s.level_gu); add(s.level_gf); add(s.lrow_ptr); add(s.lrow);
+  add(s.sn_parent); add(s.ut_sn_ptr); add(s.child_ptr); add(s.child_idx); add(s.sn_sched); add(s.leaves);
+  add(s.broots);
+  add(task4); add(con4); add(fcon4);
   add(s.fc_ptr); add(s.fc_off); add(s.fc_ld); add(s.fc_w); add(s.fc_x);
   add(s.snr_ptr); add(s.snr);
   add(s.blk_off); add(s.blk_ld); add(s.blk_kind); add(s.blk_cptr); add(s.blk_con);
   add(s.bc_ptr); add(s.bc);
   g->device = device;
+  while (buf.size() % 4) buf.push_back(0);
+  g->dbuf_bytes = buf.size() * sizeof(int32_t);
   if (device < 0) {   // host-only symbolic analysis (no device arrays; compute calls refuse it)
     *out = g;
     return DNLS_OK;
@@ -614,14 +694,27 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dg.storage = (int)s.storage; dg.nblk = (int)s.blk_off.size(); dg.n = s.N * s.D;
   dg.x_smem = (int64_t)dg.n * 8 <= 65536 ? 1 : 0;
   dg.n_pad = (dg.n + 1) & ~1;
+  dg.res_lo = s.res_lo;
+  dg.res_n = (int)((s.res_n + 1) & ~int64_t(1));
+  dg.x_smem = (int64_t)dg.n * 8 <= 65536 ? 1 : 0;
+  dg.n_pad = (dg.n + 1) & ~1;
   dg.stage_n = (int)((s.max_level_stage + 1) & ~int64_t(1));
+  dg.stage_n = std::max<int>(dg.stage_n, (int)(((s.stage_cap > 0 ? s.stage_cap : 0)) & ~int64_t(1)));
   dg.perm = d + offs[k++]; dg.iperm = d + offs[k++]; dg.edges = d + offs[k++]; dg.prior_vars = d + offs[k++];
-  dg.sn_first = d + offs[k++]; dg.sn_ncols = d + offs[k++]; dg.sn_m = d + offs[k++]; dg.sn_w = d + offs[k++];
+  dg.sn_first = d + offs[k++]; dg.sn_ncols = d + offs[k++]; dg.sn_m = d + offs[k++]; dg.sn_ld = d + offs[k++]; dg.sn_w = d + offs[k++];
   dg.sn_off = d + offs[k++];
   dg.level_ptr = d + offs[k++]; dg.level_sn = d + offs[k++];
   dg.level_off = d + offs[k++]; dg.level_stage_hi = d + offs[k++];
   dg.ut_level_ptr = d + offs[k++]; dg.ut_off = d + offs[k++]; dg.ut_ld = d + offs[k++]; dg.ut_cptr = d + offs[k++];
   dg.uc_a = d + offs[k++]; dg.uc_b = d + offs[k++]; dg.uc_ld = d + offs[k++]; dg.uc_w = d + offs[k++];
+  dg.level_gu = d + offs[k++]; dg.level_gf = d + offs[k++]; dg.lrow_ptr = d + offs[k++]; dg.lrow = d + offs[k++];
+  dg.sn_parent = d + offs[k++]; dg.ut_sn_ptr = d + offs[k++]; dg.child_ptr = d + offs[k++];
+  dg.child_idx = d + offs[k++]; dg.sn_sched = d + offs[k++]; dg.leaves = d + offs[k++]; dg.broots = d + offs[k++];
+  dg.top_level = s.top_level; dg.n_forest = s.n_forest; dg.n_leaves = (int)s.leaves.size();
+  dg.n_broots = (int)s.broots.size();
+  dg.task4 = reinterpret_cast<const int4*>(d + offs[k++]);
+  dg.con4 = reinterpret_cast<const int4*>(d + offs[k++]);
+  dg.fcon4 = reinterpret_cast<const int4*>(d + offs[k++]);
   dg.fc_ptr = d + offs[k++]; dg.fc_off = d + offs[k++]; dg.fc_ld = d + offs[k++]; dg.fc_w = d + offs[k++];
   dg.fc_x = d + offs[k++];
   dg.snr_ptr = d + offs[k++]; dg.snr = d + offs[k++];
@@ -664,6 +757,9 @@ DNLS_API dnls_status dnls_graph_stats(const dnls_graph* g, dnls_stats* o) {
   o->bytes_solve = 16.0 * s.nnz_L + 2.0 * nvec;
   o->bytes_update = 2.0 * pose_b * s.N + nvec;
   o->bytes_backward = 16.0 * s.nnz_L + pose_b * (s.N + s.E + s.P) + 2.0 * nvec;
+  o->index_bytes = (int64_t)g->dbuf_bytes;
+  o->smem_bytes = g->dbuf ? (int64_t)smem_bytes(g->dg) : 0;
+  o->resident_doubles = (int64_t)(s.storage - s.res_lo);
   return DNLS_OK;
 }
 

@@ -14,21 +14,74 @@
 
 namespace dnls {
 
+// ----------------------------------------------------------------------------- tracing (debug builds)
+// Compiled with -DDNLS_TRACE: thread 0 of block 0 records (tag, clock64) pairs so the fused
+// kernel's time can be attributed to phases / levels (tools/trace.py).  No-op otherwise.
+#ifdef DNLS_TRACE
+__device__ long long g_trace[2 * 8192];
+__device__ int g_trace_n;
+#define DNLS_TRACE_POINT(tag)                                         \
+  do {                                                                \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                        \
+      int i_ = g_trace_n;                                             \
+      if (i_ < 8192) {                                                \
+        g_trace[2 * i_] = (tag);                                      \
+        g_trace[2 * i_ + 1] = clock64();                              \
+        g_trace_n = i_ + 1;                                           \
+      }                                                               \
+    }                                                                 \
+  } while (0)
+#else
+#define DNLS_TRACE_POINT(tag) \
+  do {                        \
+  } while (0)
+#endif
+
 // device view of the symbolic analysis (all arrays int32, uploaded once per graph)
 struct DevGraph {
   int D, N, E, P, S, L, storage, nblk, n;
   int x_smem;     // 1: the solution vector x lives in shared memory (offset 0, n_pad doubles)
-  int n_pad;      // n rounded up to an even count (16-byte alignment of the staging area)
+  int n_pad;      // n rounded up to an even count (16-byte alignment of the next area)
+  int res_lo;     // storage offsets >= res_lo are resident in shared memory (top levels)
+  int res_n;      // resident doubles (even)
   int stage_n;    // doubles of the level-staging area (largest staged level prefix)
   const int *perm, *iperm, *edges, *prior_vars;
-  const int *sn_first, *sn_ncols, *sn_m, *sn_w, *sn_off;
+  const int *sn_first, *sn_ncols, *sn_m, *sn_ld, *sn_w, *sn_off;
   const int *level_ptr, *level_sn, *level_off, *level_stage_hi;
   const int *ut_level_ptr, *ut_off, *ut_ld, *ut_cptr, *uc_a, *uc_b, *uc_ld, *uc_w;
+  const int *level_gu, *level_gf, *lrow_ptr, *lrow;
+  const int *sn_parent, *ut_sn_ptr, *child_ptr, *child_idx, *sn_sched, *leaves, *broots;
+  int top_level, n_forest, n_leaves, n_broots;
   const int *fc_ptr, *fc_off, *fc_ld, *fc_w, *fc_x;
+  // packed 16-byte descriptors: task4 = (target off, target ld, contrib begin, contrib end),
+  // con4 = (source row-p off, source row-q off, ld, width), fcon4 = (source row off, ld, width, y off)
+  const int4 *task4, *con4, *fcon4;
   const int *snr_ptr, *snr;
   const int *blk_off, *blk_ld, *blk_kind, *blk_cptr, *blk_con;
   const int *bc_ptr, *bc;
+  const int* ibase;   // start of the device index buffer
+  int inum;           // its length (ints, multiple of 4)
+  int idx_smem;       // 1: kernels copy the index buffer into shared memory and read it there
 };
+
+#define DNLS_DEVGRAPH_PTRS(X)                                                                           \
+  X(perm) X(iperm) X(edges) X(prior_vars) X(sn_first) X(sn_ncols) X(sn_m) X(sn_ld) X(sn_w) X(sn_off)     \
+  X(level_ptr) X(level_sn) X(level_off) X(level_stage_hi) X(ut_level_ptr) X(ut_off) X(ut_ld) X(ut_cptr) \
+  X(uc_a) X(uc_b) X(uc_ld) X(uc_w) X(level_gu) X(level_gf) X(lrow_ptr) X(lrow) X(sn_parent) X(ut_sn_ptr)  \
+  X(child_ptr) X(child_idx) X(sn_sched) X(leaves) X(broots) X(fc_ptr) X(fc_off) X(fc_ld) X(fc_w) X(fc_x) \
+  X(snr_ptr) X(snr) X(blk_off) X(blk_ld) X(blk_kind) X(blk_cptr) X(blk_con) X(bc_ptr) X(bc)
+
+// a copy of g whose index pointers refer to the shared-memory copy `sb` of the index buffer
+__device__ __forceinline__ DevGraph remap_graph(const DevGraph& g, const int* sb) {
+  DevGraph r = g;
+#define DNLS_REMAP(f) r.f = sb + (g.f - g.ibase);
+  DNLS_DEVGRAPH_PTRS(DNLS_REMAP)
+#undef DNLS_REMAP
+  r.task4 = reinterpret_cast<const int4*>(sb + (reinterpret_cast<const int*>(g.task4) - g.ibase));
+  r.con4 = reinterpret_cast<const int4*>(sb + (reinterpret_cast<const int*>(g.con4) - g.ibase));
+  r.fcon4 = reinterpret_cast<const int4*>(sb + (reinterpret_cast<const int*>(g.fcon4) - g.ibase));
+  return r;
+}
 
 // problem inputs (see dnls_problem)
 struct DevProb {
@@ -63,14 +116,24 @@ struct GT {
   static constexpr int JS = 2 * D * D + D;        // scratch doubles per cost slot
 };
 
-// Factor storage view: offsets >= lo live in shared memory (a suffix of the storage, the
-// top of the elimination tree), the rest in global memory.  Generic pointers serve both.
+// Factor storage view.  Offsets >= rlo (the top elimination-tree levels) are RESIDENT in
+// shared memory `r`; offsets in [lo, hi) (the level being processed) are STAGED in shared
+// memory `s`; everything else is in global memory `g`.  Generic pointers serve all three.
 struct LView {
   double* g;
+  double* r;
+  int rlo;
   double* s;
   int lo, hi;
   __device__ __forceinline__ double* at(int off) const {
-    return (off >= lo && off < hi) ? s + (off - lo) : g + off;
+    return off >= rlo ? r + (off - rlo) : ((off >= lo && off < hi) ? s + (off - lo) : g + off);
+  }
+  __device__ __forceinline__ LView level(double* stage, int l0, int h0) const {
+    LView v = *this;
+    v.s = stage;
+    v.lo = l0;
+    v.hi = h0;
+    return v;
   }
 };
 
@@ -86,6 +149,55 @@ __device__ __forceinline__ void copy_range(double* __restrict__ dst, const doubl
   } else {
     for (int i = threadIdx.x; i < n; i += NT) dst[i] = src[i];
   }
+}
+
+// ----------------------------------------------------------------------------- TMA bulk copies
+// 1-D bulk async copy global -> shared (cp.async.bulk, completion through an mbarrier with a
+// transaction count).  Sizes / addresses are 16-byte multiples (panels are padded to even
+// double counts).  One elected thread issues; every thread waits on the mbarrier phase.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+  const uint32_t a = smem_u32(mbar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+// CTA-wide: every thread orders its prior generic-proxy accesses (global writes of the panels,
+// shared reads of the staging area) before the async proxy, barrier, thread 0 issues the bulk
+// copy, every thread waits on the mbarrier phase (phase toggles per use).
+template <int NT>
+__device__ __forceinline__ void bulk_load(double* dst, const double* src, int ndoubles, uint64_t* mbar,
+                                          uint32_t& phase) {
+  asm volatile("fence.proxy.async;" ::: "memory");
+  __syncthreads();
+  if (ndoubles <= 0) return;
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)ndoubles * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+    for (uint32_t o = 0; o < bytes; o += 65536u) {
+      const uint32_t sz = min(65536u, bytes - o);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(reinterpret_cast<const char*>(dst) + o)),
+          "l"(reinterpret_cast<const char*>(src) + o), "r"(sz), "r"(smem_u32(mbar))
+          : "memory");
+    }
+  }
+  mbar_wait(mbar, phase);
+  phase ^= 1u;
 }
 
 // ============================================================================= cost evaluation
@@ -324,67 +436,70 @@ struct Team {
 };
 
 // Dense right-looking Cholesky of one supernode panel P (m rows, w columns, column-major,
-// leading dim m), blocked by D columns.  Writes L in place (lower part of the diagonal block
-// and the rows below).  *fail set if a pivot <= tol.
+// leading dim m), blocked by D columns.  Per D-column block: one thread factors the D x D
+// diagonal block (rsqrt pivots) and writes its inverse X = L_jj^-1 to the team scratch `xinv`;
+// the rows below are then an independent product a_r X^T per thread (no divisions, no chain);
+// the trailing columns of the panel get the rank-D update.  *fail set if a pivot <= tol.
 template <int D>
-__device__ void panel_factor(double* P, int m, int w, double tol, const Team& tm, int* fail) {
+__device__ void panel_factor(double* P, int m, int ld, int w, double tol, const Team& tm, int* fail, double* xinv) {
   for (int c0 = 0; c0 < w; c0 += D) {
     if (tm.rank == 0) {
       double a[D][D];
 #pragma unroll
       for (int j = 0; j < D; ++j)
 #pragma unroll
-        for (int i = j; i < D; ++i) a[i][j] = P[(size_t)(c0 + j) * m + c0 + i];
+        for (int i = j; i < D; ++i) a[i][j] = P[(size_t)(c0 + j) * ld + c0 + i];
       bool bad = false;
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         double piv = a[j][j];
 #pragma unroll
-        for (int k = 0; k < j; ++k) piv -= a[j][k] * a[j][k];
+        for (int k = 0; k < j; ++k) piv = fma(-a[j][k], a[j][k], piv);
         if (!(piv > tol)) {
           bad = true;
           piv = 1.0;
         }
-        const double ljj = sqrt(piv);
-        const double inv = 1.0 / ljj;
-        a[j][j] = ljj;
+        const double inv = rsqrt(piv);
+        xinv[j] = inv;
+        a[j][j] = piv * inv;
 #pragma unroll
         for (int i = j + 1; i < D; ++i) {
           double s = a[i][j];
 #pragma unroll
-          for (int k = 0; k < j; ++k) s -= a[i][k] * a[j][k];
+          for (int k = 0; k < j; ++k) s = fma(-a[i][k], a[j][k], s);
           a[i][j] = s * inv;
         }
       }
 #pragma unroll
       for (int j = 0; j < D; ++j)
 #pragma unroll
-        for (int i = j; i < D; ++i) P[(size_t)(c0 + j) * m + c0 + i] = a[i][j];
+        for (int i = j; i < D; ++i) P[(size_t)(c0 + j) * ld + c0 + i] = a[i][j];
       if (bad) *fail = 1;
     }
     tm.sync();
     const int r0 = c0 + D;
     if (r0 < m) {
-      double l[D][D], inv[D];
+      // rows below: x L_jj^T = a  (forward substitution, inverse diagonal from the scratch)
+      double l[D][D], iv[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) {
+        iv[j] = xinv[j];
 #pragma unroll
-        for (int i = j; i < D; ++i) l[i][j] = P[(size_t)(c0 + j) * m + c0 + i];
-        inv[j] = 1.0 / l[j][j];
+        for (int i = j + 1; i < D; ++i) l[i][j] = P[(size_t)(c0 + j) * ld + c0 + i];
       }
       for (int r = r0 + tm.rank; r < m; r += tm.size) {
         double x[D];
 #pragma unroll
-        for (int q = 0; q < D; ++q) x[q] = P[(size_t)(c0 + q) * m + r];
+        for (int q = 0; q < D; ++q) x[q] = P[(size_t)(c0 + q) * ld + r];
 #pragma unroll
         for (int q = 0; q < D; ++q) {
           double s = x[q];
 #pragma unroll
-          for (int k = 0; k < q; ++k) s -= x[k] * l[q][k];
-          x[q] = s * inv[q];
+          for (int k = 0; k < q; ++k) s = fma(-x[k], l[q][k], s);
+          x[q] = s * iv[q];
         }
 #pragma unroll
-        for (int q = 0; q < D; ++q) P[(size_t)(c0 + q) * m + r] = x[q];
+        for (int q = 0; q < D; ++q) P[(size_t)(c0 + q) * ld + r] = x[q];
       }
       tm.sync();
       const int nc = w - r0;
@@ -395,10 +510,13 @@ __device__ void panel_factor(double* P, int m, int w, double tol, const Team& tm
           const int ci = it / nr, ri = it - ci * nr;
           if (ri < ci) continue;
           const int c = r0 + ci, r = r0 + ri;
-          double s = 0.0;
+          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int k = 0; k < D; ++k) s = fma(P[(size_t)(c0 + k) * m + r], P[(size_t)(c0 + k) * m + c], s);
-          P[(size_t)c * m + r] -= s;
+          for (int k = 0; k < D; k += 2) {
+            s0 = fma(P[(size_t)(c0 + k) * ld + r], P[(size_t)(c0 + k) * ld + c], s0);
+            if (k + 1 < D) s1 = fma(P[(size_t)(c0 + k + 1) * ld + r], P[(size_t)(c0 + k + 1) * ld + c], s1);
+          }
+          P[(size_t)c * ld + r] -= s0 + s1;
         }
         tm.sync();
       }
@@ -424,69 +542,18 @@ __device__ __forceinline__ void team_of(int nsn, Team& tm, int& team, int& nteam
   tm.bar = 1 + team;
 }
 
-// Supernodal left-looking Cholesky, level-synchronous.  Each level's panels are one contiguous
-// storage range; its prefix [level_off, level_stage_hi) is staged into shared memory `stage`,
-// updated (gather form, from descendant panels in global memory), factored by teams, and
-// written back.
-template <int D, int NT>
-__device__ void factor_phase(const DevGraph& g, double* Lg, double* stage, double tol, int* s_fail) {
-  for (int lv = 0; lv < g.L; ++lv) {
-    const int lo = g.level_off[lv], hi = g.level_stage_hi[lv];
-    copy_range<NT>(stage, Lg + lo, hi - lo);
-    __syncthreads();
-    LView V{Lg, stage, lo, hi};
-    // (U) gather-form updates from descendants into this level's panels
-    const int t0 = g.ut_level_ptr[lv], t1 = g.ut_level_ptr[lv + 1];
-    const int nitems = (t1 - t0) * D;
-    for (int itm = threadIdx.x; itm < nitems; itm += NT) {
-      const int t = t0 + itm / D, a = itm % D;
-      double acc[D];
-#pragma unroll
-      for (int q = 0; q < D; ++q) acc[q] = 0.0;
-      for (int ci = g.ut_cptr[t]; ci < g.ut_cptr[t + 1]; ++ci) {
-        const double* A = Lg + g.uc_a[ci];
-        const double* Bm = Lg + g.uc_b[ci];
-        const int ld = g.uc_ld[ci], w = g.uc_w[ci];
-        for (int k = 0; k < w; ++k) {
-          const double av = A[(size_t)k * ld + a];
-#pragma unroll
-          for (int q = 0; q < D; ++q) acc[q] = fma(av, Bm[(size_t)k * ld + q], acc[q]);
-        }
-      }
-      double* T = V.at(g.ut_off[t]);
-      const int ld = g.ut_ld[t];
-#pragma unroll
-      for (int q = 0; q < D; ++q) T[(size_t)q * ld + a] -= acc[q];
-    }
-    __syncthreads();
-    // (F) dense factorisation of the level's panels by teams
-    const int s0 = g.level_ptr[lv], nsn = g.level_ptr[lv + 1] - s0;
-    Team tm;
-    int team, nteams;
-    team_of<NT>(nsn, tm, team, nteams);
-    for (int i = team; i < nsn; i += nteams) {
-      const int s = g.level_sn[s0 + i];
-      panel_factor<D>(V.at(g.sn_off[s]), g.sn_m[s], g.sn_w[s], tol, tm, s_fail);
-    }
-    __syncthreads();
-    copy_range<NT>(Lg + lo, stage, hi - lo);
-    __syncthreads();
-  }
-}
-
-// ============================================================================= a4: solves
 // Warp-level dense triangular solves on a panel's w x w diagonal block (P column-major, leading
 // dim m), rows owned by lanes (row r = lane + 32 j), values held in registers, each step one
 // shuffle broadcast.  MAXR = max ceil(w / 32).
 template <int MAXR>
-__device__ __forceinline__ void warp_trsv_lower(const double* P, int m, int w, double* xs) {
+__device__ __forceinline__ void warp_trsv_lower(const double* P, int ld, int w, double* xs) {
   const int lane = threadIdx.x & 31;
   double t[MAXR], inv[MAXR];
 #pragma unroll
   for (int j = 0; j < MAXR; ++j) {
     const int r = lane + 32 * j;
     t[j] = (r < w) ? xs[r] : 0.0;
-    inv[j] = (r < w) ? 1.0 / P[(size_t)r * m + r] : 0.0;
+    inv[j] = (r < w) ? 1.0 / P[(size_t)r * ld + r] : 0.0;
   }
 #pragma unroll
   for (int sj = 0; sj < MAXR; ++sj) {
@@ -496,7 +563,7 @@ __device__ __forceinline__ void warp_trsv_lower(const double* P, int m, int w, d
       const int c = 32 * sj + cl;
       const double xc = __shfl_sync(0xffffffffu, t[sj] * inv[sj], cl);
       if (lane == cl) t[sj] = xc;
-      const double* col = P + (size_t)c * m;
+      const double* col = P + (size_t)c * ld;
 #pragma unroll
       for (int j = sj; j < MAXR; ++j) {
         const int r = lane + 32 * j;
@@ -512,7 +579,7 @@ __device__ __forceinline__ void warp_trsv_lower(const double* P, int m, int w, d
 }
 
 template <int MAXR>
-__device__ __forceinline__ void warp_trsv_upper(const double* P, int m, int w, double* xs) {
+__device__ __forceinline__ void warp_trsv_upper(const double* P, int ld, int w, double* xs) {
   // solve L^T x = t : step c from w-1 down to 0, rows r < c updated with L[c][r] = P[r*m + c]
   const int lane = threadIdx.x & 31;
   double t[MAXR], inv[MAXR];
@@ -520,7 +587,7 @@ __device__ __forceinline__ void warp_trsv_upper(const double* P, int m, int w, d
   for (int j = 0; j < MAXR; ++j) {
     const int r = lane + 32 * j;
     t[j] = (r < w) ? xs[r] : 0.0;
-    inv[j] = (r < w) ? 1.0 / P[(size_t)r * m + r] : 0.0;
+    inv[j] = (r < w) ? 1.0 / P[(size_t)r * ld + r] : 0.0;
   }
 #pragma unroll
   for (int sj = MAXR - 1; sj >= 0; --sj) {
@@ -533,7 +600,7 @@ __device__ __forceinline__ void warp_trsv_upper(const double* P, int m, int w, d
 #pragma unroll
       for (int j = 0; j <= sj; ++j) {
         const int r = lane + 32 * j;
-        if (r < c) t[j] = fma(-P[(size_t)r * m + c], xc, t[j]);
+        if (r < c) t[j] = fma(-P[(size_t)r * ld + c], xc, t[j]);
       }
     }
   }
@@ -544,69 +611,453 @@ __device__ __forceinline__ void warp_trsv_upper(const double* P, int m, int w, d
   }
 }
 
+// ---- gathers with G cooperating lanes (G | 32, groups lane-aligned): the lanes of a group split
+// the k-range (concatenated source columns, round robin) and combine with an xor-shuffle tree.
+// Every lane of the warp must call the reduction (uniform trip counts); order is fixed, so the
+// result is bitwise deterministic.
+template <int N>
+__device__ __forceinline__ void group_reduce(double (&acc)[N], int G) {
+  for (int off = G >> 1; off > 0; off >>= 1) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+  }
+}
+
+// partial row a of update task tk: acc[q] += sum_{k = lane mod G} A_k[a] B_k[q]
+template <int D>
+__device__ __forceinline__ void task_row_partial(const DevGraph& g, const LView& V, const int4 tk, int a, int lane,
+                                                 int G, double (&acc)[D]) {
+  int kb = 0;
+  for (int ci = tk.z; ci < tk.w; ++ci) {
+    const int4 c = g.con4[ci];
+    const double* A = V.at(c.x) + a;
+    const double* Bm = V.at(c.y);
+    int k = lane - kb % G;
+    if (k < 0) k += G;
+    for (; k < c.w; k += G) {
+      const double av = A[(size_t)k * c.z];
+      double bv[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) bv[q] = Bm[(size_t)k * c.z + q];
+#pragma unroll
+      for (int q = 0; q < D; ++q) acc[q] = fma(av, bv[q], acc[q]);
+    }
+    kb += c.w;
+  }
+}
+
+// partial forward-substitution sum of scalar row a of pose row p: sum_{k = lane mod G} A_k[a] y_k
+template <int D>
+__device__ __forceinline__ double fwd_row_partial(const DevGraph& g, const LView& V, const double* x, int p, int a,
+                                                  int lane, int G) {
+  double s0 = 0.0, s1 = 0.0;
+  int kb = 0;
+  const int c1 = g.fc_ptr[p + 1];
+  for (int ci = g.fc_ptr[p]; ci < c1; ++ci) {
+    const int4 c = g.fcon4[ci];
+    const double* A = V.at(c.x) + a;
+    const double* y = x + c.w;
+    int k = lane - kb % G;
+    if (k < 0) k += G;
+    for (; k + G < c.z; k += 2 * G) {
+      s0 = fma(A[(size_t)k * c.y], y[k], s0);
+      s1 = fma(A[(size_t)(k + G) * c.y], y[k + G], s1);
+    }
+    if (k < c.z) s0 = fma(A[(size_t)k * c.y], y[k], s0);
+    kb += c.z;
+  }
+  return s0 + s1;
+}
+
+// Gather-form Schur updates of one level (CTA-wide): item = (task t, row a), G = level_gu lanes.
+template <int D, int NT>
+__device__ void update_tasks(const DevGraph& g, const LView& V, int lv) {
+  const int G = g.level_gu[lv];
+  const int i0 = g.ut_level_ptr[lv] * D, i1 = g.ut_level_ptr[lv + 1] * D;
+  const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
+  for (int base = i0; base < i1; base += NT / G) {
+    const int item = base + grp;
+    const bool valid = item < i1;
+    const int t = valid ? item / D : 0, a = item - t * D;
+    double acc[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) acc[q] = 0.0;
+    int4 tk = make_int4(0, 0, 0, 0);
+    if (valid) {
+      tk = g.task4[t];
+      task_row_partial<D>(g, V, tk, a, lane, G, acc);
+    }
+    group_reduce<D>(acc, G);
+    if (valid && lane == 0) {
+      double* T = V.at(tk.x) + a;
+#pragma unroll
+      for (int q = 0; q < D; ++q) T[(size_t)q * tk.y] -= acc[q];
+    }
+  }
+}
+
+// Forward-substitution gather of one level (CTA-wide, fused into the factorisation):
+// item = (pose row p of the level, component a), G = level_gf lanes.
+template <int D, int NT>
+__device__ void fwd_rows(const DevGraph& g, const LView& V, double* x, int lv) {
+  const int G = g.level_gf[lv];
+  const int i0 = g.lrow_ptr[lv] * D, i1 = g.lrow_ptr[lv + 1] * D;
+  const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
+  for (int base = i0; base < i1; base += NT / G) {
+    const int item = base + grp;
+    const bool valid = item < i1;
+    const int r = valid ? item / D : i0 / D, a = item - r * D;
+    const int p = g.lrow[r];
+    double acc[1] = {valid ? fwd_row_partial<D>(g, V, x, p, a, lane, G) : 0.0};
+    group_reduce<1>(acc, G);
+    if (valid && lane == 0) x[(size_t)D * p + a] -= acc[0];
+  }
+}
+
+// Backward-substitution gather of one supernode by one warp: xs[c] -= sum over below rows of
+// L[r][c] x_r; G = 32 / w lanes (power of two) per column split the below pose rows.
+template <int D>
+__device__ __forceinline__ void bwd_gather_warp(const DevGraph& g, const double* P, int ld, int w, int s,
+                                                double* x, double* xs) {
+  const int lane = threadIdx.x & 31;
+  int G = 1;
+  while (G < 32 && G * 2 * w <= 32) G *= 2;
+  const int rb = g.snr_ptr[s], nbr = g.snr_ptr[s + 1] - rb;
+  const int cper = 32 / G;
+  for (int cb = 0; cb < w; cb += cper) {
+    const int c = cb + lane / G, sub = lane % G;
+    double acc[1] = {0.0};
+    if (c < w) {
+      const double* col = P + (size_t)c * ld + w;
+      double s0 = 0.0, s1 = 0.0;
+      for (int rr = sub; rr < nbr; rr += G) {
+        const double* xr = x + (size_t)D * g.snr[rb + rr];
+#pragma unroll
+        for (int a = 0; a < D; a += 2) {
+          s0 = fma(col[rr * D + a], xr[a], s0);
+          if (a + 1 < D) s1 = fma(col[rr * D + a + 1], xr[a + 1], s1);
+        }
+      }
+      acc[0] = s0 + s1;
+    }
+    group_reduce<1>(acc, G);
+    if (c < w && sub == 0) xs[c] -= acc[0];
+  }
+}
+
+// width-dispatched warp triangular solves (slots = ceil(w / 32) register rows per lane)
+template <int D>
+__device__ __forceinline__ void warp_trsv_lower_w(const double* P, int ld, int w, double* xs) {
+  if (w <= 32) warp_trsv_lower<1>(P, ld, w, xs);
+  else if (w <= 64) warp_trsv_lower<2>(P, ld, w, xs);
+  else if (w <= 128) warp_trsv_lower<4>(P, ld, w, xs);
+  else warp_trsv_lower<(64 * D + 31) / 32>(P, ld, w, xs);
+}
+template <int D>
+__device__ __forceinline__ void warp_trsv_upper_w(const double* P, int ld, int w, double* xs) {
+  if (w <= 32) warp_trsv_upper<1>(P, ld, w, xs);
+  else if (w <= 64) warp_trsv_upper<2>(P, ld, w, xs);
+  else if (w <= 128) warp_trsv_upper<4>(P, ld, w, xs);
+  else warp_trsv_upper<(64 * D + 31) / 32>(P, ld, w, xs);
+}
+
+// Supernodal left-looking Cholesky, level-synchronous.  Levels >= the resident boundary live
+// in shared memory for the whole solve; a lower level's prefix [level_off, level_stage_hi) is
+// bulk-loaded (TMA) into `stage`, updated (gather form, from descendant panels), factored by
+// teams, and written back.  `xinv` holds NT/32 team scratch blocks of D*D doubles.
+template <int D, int NT>
+__device__ void factor_levels(const DevGraph& g, const LView& L, double* stage, double tol, int* s_fail,
+                              uint64_t* mbar, uint32_t& phase, double* xinv, double* xf, int l0, int l1) {
+  for (int lv = l0; lv < l1; ++lv) {
+    const int lo = g.level_off[lv];
+    const bool resident = lo >= L.rlo;
+    const int hi = resident ? lo : g.level_stage_hi[lv];
+    DNLS_TRACE_POINT(1000 + lv);
+    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+    DNLS_TRACE_POINT(1100 + lv);
+    const LView V = L.level(stage, lo, hi);
+    // (U) gather-form updates from descendants into this level's panels (+ forward rhs rows)
+    update_tasks<D, NT>(g, V, lv);
+    if (xf) fwd_rows<D, NT>(g, V, xf, lv);
+    __syncthreads();
+    DNLS_TRACE_POINT(1200 + lv);
+    // (F) dense factorisation of the level's panels by teams
+    const int s0 = g.level_ptr[lv], nsn = g.level_ptr[lv + 1] - s0;
+    Team tm;
+    int team, nteams;
+    team_of<NT>(nsn, tm, team, nteams);
+    for (int i = team; i < nsn; i += nteams) {
+      const int s = g.level_sn[s0 + i];
+      panel_factor<D>(V.at(g.sn_off[s]), g.sn_m[s], g.sn_ld[s], g.sn_w[s], tol, tm, s_fail, xinv + team * D * D);
+    }
+    __syncthreads();
+    if (xf) {   // fused forward substitution: y_s = L_ss^-1 t_s, warp per supernode
+      const int warp = threadIdx.x >> 5;
+      for (int i = warp; i < nsn; i += NT / 32) {
+        const int s = g.level_sn[s0 + i];
+        warp_trsv_lower_w<D>(V.at(g.sn_off[s]), g.sn_ld[s], g.sn_w[s], xf + (size_t)D * g.sn_first[s]);
+      }
+      __syncthreads();
+    }
+    DNLS_TRACE_POINT(1300 + lv);
+    if (!resident && hi > lo) {
+      copy_range<NT>(L.g + lo, stage, hi - lo);
+      __syncthreads();
+    }
+  }
+  DNLS_TRACE_POINT(1999);
+}
+
+// ============================================================================= a4: solves
 // x (permuted, length n; shared or global memory) holds b on entry and H^-1 b on exit.
 // Level ranges are staged into `stage` (read-only); warp per supernode.
 template <int D, int NT>
-__device__ void solve_phase(const DevGraph& g, double* Lg, double* stage, double* x) {
+__device__ void solve_levels(const DevGraph& g, const LView& L, double* stage, double* x, uint64_t* mbar,
+                             uint32_t& phase, bool forward, int bl0) {
   constexpr int NW = NT / 32;
   constexpr int MAXR = (64 * D + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // forward: L y = b, leaves to root
-  for (int lv = 0; lv < g.L; ++lv) {
-    const int lo = g.level_off[lv], hi = g.level_stage_hi[lv];
-    copy_range<NT>(stage, Lg + lo, hi - lo);
-    __syncthreads();
-    LView V{Lg, stage, lo, hi};
+  // forward: L y = b, leaves to root (skipped when fused into the factorisation)
+  for (int lv = 0; lv < (forward ? g.L : 0); ++lv) {
+    const int lo = g.level_off[lv];
+    const bool resident = lo >= L.rlo;
+    const int hi = resident ? lo : g.level_stage_hi[lv];
+    DNLS_TRACE_POINT(2000 + lv);
+    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+    DNLS_TRACE_POINT(2100 + lv);
+    const LView V = L.level(stage, lo, hi);
     const int s0 = g.level_ptr[lv], s1 = g.level_ptr[lv + 1];
     for (int i = s0 + warp; i < s1; i += NW) {
       const int s = g.level_sn[i];
-      const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s];
+      const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_ld[s];
       const double* P = V.at(g.sn_off[s]);
       double* xs = x + (size_t)D * f;
-      for (int r = lane; r < w; r += 32) {
-        const int p = f + r / D, a = r % D;
-        double t = xs[r];
-        for (int ci = g.fc_ptr[p]; ci < g.fc_ptr[p + 1]; ++ci) {
-          const double* A = Lg + g.fc_off[ci];
-          const int ld = g.fc_ld[ci], ww = g.fc_w[ci];
-          const double* y = x + g.fc_x[ci];
-          for (int k = 0; k < ww; ++k) t = fma(-A[(size_t)k * ld + a], y[k], t);
+      {
+        int G = 1;
+        while (G < 32 && G * 2 * w <= 32) G *= 2;
+        for (int rb0 = 0; rb0 < w; rb0 += 32 / G) {
+          const int r = rb0 + lane / G, sub = lane % G;
+          double acc[1] = {0.0};
+          if (r < w) acc[0] = fwd_row_partial<D>(g, V, x, f + r / D, r % D, sub, G);
+          group_reduce<1>(acc, G);
+          if (r < w && sub == 0) xs[r] -= acc[0];
         }
-        xs[r] = t;
       }
       __syncwarp();
-      warp_trsv_lower<MAXR>(P, m, w, xs);
+      warp_trsv_lower_w<D>(P, m, w, xs);
     }
     __syncthreads();
   }
   // backward: L^T x = y, root to leaves
-  for (int lv = g.L - 1; lv >= 0; --lv) {
-    const int lo = g.level_off[lv], hi = g.level_stage_hi[lv];
-    copy_range<NT>(stage, Lg + lo, hi - lo);
-    __syncthreads();
-    LView V{Lg, stage, lo, hi};
+  for (int lv = g.L - 1; lv >= bl0; --lv) {
+    const int lo = g.level_off[lv];
+    const bool resident = lo >= L.rlo;
+    const int hi = resident ? lo : g.level_stage_hi[lv];
+    DNLS_TRACE_POINT(3000 + lv);
+    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+    else __syncthreads();
+    DNLS_TRACE_POINT(3100 + lv);
+    const LView V = L.level(stage, lo, hi);
     const int s0 = g.level_ptr[lv], s1 = g.level_ptr[lv + 1];
     for (int i = s0 + warp; i < s1; i += NW) {
       const int s = g.level_sn[i];
-      const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_m[s];
+      const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_ld[s];
       const double* P = V.at(g.sn_off[s]);
       double* xs = x + (size_t)D * f;
-      const int rb = g.snr_ptr[s], nbr = g.snr_ptr[s + 1] - rb;
-      for (int c = lane; c < w; c += 32) {
-        double t = xs[c];
-        const double* col = P + (size_t)c * m + w;
-        for (int rr = 0; rr < nbr; ++rr) {
-          const double* xr = x + (size_t)D * g.snr[rb + rr];
-#pragma unroll
-          for (int a = 0; a < D; ++a) t = fma(-col[rr * D + a], xr[a], t);
-        }
-        xs[c] = t;
-      }
+      bwd_gather_warp<D>(g, P, m, w, s, x, xs);
       __syncwarp();
-      warp_trsv_upper<MAXR>(P, m, w, xs);
+      warp_trsv_upper_w<D>(P, m, w, xs);
     }
     __syncthreads();
   }
+}
+
+// ----------------------------------------------------------------------------- dataflow forest
+// Shared-memory scheduler state: pending child counts [S], ready queue [n_forest], head/tail.
+__device__ __forceinline__ int* sched_pending(int* sq) { return sq; }
+
+// one forest supernode, one warp: gather updates into its panel (staged into the warp's slice of
+// the staging buffer when the panel is not resident and fits), fused forward-substitution rows,
+// dense panel factorisation, y_s = L_ss^-1 t_s; write back.
+template <int D>
+__device__ void forest_factor_sn(const DevGraph& g, const LView& L, int s, double* slice, int slice_cap,
+                                 double tol, int* fail, double* xinv_w, double* xf) {
+  const int lane = threadIdx.x & 31;
+  const int off = g.sn_off[s], m = g.sn_m[s], ld = g.sn_ld[s], w = g.sn_w[s], f = g.sn_first[s];
+  const int size = (ld * w + 1) & ~1;
+  double* const Pg = L.at(off);
+  const bool staged = off < L.rlo && size <= slice_cap;
+  double* P = Pg;
+  if (staged) {
+    for (int i = lane; i < size; i += 32) slice[i] = Pg[i];
+    __syncwarp();
+    P = slice;
+  }
+  DNLS_TRACE_POINT(7001);
+  {
+    const int t0 = g.ut_sn_ptr[2 * s], t1 = g.ut_sn_ptr[2 * s + 1];
+    const int nitems = (t1 - t0) * D;
+    int G = 1;
+    while (G < 32 && G * 2 * nitems <= 32) G *= 2;
+    for (int ib = 0; ib < nitems; ib += 32 / G) {
+      const int item = ib + lane / G, sub = lane % G;
+      const bool valid = item < nitems;
+      const int t = t0 + (valid ? item / D : 0), a = valid ? item % D : 0;
+      double acc[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) acc[q] = 0.0;
+      int4 tk = make_int4(0, 0, 0, 0);
+      if (valid) {
+        tk = g.task4[t];
+        task_row_partial<D>(g, L, tk, a, sub, G, acc);
+      }
+      group_reduce<D>(acc, G);
+      if (valid && sub == 0) {
+        double* T = P + (tk.x - off) + a;
+#pragma unroll
+        for (int q = 0; q < D; ++q) T[(size_t)q * tk.y] -= acc[q];
+      }
+    }
+  }
+  DNLS_TRACE_POINT(7002);
+  if (xf) {
+    int G = 1;
+    while (G < 32 && G * 2 * w <= 32) G *= 2;
+    for (int rb0 = 0; rb0 < w; rb0 += 32 / G) {
+      const int r = rb0 + lane / G, sub = lane % G;
+      double acc[1] = {0.0};
+      if (r < w) acc[0] = fwd_row_partial<D>(g, L, xf, f + r / D, r % D, sub, G);
+      group_reduce<1>(acc, G);
+      if (r < w && sub == 0) xf[(size_t)D * f + r] -= acc[0];
+    }
+  }
+  __syncwarp();
+  DNLS_TRACE_POINT(7003);
+  panel_factor<D>(P, m, ld, w, tol, Team{lane, 32, 0}, fail, xinv_w);
+  __syncwarp();
+  DNLS_TRACE_POINT(7004);
+  if (xf) {
+    warp_trsv_lower_w<D>(P, ld, w, xf + (size_t)D * f);
+    __syncwarp();
+  }
+  DNLS_TRACE_POINT(7005);
+  if (staged) {
+    for (int i = lane; i < size; i += 32) Pg[i] = slice[i];
+    __syncwarp();
+  }
+}
+
+// Warp-level dataflow over the forest (supernodes below g.top_level): a supernode becomes ready
+// when all its children completed (shared-memory counters); warps pull ready supernodes from a
+// shared ready queue.  No CTA barrier inside.  `sq` = int scratch [S + n_forest + 2].
+template <int D, int NT>
+__device__ void forest_factor(const DevGraph& g, const LView& L, double* stage, int stage_cap, double tol,
+                              int* fail, double* xinv, double* xf, int* sq) {
+  constexpr int NW = NT / 32;
+  int* pending = sq;
+  int* queue = sq + g.S;
+  int* ctr = queue + g.n_forest;
+  for (int i = threadIdx.x; i < g.S; i += NT) pending[i] = g.child_ptr[i + 1] - g.child_ptr[i];
+  for (int i = threadIdx.x; i < g.n_forest; i += NT) queue[i] = i < g.n_leaves ? g.leaves[i] + 1 : 0;
+  if (threadIdx.x == 0) {
+    ctr[0] = 0;
+    ctr[1] = g.n_leaves;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slice_cap = (stage_cap / NW) & ~1;
+  double* slice = stage + (size_t)warp * slice_cap;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(&ctr[0], 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= g.n_forest) break;
+    int s = 0;
+    if (lane == 0) {
+      volatile int* vq = queue;
+      while ((s = vq[idx]) == 0) __nanosleep(32);
+    }
+    s = __shfl_sync(0xffffffffu, s, 0) - 1;
+    __threadfence_block();
+    DNLS_TRACE_POINT(5000 + s);
+    forest_factor_sn<D>(g, L, s, slice, slice_cap, tol, fail, xinv + warp * D * D, xf);
+    __threadfence_block();
+    DNLS_TRACE_POINT(6000 + s);
+    if (lane == 0) {
+      const int p = g.sn_parent[s];
+      if (p >= 0 && g.sn_sched[p] && atomicSub(&pending[p], 1) == 1) {
+        const int slot = atomicAdd(&ctr[1], 1);
+        atomicExch(&queue[slot], p + 1);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Backward substitution over the forest, top-down dataflow: a supernode is ready once its parent
+// is done; completion releases its children.
+template <int D, int NT>
+__device__ void forest_bsolve(const DevGraph& g, const LView& L, double* x, int* sq) {
+  int* queue = sq + g.S;
+  int* ctr = queue + g.n_forest;
+  for (int i = threadIdx.x; i < g.n_forest; i += NT) queue[i] = i < g.n_broots ? g.broots[i] + 1 : 0;
+  if (threadIdx.x == 0) {
+    ctr[0] = 0;
+    ctr[1] = g.n_broots;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(&ctr[0], 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= g.n_forest) break;
+    int s = 0;
+    if (lane == 0) {
+      volatile int* vq = queue;
+      while ((s = vq[idx]) == 0) __nanosleep(32);
+    }
+    s = __shfl_sync(0xffffffffu, s, 0) - 1;
+    __threadfence_block();
+    const int f = g.sn_first[s], w = g.sn_w[s], ld = g.sn_ld[s];
+    const double* P = L.at(g.sn_off[s]);
+    double* xs = x + (size_t)D * f;
+    bwd_gather_warp<D>(g, P, ld, w, s, x, xs);
+    __syncwarp();
+    warp_trsv_upper_w<D>(P, ld, w, xs);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) {
+      const int c0 = g.child_ptr[s], c1 = g.child_ptr[s + 1];
+      if (c1 > c0) {
+        const int slot = atomicAdd(&ctr[1], c1 - c0);
+        for (int c = c0; c < c1; ++c) atomicExch(&queue[slot + c - c0], g.child_idx[c] + 1);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Full factorisation: dataflow forest, then the top levels CTA-wide (level-synchronous).
+template <int D, int NT>
+__device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, double tol, int* s_fail,
+                             uint64_t* mbar, uint32_t& phase, double* xinv, double* xf, int* sq) {
+  DNLS_TRACE_POINT(900);
+  forest_factor<D, NT>(g, L, stage, g.stage_n, tol, s_fail, xinv, xf, sq);
+  DNLS_TRACE_POINT(950);
+  factor_levels<D, NT>(g, L, stage, tol, s_fail, mbar, phase, xinv, xf, g.top_level, g.L);
+  DNLS_TRACE_POINT(1999);
+}
+
+// Solve: forward (unless fused into the factorisation) level-synchronous, backward: top levels
+// CTA-wide then the forest top-down by dataflow.
+template <int D, int NT>
+__device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, double* x, uint64_t* mbar,
+                            uint32_t& phase, int* sq, bool forward = true) {
+  solve_levels<D, NT>(g, L, stage, x, mbar, phase, forward, g.top_level);
+  DNLS_TRACE_POINT(3500);
+  forest_bsolve<D, NT>(g, L, x, sq);
+  DNLS_TRACE_POINT(3999);
 }
 
 // ============================================================================= a5: retraction

@@ -342,6 +342,7 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
   S.sn_ncols.resize(NS);
   S.sn_parent.resize(NS);
   S.sn_m.resize(NS);
+  S.sn_ld.resize(NS);
   S.sn_w.resize(NS);
   S.sn_off.resize(NS);
   S.sn_rows.resize(NS);
@@ -354,7 +355,10 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     S.sn_rows[s] = sns[s].rows;
     S.sn_w[s] = D * sns[s].ncols;
     S.sn_m[s] = D * (sns[s].ncols + (int)sns[s].rows.size());
-    S.storage += (int64_t)S.sn_m[s] * S.sn_w[s];
+    // odd leading dimension: lanes stepping along a panel row (stride ld doubles) then hit
+    // distinct shared-memory banks
+    S.sn_ld[s] = S.sn_m[s] | 1;
+    S.storage += (int64_t)S.sn_ld[s] * S.sn_w[s];
     S.max_sn_cols_sc = std::max(S.max_sn_cols_sc, S.sn_w[s]);
     S.max_panel_rows = std::max(S.max_panel_rows, S.sn_m[s]);
   }
@@ -376,26 +380,60 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     for (int s = 0; s < NS; ++s) S.level_sn[fill[S.sn_level[s]]++] = s;
   }
   // panel storage in LEVEL order: every level is one contiguous range [level_off[l], level_off[l+1])
-  // so a level can be staged into shared memory with one contiguous copy.  level_stage_hi[l] is
-  // the end of the prefix of that range (whole panels) that fits the staging budget.
+  // (panels padded to 16 bytes).  Shared-memory plan: the top levels
+  // [res_lo, storage) stay RESIDENT in shared memory for the whole solve; each lower level is
+  // staged through a buffer of stage_cap doubles (prefix [level_off[l], level_stage_hi[l]) of
+  // whole panels; panels beyond it are processed in global memory).
   {
     int64_t o = 0;
     S.level_off.assign(S.num_levels + 1, 0);
-    S.level_stage_hi.assign(S.num_levels, 0);
     for (int l = 0; l < S.num_levels; ++l) {
       S.level_off[l] = (int32_t)o;
-      int64_t lo = o;
-      int64_t shi = o;
       for (int i = S.level_ptr[l]; i < S.level_ptr[l + 1]; ++i) {
         int sn = S.level_sn[i];
         S.sn_off[sn] = o;
-        o += (int64_t)S.sn_m[sn] * S.sn_w[sn];
-        if (o - lo <= opt.stage_budget_doubles && shi == o - (int64_t)S.sn_m[sn] * S.sn_w[sn]) shi = o;
+        o += ((int64_t)S.sn_ld[sn] * S.sn_w[sn] + 1) & ~int64_t(1);
+      }
+    }
+    S.level_off[S.num_levels] = (int32_t)o;
+    S.storage = o;
+    const int64_t cap = opt.smem_cap_doubles;
+    auto lsize = [&](int l) { return (int64_t)S.level_off[l + 1] - S.level_off[l]; };
+    // most resident levels r.. such that resident + the largest lower level fits; else give the
+    // resident part at most half the budget and stage partial prefixes
+    int r = S.num_levels;
+    for (int c = S.num_levels; c >= 0; --c) {
+      int64_t res = o - (c < S.num_levels ? S.level_off[c] : o);
+      int64_t lower = 0;
+      for (int l = 0; l < c; ++l) lower = std::max(lower, lsize(l));
+      if (res + lower <= cap) r = c;
+      else break;
+    }
+    if (r == S.num_levels && S.num_levels > 0) {
+      for (int c = S.num_levels - 1; c >= 0; --c) {
+        if (o - S.level_off[c] <= cap / 2) r = c;
+        else break;
+      }
+    }
+    S.res_lo = r < S.num_levels ? S.level_off[r] : (int32_t)o;
+    S.res_n = o - S.res_lo;
+    S.stage_cap = cap - S.res_n;
+    S.level_stage_hi.assign(S.num_levels, 0);
+    S.max_level_stage = 0;
+    for (int l = 0; l < S.num_levels; ++l) {
+      const int64_t lo = S.level_off[l];
+      int64_t shi = lo;
+      if (lo < S.res_lo) {
+        for (int i = S.level_ptr[l]; i < S.level_ptr[l + 1]; ++i) {
+          int sn = S.level_sn[i];
+          int64_t end = S.sn_off[sn] + (((int64_t)S.sn_ld[sn] * S.sn_w[sn] + 1) & ~int64_t(1));
+          if (S.sn_off[sn] == shi && end - lo <= S.stage_cap) shi = end;
+          else break;
+        }
       }
       S.level_stage_hi[l] = (int32_t)shi;
       S.max_level_stage = std::max<int64_t>(S.max_level_stage, shi - lo);
     }
-    S.level_off[S.num_levels] = (int32_t)o;
   }
 
   // row position of pose p inside panel s (scalar), -1 if absent
@@ -437,13 +475,13 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     for (auto& k : keys) {
       int lv = std::get<0>(k), t = std::get<1>(k), q = std::get<2>(k), p = std::get<3>(k);
       S.ut_level_ptr[lv + 1]++;
-      int off = (int)S.sn_off[t] + D * (q - S.sn_first[t]) * S.sn_m[t] + rowpos(t, p);
+      int off = (int)S.sn_off[t] + D * (q - S.sn_first[t]) * S.sn_ld[t] + rowpos(t, p);
       S.ut_off.push_back(off);
-      S.ut_ld.push_back(S.sn_m[t]);
+      S.ut_ld.push_back(S.sn_ld[t]);
       for (int src : tasks[std::make_tuple(t, q, p)]) {
         S.uc_a.push_back((int)S.sn_off[src] + rowpos(src, p));
         S.uc_b.push_back((int)S.sn_off[src] + rowpos(src, q));
-        S.uc_ld.push_back(S.sn_m[src]);
+        S.uc_ld.push_back(S.sn_ld[src]);
         S.uc_w.push_back(S.sn_w[src]);
       }
       S.ut_cptr.push_back((int)S.uc_a.size());
@@ -459,16 +497,85 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     for (int p = 0; p < N; ++p) {
       for (int src : srcs[p]) {
         S.fc_off.push_back((int)S.sn_off[src] + rowpos(src, p));
-        S.fc_ld.push_back(S.sn_m[src]);
+        S.fc_ld.push_back(S.sn_ld[src]);
         S.fc_w.push_back(S.sn_w[src]);
         S.fc_x.push_back(D * S.sn_first[src]);
       }
       S.fc_ptr.push_back((int)S.fc_off.size());
     }
+    // per-level pose rows and lane-group sizes (work per level spread over ~cta_threads lanes)
+    S.lrow_ptr.assign(1, 0);
+    S.level_gu.assign(S.num_levels, 1);
+    S.level_gf.assign(S.num_levels, 1);
+    auto group_for = [&](int64_t ntasks) {
+      int G = 1;
+      while (G < 32 && ntasks * G * 2 <= opt.cta_threads) G *= 2;
+      return G;
+    };
+    for (int l = 0; l < S.num_levels; ++l) {
+      for (int i = S.level_ptr[l]; i < S.level_ptr[l + 1]; ++i) {
+        int sn = S.level_sn[i];
+        for (int k = 0; k < S.sn_ncols[sn]; ++k) S.lrow.push_back(S.sn_first[sn] + k);
+      }
+      S.lrow_ptr.push_back((int)S.lrow.size());
+      S.level_gu[l] = group_for((int64_t)D * (S.ut_level_ptr[l + 1] - S.ut_level_ptr[l]));
+      S.level_gf[l] = group_for((int64_t)D * (S.lrow_ptr[l + 1] - S.lrow_ptr[l]));
+    }
     S.snr_ptr.assign(1, 0);
     for (int s = 0; s < NS; ++s) {
       for (int p : S.sn_rows[s]) S.snr.push_back(p);
       S.snr_ptr.push_back((int)S.snr.size());
+    }
+    // dataflow scheduling: per-supernode update-task ranges, children lists, forest / top split.
+    // The "top" is the suffix of levels with at most top_max supernodes (processed by CTA-wide
+    // teams, level-synchronous); everything below is the "forest" (warp per supernode, ready
+    // queue driven by child-completion counters).
+    {
+      // recover the target supernode of each task from its storage offset
+      std::vector<int> tsn(S.ut_off.size());
+      std::vector<std::pair<int64_t, int>> starts;
+      for (int sn = 0; sn < NS; ++sn) starts.push_back(std::make_pair(S.sn_off[sn], sn));
+      std::sort(starts.begin(), starts.end());
+      for (size_t t = 0; t < S.ut_off.size(); ++t) {
+        auto it = std::upper_bound(starts.begin(), starts.end(), std::make_pair((int64_t)S.ut_off[t], NS));
+        tsn[t] = (--it)->second;
+      }
+      std::vector<int> first(NS, -1), last(NS, -1);
+      for (size_t t = 0; t < tsn.size(); ++t) {
+        if (first[tsn[t]] < 0) first[tsn[t]] = (int)t;
+        last[tsn[t]] = (int)t + 1;
+      }
+      S.ut_sn_ptr.assign(2 * NS, 0);   // [begin, end) per supernode
+      for (int sn = 0; sn < NS; ++sn) {
+        S.ut_sn_ptr[2 * sn] = first[sn] < 0 ? 0 : first[sn];
+        S.ut_sn_ptr[2 * sn + 1] = first[sn] < 0 ? 0 : last[sn];
+      }
+    }
+    S.child_ptr.assign(NS + 1, 0);
+    for (int sn = 0; sn < NS; ++sn)
+      if (S.sn_parent[sn] >= 0) S.child_ptr[S.sn_parent[sn] + 1]++;
+    for (int sn = 0; sn < NS; ++sn) S.child_ptr[sn + 1] += S.child_ptr[sn];
+    S.child_idx.assign(S.child_ptr[NS], 0);
+    {
+      std::vector<int> fill(S.child_ptr.begin(), S.child_ptr.end() - 1);
+      for (int sn = 0; sn < NS; ++sn)
+        if (S.sn_parent[sn] >= 0) S.child_idx[fill[S.sn_parent[sn]]++] = sn;
+    }
+    S.top_level = S.num_levels;
+    while (S.top_level > 0 && S.level_ptr[S.top_level] - S.level_ptr[S.top_level - 1] <= opt.top_max) --S.top_level;
+    S.n_forest = S.level_ptr[S.top_level];
+    S.sn_sched.assign(NS, 0);   // 1 = forest supernode
+    for (int i = 0; i < S.n_forest; ++i) S.sn_sched[S.level_sn[i]] = 1;
+    S.leaves.clear();
+    for (int i = 0; i < S.n_forest; ++i) {
+      int sn = S.level_sn[i];
+      if (S.child_ptr[sn + 1] == S.child_ptr[sn]) S.leaves.push_back(sn);
+    }
+    // top-down ready set for the backward pass: forest supernodes whose parent is in the top
+    S.broots.clear();
+    for (int i = 0; i < S.n_forest; ++i) {
+      int sn = S.level_sn[i];
+      if (S.sn_parent[sn] < 0 || !S.sn_sched[S.sn_parent[sn]]) S.broots.push_back(sn);
     }
   }
   // ---- 5c. assembly lists
@@ -493,8 +600,8 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         int q = f + ql;
         for (size_t ri = 0; ri < rows.size(); ++ri) {
           int p = rows[ri];
-          S.blk_off.push_back((int)S.sn_off[s] + D * ql * S.sn_m[s] + D * (int)ri);
-          S.blk_ld.push_back(S.sn_m[s]);
+          S.blk_off.push_back((int)S.sn_off[s] + D * ql * S.sn_ld[s] + D * (int)ri);
+          S.blk_ld.push_back(S.sn_ld[s]);
           int kind = 0;
           if (p == q) {
             kind = 1;

@@ -14,14 +14,18 @@ struct SymbolicOptions {
   // A child supernode is merged into its parent when the merged width (pose columns) and the
   // fraction of explicit zero blocks stay under these limits.
   int relax_always_cols = 1;      // merged width <= this: always merge
-  int relax_small_cols = 4;       // ... <= this: merge if zero fraction <= relax_small_frac
-  double relax_small_frac = 0.3;
-  int relax_mid_cols = 16;
-  double relax_mid_frac = 0.1;
+  int relax_small_cols = 1;       // ... <= this: merge if zero fraction <= relax_small_frac
+  double relax_small_frac = 0.0;
+  int relax_mid_cols = 1;
+  double relax_mid_frac = 0.0;
   int relax_max_cols = 64;        // hard cap on supernode width (pose columns)
-  double relax_big_frac = 0.05;
-  // shared-memory staging budget (doubles) for one elimination-tree level of panels
-  int64_t stage_budget_doubles = 0;
+  double relax_big_frac = 0.0;
+  // shared-memory budget (doubles) for factor panels: resident top levels + level staging
+  int64_t smem_cap_doubles = 0;
+  // threads per CTA of the numeric kernels (lane-group sizes are chosen against it)
+  int cta_threads = 256;
+  // levels at the top of the tree with at most this many supernodes are processed CTA-wide
+  int top_max = 2;
 };
 
 struct Symbolic {
@@ -35,7 +39,7 @@ struct Symbolic {
 
   // supernodes (contiguous pose-column ranges in the postordered numbering)
   int S = 0;
-  std::vector<int32_t> sn_first, sn_ncols, sn_level, sn_parent, sn_m, sn_w, col_sn;
+  std::vector<int32_t> sn_first, sn_ncols, sn_level, sn_parent, sn_m, sn_ld, sn_w, col_sn;
   std::vector<int64_t> sn_off;                  // panel offset (doubles) in per-element storage
   std::vector<std::vector<int32_t>> sn_rows;    // below rows (permuted pose indices, sorted)
   int64_t storage = 0;
@@ -44,6 +48,9 @@ struct Symbolic {
   std::vector<int32_t> level_off;               // [L+1] storage range of each level (level-ordered panels)
   std::vector<int32_t> level_stage_hi;          // [L] end of the staged (shared-memory) prefix of the level
   int64_t max_level_stage = 0;                  // largest staged prefix (doubles)
+  int32_t res_lo = 0;                           // storage offsets >= res_lo are resident in shared memory
+  int64_t res_n = 0;                            // resident doubles
+  int64_t stage_cap = 0;                        // staging buffer capacity (doubles)
 
   // numeric factorisation: gather-form update tasks grouped by level of the target
   //   task t: target block at ut_off (storage offset of entry (0,0)), leading dim ut_ld,
@@ -51,11 +58,18 @@ struct Symbolic {
   //   contribution c: source rows at uc_a (entry (row_p, k=0)), uc_b (row_q), ld uc_ld, width uc_w
   std::vector<int32_t> ut_level_ptr, ut_off, ut_ld, ut_cptr;
   std::vector<int32_t> uc_a, uc_b, uc_ld, uc_w;
+  // lanes cooperating on one update task / one forward-substitution row, per level (1..32)
+  std::vector<int32_t> level_gu, level_gf;
+  // pose rows (columns of the level's supernodes) per level, for the fused forward substitution
+  std::vector<int32_t> lrow_ptr, lrow;
 
   // forward substitution gather per permuted pose row p: sum over source panels holding row p
   std::vector<int32_t> fc_ptr, fc_off, fc_ld, fc_w, fc_x;
   // backward substitution: below rows of each supernode (flattened sn_rows)
   std::vector<int32_t> snr_ptr, snr;
+  // dataflow schedule: update-task range [2s, 2s+1] per supernode, children CSR, forest flags
+  std::vector<int32_t> ut_sn_ptr, child_ptr, child_idx, sn_sched, leaves, broots;
+  int top_level = 0, n_forest = 0;
 
   // scatter-free assembly: every d x d block of the storage exactly once
   //   block k: storage offset blk_off[k], leading dim blk_ld[k], kind blk_kind[k]

@@ -102,6 +102,7 @@ def brute_force(d, N, edges, prior_vars, Z, Zp, w, wp, Tref):
             out.append(wp[p] * _vee_log(np.linalg.inv(Zp[p]) @ T[k], d))
         return np.concatenate(out)
     sol = least_squares(fun, np.zeros(N * d), method="trf", xtol=1e-15, ftol=1e-15, gtol=1e-15, max_nfev=2000)
+    sol = least_squares(fun, sol.x, method="lm", xtol=1e-15, ftol=1e-15, gtol=1e-15, max_nfev=4000)  # polish
     x = sol.x.reshape(N, d)
     return np.stack([Tref[k] @ expm(_hat(x[k], d)) for k in range(N)])
 
@@ -113,6 +114,7 @@ def brute_force(d, N, edges, prior_vars, Z, Zp, w, wp, Tref):
     (lie.SE2, [(0, 1), (1, 2), (2, 3), (0, 3), (1, 3)]),
 ])
 def test_converged_gn_matches_brute_force(G, edges):
+    rng = np.random.default_rng(len(edges) * 10 + G.d)
     d = G.d
     N = 1 + max(max(e) for e in edges)
     edges = np.array(edges)
@@ -125,8 +127,22 @@ def test_converged_gn_matches_brute_force(G, edges):
     prob = nls.PGOProblem(G, N, edges, [0], Z, Zp, w, wp)
     res = nls.gauss_newton(prob, T0, nls.Options(max_iterations=30))
     Tb = brute_force(d, N, edges, [0], Z, Zp, w, wp, T0)
-    np.testing.assert_allclose(res.x, Tb, atol=1e-10)
+    # the independent solver stops on its own tolerances, so poses agree to ~1e-8; the objective
+    # at both optima agrees to rounding, and GN's iterate is stationary for the independent
+    # (logm/expm) residuals: central-difference gradient ~ 0
+    np.testing.assert_allclose(res.x, Tb, atol=1e-8)
     assert abs(res.objective - prob.objective(Tb)) <= 1e-12 * max(1e-12, res.objective) + 1e-20
+
+    def S_ind(x):
+        x = x.reshape(N, d)
+        T = [res.x[k] @ expm(_hat(x[k], d)) for k in range(N)]
+        r = [w[e] * _vee_log(np.linalg.inv(Z[e]) @ np.linalg.inv(T[i]) @ T[j], d) for e, (i, j) in enumerate(edges)]
+        r.append(wp[0] * _vee_log(np.linalg.inv(Zp[0]) @ T[0], d))
+        r = np.concatenate(r)
+        return 0.5 * float(r @ r)
+    h = 1e-6
+    grad = np.array([(S_ind(h * e) - S_ind(-h * e)) / (2 * h) for e in np.eye(N * d)])
+    assert np.max(np.abs(grad)) <= 1e-8 * max(1.0, np.sqrt(res.objective))
 
 
 # ---------------------------------------------------------------- invariants
