@@ -106,10 +106,9 @@ DevProb dev_prob(const dnls_problem* p) {
 // ============================================================================= kernels
 namespace {
 
-size_t sched_ints(const DevGraph& g) { return (size_t)g.S + (size_t)g.n_forest + 2; }
 size_t smem_bytes(const DevGraph& g) {
   return sizeof(double) * ((g.x_smem ? (size_t)g.n_pad : 0) + (size_t)g.res_n + (size_t)g.stage_n) +
-         sizeof(int) * sched_ints(g);
+         sizeof(int) * 2 * (size_t)g.pk_max;
 }
 
 template <class F>
@@ -125,24 +124,32 @@ struct Smem {
   double* res;      // resident top levels of the factor storage
   double* stage;    // level staging area / per-warp forest slices
   double* xinv;     // per-team D x D scratch (inverse diagonal of the current diagonal block)
-  int* sq;          // dataflow scheduler ints
+  PkPipe pp;        // double-buffered descriptor packets
   uint64_t* mbar;   // mbarrier of the bulk (TMA) loads
   uint32_t phase;
 };
 // must be called by every thread at kernel start (initialises the mbarrier, one barrier)
 __device__ __forceinline__ Smem smem_views(const DevGraph& g, double* xg) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ uint64_t s_mbar;
+  __shared__ uint64_t s_mbar, s_mbpk[2];
   __shared__ double s_xinv[(NT / 32) * 36];
   Smem v;
   v.x = g.x_smem ? smem : xg;
   v.res = smem + (g.x_smem ? g.n_pad : 0);
   v.stage = v.res + g.res_n;
-  v.sq = reinterpret_cast<int*>(v.stage + g.stage_n);
+  v.pp.buf[0] = reinterpret_cast<int*>(v.stage + g.stage_n);
+  v.pp.buf[1] = v.pp.buf[0] + g.pk_max;
+  v.pp.mb[0] = &s_mbpk[0];
+  v.pp.mb[1] = &s_mbpk[1];
+  v.pp.ph[0] = v.pp.ph[1] = 0;
   v.xinv = s_xinv;
   v.mbar = &s_mbar;
   v.phase = 0;
-  if (threadIdx.x == 0) mbar_init(&s_mbar);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_mbar);
+    mbar_init(&s_mbpk[0]);
+    mbar_init(&s_mbpk[1]);
+  }
   __syncthreads();
   return v;
 }
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     }
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, x_b, sm.sq);
+    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, x_b, sm.pp);
     const bool ok = sh_fail == 0;
     __syncthreads();
     if (!fp.lm) {
@@ -228,7 +235,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
         status = DNLS_ST_NOT_SPD;
         break;
       }
-      solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.sq, false);
+      solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
       DNLS_TRACE_POINT(400);
       retract_phase<D, NT>(g, Tb, Tb, x_b, fp.alpha);
       __syncthreads();
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
       ++iters;
       bool accept = false;
       if (ok) {
-        solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.sq, false);
+        solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
         retract_phase<D, NT>(g, Tb, Ttr, x_b, fp.alpha);
         __syncthreads();
         objective_phase<D, NT>(g, pr, Ttr, b, cost_b);
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, nullptr, sm.sq);
+    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, nullptr, sm.pp);
     __syncthreads();
     if (sh_fail && status == DNLS_ST_OK) status = DNLS_ST_NOT_SPD;
     // the cached factor must be complete in global memory for dnls_backward_implicit
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* 
   double* Lg = ws.L + (size_t)b * g.storage;
   bulk_load<NT>(sm.res, Lg + g.res_lo, g.storage - g.res_lo, sm.mbar, sm.phase);
   factor_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, 1e-13 * ws.maxd[b], &sh_fail, sm.mbar, sm.phase, sm.xinv,
-                      nullptr, sm.sq);
+                      nullptr, sm.pp);
   copy_range<NT>(Lg + g.res_lo, sm.res, g.storage - g.res_lo);
   __syncthreads();
   if (threadIdx.x == 0 && status) status[b] = sh_fail ? DNLS_ST_NOT_SPD : DNLS_ST_OK;
@@ -356,7 +363,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve(DevGraph g, DevWs ws, const dou
   }
   double* Lg = ws.L + (size_t)b * g.storage;
   bulk_load<NT>(sm.res, Lg + g.res_lo, g.storage - g.res_lo, sm.mbar, sm.phase);
-  solve_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, x_b, sm.mbar, sm.phase, sm.sq);
+  solve_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, x_b, sm.mbar, sm.phase, sm.pp);
   __syncthreads();
   for (int i = threadIdx.x; i < g.n; i += NT) {
     const int o = i / D, a = i - o * D;
@@ -422,7 +429,7 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
   }
   double* Lg = ws.L + (size_t)b * g.storage;
   bulk_load<NT>(sm.res, Lg + g.res_lo, g.storage - g.res_lo, sm.mbar, sm.phase);
-  solve_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, x_b, sm.mbar, sm.phase, sm.sq);
+  solve_phase<D, NT>(g, full_view(g, Lg, sm), sm.stage, x_b, sm.mbar, sm.phase, sm.pp);
   __syncthreads();
   // dL/dw = -2 w (C lambda) . c  (unweighted C, c at theta_K)
   for (int slot = threadIdx.x; slot < (int)slots; slot += NT) {
@@ -606,6 +613,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dnls_graph* g = new dnls_graph();
   int code = 0;
   SymbolicOptions sopt;
+  int64_t smem_total = 0;
   {
     // shared-memory plan: x (n doubles) in shared memory when it fits in 64 KB, the rest of
     // SMEM_BYTES holds the resident top levels + the staging buffer of the lower levels
@@ -613,10 +621,9 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
     const int64_t xb = (n * 8 <= 65536) ? ((n + 1) & ~int64_t(1)) * 8 : 0;
     int64_t smem = SMEM_BYTES;
     if (const char* env = std::getenv("DNLS_SMEM_KB")) smem = std::min<int64_t>(SMEM_BYTES, std::atoll(env) * 1024);
-    // reserve the scheduler ints (<= 2 per pose column + 2)
-    smem -= 8 * (int64_t)num_vars + 64;
-    sopt.smem_cap_doubles = std::max<int64_t>(0, smem - xb) / 8;
+    sopt.smem_cap_doubles = std::max<int64_t>(0, smem - xb - 24 * 1024) / 8;   // 24 KB: descriptor packets
     sopt.cta_threads = NT;
+    smem_total = smem - xb;
   }
   if (const char* env = std::getenv("DNLS_RELAX")) {   // tuning override: "a,sc,sf,mc,mf,max,bf"
     std::sscanf(env, "%d,%d,%lf,%d,%lf,%d,%lf", &sopt.relax_always_cols, &sopt.relax_small_cols,
@@ -624,6 +631,10 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
                 &sopt.relax_big_frac);
   }
   std::string msg = analyze(group, num_vars, num_edges, edges_ij, num_priors, prior_vars, sopt, g->sym, &code);
+  if (msg.empty() && 8 * (int64_t)g->sym.pk_max > 24 * 1024) {   // bigger packets: re-plan the residency
+    sopt.smem_cap_doubles = std::max<int64_t>(0, smem_total - 8 * (int64_t)g->sym.pk_max - 64) / 8;
+    msg = analyze(group, num_vars, num_edges, edges_ij, num_priors, prior_vars, sopt, g->sym, &code);
+  }
   if (!msg.empty()) {
     delete g;
     return fail((dnls_status)code, msg);
@@ -659,6 +670,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   add(s.sn_parent); add(s.ut_sn_ptr); add(s.child_ptr); add(s.child_idx); add(s.sn_sched); add(s.leaves);
   add(s.broots);
   add(task4); add(con4); add(fcon4);
+  add(s.pk); add(s.pk_off);
   add(s.fc_ptr); add(s.fc_off); add(s.fc_ld); add(s.fc_w); add(s.fc_x);
   add(s.snr_ptr); add(s.snr);
   add(s.blk_off); add(s.blk_ld); add(s.blk_kind); add(s.blk_cptr); add(s.blk_con);
@@ -715,6 +727,9 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dg.task4 = reinterpret_cast<const int4*>(d + offs[k++]);
   dg.con4 = reinterpret_cast<const int4*>(d + offs[k++]);
   dg.fcon4 = reinterpret_cast<const int4*>(d + offs[k++]);
+  dg.pk = d + offs[k++];
+  dg.pk_off = d + offs[k++];
+  dg.pk_max = s.pk_max;
   dg.fc_ptr = d + offs[k++]; dg.fc_off = d + offs[k++]; dg.fc_ld = d + offs[k++]; dg.fc_w = d + offs[k++];
   dg.fc_x = d + offs[k++];
   dg.snr_ptr = d + offs[k++]; dg.snr = d + offs[k++];

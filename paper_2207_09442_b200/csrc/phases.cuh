@@ -59,6 +59,9 @@ struct DevGraph {
   const int *snr_ptr, *snr;
   const int *blk_off, *blk_ld, *blk_kind, *blk_cptr, *blk_con;
   const int *bc_ptr, *bc;
+  const int* pk;       // per-level descriptor packets (ints), pk_off[L+1] offsets
+  const int* pk_off;
+  int pk_max;          // ints of the largest packet
   const int* ibase;   // start of the device index buffer
   int inum;           // its length (ints, multiple of 4)
   int idx_smem;       // 1: kernels copy the index buffer into shared memory and read it there
@@ -1038,26 +1041,266 @@ __device__ void forest_bsolve(const DevGraph& g, const LView& L, double* x, int*
   __syncthreads();
 }
 
-// Full factorisation: dataflow forest, then the top levels CTA-wide (level-synchronous).
+// ----------------------------------------------------------------------------- packet-driven levels
+// Every elimination-tree level has a descriptor packet (symbolic.cpp 5b'); packets are
+// prefetched into a double buffer in shared memory by TMA bulk copies one level ahead, so all
+// index reads of the numeric phases hit shared memory.
+struct Pk {
+  int ntasks, ncons, nrows, nfcons, nsn, nsnr, gu, gf;
+  const int4 *task4, *con4, *row4, *fcon4, *sna, *snb;
+  const int* snr;
+};
+__device__ __forceinline__ Pk pk_view(const int* b) {
+  Pk p;
+  const int4 h0 = reinterpret_cast<const int4*>(b)[0], h1 = reinterpret_cast<const int4*>(b)[1];
+  p.ntasks = h0.x; p.ncons = h0.y; p.nrows = h0.z; p.nfcons = h0.w;
+  p.nsn = h1.x; p.nsnr = h1.y; p.gu = h1.z; p.gf = h1.w;
+  p.task4 = reinterpret_cast<const int4*>(b) + 2;
+  p.con4 = p.task4 + p.ntasks;
+  p.row4 = p.con4 + p.ncons;
+  p.fcon4 = p.row4 + p.nrows;
+  p.sna = p.fcon4 + p.nfcons;
+  p.snb = p.sna + p.nsn;
+  p.snr = reinterpret_cast<const int*>(p.snb + p.nsn);
+  return p;
+}
+
+// double-buffered packet prefetcher (state identical in every thread)
+struct PkPipe {
+  int* buf[2];
+  uint64_t* mb[2];
+  uint32_t ph[2];
+};
+// thread 0 issues the copy of packet `lv` into buffer lv & 1 (caller: after a CTA barrier that
+// follows the last read of that buffer, with every thread having executed fence.proxy.async)
+__device__ __forceinline__ void pk_issue(const DevGraph& g, PkPipe& pp, int lv) {
+  if (threadIdx.x == 0 && lv >= 0 && lv < g.L) {
+    const int o0 = g.pk_off[lv], o1 = g.pk_off[lv + 1];
+    const uint32_t bytes = (uint32_t)(o1 - o0) * 4u;
+    uint64_t* mb = pp.mb[lv & 1];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(pp.buf[lv & 1])),
+        "l"(g.pk + o0), "r"(bytes), "r"(smem_u32(mb))
+        : "memory");
+  }
+}
+__device__ __forceinline__ Pk pk_wait(PkPipe& pp, int lv) {
+  mbar_wait(pp.mb[lv & 1], pp.ph[lv & 1]);
+  pp.ph[lv & 1] ^= 1u;
+  return pk_view(pp.buf[lv & 1]);
+}
+// all threads: order prior generic accesses before the async proxy, then barrier
+__device__ __forceinline__ void proxy_barrier() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+  __syncthreads();
+}
+
+template <int D>
+__device__ __forceinline__ void pk_task_row_partial(const Pk& P, const LView& V, const int4 tk, int a, int lane,
+                                                    int G, double (&acc)[D]) {
+  int kb = 0;
+  for (int ci = tk.z; ci < tk.w; ++ci) {
+    const int4 c = P.con4[ci];
+    const double* A = V.at(c.x) + a;
+    const double* Bm = V.at(c.y);
+    int k = lane - kb % G;
+    if (k < 0) k += G;
+    for (; k < c.w; k += G) {
+      const double av = A[(size_t)k * c.z];
+      double bv[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) bv[q] = Bm[(size_t)k * c.z + q];
+#pragma unroll
+      for (int q = 0; q < D; ++q) acc[q] = fma(av, bv[q], acc[q]);
+    }
+    kb += c.w;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ double pk_fwd_row_partial(const Pk& P, const LView& V, const double* x, int4 rw, int a,
+                                                     int lane, int G) {
+  double s0 = 0.0, s1 = 0.0;
+  int kb = 0;
+  for (int ci = rw.y; ci < rw.z; ++ci) {
+    const int4 c = P.fcon4[ci];
+    const double* A = V.at(c.x) + a;
+    const double* y = x + c.w;
+    int k = lane - kb % G;
+    if (k < 0) k += G;
+    for (; k + G < c.z; k += 2 * G) {
+      s0 = fma(A[(size_t)k * c.y], y[k], s0);
+      s1 = fma(A[(size_t)(k + G) * c.y], y[k + G], s1);
+    }
+    if (k < c.z) s0 = fma(A[(size_t)k * c.y], y[k], s0);
+    kb += c.z;
+  }
+  return s0 + s1;
+}
+
+// forward-substitution gather of a level's pose rows (CTA-wide): x_pa -= sum L_d[p_a,:] y_d
+template <int D, int NT>
+__device__ void pk_fwd_rows(const Pk& P, const LView& V, double* x) {
+  const int G = P.gf;
+  const int n = P.nrows * D;
+  const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
+  for (int base = 0; base < n; base += NT / G) {
+    const int item = base + grp;
+    const bool valid = item < n;
+    const int r = valid ? item / D : 0, a = item - r * D;
+    const int4 rw = P.row4[r];
+    double acc[1] = {valid ? pk_fwd_row_partial<D>(P, V, x, rw, a, lane, G) : 0.0};
+    group_reduce<1>(acc, G);
+    if (valid && lane == 0) x[(size_t)D * rw.x + a] -= acc[0];
+  }
+}
+
+// Full numeric factorisation, level-synchronous with packet prefetch.  xf != nullptr fuses the
+// forward substitution (y = L^-1 x in place).
 template <int D, int NT>
 __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, double tol, int* s_fail,
-                             uint64_t* mbar, uint32_t& phase, double* xinv, double* xf, int* sq) {
-  DNLS_TRACE_POINT(900);
-  forest_factor<D, NT>(g, L, stage, g.stage_n, tol, s_fail, xinv, xf, sq);
-  DNLS_TRACE_POINT(950);
-  factor_levels<D, NT>(g, L, stage, tol, s_fail, mbar, phase, xinv, xf, g.top_level, g.L);
+                             uint64_t* mbar, uint32_t& phase, double* xinv, double* xf, PkPipe& pp) {
+  proxy_barrier();
+  pk_issue(g, pp, 0);
+  pk_issue(g, pp, 1);
+  for (int lv = 0; lv < g.L; ++lv) {
+    const Pk P = pk_wait(pp, lv);
+    const int lo = g.level_off[lv];
+    const bool resident = lo >= L.rlo;
+    const int hi = resident ? lo : g.level_stage_hi[lv];
+    DNLS_TRACE_POINT(1000 + lv);
+    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+    DNLS_TRACE_POINT(1100 + lv);
+    const LView V = L.level(stage, lo, hi);
+    {   // (U) gather-form updates: item = (task, row a), G lanes per item
+      const int G = P.gu;
+      const int n = P.ntasks * D;
+      const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
+      for (int base = 0; base < n; base += NT / G) {
+        const int item = base + grp;
+        const bool valid = item < n;
+        const int t = valid ? item / D : 0, a = item - t * D;
+        double acc[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[q] = 0.0;
+        const int4 tk = P.task4[t];
+        if (valid) pk_task_row_partial<D>(P, V, tk, a, lane, G, acc);
+        group_reduce<D>(acc, G);
+        if (valid && lane == 0) {
+          double* T = V.at(tk.x) + a;
+#pragma unroll
+          for (int q = 0; q < D; ++q) T[(size_t)q * tk.y] -= acc[q];
+        }
+      }
+    }
+    if (xf) pk_fwd_rows<D, NT>(P, V, xf);
+    __syncthreads();
+    DNLS_TRACE_POINT(1200 + lv);
+    // (F) dense factorisation of the level's panels by teams
+    {
+      Team tm;
+      int team, nteams;
+      team_of<NT>(P.nsn, tm, team, nteams);
+      for (int i = team; i < P.nsn; i += nteams) {
+        const int4 sa = P.sna[i];
+        panel_factor<D>(V.at(sa.x), sa.y, sa.z, sa.w, tol, tm, s_fail, xinv + team * D * D);
+      }
+    }
+    __syncthreads();
+    if (xf) {   // fused forward substitution: y_s = L_ss^-1 t_s, warp per supernode
+      const int warp = threadIdx.x >> 5;
+      for (int i = warp; i < P.nsn; i += NT / 32) {
+        const int4 sa = P.sna[i], sb = P.snb[i];
+        warp_trsv_lower_w<D>(V.at(sa.x), sa.z, sa.w, xf + (size_t)D * sb.x);
+      }
+      __syncthreads();
+    }
+    DNLS_TRACE_POINT(1300 + lv);
+    if (!resident && hi > lo) copy_range<NT>(L.g + lo, stage, hi - lo);
+    proxy_barrier();
+    pk_issue(g, pp, lv + 2);
+  }
   DNLS_TRACE_POINT(1999);
 }
 
-// Solve: forward (unless fused into the factorisation) level-synchronous, backward: top levels
-// CTA-wide then the forest top-down by dataflow.
+// Solve with the factor: forward (unless fused into the factorisation) and backward
+// substitution, level-synchronous with packet prefetch; warp per supernode for the dense parts.
 template <int D, int NT>
 __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, double* x, uint64_t* mbar,
-                            uint32_t& phase, int* sq, bool forward = true) {
-  solve_levels<D, NT>(g, L, stage, x, mbar, phase, forward, g.top_level);
-  DNLS_TRACE_POINT(3500);
-  forest_bsolve<D, NT>(g, L, x, sq);
-  DNLS_TRACE_POINT(3999);
+                            uint32_t& phase, PkPipe& pp, bool forward = true) {
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5;
+  if (forward) {
+    proxy_barrier();
+    pk_issue(g, pp, 0);
+    pk_issue(g, pp, 1);
+    for (int lv = 0; lv < g.L; ++lv) {
+      const Pk P = pk_wait(pp, lv);
+      const int lo = g.level_off[lv];
+      const bool resident = lo >= L.rlo;
+      const int hi = resident ? lo : g.level_stage_hi[lv];
+      if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+      const LView V = L.level(stage, lo, hi);
+      pk_fwd_rows<D, NT>(P, V, x);
+      __syncthreads();
+      for (int i = warp; i < P.nsn; i += NW) {
+        const int4 sa = P.sna[i], sb = P.snb[i];
+        warp_trsv_lower_w<D>(V.at(sa.x), sa.z, sa.w, x + (size_t)D * sb.x);
+      }
+      proxy_barrier();
+      pk_issue(g, pp, lv + 2);
+    }
+  }
+  // backward: root to leaves
+  proxy_barrier();
+  pk_issue(g, pp, g.L - 1);
+  pk_issue(g, pp, g.L - 2);
+  for (int lv = g.L - 1; lv >= 0; --lv) {
+    const Pk P = pk_wait(pp, lv);
+    const int lo = g.level_off[lv];
+    const bool resident = lo >= L.rlo;
+    const int hi = resident ? lo : g.level_stage_hi[lv];
+    DNLS_TRACE_POINT(3000 + lv);
+    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+    DNLS_TRACE_POINT(3100 + lv);
+    const LView V = L.level(stage, lo, hi);
+    for (int i = warp; i < P.nsn; i += NW) {
+      const int4 sa = P.sna[i], sb = P.snb[i];
+      const double* Pn = V.at(sa.x);
+      const int ld = sa.z, w = sa.w;
+      double* xs = x + (size_t)D * sb.x;
+      // xs[c] -= sum_r L[r][c] x_r over below rows; G lanes per column
+      const int lane = threadIdx.x & 31;
+      int G = 1;
+      while (G < 32 && G * 2 * w <= 32) G *= 2;
+      const int nbr = sb.z - sb.y;
+      for (int cb = 0; cb < w; cb += 32 / G) {
+        const int c = cb + lane / G, sub = lane % G;
+        double acc[1] = {0.0};
+        if (c < w) {
+          const double* col = Pn + (size_t)c * ld + w;
+          double s0 = 0.0, s1 = 0.0;
+          for (int rr = sub; rr < nbr; rr += G) {
+            const double* xr = x + (size_t)D * P.snr[sb.y + rr];
+#pragma unroll
+            for (int a = 0; a < D; a += 2) {
+              s0 = fma(col[rr * D + a], xr[a], s0);
+              if (a + 1 < D) s1 = fma(col[rr * D + a + 1], xr[a + 1], s1);
+            }
+          }
+          acc[0] = s0 + s1;
+        }
+        group_reduce<1>(acc, G);
+        if (c < w && sub == 0) xs[c] -= acc[0];
+      }
+      __syncwarp();
+      warp_trsv_upper_w<D>(Pn, ld, w, xs);
+    }
+    proxy_barrier();
+    pk_issue(g, pp, lv - 2);
+  }
 }
 
 // ============================================================================= a5: retraction

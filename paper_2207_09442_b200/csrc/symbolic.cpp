@@ -578,6 +578,64 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       if (S.sn_parent[sn] < 0 || !S.sn_sched[S.sn_parent[sn]]) S.broots.push_back(sn);
     }
   }
+  // ---- 5b'. per-level descriptor packets (prefetched into shared memory one level ahead)
+  //   int4 header (ntasks, ncons, nrows, nfcons), int4 (nsn, nsnr, 0, 0),
+  //   task4[ntasks] = (target off, ld, c0, c1)   c0/c1 index con4 of this packet
+  //   con4[ncons]   = (src row-p off, src row-q off, ld, width)
+  //   row4[nrows]   = (pose row p, fc0, fc1, 0)   fc0/fc1 index fcon4 of this packet
+  //   fcon4[nfcons] = (src row off, ld, width, y off)
+  //   sna4[nsn] = (off, m, ld, w), snb4[nsn] = (first, snr0, snr1, 0), snr[nsnr] (padded to 4)
+  {
+    S.pk.clear();
+    S.pk_off.assign(S.num_levels + 1, 0);
+    S.pk_max = 0;
+    auto push4 = [&](int a, int b, int c, int d) {
+      S.pk.push_back(a); S.pk.push_back(b); S.pk.push_back(c); S.pk.push_back(d);
+    };
+    for (int l = 0; l < S.num_levels; ++l) {
+      const int base = (int)S.pk.size();
+      S.pk_off[l] = base;
+      const int t0 = S.ut_level_ptr[l], t1 = S.ut_level_ptr[l + 1];
+      const int cb = t0 < t1 ? S.ut_cptr[t0] : 0, ce = t0 < t1 ? S.ut_cptr[t1] : 0;
+      const int r0 = S.lrow_ptr[l], r1 = S.lrow_ptr[l + 1];
+      int nf = 0;
+      for (int r = r0; r < r1; ++r) nf += S.fc_ptr[S.lrow[r] + 1] - S.fc_ptr[S.lrow[r]];
+      const int s0 = S.level_ptr[l], s1 = S.level_ptr[l + 1];
+      int nsnr = 0;
+      for (int i = s0; i < s1; ++i) nsnr += (int)S.sn_rows[S.level_sn[i]].size();
+      push4(t1 - t0, ce - cb, r1 - r0, nf);
+      push4(s1 - s0, nsnr, S.level_gu[l], S.level_gf[l]);
+      for (int t = t0; t < t1; ++t) push4(S.ut_off[t], S.ut_ld[t], S.ut_cptr[t] - cb, S.ut_cptr[t + 1] - cb);
+      for (int c = cb; c < ce; ++c) push4(S.uc_a[c], S.uc_b[c], S.uc_ld[c], S.uc_w[c]);
+      int fcur = 0;
+      for (int r = r0; r < r1; ++r) {
+        const int p = S.lrow[r];
+        const int n = S.fc_ptr[p + 1] - S.fc_ptr[p];
+        push4(p, fcur, fcur + n, 0);
+        fcur += n;
+      }
+      for (int r = r0; r < r1; ++r) {
+        const int p = S.lrow[r];
+        for (int c = S.fc_ptr[p]; c < S.fc_ptr[p + 1]; ++c) push4(S.fc_off[c], S.fc_ld[c], S.fc_w[c], S.fc_x[c]);
+      }
+      for (int i = s0; i < s1; ++i) {
+        const int sn = S.level_sn[i];
+        push4((int)S.sn_off[sn], S.sn_m[sn], S.sn_ld[sn], S.sn_w[sn]);
+      }
+      int rcur = 0;
+      for (int i = s0; i < s1; ++i) {
+        const int sn = S.level_sn[i];
+        const int n = (int)S.sn_rows[sn].size();
+        push4(S.sn_first[sn], rcur, rcur + n, 0);
+        rcur += n;
+      }
+      for (int i = s0; i < s1; ++i)
+        for (int p : S.sn_rows[S.level_sn[i]]) S.pk.push_back(p);
+      while (S.pk.size() % 4) S.pk.push_back(0);
+      S.pk_max = std::max(S.pk_max, (int)S.pk.size() - base);
+    }
+    S.pk_off[S.num_levels] = (int)S.pk.size();
+  }
   // ---- 5c. assembly lists
   {
     std::map<std::pair<int, int>, VI> pair_edges;   // original (min, max) -> edges

@@ -69,6 +69,9 @@ struct Symbolic {
   std::vector<int32_t> snr_ptr, snr;
   // dataflow schedule: update-task range [2s, 2s+1] per supernode, children CSR, forest flags
   std::vector<int32_t> ut_sn_ptr, child_ptr, child_idx, sn_sched, leaves, broots;
+  // per-level descriptor packets (see symbolic.cpp 5b'), offsets in ints, largest packet
+  std::vector<int32_t> pk, pk_off;
+  int pk_max = 0;
   int top_level = 0, n_forest = 0;
 
   // scatter-free assembly: every d x d block of the storage exactly once
