@@ -183,10 +183,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
 template <int NT>
 __device__ __forceinline__ void bulk_load(double* dst, const double* src, int ndoubles, uint64_t* mbar,
                                           uint32_t& phase) {
-  asm volatile("fence.proxy.async;" ::: "memory");
   __syncthreads();
   if (ndoubles <= 0) return;
   if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async;" ::: "memory");
     const uint32_t bytes = (uint32_t)ndoubles * 8u;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
                  : "memory");
@@ -626,6 +626,19 @@ __device__ __forceinline__ void group_reduce(double (&acc)[N], int G) {
   }
 }
 
+// variable-size aligned lane groups in one warp: 5 uniform xor steps, accumulate when off < G
+template <int N>
+__device__ __forceinline__ void group_reduce_var(double (&acc)[N], int G) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const double v = __shfl_xor_sync(0xffffffffu, acc[q], off);
+      if (off < G) acc[q] += v;
+    }
+  }
+}
+
 // partial row a of update task tk: acc[q] += sum_{k = lane mod G} A_k[a] B_k[q]
 template <int D>
 __device__ __forceinline__ void task_row_partial(const DevGraph& g, const LView& V, const int4 tk, int a, int lane,
@@ -1046,15 +1059,15 @@ __device__ void forest_bsolve(const DevGraph& g, const LView& L, double* x, int*
 // prefetched into a double buffer in shared memory by TMA bulk copies one level ahead, so all
 // index reads of the numeric phases hit shared memory.
 struct Pk {
-  int ntasks, ncons, nrows, nfcons, nsn, nsnr, gu, gf;
+  int ntasks, ncons, nrows, nfcons, nsn, nsnr, nul, nfl;
   const int4 *task4, *con4, *row4, *fcon4, *sna, *snb;
-  const int* snr;
+  const int *snr, *ulane, *flane;
 };
 __device__ __forceinline__ Pk pk_view(const int* b) {
   Pk p;
   const int4 h0 = reinterpret_cast<const int4*>(b)[0], h1 = reinterpret_cast<const int4*>(b)[1];
   p.ntasks = h0.x; p.ncons = h0.y; p.nrows = h0.z; p.nfcons = h0.w;
-  p.nsn = h1.x; p.nsnr = h1.y; p.gu = h1.z; p.gf = h1.w;
+  p.nsn = h1.x; p.nsnr = h1.y; p.nul = h1.z; p.nfl = h1.w;
   p.task4 = reinterpret_cast<const int4*>(b) + 2;
   p.con4 = p.task4 + p.ntasks;
   p.row4 = p.con4 + p.ncons;
@@ -1062,6 +1075,8 @@ __device__ __forceinline__ Pk pk_view(const int* b) {
   p.sna = p.fcon4 + p.nfcons;
   p.snb = p.sna + p.nsn;
   p.snr = reinterpret_cast<const int*>(p.snb + p.nsn);
+  p.ulane = p.snr + p.nsnr;
+  p.flane = p.ulane + p.nul;
   return p;
 }
 
@@ -1093,67 +1108,78 @@ __device__ __forceinline__ Pk pk_wait(PkPipe& pp, int lv) {
 }
 // all threads: order prior generic accesses before the async proxy, then barrier
 __device__ __forceinline__ void proxy_barrier() {
-  asm volatile("fence.proxy.async;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
 }
 
+// partial row a of update task tk over the contributions ci = lane (mod G) of the task: the G
+// lanes of a group take whole source panels, so their (independent) loads overlap.
 template <int D>
 __device__ __forceinline__ void pk_task_row_partial(const Pk& P, const LView& V, const int4 tk, int a, int lane,
                                                     int G, double (&acc)[D]) {
-  int kb = 0;
-  for (int ci = tk.z; ci < tk.w; ++ci) {
+  for (int ci = tk.z + lane; ci < tk.w; ci += G) {
     const int4 c = P.con4[ci];
     const double* A = V.at(c.x) + a;
     const double* Bm = V.at(c.y);
-    int k = lane - kb % G;
-    if (k < 0) k += G;
-    for (; k < c.w; k += G) {
-      const double av = A[(size_t)k * c.z];
-      double bv[D];
+    const size_t ld = c.z;
+    int k = 0;
+    for (; k + 3 <= c.w; k += 3) {   // 3 columns of loads in flight
+      double av[3], bv[3][D];
 #pragma unroll
-      for (int q = 0; q < D; ++q) bv[q] = Bm[(size_t)k * c.z + q];
+      for (int u = 0; u < 3; ++u) {
+        av[u] = A[(k + u) * ld];
 #pragma unroll
-      for (int q = 0; q < D; ++q) acc[q] = fma(av, bv[q], acc[q]);
+        for (int q = 0; q < D; ++q) bv[u][q] = Bm[(k + u) * ld + q];
+      }
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[q] = fma(av[u], bv[u][q], acc[q]);
     }
-    kb += c.w;
+    for (; k < c.w; ++k) {
+      const double av = A[k * ld];
+#pragma unroll
+      for (int q = 0; q < D; ++q) acc[q] = fma(av, Bm[k * ld + q], acc[q]);
+    }
   }
 }
 
+// partial forward-substitution sum of scalar row a of pose row rw.x over the contributions
+// ci = lane (mod G)
 template <int D>
 __device__ __forceinline__ double pk_fwd_row_partial(const Pk& P, const LView& V, const double* x, int4 rw, int a,
                                                      int lane, int G) {
-  double s0 = 0.0, s1 = 0.0;
-  int kb = 0;
-  for (int ci = rw.y; ci < rw.z; ++ci) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int ci = rw.y + lane; ci < rw.z; ci += G) {
     const int4 c = P.fcon4[ci];
     const double* A = V.at(c.x) + a;
     const double* y = x + c.w;
-    int k = lane - kb % G;
-    if (k < 0) k += G;
-    for (; k + G < c.z; k += 2 * G) {
-      s0 = fma(A[(size_t)k * c.y], y[k], s0);
-      s1 = fma(A[(size_t)(k + G) * c.y], y[k + G], s1);
+    const size_t ld = c.y;
+    int k = 0;
+    for (; k + 3 <= c.z; k += 3) {
+      s0 = fma(A[k * ld], y[k], s0);
+      s1 = fma(A[(k + 1) * ld], y[k + 1], s1);
+      s2 = fma(A[(k + 2) * ld], y[k + 2], s2);
     }
-    if (k < c.z) s0 = fma(A[(size_t)k * c.y], y[k], s0);
-    kb += c.z;
+    for (; k < c.z; ++k) s0 = fma(A[k * ld], y[k], s0);
   }
-  return s0 + s1;
+  return (s0 + s1) + s2;
 }
 
-// forward-substitution gather of a level's pose rows (CTA-wide): x_pa -= sum L_d[p_a,:] y_d
+// forward-substitution gather of a level's pose rows (CTA-wide): x_pa -= sum L_d[p_a,:] y_d.
+// Lane map (packet): each (row, component) item owns an aligned group of G lanes.
 template <int D, int NT>
 __device__ void pk_fwd_rows(const Pk& P, const LView& V, double* x) {
-  const int G = P.gf;
-  const int n = P.nrows * D;
-  const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
-  for (int base = 0; base < n; base += NT / G) {
-    const int item = base + grp;
-    const bool valid = item < n;
-    const int r = valid ? item / D : 0, a = item - r * D;
+  for (int base = 0; base < P.nfl; base += NT) {
+    const int L = base + threadIdx.x;
+    const int e = L < P.nfl ? P.flane[L] : -1;
+    const int G = e >= 0 ? 1 << ((e >> 5) & 7) : 1, sub = e >= 0 ? (e & 31) : 0;
+    const int item = e >= 0 ? e >> 8 : 0;
+    const int r = item / D, a = item - r * D;
     const int4 rw = P.row4[r];
-    double acc[1] = {valid ? pk_fwd_row_partial<D>(P, V, x, rw, a, lane, G) : 0.0};
-    group_reduce<1>(acc, G);
-    if (valid && lane == 0) x[(size_t)D * rw.x + a] -= acc[0];
+    double acc[1] = {e >= 0 ? pk_fwd_row_partial<D>(P, V, x, rw, a, sub, G) : 0.0};
+    group_reduce_var<1>(acc, G);
+    if (e >= 0 && sub == 0) x[(size_t)D * rw.x + a] -= acc[0];
   }
 }
 
@@ -1174,20 +1200,20 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
     DNLS_TRACE_POINT(1100 + lv);
     const LView V = L.level(stage, lo, hi);
-    {   // (U) gather-form updates: item = (task, row a), G lanes per item
-      const int G = P.gu;
-      const int n = P.ntasks * D;
-      const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
-      for (int base = 0; base < n; base += NT / G) {
-        const int item = base + grp;
-        const bool valid = item < n;
-        const int t = valid ? item / D : 0, a = item - t * D;
+    {   // (U) gather-form updates: item = (task, row a) owns an aligned group of G lanes (lane map)
+      for (int base = 0; base < P.nul; base += NT) {
+        const int Ln = base + threadIdx.x;
+        const int e = Ln < P.nul ? P.ulane[Ln] : -1;
+        const bool valid = e >= 0;
+        const int G = valid ? 1 << ((e >> 5) & 7) : 1, lane = valid ? (e & 31) : 0;
+        const int item = valid ? e >> 8 : 0;
+        const int t = item / D, a = item - t * D;
         double acc[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) acc[q] = 0.0;
         const int4 tk = P.task4[t];
         if (valid) pk_task_row_partial<D>(P, V, tk, a, lane, G, acc);
-        group_reduce<D>(acc, G);
+        group_reduce_var<D>(acc, G);
         if (valid && lane == 0) {
           double* T = V.at(tk.x) + a;
 #pragma unroll
@@ -1195,6 +1221,9 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
         }
       }
     }
+    DNLS_TRACE_POINT(1150 + lv);
+    __syncthreads();
+    DNLS_TRACE_POINT(1160 + lv);
     if (xf) pk_fwd_rows<D, NT>(P, V, xf);
     __syncthreads();
     DNLS_TRACE_POINT(1200 + lv);

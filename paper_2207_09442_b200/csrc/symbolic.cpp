@@ -603,8 +603,44 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       const int s0 = S.level_ptr[l], s1 = S.level_ptr[l + 1];
       int nsnr = 0;
       for (int i = s0; i < s1; ++i) nsnr += (int)S.sn_rows[S.level_sn[i]].size();
+      // lane maps: every (task, row) / (pose row, component) item gets a power-of-two group of
+      // G lanes sized to its k-work, packed into one round of cta_threads lanes when possible
+      // (groups placed in decreasing size stay aligned); entry = item << 8 | log2(G) << 5 | sub
+      auto lane_map = [&](const std::vector<int>& work) {
+        std::vector<int> order(work.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+        auto gsize = [&](int k, int kc) {
+          int need = (k + kc - 1) / kc, G = 1;
+          while (G < need && G < 32) G *= 2;
+          return G;
+        };
+        int kc = 1;
+        for (; kc < (1 << 20); kc *= 2) {
+          int64_t tot = 0;
+          for (int i : order) tot += gsize(work[i], kc);
+          if (tot <= opt.cta_threads) break;
+        }
+        std::vector<int> lanes;
+        for (int i : order) {
+          const int G = gsize(work[i], kc);
+          int lg = 0;
+          while ((1 << lg) < G) ++lg;
+          for (int sub = 0; sub < G; ++sub) lanes.push_back((i << 8) | (lg << 5) | sub);
+        }
+        return lanes;
+      };
+      std::vector<int> uwork, fwork;
+      // work unit = one source contribution (lanes take whole contributions)
+      for (int t = t0; t < t1; ++t)
+        for (int a = 0; a < D; ++a) uwork.push_back(S.ut_cptr[t + 1] - S.ut_cptr[t]);
+      for (int r = r0; r < r1; ++r) {
+        const int p = S.lrow[r];
+        for (int a = 0; a < D; ++a) fwork.push_back(S.fc_ptr[p + 1] - S.fc_ptr[p]);
+      }
+      const std::vector<int> ulanes = lane_map(uwork), flanes = lane_map(fwork);
       push4(t1 - t0, ce - cb, r1 - r0, nf);
-      push4(s1 - s0, nsnr, S.level_gu[l], S.level_gf[l]);
+      push4(s1 - s0, nsnr, (int)ulanes.size(), (int)flanes.size());
       for (int t = t0; t < t1; ++t) push4(S.ut_off[t], S.ut_ld[t], S.ut_cptr[t] - cb, S.ut_cptr[t + 1] - cb);
       for (int c = cb; c < ce; ++c) push4(S.uc_a[c], S.uc_b[c], S.uc_ld[c], S.uc_w[c]);
       int fcur = 0;
@@ -631,6 +667,8 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       }
       for (int i = s0; i < s1; ++i)
         for (int p : S.sn_rows[S.level_sn[i]]) S.pk.push_back(p);
+      for (int v : ulanes) S.pk.push_back(v);
+      for (int v : flanes) S.pk.push_back(v);
       while (S.pk.size() % 4) S.pk.push_back(0);
       S.pk_max = std::max(S.pk_max, (int)S.pk.size() - base);
     }

@@ -63,9 +63,15 @@ def main():
             dur["bsolve->retract"] += d
         elif 1000 <= tg < 1100:
             dur["factor:stage_in"] += d
-        elif 1100 <= tg < 1200:
-            dur[f"factor:U(l{tg - 1100})"] += d
-            dur["factor:U"] += d
+        elif 1100 <= tg < 1150:
+            dur[f"factor:U-own(l{tg - 1100})"] += d
+            dur["factor:U-own(thread0)"] += d
+        elif 1150 <= tg < 1160:
+            dur["factor:U-waitsync"] += d
+            dur[f"factor:U-waitsync(l{tg - 1150})"] += d
+        elif 1160 <= tg < 1200:
+            dur["factor:fwdrows"] += d
+            dur[f"factor:fwdrows(l{tg - 1160})"] += d
         elif 1200 <= tg < 1300:
             dur[f"factor:F(l{tg - 1200})"] += d
             dur["factor:F"] += d
