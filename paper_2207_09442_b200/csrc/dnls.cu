@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
     __syncthreads();
     DNLS_TRACE_POINT(200);
-    assemble_phase<D, NT>(g, L, jac_b, x_b, fp.lm ? lam : -1.0, fp.damping, s_red);
+    assemble_colored<D, NT>(g, L, jac_b, x_b, fp.lm ? lam : -1.0, fp.damping, s_red);
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     DNLS_TRACE_POINT(300);
     const double S = sh_S;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
   if (fp.implicit) {
     jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
     __syncthreads();
-    assemble_phase<D, NT>(g, L, jac_b, x_b, -1.0, 0, s_red);
+    assemble_colored<D, NT>(g, L, jac_b, x_b, -1.0, 0, s_red);
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, Dev
   Smem sm = smem_views(g, xg);
   jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
   __syncthreads();
-  assemble_phase<D, NT>(g, L, jac_b, sm.x, lam ? lam[b] : -1.0, damping, s_red);
+  assemble_colored<D, NT>(g, L, jac_b, sm.x, lam ? lam[b] : -1.0, damping, s_red);
   finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
   if (g.x_smem)
     for (int i = threadIdx.x; i < g.n; i += NT) xg[i] = sm.x[i];
@@ -671,6 +671,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   add(s.broots);
   add(task4); add(con4); add(fcon4);
   add(s.pk); add(s.pk_off);
+  add(s.cls_ptr); add(s.cls_slot); add(s.slot_desc); add(s.col_sn);
   add(s.fc_ptr); add(s.fc_off); add(s.fc_ld); add(s.fc_w); add(s.fc_x);
   add(s.snr_ptr); add(s.snr);
   add(s.blk_off); add(s.blk_ld); add(s.blk_kind); add(s.blk_cptr); add(s.blk_con);
@@ -730,6 +731,11 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dg.pk = d + offs[k++];
   dg.pk_off = d + offs[k++];
   dg.pk_max = s.pk_max;
+  dg.cls_ptr = d + offs[k++];
+  dg.cls_slot = d + offs[k++];
+  dg.slot_desc = reinterpret_cast<const int4*>(d + offs[k++]);
+  dg.pose_sn = d + offs[k++];
+  dg.ncls = (int)s.cls_ptr.size() - 1;
   dg.fc_ptr = d + offs[k++]; dg.fc_off = d + offs[k++]; dg.fc_ld = d + offs[k++]; dg.fc_w = d + offs[k++];
   dg.fc_x = d + offs[k++];
   dg.snr_ptr = d + offs[k++]; dg.snr = d + offs[k++];

@@ -59,6 +59,10 @@ struct DevGraph {
   const int *snr_ptr, *snr;
   const int *blk_off, *blk_ld, *blk_kind, *blk_cptr, *blk_con;
   const int *bc_ptr, *bc;
+  const int *cls_ptr, *cls_slot;   // edge-coloured assembly classes
+  const int4* slot_desc;            // 3 int4 per cost slot
+  const int* pose_sn;               // supernode of each permuted pose column
+  int ncls;
   const int* pk;       // per-level descriptor packets (ints), pk_off[L+1] offsets
   const int* pk_off;
   int pk_max;          // ints of the largest packet
@@ -423,6 +427,123 @@ __device__ void assemble_phase(const DevGraph& g, LView L, const double* jac_b, 
     x_b[itm] = acc;
   }
   // max diagonal (CTA reduce, max is order independent)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
+}
+
+// T (leading dim ld) += lower triangle of A^T B; all old values loaded before any store (the
+// target may be in global memory: one round trip instead of one per entry)
+template <int D>
+__device__ __forceinline__ void add_gram_lower(double* __restrict__ T, int ld, const double* A, const double* B) {
+  constexpr int NE = D * (D + 1) / 2;
+  double old[NE];
+  {
+    int e = 0;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int a = q; a < D; ++a) old[e++] = T[(size_t)q * ld + a];
+  }
+  int e = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = q; a < D; ++a) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; k += 2) {
+        s0 = fma(A[k * D + a], B[k * D + q], s0);
+        if (k + 1 < D) s1 = fma(A[(k + 1) * D + a], B[(k + 1) * D + q], s1);
+      }
+      T[(size_t)q * ld + a] = old[e++] + (s0 + s1);
+    }
+}
+template <int D>
+__device__ __forceinline__ void add_gram_full(double* __restrict__ T, int ld, const double* A, const double* B) {
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    double old[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) old[a] = T[(size_t)q * ld + a];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; k += 2) {
+        s0 = fma(A[k * D + a], B[k * D + q], s0);
+        if (k + 1 < D) s1 = fma(A[(k + 1) * D + a], B[(k + 1) * D + q], s1);
+      }
+      T[(size_t)q * ld + a] = old[a] + (s0 + s1);
+    }
+  }
+}
+template <int D>
+__device__ __forceinline__ void add_jtr(double* __restrict__ xb, const double* J, const double* r) {
+  double old[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) old[a] = xb[a];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double s0 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) s0 = fma(J[k * D + a], r[k], s0);
+    xb[a] = old[a] + s0;
+  }
+}
+
+// Edge-coloured scatter assembly (replaces the gather assembly in the numeric kernels): zero the
+// factor storage and b, then for each colour class (no two slots of a class share a pose) every
+// slot adds J_i^T J_i, J_j^T J_j, J_i^T J_j (lower triangles of the diagonal blocks) and J^T r into
+// the storage (shared or global through L).  Classes run in a fixed order -> deterministic.
+// Then damping (lam > 0) and the max diagonal (s_red per warp).
+template <int D, int NT>
+__device__ void assemble_colored(const DevGraph& g, const LView& L, const double* jac_b, double* x_b, double lam,
+                                 int damping, double* s_red) {
+  constexpr int JS = GT<D>::JS;
+  for (int i = threadIdx.x; i < L.rlo; i += NT) L.g[i] = 0.0;
+  for (int i = L.rlo + threadIdx.x; i < g.storage; i += NT) L.r[i - L.rlo] = 0.0;
+  for (int i = threadIdx.x; i < g.n; i += NT) x_b[i] = 0.0;
+  __syncthreads();
+  for (int c = 0; c < g.ncls; ++c) {
+    for (int ii = g.cls_ptr[c] + threadIdx.x; ii < g.cls_ptr[c + 1]; ii += NT) {
+      const int slot = g.cls_slot[ii];
+      const int4 d0 = g.slot_desc[3 * slot], d1 = g.slot_desc[3 * slot + 1], d2 = g.slot_desc[3 * slot + 2];
+      const double* Jb = jac_b + (size_t)slot * JS;
+      double Ji[D * D], r[D];
+#pragma unroll
+      for (int q = 0; q < D * D; ++q) Ji[q] = Jb[q];
+#pragma unroll
+      for (int q = 0; q < D; ++q) r[q] = Jb[2 * D * D + q];
+      add_gram_lower<D>(L.at(d0.x), d1.x, Ji, Ji);
+      add_jtr<D>(x_b + (size_t)D * d2.x, Ji, r);
+      if (d0.y >= 0) {
+        double Jj[D * D];
+#pragma unroll
+        for (int q = 0; q < D * D; ++q) Jj[q] = Jb[D * D + q];
+        add_gram_lower<D>(L.at(d0.y), d1.y, Jj, Jj);
+        add_jtr<D>(x_b + (size_t)D * d2.y, Jj, r);
+        // off-diagonal block (row pose, col pose): J_row^T J_col
+        add_gram_full<D>(L.at(d0.z), d1.z, d0.w ? Jj : Ji, d0.w ? Ji : Jj);
+      }
+    }
+    __syncthreads();
+  }
+  // damping + max diagonal over the pose diagonal blocks
+  double mymax = 0.0;
+  for (int it = threadIdx.x; it < g.n; it += NT) {
+    const int p = it / D, a = it - p * D;
+    // diagonal entry (col, col) of pose p's panel, col = D (p - first) + a
+    const int s = g.pose_sn[p];
+    const int col = D * (p - g.sn_first[s]) + a;
+    double* T = L.at(g.sn_off[s] + col * g.sn_ld[s] + col);
+    double v = *T;
+    if (lam > 0.0) {
+      v = (damping == 0) ? v * (1.0 + lam) : v + lam;
+      *T = v;
+    }
+    mymax = fmax(mymax, v);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
@@ -1059,16 +1180,18 @@ __device__ void forest_bsolve(const DevGraph& g, const LView& L, double* x, int*
 // prefetched into a double buffer in shared memory by TMA bulk copies one level ahead, so all
 // index reads of the numeric phases hit shared memory.
 struct Pk {
-  int ntasks, ncons, nrows, nfcons, nsn, nsnr, nul, nfl;
+  int ntasks, ncons, nrows, nfcons, nsn, nsnr, nul, nfl, maxb;
   const int4 *task4, *con4, *row4, *fcon4, *sna, *snb;
-  const int *snr, *ulane, *flane;
+  const int *snr, *ulane, *flane, *snm, *snw;
 };
 __device__ __forceinline__ Pk pk_view(const int* b) {
   Pk p;
   const int4 h0 = reinterpret_cast<const int4*>(b)[0], h1 = reinterpret_cast<const int4*>(b)[1];
+  const int4 h2 = reinterpret_cast<const int4*>(b)[2];
   p.ntasks = h0.x; p.ncons = h0.y; p.nrows = h0.z; p.nfcons = h0.w;
   p.nsn = h1.x; p.nsnr = h1.y; p.nul = h1.z; p.nfl = h1.w;
-  p.task4 = reinterpret_cast<const int4*>(b) + 2;
+  p.maxb = h2.x;
+  p.task4 = reinterpret_cast<const int4*>(b) + 3;
   p.con4 = p.task4 + p.ntasks;
   p.row4 = p.con4 + p.ncons;
   p.fcon4 = p.row4 + p.nrows;
@@ -1077,6 +1200,8 @@ __device__ __forceinline__ Pk pk_view(const int* b) {
   p.snr = reinterpret_cast<const int*>(p.snb + p.nsn);
   p.ulane = p.snr + p.nsnr;
   p.flane = p.ulane + p.nul;
+  p.snm = p.flane + p.nfl;
+  p.snw = p.snm + p.nsn + 1;
   return p;
 }
 
@@ -1107,9 +1232,215 @@ __device__ __forceinline__ Pk pk_wait(PkPipe& pp, int lv) {
   return pk_view(pp.buf[lv & 1]);
 }
 // all threads: order prior generic accesses before the async proxy, then barrier
-__device__ __forceinline__ void proxy_barrier() {
+// packets are read-only (never written by the generic proxy), so a plain barrier orders the
+// last reads of a buffer before the next bulk copy into it
+__device__ __forceinline__ void proxy_barrier() { __syncthreads(); }
+
+// level staging with plain vector loads (the staged panels were written back by generic stores
+// earlier in the same kernel; the generic proxy keeps that ordering without proxy fences)
+template <int NT>
+__device__ __forceinline__ void stage_in(double* __restrict__ dst, const double* __restrict__ src, int n) {
+  const int n2 = n >> 1;
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  int i = threadIdx.x;
+  for (; i + 3 * NT < n2; i += 4 * NT) {
+    const double2 a = s2[i], b = s2[i + NT], c = s2[i + 2 * NT], d = s2[i + 3 * NT];
+    d2[i] = a;
+    d2[i + NT] = b;
+    d2[i + 2 * NT] = c;
+    d2[i + 3 * NT] = d;
+  }
+  for (; i < n2; i += NT) d2[i] = s2[i];
+  if ((n & 1) && threadIdx.x == 0) dst[n - 1] = src[n - 1];
   __syncthreads();
-  if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
+}
+
+// ---- level-wide dense kernels (all panels of a level at once)
+// inverse pivots 1/L_jj of the D x D diagonal block at (c0, c0) live in its unused strict upper
+// triangle: (c0+j, c0+j+1) for j < D-1 and (c0, c0+D-1) for j = D-1
+template <int D>
+__device__ __forceinline__ int ivpos(int c0, int j, int ld) {
+  return j < D - 1 ? (c0 + j + 1) * ld + (c0 + j) : (c0 + D - 1) * ld + c0;
+}
+template <int D>
+__device__ __forceinline__ void chol_block(double* P, int ld, int c0, double tol, int* fail) {
+  double a[D][D];
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = j; i < D; ++i) a[i][j] = P[(size_t)(c0 + j) * ld + c0 + i];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double piv = a[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) piv = fma(-a[j][k], a[j][k], piv);
+    if (!(piv > tol)) {
+      bad = true;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    P[ivpos<D>(c0, j, ld)] = inv;
+    a[j][j] = piv * inv;
+#pragma unroll
+    for (int i = j + 1; i < D; ++i) {
+      double s = a[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s = fma(-a[i][k], a[j][k], s);
+      a[i][j] = s * inv;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = j; i < D; ++i) P[(size_t)(c0 + j) * ld + c0 + i] = a[i][j];
+  if (bad) *fail = 1;
+}
+// row r below the diagonal block: x L_jj^T = a
+template <int D>
+__device__ __forceinline__ void trsm_row(double* P, int ld, int c0, int r) {
+  double x[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) x[q] = P[(size_t)(c0 + q) * ld + r];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    double s = x[q];
+#pragma unroll
+    for (int k = 0; k < q; ++k) s = fma(-x[k], P[(size_t)(c0 + k) * ld + c0 + q], s);
+    x[q] = s * P[ivpos<D>(c0, q, ld)];
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) P[(size_t)(c0 + q) * ld + r] = x[q];
+}
+// single-block panel solves (w == D), one thread: forward y = L^-1 t / backward x = L^-T t
+template <int D>
+__device__ __forceinline__ void trsv_lower_block(const double* P, int ld, double* xs) {
+  double y[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    double s = xs[q];
+#pragma unroll
+    for (int k = 0; k < q; ++k) s = fma(-P[(size_t)k * ld + q], y[k], s);
+    y[q] = s * P[ivpos<D>(0, q, ld)];
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) xs[q] = y[q];
+}
+template <int D>
+__device__ __forceinline__ void trsv_upper_block(const double* P, int ld, double* xs) {
+  double y[D];
+#pragma unroll
+  for (int q = D - 1; q >= 0; --q) {
+    double s = xs[q];
+#pragma unroll
+    for (int k = q + 1; k < D; ++k) s = fma(-P[(size_t)q * ld + k], y[k], s);
+    y[q] = s * P[ivpos<D>(0, q, ld)];
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) xs[q] = y[q];
+}
+// index of the panel owning flattened item it (prefix array pre[0..n], pre[0] = 0)
+__device__ __forceinline__ int find_panel(const int* pre, int n, int it) {
+  int lo = 0, hi = n;   // pre[lo] <= it < pre[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] <= it) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// dense factorisation of all panels of a level: per D-column block, thread per panel for the
+// diagonal block, CTA-wide rows for the TRSM, CTA-wide trailing update of multi-block panels
+template <int D, int NT>
+__device__ void level_factor(const Pk& P, const LView& V, double tol, int* fail) {
+  for (int cb = 0; cb < P.maxb; ++cb) {
+    const int c0 = cb * D;
+    for (int i = threadIdx.x; i < P.nsn; i += NT) {
+      const int4 sa = P.sna[i];
+      if (c0 < sa.w) chol_block<D>(V.at(sa.x), sa.z, c0, tol, fail);
+    }
+    __syncthreads();
+    const int total = P.snm[P.nsn];
+    for (int it = threadIdx.x; it < total; it += NT) {
+      const int i = find_panel(P.snm, P.nsn, it);
+      const int4 sa = P.sna[i];
+      const int r = it - P.snm[i];
+      if (c0 < sa.w && r >= c0 + D) trsm_row<D>(V.at(sa.x), sa.z, c0, r);
+    }
+    __syncthreads();
+    if (cb + 1 < P.maxb) {
+      bool any = false;
+      for (int i = 0; i < P.nsn; ++i) {
+        const int4 sa = P.sna[i];
+        const int r0 = c0 + D;
+        if (sa.w <= r0) continue;
+        any = true;
+        double* Pn = V.at(sa.x);
+        const int ld = sa.z, nc = sa.w - r0, nr = sa.y - r0, nit = nc * nr;
+        for (int t = threadIdx.x; t < nit; t += NT) {
+          const int ci = t / nr, ri = t - ci * nr;
+          if (ri < ci) continue;
+          const int c = r0 + ci, r = r0 + ri;
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; k += 2) {
+            s0 = fma(Pn[(size_t)(c0 + k) * ld + r], Pn[(size_t)(c0 + k) * ld + c], s0);
+            if (k + 1 < D) s1 = fma(Pn[(size_t)(c0 + k + 1) * ld + r], Pn[(size_t)(c0 + k + 1) * ld + c], s1);
+          }
+          Pn[(size_t)c * ld + r] -= s0 + s1;
+        }
+      }
+      if (any) __syncthreads();
+    }
+  }
+}
+
+// y_s = L_ss^-1 t_s for every panel of a level (thread per single-block panel, warp otherwise)
+template <int D, int NT>
+__device__ void level_trsv_lower(const Pk& P, const LView& V, double* x) {
+  for (int i = threadIdx.x; i < P.nsn; i += NT) {
+    const int4 sa = P.sna[i];
+    if (sa.w == D) trsv_lower_block<D>(V.at(sa.x), sa.z, x + (size_t)D * P.snb[i].x);
+  }
+  for (int i = threadIdx.x >> 5; i < P.nsn; i += NT / 32) {
+    const int4 sa = P.sna[i];
+    if (sa.w > D) warp_trsv_lower_w<D>(V.at(sa.x), sa.z, sa.w, x + (size_t)D * P.snb[i].x);
+  }
+}
+template <int D, int NT>
+__device__ void level_trsv_upper(const Pk& P, const LView& V, double* x) {
+  for (int i = threadIdx.x; i < P.nsn; i += NT) {
+    const int4 sa = P.sna[i];
+    if (sa.w == D) trsv_upper_block<D>(V.at(sa.x), sa.z, x + (size_t)D * P.snb[i].x);
+  }
+  for (int i = threadIdx.x >> 5; i < P.nsn; i += NT / 32) {
+    const int4 sa = P.sna[i];
+    if (sa.w > D) warp_trsv_upper_w<D>(V.at(sa.x), sa.z, sa.w, x + (size_t)D * P.snb[i].x);
+  }
+}
+// backward gather of a level: item (panel, column c): x_c -= sum over below rows L[r][c] x_r
+template <int D, int NT>
+__device__ void level_bwd_gather(const Pk& P, const LView& V, double* x) {
+  const int total = P.snw[P.nsn];
+  for (int it = threadIdx.x; it < total; it += NT) {
+    const int i = find_panel(P.snw, P.nsn, it);
+    const int4 sa = P.sna[i], sb = P.snb[i];
+    const int c = it - P.snw[i];
+    const double* col = V.at(sa.x) + (size_t)c * sa.z + sa.w;
+    double s0 = 0.0, s1 = 0.0;
+    for (int rr = sb.y; rr < sb.z; ++rr) {
+      const double* xr = x + (size_t)D * P.snr[rr];
+      const double* cr = col + (rr - sb.y) * D;
+#pragma unroll
+      for (int a = 0; a < D; a += 2) {
+        s0 = fma(cr[a], xr[a], s0);
+        if (a + 1 < D) s1 = fma(cr[a + 1], xr[a + 1], s1);
+      }
+    }
+    x[(size_t)D * sb.x + c] -= s0 + s1;
+  }
 }
 
 // partial row a of update task tk over the contributions ci = lane (mod G) of the task: the G
@@ -1197,7 +1528,7 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     const bool resident = lo >= L.rlo;
     const int hi = resident ? lo : g.level_stage_hi[lv];
     DNLS_TRACE_POINT(1000 + lv);
-    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+    if (!resident) stage_in<NT>(stage, L.g + lo, hi - lo);
     DNLS_TRACE_POINT(1100 + lv);
     const LView V = L.level(stage, lo, hi);
     {   // (U) gather-form updates: item = (task, row a) owns an aligned group of G lanes (lane map)
@@ -1227,23 +1558,10 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     if (xf) pk_fwd_rows<D, NT>(P, V, xf);
     __syncthreads();
     DNLS_TRACE_POINT(1200 + lv);
-    // (F) dense factorisation of the level's panels by teams
-    {
-      Team tm;
-      int team, nteams;
-      team_of<NT>(P.nsn, tm, team, nteams);
-      for (int i = team; i < P.nsn; i += nteams) {
-        const int4 sa = P.sna[i];
-        panel_factor<D>(V.at(sa.x), sa.y, sa.z, sa.w, tol, tm, s_fail, xinv + team * D * D);
-      }
-    }
-    __syncthreads();
-    if (xf) {   // fused forward substitution: y_s = L_ss^-1 t_s, warp per supernode
-      const int warp = threadIdx.x >> 5;
-      for (int i = warp; i < P.nsn; i += NT / 32) {
-        const int4 sa = P.sna[i], sb = P.snb[i];
-        warp_trsv_lower_w<D>(V.at(sa.x), sa.z, sa.w, xf + (size_t)D * sb.x);
-      }
+    // (F) dense factorisation of the level's panels, level-wide
+    level_factor<D, NT>(P, V, tol, s_fail);
+    if (xf) {   // fused forward substitution: y_s = L_ss^-1 t_s
+      level_trsv_lower<D, NT>(P, V, xf);
       __syncthreads();
     }
     DNLS_TRACE_POINT(1300 + lv);
@@ -1270,14 +1588,11 @@ __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, do
       const int lo = g.level_off[lv];
       const bool resident = lo >= L.rlo;
       const int hi = resident ? lo : g.level_stage_hi[lv];
-      if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+      if (!resident) stage_in<NT>(stage, L.g + lo, hi - lo);
       const LView V = L.level(stage, lo, hi);
       pk_fwd_rows<D, NT>(P, V, x);
       __syncthreads();
-      for (int i = warp; i < P.nsn; i += NW) {
-        const int4 sa = P.sna[i], sb = P.snb[i];
-        warp_trsv_lower_w<D>(V.at(sa.x), sa.z, sa.w, x + (size_t)D * sb.x);
-      }
+      level_trsv_lower<D, NT>(P, V, x);
       proxy_barrier();
       pk_issue(g, pp, lv + 2);
     }
@@ -1292,41 +1607,12 @@ __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, do
     const bool resident = lo >= L.rlo;
     const int hi = resident ? lo : g.level_stage_hi[lv];
     DNLS_TRACE_POINT(3000 + lv);
-    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+    if (!resident) stage_in<NT>(stage, L.g + lo, hi - lo);
     DNLS_TRACE_POINT(3100 + lv);
     const LView V = L.level(stage, lo, hi);
-    for (int i = warp; i < P.nsn; i += NW) {
-      const int4 sa = P.sna[i], sb = P.snb[i];
-      const double* Pn = V.at(sa.x);
-      const int ld = sa.z, w = sa.w;
-      double* xs = x + (size_t)D * sb.x;
-      // xs[c] -= sum_r L[r][c] x_r over below rows; G lanes per column
-      const int lane = threadIdx.x & 31;
-      int G = 1;
-      while (G < 32 && G * 2 * w <= 32) G *= 2;
-      const int nbr = sb.z - sb.y;
-      for (int cb = 0; cb < w; cb += 32 / G) {
-        const int c = cb + lane / G, sub = lane % G;
-        double acc[1] = {0.0};
-        if (c < w) {
-          const double* col = Pn + (size_t)c * ld + w;
-          double s0 = 0.0, s1 = 0.0;
-          for (int rr = sub; rr < nbr; rr += G) {
-            const double* xr = x + (size_t)D * P.snr[sb.y + rr];
-#pragma unroll
-            for (int a = 0; a < D; a += 2) {
-              s0 = fma(col[rr * D + a], xr[a], s0);
-              if (a + 1 < D) s1 = fma(col[rr * D + a + 1], xr[a + 1], s1);
-            }
-          }
-          acc[0] = s0 + s1;
-        }
-        group_reduce<1>(acc, G);
-        if (c < w && sub == 0) xs[c] -= acc[0];
-      }
-      __syncwarp();
-      warp_trsv_upper_w<D>(Pn, ld, w, xs);
-    }
+    level_bwd_gather<D, NT>(P, V, x);
+    __syncthreads();
+    level_trsv_upper<D, NT>(P, V, x);
     proxy_barrier();
     pk_issue(g, pp, lv - 2);
   }

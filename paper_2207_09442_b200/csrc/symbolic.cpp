@@ -639,8 +639,11 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         for (int a = 0; a < D; ++a) fwork.push_back(S.fc_ptr[p + 1] - S.fc_ptr[p]);
       }
       const std::vector<int> ulanes = lane_map(uwork), flanes = lane_map(fwork);
+      int maxb = 0;
+      for (int i = s0; i < s1; ++i) maxb = std::max(maxb, S.sn_ncols[S.level_sn[i]]);
       push4(t1 - t0, ce - cb, r1 - r0, nf);
       push4(s1 - s0, nsnr, (int)ulanes.size(), (int)flanes.size());
+      push4(maxb, 0, 0, 0);
       for (int t = t0; t < t1; ++t) push4(S.ut_off[t], S.ut_ld[t], S.ut_cptr[t] - cb, S.ut_cptr[t + 1] - cb);
       for (int c = cb; c < ce; ++c) push4(S.uc_a[c], S.uc_b[c], S.uc_ld[c], S.uc_w[c]);
       int fcur = 0;
@@ -669,6 +672,13 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         for (int p : S.sn_rows[S.level_sn[i]]) S.pk.push_back(p);
       for (int v : ulanes) S.pk.push_back(v);
       for (int v : flanes) S.pk.push_back(v);
+      {   // prefix sums of panel rows m and widths w (flattened level-wide dense items)
+        int pm = 0, pw = 0;
+        S.pk.push_back(0);
+        for (int i = s0; i < s1; ++i) S.pk.push_back(pm += S.sn_m[S.level_sn[i]]);
+        S.pk.push_back(0);
+        for (int i = s0; i < s1; ++i) S.pk.push_back(pw += S.sn_w[S.level_sn[i]]);
+      }
       while (S.pk.size() % 4) S.pk.push_back(0);
       S.pk_max = std::max(S.pk_max, (int)S.pk.size() - base);
     }
@@ -729,6 +739,69 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       for (int e : inc[o]) S.bc.push_back(e * 2 + ((edges[2 * e] == o) ? 0 : 1));
       for (int k : pri[o]) S.bc.push_back((E + k) * 2);
       S.bc_ptr.push_back((int)S.bc.size());
+    }
+  }
+  // ---- 5d. edge-coloured scatter assembly: cost slots (edges, then priors) are coloured so that
+  // no two slots of a class touch the same pose; classes are applied in order, so every H block
+  // receives its contributions in a fixed order (deterministic) without atomics.
+  {
+    const int slots = E + P;
+    std::vector<uint64_t> used(N, 0);
+    std::vector<int> color(slots, 0);
+    int ncol = 0;
+    for (int sl = 0; sl < slots; ++sl) {
+      const int a = sl < E ? edges[2 * sl] : priors[sl - E];
+      const int b = sl < E ? edges[2 * sl + 1] : a;
+      const uint64_t m = used[a] | used[b];
+      int c = 0;
+      while (c < 64 && (m >> c) & 1) ++c;
+      if (c >= 64) {
+        *code = 8;
+        err << "dnls_graph_create: pose degree too high for the 64-class edge colouring";
+        return err.str();
+      }
+      color[sl] = c;
+      used[a] |= 1ull << c;
+      used[b] |= 1ull << c;
+      ncol = std::max(ncol, c + 1);
+    }
+    S.cls_ptr.assign(ncol + 1, 0);
+    for (int sl = 0; sl < slots; ++sl) S.cls_ptr[color[sl] + 1]++;
+    for (int c = 0; c < ncol; ++c) S.cls_ptr[c + 1] += S.cls_ptr[c];
+    S.cls_slot.assign(slots, 0);
+    {
+      std::vector<int> fill(S.cls_ptr.begin(), S.cls_ptr.end() - 1);
+      for (int sl = 0; sl < slots; ++sl) S.cls_slot[fill[color[sl]]++] = sl;
+    }
+    auto diag_off = [&](int p) {
+      const int sn = col_sn[p];
+      return (int)S.sn_off[sn] + D * (p - S.sn_first[sn]) * (S.sn_ld[sn] + 1);
+    };
+    S.slot_desc.assign(12 * (size_t)slots, 0);
+    for (int sl = 0; sl < slots; ++sl) {
+      int32_t* d = &S.slot_desc[12 * (size_t)sl];
+      if (sl < E) {
+        const int pi = S.iperm[edges[2 * sl]], pj = S.iperm[edges[2 * sl + 1]];
+        const int P_ = std::max(pi, pj), Q = std::min(pi, pj);
+        const int t = col_sn[Q];
+        d[0] = diag_off(pi);
+        d[1] = diag_off(pj);
+        d[2] = (int)S.sn_off[t] + D * (Q - S.sn_first[t]) * S.sn_ld[t] + rowpos(t, P_);
+        d[3] = (P_ == pj) ? 1 : 0;   // off-diagonal block = J_j^T J_i (row pose is endpoint j)
+        d[4] = S.sn_ld[col_sn[pi]];
+        d[5] = S.sn_ld[col_sn[pj]];
+        d[6] = S.sn_ld[t];
+        d[8] = pi;
+        d[9] = pj;
+      } else {
+        const int pp = S.iperm[priors[sl - E]];
+        d[0] = diag_off(pp);
+        d[1] = -1;
+        d[2] = -1;
+        d[4] = S.sn_ld[col_sn[pp]];
+        d[8] = pp;
+        d[9] = -1;
+      }
     }
   }
   return std::string();
