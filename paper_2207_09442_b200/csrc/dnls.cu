@@ -22,7 +22,7 @@
 using namespace dnls;
 
 namespace {
-constexpr int NT = 512;   // threads per CTA (one batch element per CTA)
+constexpr int NT = 256;   // threads per CTA (one batch element per CTA)
 constexpr int64_t SMEM_BYTES = 218 * 1024;   // dynamic shared memory per CTA (x + resident + staging)
 thread_local std::string g_err;
 
@@ -214,10 +214,8 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
   for (int k = 0; k < fp.K; ++k) {
     // a1 + a2 at theta_k
     DNLS_TRACE_POINT(100);
-    jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
-    __syncthreads();
     DNLS_TRACE_POINT(200);
-    assemble_colored<D, NT>(g, L, jac_b, x_b, fp.lm ? lam : -1.0, fp.damping, s_red);
+    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, fp.lm ? lam : -1.0, fp.damping, s_red);
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     DNLS_TRACE_POINT(300);
     const double S = sh_S;
@@ -277,9 +275,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
   __syncthreads();
   // final objective S(theta_K); implicit: undamped H(theta_K) and its factor stay in ws
   if (fp.implicit) {
-    jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
-    __syncthreads();
-    assemble_colored<D, NT>(g, L, jac_b, x_b, -1.0, 0, s_red);
+    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, -1.0, 0, s_red);
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
@@ -322,9 +318,7 @@ __global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, Dev
   const LView L = global_view(g, ws.L + (size_t)b * g.storage);
   double* xg = ws.x + (size_t)b * g.n;
   Smem sm = smem_views(g, xg);
-  jac_phase<D, NT>(g, pr, Tb, b, jac_b, cost_b);
-  __syncthreads();
-  assemble_colored<D, NT>(g, L, jac_b, sm.x, lam ? lam[b] : -1.0, damping, s_red);
+  linearize_phase<D, NT>(g, pr, Tb, b, L, sm.x, cost_b, lam ? lam[b] : -1.0, damping, s_red);
   finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
   if (g.x_smem)
     for (int i = threadIdx.x; i < g.n; i += NT) xg[i] = sm.x[i];

@@ -549,6 +549,262 @@ __device__ void assemble_colored(const DevGraph& g, const LView& L, const double
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
 }
 
+// ---------------------------------------------------------------------------- fused linearisation
+// Compact weighted-Jacobian form of one cost slot, kept in registers:
+//  SE3: C_j = Jr^-1(c) = [[A, U], [0, A]],  C_i = -[[P, Q], [0, P]] with P = A R, Q = A t^R + U R
+//       (R, t of T_j^-1 T_i); a prior has C = [[A, U], [0, A]].
+//  SE2: full 3x3 C_j = Jr^-1(c), C_i = -C_j Ad(T_j^-1 T_i).
+template <int D>
+struct SlotJ;
+template <>
+struct SlotJ<6> {
+  double c[6], A[3][3], U[3][3], P[3][3], Q[3][3], ww;
+};
+template <>
+struct SlotJ<3> {
+  double c[3], Cj[3][3], Ci[3][3], ww;
+};
+
+template <int D>
+__device__ __forceinline__ void slot_jac(const DevGraph& g, const DevProb& pr, const double* Tb, int b, int slot,
+                                         SlotJ<D>& J);
+template <>
+__device__ __forceinline__ void slot_jac<6>(const DevGraph& g, const DevProb& pr, const double* Tb, int b, int slot,
+                                            SlotJ<6>& J) {
+  using namespace dev;
+  constexpr int PS = 12;
+  dev::M3 Ji, U;
+  if (slot < g.E) {
+    const int i = g.edges[2 * slot], j = g.edges[2 * slot + 1];
+    SE3 Ti = se3_load(Tb + (size_t)i * PS), Tj = se3_load(Tb + (size_t)j * PS);
+    SE3 Z = se3_load(pr.meas + ((size_t)b * g.E + slot) * PS);
+    se3_log(se3_between(Z, se3_between(Ti, Tj)), J.c);
+    se3_jr_inv(J.c, Ji, U);
+    SE3 M = se3_between(Tj, Ti);
+    M3 R;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) R.m[r][q] = M.R[r][q];
+    const M3 AR = mul(Ji, R);
+    const M3 AtR = mul(Ji, mul(hat(M.t), R));
+    const M3 UR = mul(U, R);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        J.P[r][q] = AR.m[r][q];
+        J.Q[r][q] = AtR.m[r][q] + UR.m[r][q];
+      }
+  } else {
+    const int k = slot - g.E;
+    SE3 T = se3_load(Tb + (size_t)g.prior_vars[k] * PS);
+    SE3 Z = se3_load(pr.prior_meas + (size_t)b * pr.pm_bstride + (size_t)k * PS);
+    se3_log(se3_between(Z, T), J.c);
+    se3_jr_inv(J.c, Ji, U);
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      J.A[r][q] = Ji.m[r][q];
+      J.U[r][q] = U.m[r][q];
+    }
+  const double w = slot_weight<6>(g, pr, b, slot);
+  J.ww = w * w;
+}
+template <>
+__device__ __forceinline__ void slot_jac<3>(const DevGraph& g, const DevProb& pr, const double* Tb, int b, int slot,
+                                            SlotJ<3>& J) {
+  double Ci[9], Cj[9];
+  eval_slot<3>(g, pr, Tb, b, slot, J.c, Ci, Cj, true);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      J.Ci[r][q] = Ci[r * 3 + q];
+      J.Cj[r][q] = (slot < g.E) ? Cj[r * 3 + q] : 0.0;
+    }
+  const double w = slot_weight<3>(g, pr, b, slot);
+  J.ww = w * w;
+}
+
+// (X^T Y)[a][q] for 3x3 blocks
+__device__ __forceinline__ double tdot3(const double (&X)[3][3], const double (&Y)[3][3], int a, int q) {
+  return fma(X[0][a], Y[0][q], fma(X[1][a], Y[1][q], X[2][a] * Y[2][q]));
+}
+
+// SE3 6x6 blocks of the compact Jacobian: which = 0: C_j^T C_j (or prior), 1: C_i^T C_i,
+// 2: C_i^T C_j (row i, col j), 3: C_j^T C_i.  Entry (a, q), a, q in 0..5 (rho first).
+__device__ __forceinline__ double se3_block(const SlotJ<6>& J, int which, int a, int q) {
+  const int ba = a / 3, ra = a - 3 * ba, bq = q / 3, rq = q - 3 * bq;
+  // column blocks: C_j: [A;0], [U;A]   C_i: -[P;0], -[Q;P]
+  double v;
+  if (which == 0) {   // [[A'A, A'U], [U'A, U'U + A'A]]
+    if (ba == 0 && bq == 0) v = tdot3(J.A, J.A, ra, rq);
+    else if (ba == 0) v = tdot3(J.A, J.U, ra, rq);
+    else if (bq == 0) v = tdot3(J.U, J.A, ra, rq);
+    else v = tdot3(J.U, J.U, ra, rq) + tdot3(J.A, J.A, ra, rq);
+  } else if (which == 1) {   // [[P'P, P'Q], [Q'P, Q'Q + P'P]]
+    if (ba == 0 && bq == 0) v = tdot3(J.P, J.P, ra, rq);
+    else if (ba == 0) v = tdot3(J.P, J.Q, ra, rq);
+    else if (bq == 0) v = tdot3(J.Q, J.P, ra, rq);
+    else v = tdot3(J.Q, J.Q, ra, rq) + tdot3(J.P, J.P, ra, rq);
+  } else if (which == 2) {   // -[[P'A, P'U], [Q'A, Q'U + P'A]]
+    if (ba == 0 && bq == 0) v = -tdot3(J.P, J.A, ra, rq);
+    else if (ba == 0) v = -tdot3(J.P, J.U, ra, rq);
+    else if (bq == 0) v = -tdot3(J.Q, J.A, ra, rq);
+    else v = -(tdot3(J.Q, J.U, ra, rq) + tdot3(J.P, J.A, ra, rq));
+  } else {   // transpose of which == 2: (C_j^T C_i)[a][q] = (C_i^T C_j)[q][a]
+    if (bq == 0 && ba == 0) v = -tdot3(J.P, J.A, rq, ra);
+    else if (bq == 0) v = -tdot3(J.P, J.U, rq, ra);
+    else if (ba == 0) v = -tdot3(J.Q, J.A, rq, ra);
+    else v = -(tdot3(J.Q, J.U, rq, ra) + tdot3(J.P, J.A, rq, ra));
+  }
+  return J.ww * v;
+}
+__device__ __forceinline__ double se3_rhs(const SlotJ<6>& J, int side, int a) {
+  // side 0: C_j^T c (or prior), side 1: C_i^T c
+  const int ba = a / 3, ra = a - 3 * ba;
+  const double* cr = J.c;
+  const double* cw = J.c + 3;
+  double v;
+  if (side == 0)
+    v = ba == 0 ? fma(J.A[0][ra], cr[0], fma(J.A[1][ra], cr[1], J.A[2][ra] * cr[2]))
+                : fma(J.U[0][ra], cr[0], fma(J.U[1][ra], cr[1], J.U[2][ra] * cr[2])) +
+                      fma(J.A[0][ra], cw[0], fma(J.A[1][ra], cw[1], J.A[2][ra] * cw[2]));
+  else
+    v = -(ba == 0 ? fma(J.P[0][ra], cr[0], fma(J.P[1][ra], cr[1], J.P[2][ra] * cr[2]))
+                  : fma(J.Q[0][ra], cr[0], fma(J.Q[1][ra], cr[1], J.Q[2][ra] * cr[2])) +
+                        fma(J.P[0][ra], cw[0], fma(J.P[1][ra], cw[1], J.P[2][ra] * cw[2])));
+  return J.ww * v;
+}
+__device__ __forceinline__ double se2_block(const SlotJ<3>& J, int which, int a, int q) {
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double xa = (which == 0 || which == 3) ? J.Cj[k][a] : J.Ci[k][a];
+    const double yq = (which == 0 || which == 2) ? J.Cj[k][q] : J.Ci[k][q];
+    v = fma(xa, yq, v);
+  }
+  return J.ww * v;
+}
+__device__ __forceinline__ double se2_rhs(const SlotJ<3>& J, int side, int a) {
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v = fma(side == 0 ? J.Cj[k][a] : J.Ci[k][a], J.c[k], v);
+  return J.ww * v;
+}
+template <int D, class JT>
+__device__ __forceinline__ double blk(const JT& J, int which, int a, int q) {
+  if constexpr (D == 6) return se3_block(J, which, a, q);
+  else return se2_block(J, which, a, q);
+}
+template <int D, class JT>
+__device__ __forceinline__ double rhs(const JT& J, int side, int a) {
+  if constexpr (D == 6) return se3_rhs(J, side, a);
+  else return se2_rhs(J, side, a);
+}
+
+// Fused linearisation: zero the factor storage and b, then for every cost slot compute the
+// compact Jacobian in registers and scatter its H blocks and J^T r in its colour class (classes in
+// fixed order, no two slots of a class share a pose -> no races, deterministic); 1/2 |w c|^2 per
+// slot to cost_b; then damping (lam > 0) and the max diagonal (s_red per warp).
+template <int D, int NT>
+__device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, const LView& L,
+                                double* x_b, double* cost_b, double lam, int damping, double* s_red) {
+  for (int i = threadIdx.x; i < L.rlo; i += NT) L.g[i] = 0.0;
+  for (int i = L.rlo + threadIdx.x; i < g.storage; i += NT) L.r[i - L.rlo] = 0.0;
+  for (int i = threadIdx.x; i < g.n; i += NT) x_b[i] = 0.0;
+  __syncthreads();
+  const int nslot = g.E + g.P;
+  for (int base = 0; base < nslot; base += NT) {
+    const int slot = base + threadIdx.x;
+    const bool valid = slot < nslot;
+    SlotJ<D> J;
+    int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0;
+    if (valid) {
+      slot_jac<D>(g, pr, Tb, b, slot, J);
+      double n2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) n2 = fma(J.c[q], J.c[q], n2);
+      cost_b[slot] = 0.5 * J.ww * n2;
+      d0 = g.slot_desc[3 * slot];
+      d1 = g.slot_desc[3 * slot + 1];
+      d2 = g.slot_desc[3 * slot + 2];
+    }
+    for (int cc = 0; cc < g.ncls; ++cc) {
+      if (valid && d1.w == cc) {
+        const bool edge = d0.y >= 0;
+        {   // diagonal block of endpoint i (prior: its pose), lower triangle
+          double* T = L.at(d0.x);
+          const int which = edge ? 1 : 0;
+          double old[D * (D + 1) / 2];
+          int e = 0;
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+#pragma unroll
+            for (int a = q; a < D; ++a) old[e++] = T[(size_t)q * d1.x + a];
+          e = 0;
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+#pragma unroll
+            for (int a = q; a < D; ++a) T[(size_t)q * d1.x + a] = old[e++] + blk<D>(J, which, a, q);
+          double* xb = x_b + (size_t)D * d2.x;
+#pragma unroll
+          for (int a = 0; a < D; ++a) xb[a] += rhs<D>(J, edge ? 1 : 0, a);
+        }
+        if (edge) {
+          double* T = L.at(d0.y);
+          double old[D * (D + 1) / 2];
+          int e = 0;
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+#pragma unroll
+            for (int a = q; a < D; ++a) old[e++] = T[(size_t)q * d1.y + a];
+          e = 0;
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+#pragma unroll
+            for (int a = q; a < D; ++a) T[(size_t)q * d1.y + a] = old[e++] + blk<D>(J, 0, a, q);
+          double* xb = x_b + (size_t)D * d2.y;
+#pragma unroll
+          for (int a = 0; a < D; ++a) xb[a] += rhs<D>(J, 0, a);
+          // off-diagonal block at (row pose, col pose): C_i^T C_j if the row pose is i, else C_j^T C_i
+          double* O = L.at(d0.z);
+          const int which2 = d0.w ? 3 : 2;
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            double o2[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) o2[a] = O[(size_t)q * d1.z + a];
+#pragma unroll
+            for (int a = 0; a < D; ++a) O[(size_t)q * d1.z + a] = o2[a] + blk<D>(J, which2, a, q);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // damping + max diagonal over the pose diagonal blocks
+  double mymax = 0.0;
+  for (int it = threadIdx.x; it < g.n; it += NT) {
+    const int p = it / D, a = it - p * D;
+    const int s = g.pose_sn[p];
+    const int col = D * (p - g.sn_first[s]) + a;
+    double* T = L.at(g.sn_off[s] + col * g.sn_ld[s] + col);
+    double v = *T;
+    if (lam > 0.0) {
+      v = (damping == 0) ? v * (1.0 + lam) : v + lam;
+      *T = v;
+    }
+    mymax = fmax(mymax, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
+}
+
 // ============================================================================= a3: factorisation
 // A team is a warp, a group of warps synchronised by a named barrier, or the whole CTA.
 struct Team {

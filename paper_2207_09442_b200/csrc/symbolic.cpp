@@ -791,6 +791,7 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         d[4] = S.sn_ld[col_sn[pi]];
         d[5] = S.sn_ld[col_sn[pj]];
         d[6] = S.sn_ld[t];
+        d[7] = color[sl];
         d[8] = pi;
         d[9] = pj;
       } else {
@@ -799,6 +800,7 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         d[1] = -1;
         d[2] = -1;
         d[4] = S.sn_ld[col_sn[pp]];
+        d[7] = color[sl];
         d[8] = pp;
         d[9] = -1;
       }
