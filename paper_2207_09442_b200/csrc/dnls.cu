@@ -615,7 +615,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
     const int64_t xb = (n * 8 <= 65536) ? ((n + 1) & ~int64_t(1)) * 8 : 0;
     int64_t smem = SMEM_BYTES;
     if (const char* env = std::getenv("DNLS_SMEM_KB")) smem = std::min<int64_t>(SMEM_BYTES, std::atoll(env) * 1024);
-    sopt.smem_cap_doubles = std::max<int64_t>(0, smem - xb - 24 * 1024) / 8;   // 24 KB: descriptor packets
+    sopt.smem_cap_doubles = std::max<int64_t>(0, smem - xb - 2 * 4 * (int64_t)sopt.packet_ints) / 8;   // packets
     sopt.cta_threads = NT;
     smem_total = smem - xb;
   }
@@ -625,7 +625,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
                 &sopt.relax_big_frac);
   }
   std::string msg = analyze(group, num_vars, num_edges, edges_ij, num_priors, prior_vars, sopt, g->sym, &code);
-  if (msg.empty() && 8 * (int64_t)g->sym.pk_max > 24 * 1024) {   // bigger packets: re-plan the residency
+  if (msg.empty() && g->sym.pk_max != sopt.packet_ints) {   // re-plan the residency for the actual packets
     sopt.smem_cap_doubles = std::max<int64_t>(0, smem_total - 8 * (int64_t)g->sym.pk_max - 64) / 8;
     msg = analyze(group, num_vars, num_edges, edges_ij, num_priors, prior_vars, sopt, g->sym, &code);
   }
@@ -670,6 +670,15 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   add(s.snr_ptr); add(s.snr);
   add(s.blk_off); add(s.blk_ld); add(s.blk_kind); add(s.blk_cptr); add(s.blk_con);
   add(s.bc_ptr); add(s.bc);
+  if (std::getenv("DNLS_VERBOSE")) {
+    int64_t maxlev = 0;
+    for (int l = 0; l < s.num_levels; ++l) maxlev = std::max<int64_t>(maxlev, s.level_off[l + 1] - s.level_off[l]);
+    std::fprintf(stderr,
+                 "[dnls] N=%d levels=%d storage=%lld res_lo=%d res_n=%lld stage_cap=%lld max_level=%lld "
+                 "max_stage=%lld pk_max=%d ints packets=%d colours=%d\n",
+                 s.N, s.num_levels, (long long)s.storage, s.res_lo, (long long)s.res_n, (long long)s.stage_cap,
+                 (long long)maxlev, (long long)s.max_level_stage, s.pk_max, s.npk, (int)s.cls_ptr.size() - 1);
+  }
   g->device = device;
   while (buf.size() % 4) buf.push_back(0);
   g->dbuf_bytes = buf.size() * sizeof(int32_t);
@@ -725,6 +734,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dg.pk = d + offs[k++];
   dg.pk_off = d + offs[k++];
   dg.pk_max = s.pk_max;
+  dg.npk = s.npk;
   dg.cls_ptr = d + offs[k++];
   dg.cls_slot = d + offs[k++];
   dg.slot_desc = reinterpret_cast<const int4*>(d + offs[k++]);

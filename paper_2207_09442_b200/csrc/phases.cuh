@@ -66,6 +66,7 @@ struct DevGraph {
   const int* pk;       // per-level descriptor packets (ints), pk_off[L+1] offsets
   const int* pk_off;
   int pk_max;          // ints of the largest packet
+  int npk;             // number of packets (levels split into size-bounded chunks)
   const int* ibase;   // start of the device index buffer
   int inum;           // its length (ints, multiple of 4)
   int idx_smem;       // 1: kernels copy the index buffer into shared memory and read it there
@@ -618,12 +619,14 @@ __device__ __forceinline__ void slot_jac<3>(const DevGraph& g, const DevProb& pr
                                             SlotJ<3>& J) {
   double Ci[9], Cj[9];
   eval_slot<3>(g, pr, Tb, b, slot, J.c, Ci, Cj, true);
+  // a prior's Jacobian plays the role of C_j (block 0 / rhs side 0), as for SE3
+  const bool edge = slot < g.E;
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      J.Ci[r][q] = Ci[r * 3 + q];
-      J.Cj[r][q] = (slot < g.E) ? Cj[r * 3 + q] : 0.0;
+      J.Ci[r][q] = edge ? Ci[r * 3 + q] : 0.0;
+      J.Cj[r][q] = edge ? Cj[r * 3 + q] : Ci[r * 3 + q];
     }
   const double w = slot_weight<3>(g, pr, b, slot);
   J.ww = w * w;
@@ -1436,7 +1439,7 @@ __device__ void forest_bsolve(const DevGraph& g, const LView& L, double* x, int*
 // prefetched into a double buffer in shared memory by TMA bulk copies one level ahead, so all
 // index reads of the numeric phases hit shared memory.
 struct Pk {
-  int ntasks, ncons, nrows, nfcons, nsn, nsnr, nul, nfl, maxb;
+  int ntasks, ncons, nrows, nfcons, nsn, nsnr, nul, nfl, maxb, level, first, last;
   const int4 *task4, *con4, *row4, *fcon4, *sna, *snb;
   const int *snr, *ulane, *flane, *snm, *snw;
 };
@@ -1447,6 +1450,9 @@ __device__ __forceinline__ Pk pk_view(const int* b) {
   p.ntasks = h0.x; p.ncons = h0.y; p.nrows = h0.z; p.nfcons = h0.w;
   p.nsn = h1.x; p.nsnr = h1.y; p.nul = h1.z; p.nfl = h1.w;
   p.maxb = h2.x;
+  p.level = h2.y;
+  p.first = h2.z;
+  p.last = h2.w;
   p.task4 = reinterpret_cast<const int4*>(b) + 3;
   p.con4 = p.task4 + p.ntasks;
   p.row4 = p.con4 + p.ncons;
@@ -1470,7 +1476,7 @@ struct PkPipe {
 // thread 0 issues the copy of packet `lv` into buffer lv & 1 (caller: after a CTA barrier that
 // follows the last read of that buffer, with every thread having executed fence.proxy.async)
 __device__ __forceinline__ void pk_issue(const DevGraph& g, PkPipe& pp, int lv) {
-  if (threadIdx.x == 0 && lv >= 0 && lv < g.L) {
+  if (threadIdx.x == 0 && lv >= 0 && lv < g.npk) {
     const int o0 = g.pk_off[lv], o1 = g.pk_off[lv + 1];
     const uint32_t bytes = (uint32_t)(o1 - o0) * 4u;
     uint64_t* mb = pp.mb[lv & 1];
@@ -1778,13 +1784,14 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
   proxy_barrier();
   pk_issue(g, pp, 0);
   pk_issue(g, pp, 1);
-  for (int lv = 0; lv < g.L; ++lv) {
-    const Pk P = pk_wait(pp, lv);
+  for (int k = 0; k < g.npk; ++k) {
+    const Pk P = pk_wait(pp, k);
+    const int lv = P.level;
     const int lo = g.level_off[lv];
     const bool resident = lo >= L.rlo;
     const int hi = resident ? lo : g.level_stage_hi[lv];
     DNLS_TRACE_POINT(1000 + lv);
-    if (!resident) stage_in<NT>(stage, L.g + lo, hi - lo);
+    if (P.first && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
     DNLS_TRACE_POINT(1100 + lv);
     const LView V = L.level(stage, lo, hi);
     {   // (U) gather-form updates: item = (task, row a) owns an aligned group of G lanes (lane map)
@@ -1798,7 +1805,7 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
         double acc[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) acc[q] = 0.0;
-        const int4 tk = P.task4[t];
+        const int4 tk = P.ntasks > 0 ? P.task4[t] : make_int4(0, 0, 0, 0);
         if (valid) pk_task_row_partial<D>(P, V, tk, a, lane, G, acc);
         group_reduce_var<D>(acc, G);
         if (valid && lane == 0) {
@@ -1814,16 +1821,16 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     if (xf) pk_fwd_rows<D, NT>(P, V, xf);
     __syncthreads();
     DNLS_TRACE_POINT(1200 + lv);
-    // (F) dense factorisation of the level's panels, level-wide
+    // (F) dense factorisation of this packet's panels, level-wide
     level_factor<D, NT>(P, V, tol, s_fail);
     if (xf) {   // fused forward substitution: y_s = L_ss^-1 t_s
       level_trsv_lower<D, NT>(P, V, xf);
       __syncthreads();
     }
     DNLS_TRACE_POINT(1300 + lv);
-    if (!resident && hi > lo) copy_range<NT>(L.g + lo, stage, hi - lo);
+    if (P.last && !resident && hi > lo) copy_range<NT>(L.g + lo, stage, hi - lo);
     proxy_barrier();
-    pk_issue(g, pp, lv + 2);
+    pk_issue(g, pp, k + 2);
   }
   DNLS_TRACE_POINT(1999);
 }
@@ -1833,44 +1840,44 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
 template <int D, int NT>
 __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, double* x, uint64_t* mbar,
                             uint32_t& phase, PkPipe& pp, bool forward = true) {
-  constexpr int NW = NT / 32;
-  const int warp = threadIdx.x >> 5;
   if (forward) {
     proxy_barrier();
     pk_issue(g, pp, 0);
     pk_issue(g, pp, 1);
-    for (int lv = 0; lv < g.L; ++lv) {
-      const Pk P = pk_wait(pp, lv);
+    for (int k = 0; k < g.npk; ++k) {
+      const Pk P = pk_wait(pp, k);
+      const int lv = P.level;
       const int lo = g.level_off[lv];
       const bool resident = lo >= L.rlo;
       const int hi = resident ? lo : g.level_stage_hi[lv];
-      if (!resident) stage_in<NT>(stage, L.g + lo, hi - lo);
+      if (P.first && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
       const LView V = L.level(stage, lo, hi);
       pk_fwd_rows<D, NT>(P, V, x);
       __syncthreads();
       level_trsv_lower<D, NT>(P, V, x);
       proxy_barrier();
-      pk_issue(g, pp, lv + 2);
+      pk_issue(g, pp, k + 2);
     }
   }
-  // backward: root to leaves
+  // backward: root to leaves (packets in reverse; a level's chunks are independent here)
   proxy_barrier();
-  pk_issue(g, pp, g.L - 1);
-  pk_issue(g, pp, g.L - 2);
-  for (int lv = g.L - 1; lv >= 0; --lv) {
-    const Pk P = pk_wait(pp, lv);
+  pk_issue(g, pp, g.npk - 1);
+  pk_issue(g, pp, g.npk - 2);
+  for (int k = g.npk - 1; k >= 0; --k) {
+    const Pk P = pk_wait(pp, k);
+    const int lv = P.level;
     const int lo = g.level_off[lv];
     const bool resident = lo >= L.rlo;
     const int hi = resident ? lo : g.level_stage_hi[lv];
     DNLS_TRACE_POINT(3000 + lv);
-    if (!resident) stage_in<NT>(stage, L.g + lo, hi - lo);
+    if (P.last && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
     DNLS_TRACE_POINT(3100 + lv);
     const LView V = L.level(stage, lo, hi);
     level_bwd_gather<D, NT>(P, V, x);
     __syncthreads();
     level_trsv_upper<D, NT>(P, V, x);
     proxy_barrier();
-    pk_issue(g, pp, lv - 2);
+    pk_issue(g, pp, k - 2);
   }
 }
 

@@ -410,8 +410,10 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       else break;
     }
     if (r == S.num_levels && S.num_levels > 0) {
+      // lower levels cannot be staged whole: keep the largest resident suffix that leaves a
+      // third of the budget for (partial) staging
       for (int c = S.num_levels - 1; c >= 0; --c) {
-        if (o - S.level_off[c] <= cap / 2) r = c;
+        if (o - S.level_off[c] <= cap - cap / 3) r = c;
         else break;
       }
     }
@@ -578,111 +580,161 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       if (S.sn_parent[sn] < 0 || !S.sn_sched[S.sn_parent[sn]]) S.broots.push_back(sn);
     }
   }
-  // ---- 5b'. per-level descriptor packets (prefetched into shared memory one level ahead)
-  //   int4 header (ntasks, ncons, nrows, nfcons), int4 (nsn, nsnr, 0, 0),
+  // ---- 5b'. descriptor packets (prefetched into shared memory one packet ahead).  A level is
+  // emitted as one or more size-bounded packets ("chunks"); a panel is placed after all its
+  // update tasks and its forward-substitution rows, so chunks of a level run in order.
+  //   int4 h0 = (ntasks, ncons, nrows, nfcons), h1 = (nsn, nsnr, nul, nfl),
+  //   int4 h2 = (max column blocks, level, first chunk of level, last chunk of level),
   //   task4[ntasks] = (target off, ld, c0, c1)   c0/c1 index con4 of this packet
   //   con4[ncons]   = (src row-p off, src row-q off, ld, width)
   //   row4[nrows]   = (pose row p, fc0, fc1, 0)   fc0/fc1 index fcon4 of this packet
   //   fcon4[nfcons] = (src row off, ld, width, y off)
-  //   sna4[nsn] = (off, m, ld, w), snb4[nsn] = (first, snr0, snr1, 0), snr[nsnr] (padded to 4)
+  //   sna4[nsn] = (off, m, ld, w), snb4[nsn] = (first, snr0, snr1, 0), snr[nsnr],
+  //   ulane[nul], flane[nfl] (lane maps), snm[nsn+1], snw[nsn+1] (prefix sums), pad to 4
   {
     S.pk.clear();
-    S.pk_off.assign(S.num_levels + 1, 0);
+    S.pk_off.assign(1, 0);
     S.pk_max = 0;
-    auto push4 = [&](int a, int b, int c, int d) {
-      S.pk.push_back(a); S.pk.push_back(b); S.pk.push_back(c); S.pk.push_back(d);
+    const int budget = opt.packet_ints;
+    auto lane_map = [&](const std::vector<int>& work) {
+      // every item gets a power-of-two group of G lanes sized to its work, packed into one round
+      // of cta_threads lanes when possible (groups placed in decreasing size stay aligned);
+      // entry = item << 8 | log2(G) << 5 | sub
+      std::vector<int> order(work.size());
+      for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return work[x] > work[y]; });
+      auto gsize = [&](int k, int kc) {
+        int need = (k + kc - 1) / kc, G = 1;
+        while (G < need && G < 32) G *= 2;
+        return G;
+      };
+      int kc = 1;
+      for (; kc < (1 << 20); kc *= 2) {
+        int64_t tot = 0;
+        for (int i : order) tot += gsize(work[i], kc);
+        if (tot <= opt.cta_threads) break;
+      }
+      std::vector<int> lanes;
+      for (int i : order) {
+        const int G = gsize(work[i], kc);
+        int lg = 0;
+        while ((1 << lg) < G) ++lg;
+        for (int sub = 0; sub < G; ++sub) lanes.push_back((i << 8) | (lg << 5) | sub);
+      }
+      return lanes;
     };
-    for (int l = 0; l < S.num_levels; ++l) {
+    struct Chunk {
+      std::vector<int> tasks, rows, sns;
+      int ncons = 0, nfcons = 0, nsnr = 0;
+    };
+    auto chunk_ints = [&](const Chunk& c) {
+      // header + descriptors + lane maps (upper bound: one lane per work unit, capped at 32) + prefixes
+      int64_t n = 12 + 4LL * ((int64_t)c.tasks.size() + c.ncons + (int64_t)c.rows.size() + c.nfcons +
+                              2LL * (int64_t)c.sns.size()) + c.nsnr;
+      const int64_t ui = (int64_t)D * c.tasks.size(), fi = (int64_t)D * c.rows.size();
+      n += std::max<int64_t>(ui, std::min<int64_t>(opt.cta_threads, 32 * ui));
+      n += std::max<int64_t>(fi, std::min<int64_t>(opt.cta_threads, 32 * fi));
+      n += 2LL * (c.sns.size() + 1) + 4;
+      return n;
+    };
+    auto emit = [&](const Chunk& c, int lv, bool first, bool last) {
       const int base = (int)S.pk.size();
-      S.pk_off[l] = base;
-      const int t0 = S.ut_level_ptr[l], t1 = S.ut_level_ptr[l + 1];
-      const int cb = t0 < t1 ? S.ut_cptr[t0] : 0, ce = t0 < t1 ? S.ut_cptr[t1] : 0;
-      const int r0 = S.lrow_ptr[l], r1 = S.lrow_ptr[l + 1];
-      int nf = 0;
-      for (int r = r0; r < r1; ++r) nf += S.fc_ptr[S.lrow[r] + 1] - S.fc_ptr[S.lrow[r]];
-      const int s0 = S.level_ptr[l], s1 = S.level_ptr[l + 1];
-      int nsnr = 0;
-      for (int i = s0; i < s1; ++i) nsnr += (int)S.sn_rows[S.level_sn[i]].size();
-      // lane maps: every (task, row) / (pose row, component) item gets a power-of-two group of
-      // G lanes sized to its k-work, packed into one round of cta_threads lanes when possible
-      // (groups placed in decreasing size stay aligned); entry = item << 8 | log2(G) << 5 | sub
-      auto lane_map = [&](const std::vector<int>& work) {
-        std::vector<int> order(work.size());
-        for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
-        auto gsize = [&](int k, int kc) {
-          int need = (k + kc - 1) / kc, G = 1;
-          while (G < need && G < 32) G *= 2;
-          return G;
-        };
-        int kc = 1;
-        for (; kc < (1 << 20); kc *= 2) {
-          int64_t tot = 0;
-          for (int i : order) tot += gsize(work[i], kc);
-          if (tot <= opt.cta_threads) break;
-        }
-        std::vector<int> lanes;
-        for (int i : order) {
-          const int G = gsize(work[i], kc);
-          int lg = 0;
-          while ((1 << lg) < G) ++lg;
-          for (int sub = 0; sub < G; ++sub) lanes.push_back((i << 8) | (lg << 5) | sub);
-        }
-        return lanes;
+      auto push4 = [&](int x0, int x1, int x2, int x3) {
+        S.pk.push_back(x0); S.pk.push_back(x1); S.pk.push_back(x2); S.pk.push_back(x3);
       };
       std::vector<int> uwork, fwork;
-      // work unit = one source contribution (lanes take whole contributions)
-      for (int t = t0; t < t1; ++t)
+      for (int t : c.tasks)
         for (int a = 0; a < D; ++a) uwork.push_back(S.ut_cptr[t + 1] - S.ut_cptr[t]);
-      for (int r = r0; r < r1; ++r) {
-        const int p = S.lrow[r];
+      for (int p : c.rows)
         for (int a = 0; a < D; ++a) fwork.push_back(S.fc_ptr[p + 1] - S.fc_ptr[p]);
-      }
       const std::vector<int> ulanes = lane_map(uwork), flanes = lane_map(fwork);
       int maxb = 0;
-      for (int i = s0; i < s1; ++i) maxb = std::max(maxb, S.sn_ncols[S.level_sn[i]]);
-      push4(t1 - t0, ce - cb, r1 - r0, nf);
-      push4(s1 - s0, nsnr, (int)ulanes.size(), (int)flanes.size());
-      push4(maxb, 0, 0, 0);
-      for (int t = t0; t < t1; ++t) push4(S.ut_off[t], S.ut_ld[t], S.ut_cptr[t] - cb, S.ut_cptr[t + 1] - cb);
-      for (int c = cb; c < ce; ++c) push4(S.uc_a[c], S.uc_b[c], S.uc_ld[c], S.uc_w[c]);
+      for (int sn : c.sns) maxb = std::max(maxb, S.sn_ncols[sn]);
+      push4((int)c.tasks.size(), c.ncons, (int)c.rows.size(), c.nfcons);
+      push4((int)c.sns.size(), c.nsnr, (int)ulanes.size(), (int)flanes.size());
+      push4(maxb, lv, first ? 1 : 0, last ? 1 : 0);
+      int ccur = 0;
+      for (int t : c.tasks) {
+        const int n = S.ut_cptr[t + 1] - S.ut_cptr[t];
+        push4(S.ut_off[t], S.ut_ld[t], ccur, ccur + n);
+        ccur += n;
+      }
+      for (int t : c.tasks)
+        for (int cc = S.ut_cptr[t]; cc < S.ut_cptr[t + 1]; ++cc) push4(S.uc_a[cc], S.uc_b[cc], S.uc_ld[cc], S.uc_w[cc]);
       int fcur = 0;
-      for (int r = r0; r < r1; ++r) {
-        const int p = S.lrow[r];
+      for (int p : c.rows) {
         const int n = S.fc_ptr[p + 1] - S.fc_ptr[p];
         push4(p, fcur, fcur + n, 0);
         fcur += n;
       }
-      for (int r = r0; r < r1; ++r) {
-        const int p = S.lrow[r];
-        for (int c = S.fc_ptr[p]; c < S.fc_ptr[p + 1]; ++c) push4(S.fc_off[c], S.fc_ld[c], S.fc_w[c], S.fc_x[c]);
-      }
-      for (int i = s0; i < s1; ++i) {
-        const int sn = S.level_sn[i];
-        push4((int)S.sn_off[sn], S.sn_m[sn], S.sn_ld[sn], S.sn_w[sn]);
-      }
+      for (int p : c.rows)
+        for (int cc = S.fc_ptr[p]; cc < S.fc_ptr[p + 1]; ++cc) push4(S.fc_off[cc], S.fc_ld[cc], S.fc_w[cc], S.fc_x[cc]);
+      for (int sn : c.sns) push4((int)S.sn_off[sn], S.sn_m[sn], S.sn_ld[sn], S.sn_w[sn]);
       int rcur = 0;
-      for (int i = s0; i < s1; ++i) {
-        const int sn = S.level_sn[i];
+      for (int sn : c.sns) {
         const int n = (int)S.sn_rows[sn].size();
         push4(S.sn_first[sn], rcur, rcur + n, 0);
         rcur += n;
       }
-      for (int i = s0; i < s1; ++i)
-        for (int p : S.sn_rows[S.level_sn[i]]) S.pk.push_back(p);
+      for (int sn : c.sns)
+        for (int p : S.sn_rows[sn]) S.pk.push_back(p);
       for (int v : ulanes) S.pk.push_back(v);
       for (int v : flanes) S.pk.push_back(v);
-      {   // prefix sums of panel rows m and widths w (flattened level-wide dense items)
-        int pm = 0, pw = 0;
-        S.pk.push_back(0);
-        for (int i = s0; i < s1; ++i) S.pk.push_back(pm += S.sn_m[S.level_sn[i]]);
-        S.pk.push_back(0);
-        for (int i = s0; i < s1; ++i) S.pk.push_back(pw += S.sn_w[S.level_sn[i]]);
-      }
+      int pm = 0, pw = 0;
+      S.pk.push_back(0);
+      for (int sn : c.sns) S.pk.push_back(pm += S.sn_m[sn]);
+      S.pk.push_back(0);
+      for (int sn : c.sns) S.pk.push_back(pw += S.sn_w[sn]);
       while (S.pk.size() % 4) S.pk.push_back(0);
       S.pk_max = std::max(S.pk_max, (int)S.pk.size() - base);
+      S.pk_off.push_back((int)S.pk.size());
+      S.pk_level.push_back(lv);
+    };
+    for (int l = 0; l < S.num_levels; ++l) {
+      std::vector<Chunk> chunks(1);
+      auto fits = [&](const Chunk& c) { return chunk_ints(c) <= budget; };
+      for (int i = S.level_ptr[l]; i < S.level_ptr[l + 1]; ++i) {
+        const int sn = S.level_sn[i];
+        for (int t = S.ut_sn_ptr[2 * sn]; t < S.ut_sn_ptr[2 * sn + 1]; ++t) {
+          Chunk& c = chunks.back();
+          c.tasks.push_back(t);
+          c.ncons += S.ut_cptr[t + 1] - S.ut_cptr[t];
+          if (!fits(c) && c.tasks.size() + c.rows.size() + c.sns.size() > 1) {
+            c.tasks.pop_back();
+            c.ncons -= S.ut_cptr[t + 1] - S.ut_cptr[t];
+            chunks.emplace_back();
+            chunks.back().tasks.push_back(t);
+            chunks.back().ncons = S.ut_cptr[t + 1] - S.ut_cptr[t];
+          }
+        }
+        for (int p = S.sn_first[sn]; p < S.sn_first[sn] + S.sn_ncols[sn]; ++p) {
+          Chunk& c = chunks.back();
+          c.rows.push_back(p);
+          c.nfcons += S.fc_ptr[p + 1] - S.fc_ptr[p];
+          if (!fits(c) && c.tasks.size() + c.rows.size() + c.sns.size() > 1) {
+            c.rows.pop_back();
+            c.nfcons -= S.fc_ptr[p + 1] - S.fc_ptr[p];
+            chunks.emplace_back();
+            chunks.back().rows.push_back(p);
+            chunks.back().nfcons = S.fc_ptr[p + 1] - S.fc_ptr[p];
+          }
+        }
+        {
+          Chunk& c = chunks.back();
+          c.sns.push_back(sn);
+          c.nsnr += (int)S.sn_rows[sn].size();
+          if (!fits(c) && c.tasks.size() + c.rows.size() + c.sns.size() > 1) {
+            c.sns.pop_back();
+            c.nsnr -= (int)S.sn_rows[sn].size();
+            chunks.emplace_back();
+            chunks.back().sns.push_back(sn);
+            chunks.back().nsnr = (int)S.sn_rows[sn].size();
+          }
+        }
+      }
+      for (size_t k = 0; k < chunks.size(); ++k) emit(chunks[k], l, k == 0, k + 1 == chunks.size());
     }
-    S.pk_off[S.num_levels] = (int)S.pk.size();
+    S.npk = (int)S.pk_level.size();
   }
   // ---- 5c. assembly lists
   {

@@ -26,6 +26,8 @@ struct SymbolicOptions {
   int cta_threads = 256;
   // levels at the top of the tree with at most this many supernodes are processed CTA-wide
   int top_max = 2;
+  // size bound of one descriptor packet (ints); larger levels are split into chunks
+  int packet_ints = 4096;
 };
 
 struct Symbolic {
@@ -70,8 +72,8 @@ struct Symbolic {
   // dataflow schedule: update-task range [2s, 2s+1] per supernode, children CSR, forest flags
   std::vector<int32_t> ut_sn_ptr, child_ptr, child_idx, sn_sched, leaves, broots;
   // per-level descriptor packets (see symbolic.cpp 5b'), offsets in ints, largest packet
-  std::vector<int32_t> pk, pk_off;
-  int pk_max = 0;
+  std::vector<int32_t> pk, pk_off, pk_level;
+  int pk_max = 0, npk = 0;
   int top_level = 0, n_forest = 0;
 
   // scatter-free assembly: every d x d block of the storage exactly once
