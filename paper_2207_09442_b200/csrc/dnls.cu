@@ -55,7 +55,7 @@ struct WsLayout {
   size_t L, x, jac, cost, trial, S, Sprev, lam, maxd, st, it, total;
 };
 WsLayout ws_layout(const Symbolic& s, int B) {
-  const int D = s.D, PS = D == 6 ? 12 : 6, JS = 2 * D * D + D;
+  const int D = s.D, PS = D == 6 ? 12 : 6, JS = D * (D + 1) + 2 * D + D * D;   // GT<D>::JS
   const size_t n = (size_t)s.N * D, slots = (size_t)s.E + s.P;
   WsLayout w{};
   size_t o = 0;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     // a1 + a2 at theta_k
     DNLS_TRACE_POINT(100);
     DNLS_TRACE_POINT(200);
-    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, fp.lm ? lam : -1.0, fp.damping, s_red);
+    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, jac_b, fp.lm ? lam : -1.0, fp.damping, s_red);
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     DNLS_TRACE_POINT(300);
     const double S = sh_S;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
   __syncthreads();
   // final objective S(theta_K); implicit: undamped H(theta_K) and its factor stay in ws
   if (fp.implicit) {
-    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, -1.0, 0, s_red);
+    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, jac_b, -1.0, 0, s_red);
     finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, Dev
   const LView L = global_view(g, ws.L + (size_t)b * g.storage);
   double* xg = ws.x + (size_t)b * g.n;
   Smem sm = smem_views(g, xg);
-  linearize_phase<D, NT>(g, pr, Tb, b, L, sm.x, cost_b, lam ? lam[b] : -1.0, damping, s_red);
+  linearize_phase<D, NT>(g, pr, Tb, b, L, sm.x, cost_b, jac_b, lam ? lam[b] : -1.0, damping, s_red);
   finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
   if (g.x_smem)
     for (int i = threadIdx.x; i < g.n; i += NT) xg[i] = sm.x[i];
@@ -670,6 +670,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   add(s.snr_ptr); add(s.snr);
   add(s.blk_off); add(s.blk_ld); add(s.blk_kind); add(s.blk_cptr); add(s.blk_con);
   add(s.bc_ptr); add(s.bc);
+  add(s.dup_blk);
   if (std::getenv("DNLS_VERBOSE")) {
     int64_t maxlev = 0;
     for (int l = 0; l < s.num_levels; ++l) maxlev = std::max<int64_t>(maxlev, s.level_off[l + 1] - s.level_off[l]);
@@ -746,6 +747,8 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dg.blk_off = d + offs[k++]; dg.blk_ld = d + offs[k++]; dg.blk_kind = d + offs[k++]; dg.blk_cptr = d + offs[k++];
   dg.blk_con = d + offs[k++];
   dg.bc_ptr = d + offs[k++]; dg.bc = d + offs[k++];
+  dg.dup_blk = d + offs[k++];
+  dg.ndup = (int)s.dup_blk.size();
   *out = g;
   return DNLS_OK;
 }

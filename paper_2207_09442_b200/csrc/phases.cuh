@@ -63,6 +63,8 @@ struct DevGraph {
   const int4* slot_desc;            // 3 int4 per cost slot
   const int* pose_sn;               // supernode of each permuted pose column
   int ncls;
+  const int* dup_blk;               // blk_* indices of off-diagonal blocks shared by several edges
+  int ndup;
   const int* pk;       // per-level descriptor packets (ints), pk_off[L+1] offsets
   const int* pk_off;
   int pk_max;          // ints of the largest packet
@@ -121,7 +123,7 @@ struct DevWs {
 template <int D>
 struct GT {
   static constexpr int PS = (D == 6) ? 12 : 6;   // doubles per pose
-  static constexpr int JS = 2 * D * D + D;        // scratch doubles per cost slot
+  static constexpr int JS = D * (D + 1) + 2 * D + D * D;   // scratch doubles per cost slot (Scr<D>)
 };
 
 // Factor storage view.  Offsets >= rlo (the top elimination-tree levels) are RESIDENT in
@@ -709,99 +711,121 @@ __device__ __forceinline__ double rhs(const JT& J, int side, int a) {
   else return se2_rhs(J, side, a);
 }
 
-// Fused linearisation: zero the factor storage and b, then for every cost slot compute the
-// compact Jacobian in registers and scatter its H blocks and J^T r in its colour class (classes in
-// fixed order, no two slots of a class share a pose -> no races, deterministic); 1/2 |w c|^2 per
-// slot to cost_b; then damping (lam > 0) and the max diagonal (s_red per warp).
+// Fused linearisation, single-writer:
+//  1. zero the factor storage (fill blocks and the unused upper triangles of diagonal blocks);
+//  2. thread per cost slot: compact Jacobian in registers, 1/2 |w c|^2 to cost_b; the slot's
+//     off-diagonal H block J_row^T J_col is STORED directly (plain stores, no read-modify-write)
+//     when the slot is the only edge between its two poses; its two diagonal contributions
+//     J_i^T J_i, J_j^T J_j (lower triangles), its two J^T r parts (and a shared off-diagonal
+//     block) go to the per-slot scratch `scr` (fire-and-forget stores, no barriers between slots);
+//  3. one barrier, then thread per pose: its diagonal block and b segment are the sums of its
+//     slots' scratch contributions in the fixed order of the symbolic list bc (deterministic, no
+//     atomics), damped (lam > 0; damping 0: Marquardt diag *= 1 + lam, 1: diag += lam) and written
+//     once; shared off-diagonal blocks are summed the same way.  Max diagonal -> s_red per warp.
+template <int D>
+struct Scr {   // per-slot scratch layout (doubles)
+  static constexpr int NL = D * (D + 1) / 2;
+  static constexpr int H0 = 0, H1 = NL, B0 = 2 * NL, B1 = 2 * NL + D, HIJ = 2 * NL + 2 * D;
+  static constexpr int SIZE = HIJ + D * D;
+};
 template <int D, int NT>
 __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, const LView& L,
-                                double* x_b, double* cost_b, double lam, int damping, double* s_red) {
+                                double* x_b, double* cost_b, double* scr, double lam, int damping, double* s_red) {
+  using SC = Scr<D>;
+  constexpr int NL = SC::NL;
   for (int i = threadIdx.x; i < L.rlo; i += NT) L.g[i] = 0.0;
   for (int i = L.rlo + threadIdx.x; i < g.storage; i += NT) L.r[i - L.rlo] = 0.0;
-  for (int i = threadIdx.x; i < g.n; i += NT) x_b[i] = 0.0;
   __syncthreads();
+  DNLS_TRACE_POINT(210);
   const int nslot = g.E + g.P;
-  for (int base = 0; base < nslot; base += NT) {
-    const int slot = base + threadIdx.x;
-    const bool valid = slot < nslot;
+  for (int slot = threadIdx.x; slot < nslot; slot += NT) {
     SlotJ<D> J;
-    int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0;
-    if (valid) {
-      slot_jac<D>(g, pr, Tb, b, slot, J);
-      double n2 = 0.0;
+    slot_jac<D>(g, pr, Tb, b, slot, J);
+    double n2 = 0.0;
 #pragma unroll
-      for (int q = 0; q < D; ++q) n2 = fma(J.c[q], J.c[q], n2);
-      cost_b[slot] = 0.5 * J.ww * n2;
-      d0 = g.slot_desc[3 * slot];
-      d1 = g.slot_desc[3 * slot + 1];
-      d2 = g.slot_desc[3 * slot + 2];
-    }
-    for (int cc = 0; cc < g.ncls; ++cc) {
-      if (valid && d1.w == cc) {
-        const bool edge = d0.y >= 0;
-        {   // diagonal block of endpoint i (prior: its pose), lower triangle
-          double* T = L.at(d0.x);
-          const int which = edge ? 1 : 0;
-          double old[D * (D + 1) / 2];
-          int e = 0;
+    for (int q = 0; q < D; ++q) n2 = fma(J.c[q], J.c[q], n2);
+    cost_b[slot] = 0.5 * J.ww * n2;
+    const int4 d0 = g.slot_desc[3 * slot], d1 = g.slot_desc[3 * slot + 1], d2 = g.slot_desc[3 * slot + 2];
+    const bool edge = d0.y >= 0;
+    double* o = scr + (size_t)slot * SC::SIZE;
+    // side 0 = endpoint i (a prior's pose: its Jacobian has the C_j form, block 0 / rhs 0)
+    int e = 0;
 #pragma unroll
-          for (int q = 0; q < D; ++q)
+    for (int q = 0; q < D; ++q)
 #pragma unroll
-            for (int a = q; a < D; ++a) old[e++] = T[(size_t)q * d1.x + a];
-          e = 0;
-#pragma unroll
-          for (int q = 0; q < D; ++q)
-#pragma unroll
-            for (int a = q; a < D; ++a) T[(size_t)q * d1.x + a] = old[e++] + blk<D>(J, which, a, q);
-          double* xb = x_b + (size_t)D * d2.x;
-#pragma unroll
-          for (int a = 0; a < D; ++a) xb[a] += rhs<D>(J, edge ? 1 : 0, a);
-        }
-        if (edge) {
-          double* T = L.at(d0.y);
-          double old[D * (D + 1) / 2];
-          int e = 0;
-#pragma unroll
-          for (int q = 0; q < D; ++q)
-#pragma unroll
-            for (int a = q; a < D; ++a) old[e++] = T[(size_t)q * d1.y + a];
-          e = 0;
-#pragma unroll
-          for (int q = 0; q < D; ++q)
-#pragma unroll
-            for (int a = q; a < D; ++a) T[(size_t)q * d1.y + a] = old[e++] + blk<D>(J, 0, a, q);
-          double* xb = x_b + (size_t)D * d2.y;
-#pragma unroll
-          for (int a = 0; a < D; ++a) xb[a] += rhs<D>(J, 0, a);
-          // off-diagonal block at (row pose, col pose): C_i^T C_j if the row pose is i, else C_j^T C_i
-          double* O = L.at(d0.z);
-          const int which2 = d0.w ? 3 : 2;
-#pragma unroll
-          for (int q = 0; q < D; ++q) {
-            double o2[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) o2[a] = O[(size_t)q * d1.z + a];
-#pragma unroll
-            for (int a = 0; a < D; ++a) O[(size_t)q * d1.z + a] = o2[a] + blk<D>(J, which2, a, q);
-          }
-        }
+      for (int a = q; a < D; ++a) {
+        o[SC::H0 + e] = blk<D>(J, edge ? 1 : 0, a, q);
+        if (edge) o[SC::H1 + e] = blk<D>(J, 0, a, q);
+        ++e;
       }
-      __syncthreads();
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      o[SC::B0 + a] = rhs<D>(J, edge ? 1 : 0, a);
+      if (edge) o[SC::B1 + a] = rhs<D>(J, 0, a);
+    }
+    if (edge) {   // off-diagonal block at (row pose, col pose): C_i^T C_j if the row pose is i, else C_j^T C_i
+      const int which2 = d0.w ? 3 : 2;
+      double* O = d2.z ? L.at(d0.z) + 0 : o + SC::HIJ;
+      const int ld = d2.z ? d1.z : D;
+#pragma unroll
+      for (int q = 0; q < D; ++q)
+#pragma unroll
+        for (int a = 0; a < D; ++a) O[(size_t)q * ld + a] = blk<D>(J, which2, a, q);
     }
   }
-  // damping + max diagonal over the pose diagonal blocks
+  __syncthreads();
+  DNLS_TRACE_POINT(220);
   double mymax = 0.0;
-  for (int it = threadIdx.x; it < g.n; it += NT) {
-    const int p = it / D, a = it - p * D;
-    const int s = g.pose_sn[p];
-    const int col = D * (p - g.sn_first[s]) + a;
-    double* T = L.at(g.sn_off[s] + col * g.sn_ld[s] + col);
-    double v = *T;
-    if (lam > 0.0) {
-      v = (damping == 0) ? v * (1.0 + lam) : v + lam;
-      *T = v;
+  for (int p = threadIdx.x; p < g.N; p += NT) {
+    double h[NL], r[D];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) h[i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) r[a] = 0.0;
+    const int c0 = g.bc_ptr[p], c1 = g.bc_ptr[p + 1];
+    for (int c = c0; c < c1; ++c) {
+      const int code = g.bc[c];
+      const double* o = scr + (size_t)(code >> 1) * SC::SIZE;
+      const int side = code & 1;
+#pragma unroll
+      for (int i = 0; i < NL; ++i) h[i] += o[side * NL + i];
+#pragma unroll
+      for (int a = 0; a < D; ++a) r[a] += o[SC::B0 + side * D + a];
     }
-    mymax = fmax(mymax, v);
+    const int s = g.pose_sn[p], ld = g.sn_ld[s];
+    const int cc = D * (p - g.sn_first[s]);
+    double* T = L.at(g.sn_off[s] + cc * ld + cc);
+    int e = 0;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int a = q; a < D; ++a) {
+        double v = h[e++];
+        if (a == q) {
+          if (lam > 0.0) v = (damping == 0) ? v * (1.0 + lam) : v + lam;
+          mymax = fmax(mymax, v);
+        }
+        T[(size_t)q * ld + a] = v;
+      }
+#pragma unroll
+    for (int a = 0; a < D; ++a) x_b[(size_t)D * p + a] = r[a];
+  }
+  for (int k = threadIdx.x; k < g.ndup; k += NT) {   // off-diagonal blocks shared by several edges
+    const int bk = g.dup_blk[k];
+    double h[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) h[i] = 0.0;
+    for (int c = g.blk_cptr[bk]; c < g.blk_cptr[bk + 1]; ++c) {
+      const double* o = scr + (size_t)(g.blk_con[c] >> 2) * SC::SIZE + SC::HIJ;
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) h[i] += o[i];
+    }
+    double* T = L.at(g.blk_off[bk]);
+    const int ld = g.blk_ld[bk];
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int a = 0; a < D; ++a) T[(size_t)q * ld + a] = h[q * D + a];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
@@ -1659,6 +1683,177 @@ __device__ void level_factor(const Pk& P, const LView& V, double tol, int* fail)
   }
 }
 
+// ---- team-wise level factorisation (replaces the CTA-phase version above on the hot path)
+// Redundant in-register Cholesky of the D x D diagonal block at (c0, c0): every lane of a team
+// loads the lower triangle (a shared-memory broadcast) and factors it, so no barrier separates
+// the diagonal factorisation from the TRSM rows that need it.  Same arithmetic and order as
+// chol_block (bitwise identical factor).  Returns true if a pivot <= tol.
+template <int D>
+__device__ __forceinline__ bool chol_regs(const double* P, int ld, int c0, double tol, double (&a)[D][D],
+                                          double (&iv)[D]) {
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = j; i < D; ++i) a[i][j] = P[(size_t)(c0 + j) * ld + c0 + i];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double piv = a[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) piv = fma(-a[j][k], a[j][k], piv);
+    if (!(piv > tol)) {
+      bad = true;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    iv[j] = inv;
+    a[j][j] = piv * inv;
+#pragma unroll
+    for (int i = j + 1; i < D; ++i) {
+      double s = a[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s = fma(-a[i][k], a[j][k], s);
+      a[i][j] = s * inv;
+    }
+  }
+  return bad;
+}
+template <int D>
+__device__ __forceinline__ void store_diag(double* P, int ld, int c0, const double (&a)[D][D], const double (&iv)[D]) {
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = j; i < D; ++i) P[(size_t)(c0 + j) * ld + c0 + i] = a[i][j];
+#pragma unroll
+  for (int j = 0; j < D; ++j) P[ivpos<D>(c0, j, ld)] = iv[j];
+}
+// row r below the diagonal block, L_jj from registers (same arithmetic as trsm_row)
+template <int D>
+__device__ __forceinline__ void trsm_row_regs(double* P, int ld, int c0, int r, const double (&a)[D][D],
+                                              const double (&iv)[D]) {
+  double x[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) x[q] = P[(size_t)(c0 + q) * ld + r];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    double s = x[q];
+#pragma unroll
+    for (int k = 0; k < q; ++k) s = fma(-x[k], a[q][k], s);
+    x[q] = s * iv[q];
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) P[(size_t)(c0 + q) * ld + r] = x[q];
+}
+
+struct TeamSync {
+  int size, bar;
+  unsigned mask;
+  __device__ __forceinline__ void sync() const {
+    if (size <= 32) __syncwarp(mask);
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(size) : "memory");
+  }
+};
+
+// Dense factorisation of every panel of a level by teams: sub-warp lane groups when the level
+// has more panels than warps, groups of warps (named barriers) otherwise.  Per D-column block:
+// redundant register Cholesky, TRSM rows split over the team, one team barrier, trailing update,
+// one team barrier.  Single-block panels (the common case) need no barrier at all.  x != nullptr
+// fuses the forward substitution of the panel's diagonal block (y_s = L_ss^-1 t_s).
+// The caller places a CTA barrier after this function.
+template <int D, int NT>
+__device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int* fail, double* x) {
+  constexpr int NW = NT / 32;
+  const int nsn = P.nsn;
+  if (nsn <= 0) return;
+  int G;
+  if (nsn >= NT) {
+    G = 1;
+  } else if (nsn > NW) {
+    G = NT / nsn;
+    while (G & (G - 1)) G &= G - 1;
+    if (G > 32) G = 32;
+  } else {
+    int tw = NW / nsn;
+    while (tw & (tw - 1)) tw &= tw - 1;
+    G = 32 * tw;
+  }
+  const int nteams = NT / G;
+  const int team = threadIdx.x / G, rank = threadIdx.x - team * G;
+  TeamSync ts;
+  ts.size = G;
+  ts.bar = 1 + team;
+  ts.mask = G >= 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  for (int i = team; i < nsn; i += nteams) {
+    const int4 sa = P.sna[i];
+    double* Pn = V.at(sa.x);
+    const int m = sa.y, ld = sa.z, w = sa.w;
+    double* xs = x ? x + (size_t)D * P.snb[i].x : nullptr;
+    if (w == D) {
+      double a[D][D], iv[D];
+      const bool bad = chol_regs<D>(Pn, ld, 0, tol, a, iv);
+      for (int r = D + rank; r < m; r += G) trsm_row_regs<D>(Pn, ld, 0, r, a, iv);
+      if (rank == 0) {
+        store_diag<D>(Pn, ld, 0, a, iv);
+        if (bad) *fail = 1;
+        if (xs) {
+          double y[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            double s = xs[q];
+#pragma unroll
+            for (int k = 0; k < q; ++k) s = fma(-a[q][k], y[k], s);
+            y[q] = s * iv[q];
+          }
+#pragma unroll
+          for (int q = 0; q < D; ++q) xs[q] = y[q];
+        }
+      }
+      continue;
+    }
+    for (int c0 = 0; c0 < w; c0 += D) {
+      double a[D][D], iv[D];
+      const bool bad = chol_regs<D>(Pn, ld, c0, tol, a, iv);
+      for (int r = c0 + D + rank; r < m; r += G) trsm_row_regs<D>(Pn, ld, c0, r, a, iv);
+      if (rank == 0) {
+        store_diag<D>(Pn, ld, c0, a, iv);
+        if (bad) *fail = 1;
+      }
+      ts.sync();
+      const int r0 = c0 + D;
+      if (r0 < w) {
+        const int nc = w - r0, nr = m - r0, nit = nc * nr;
+        for (int t = rank; t < nit; t += G) {
+          const int ci = t / nr, ri = t - ci * nr;
+          if (ri < ci) continue;
+          const int c = r0 + ci, r = r0 + ri;
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; k += 2) {
+            s0 = fma(Pn[(size_t)(c0 + k) * ld + r], Pn[(size_t)(c0 + k) * ld + c], s0);
+            if (k + 1 < D) s1 = fma(Pn[(size_t)(c0 + k + 1) * ld + r], Pn[(size_t)(c0 + k + 1) * ld + c], s1);
+          }
+          Pn[(size_t)c * ld + r] -= s0 + s1;
+        }
+        ts.sync();
+      }
+    }
+    if (xs) {
+      if (G >= 32) {
+        if (rank < 32) warp_trsv_lower_w<D>(Pn, ld, w, xs);
+      } else if (rank == 0) {   // y = L_ss^-1 t, column-oriented, inverse pivots from ivpos
+        for (int c = 0; c < w; ++c) {
+          const int cb = c - c % D, j = c - cb;
+          const double yc = xs[c] * Pn[ivpos<D>(cb, j, ld)];
+          xs[c] = yc;
+          const double* col = Pn + (size_t)c * ld;
+          for (int r = c + 1; r < w; ++r) xs[r] = fma(-col[r], yc, xs[r]);
+        }
+      }
+      ts.sync();
+    }
+  }
+}
+
 // y_s = L_ss^-1 t_s for every panel of a level (thread per single-block panel, warp otherwise)
 template <int D, int NT>
 __device__ void level_trsv_lower(const Pk& P, const LView& V, double* x) {
@@ -1815,18 +2010,15 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
         }
       }
     }
-    DNLS_TRACE_POINT(1150 + lv);
-    __syncthreads();
     DNLS_TRACE_POINT(1160 + lv);
+    // forward-substitution rows read descendant panels and y of earlier levels only: no barrier
+    // between them and the updates of this level's panels
     if (xf) pk_fwd_rows<D, NT>(P, V, xf);
     __syncthreads();
     DNLS_TRACE_POINT(1200 + lv);
     // (F) dense factorisation of this packet's panels, level-wide
-    level_factor<D, NT>(P, V, tol, s_fail);
-    if (xf) {   // fused forward substitution: y_s = L_ss^-1 t_s
-      level_trsv_lower<D, NT>(P, V, xf);
-      __syncthreads();
-    }
+    level_factor_teams<D, NT>(P, V, tol, s_fail, xf);   // + fused y_s = L_ss^-1 t_s
+    __syncthreads();
     DNLS_TRACE_POINT(1300 + lv);
     if (P.last && !resident && hi > lo) copy_range<NT>(L.g + lo, stage, hi - lo);
     proxy_barrier();

@@ -749,6 +749,7 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     std::vector<VI> pri(N);
     for (int k = 0; k < P; ++k) pri[priors[k]].push_back(k);
     S.blk_cptr.assign(1, 0);
+    S.dup_blk.clear();
     for (int s = 0; s < NS; ++s) {
       int f = S.sn_first[s], n = S.sn_ncols[s];
       VI rows;
@@ -782,6 +783,8 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
           }
           S.blk_kind.push_back(kind);
           S.blk_cptr.push_back((int)S.blk_con.size());
+          if (kind == 2 && S.blk_cptr.back() - S.blk_cptr[S.blk_cptr.size() - 2] > 1)
+            S.dup_blk.push_back((int)S.blk_kind.size() - 1);
         }
       }
     }
@@ -829,6 +832,11 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       const int sn = col_sn[p];
       return (int)S.sn_off[sn] + D * (p - S.sn_first[sn]) * (S.sn_ld[sn] + 1);
     };
+    std::map<std::pair<int, int>, int> pair_count;   // edges per (min, max) permuted pose pair
+    for (int e = 0; e < E; ++e) {
+      const int pi = S.iperm[edges[2 * e]], pj = S.iperm[edges[2 * e + 1]];
+      pair_count[std::make_pair(std::min(pi, pj), std::max(pi, pj))]++;
+    }
     S.slot_desc.assign(12 * (size_t)slots, 0);
     for (int sl = 0; sl < slots; ++sl) {
       int32_t* d = &S.slot_desc[12 * (size_t)sl];
@@ -846,6 +854,7 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         d[7] = color[sl];
         d[8] = pi;
         d[9] = pj;
+        d[10] = pair_count[std::make_pair(Q, P_)] == 1 ? 1 : 0;   // only edge between its poses
       } else {
         const int pp = S.iperm[priors[sl - E]];
         d[0] = diag_off(pp);

@@ -84,6 +84,8 @@ struct Symbolic {
   std::vector<int32_t> blk_off, blk_ld, blk_kind, blk_cptr, blk_con;
   // b = J^T r per permuted pose: bc[bc_ptr[p] .. bc_ptr[p+1]) = slot*2 + side
   std::vector<int32_t> bc_ptr, bc;
+  // off-diagonal blocks (blk_* indices) that receive contributions from more than one edge
+  std::vector<int32_t> dup_blk;
   // edge-coloured scatter assembly: classes cls_ptr[C+1] over slots cls_slot; per slot 3 int4:
   // (off_ii, off_jj, off_ij, row-is-j flag), (ld_ii, ld_jj, ld_ij, 0), (perm pose i, perm pose j, 0, 0)
   std::vector<int32_t> cls_ptr, cls_slot, slot_desc;

@@ -330,3 +330,25 @@ def test_workspace_too_small():
     with pytest.raises(Exception) as ei:
         D.dnls_forward(g, 2, D.dnls_options_default(), pr, ws)
     assert ei.value.status == 4
+
+
+@pytest.mark.parametrize("dim", [3, 2])
+def test_forward_with_parallel_edges(dim):
+    """Several edges between the same two poses (one reversed): their off-diagonal H block is a
+    sum of contributions (the shared-block gather path of the linearisation), GN + implicit."""
+    import dataclasses
+    topo, data = make_case(40, dim=dim, p=0.3, mode="local", seed=7, B=3)
+    pick = np.array([0, 3, 5, 10])
+    extra = topo.edges[pick].copy()
+    extra[1] = extra[1][::-1]            # reversed orientation: (j, i)
+    topo2 = dataclasses.replace(topo, edges=np.concatenate([topo.edges, extra]).astype(np.int32),
+                                outlier=np.concatenate([topo.outlier, np.zeros(len(pick), bool)]))
+    data2 = dict(data)
+    data2["meas"] = np.concatenate([data["meas"], data["meas"][:, pick]], axis=1)
+    data2["w_edge"] = np.concatenate([data["w_edge"], 0.5 + 0.1 * np.arange(len(pick))])
+    _, _, poses, obj, st, it = run_forward(topo2, data2, max_iterations=6)
+    res = oracle_results(topo2, data2, max_iterations=6)
+    P = poses.cpu().numpy()
+    for b, r in enumerate(res):
+        assert pose_err(P[b], r.x) <= TOL_POSE
+        assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20

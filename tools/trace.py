@@ -51,6 +51,13 @@ def main():
             dur["jac"] += d
         elif tg == 200:
             dur["assemble"] += d
+            dur["lin:zero"] += d
+        elif tg == 210:
+            dur["assemble"] += d
+            dur["lin:jac"] += d
+        elif tg == 220:
+            dur["assemble"] += d
+            dur["lin:scatter"] += d
         elif tg == 300:
             dur["factor:prologue"] += d
         elif tg == 900 or 5000 <= tg < 8000:
