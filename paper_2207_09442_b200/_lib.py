@@ -10,7 +10,9 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdnls_trace.so" if os.environ.get("DNLS_LIB") == "trace" else "libdnls.so")
+# DNLS_LIB selects a development variant built next to it (lib/libdnls_<name>.so, e.g. "trace")
+_VARIANT = os.environ.get("DNLS_LIB", "")
+LIB_PATH = os.path.join(HERE, "lib", f"libdnls_{_VARIANT}.so" if _VARIANT else "libdnls.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "dnls.h")
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)

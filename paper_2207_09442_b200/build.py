@@ -23,14 +23,18 @@ def up_to_date(out: str = OUT) -> bool:
     return all(os.path.getmtime(p) <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
-    """Compile libdnls.so (or, trace=True, the -DDNLS_TRACE debug variant libdnls_trace.so)."""
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str = "",
+          defines=()) -> str:
+    """Compile libdnls.so (or, trace=True, the -DDNLS_TRACE debug variant libdnls_trace.so; or a
+    development variant lib/libdnls_<variant>.so with extra -D defines, loaded with DNLS_LIB)."""
     out = OUT_TRACE if trace else OUT
+    if variant:
+        out = os.path.join(os.path.dirname(OUT), f"libdnls_{variant}.so")
     if not force and up_to_date(out):
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
     tmp = out + ".tmp"
-    cmd = [NVCC] + FLAGS + (["-DDNLS_TRACE"] if trace else []) + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
+    cmd = [NVCC] + FLAGS + (["-DDNLS_TRACE"] if trace else []) + [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

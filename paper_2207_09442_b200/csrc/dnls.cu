@@ -22,7 +22,10 @@
 using namespace dnls;
 
 namespace {
-constexpr int NT = 256;   // threads per CTA (one batch element per CTA)
+#ifndef DNLS_NT
+#define DNLS_NT 384
+#endif
+constexpr int NT = DNLS_NT;   // threads per CTA (one batch element per CTA)
 constexpr int64_t SMEM_BYTES = 218 * 1024;   // dynamic shared memory per CTA (x + resident + staging)
 thread_local std::string g_err;
 
