@@ -26,7 +26,7 @@ namespace {
 #define DNLS_NT 384
 #endif
 constexpr int NT = DNLS_NT;   // threads per CTA (one batch element per CTA)
-constexpr int64_t SMEM_BYTES = 218 * 1024;   // dynamic shared memory per CTA (x + resident + staging)
+constexpr int64_t SMEM_BYTES = 190 * 1024;   // dynamic shared memory per CTA (x + resident + staging); the rest of the 256 KB unified L1 caches the global panels (measured optimum, tools/smem_sweep.sh)
 thread_local std::string g_err;
 
 dnls_status fail(dnls_status s, const std::string& msg) {
@@ -682,6 +682,13 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
                  "max_stage=%lld pk_max=%d ints packets=%d colours=%d\n",
                  s.N, s.num_levels, (long long)s.storage, s.res_lo, (long long)s.res_n, (long long)s.stage_cap,
                  (long long)maxlev, (long long)s.max_level_stage, s.pk_max, s.npk, (int)s.cls_ptr.size() - 1);
+    if (std::atoi(std::getenv("DNLS_VERBOSE")) > 1)
+      for (int k = 0; k < s.npk; ++k) {
+        const int32_t* h = s.pk.data() + s.pk_off[k];
+        const int lv = h[9];
+        std::fprintf(stderr, "  packet %d level %d res %d: tasks %d cons %d rows %d fcons %d sn %d ulanes %d flanes %d maxb %d\n",
+                     k, lv, s.level_off[lv] >= s.res_lo ? 1 : 0, h[0], h[1], h[2], h[3], h[4], h[6], h[7], h[8]);
+      }
   }
   g->device = device;
   while (buf.size() % 4) buf.push_back(0);

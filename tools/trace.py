@@ -28,7 +28,8 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "C2"
     cfg = CONFIGS[name]
     B = int(os.environ.get("TRACE_B", cfg["B"]))
-    topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
+    N = int(os.environ.get("TRACE_N", cfg["N"]))
+    topo = synth.cube_topology(N, dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
     data = synth.cube_batch(topo, B, seed=0)
     dev = torch.device("cuda", 0)
     t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in data.items()}
