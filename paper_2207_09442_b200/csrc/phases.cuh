@@ -1033,8 +1033,8 @@ __device__ __forceinline__ void group_reduce(double (&acc)[N], int G) {
 // variable-size aligned lane groups in one warp: 5 uniform xor steps, accumulate when off < G
 template <int N>
 __device__ __forceinline__ void group_reduce_var(double (&acc)[N], int G) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
+  const int gmax = __reduce_max_sync(0xffffffffu, (unsigned)G);
+  for (int off = gmax >> 1; off > 0; off >>= 1) {
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       const double v = __shfl_xor_sync(0xffffffffu, acc[q], off);
@@ -1911,7 +1911,20 @@ __device__ __forceinline__ void pk_task_row_partial(const Pk& P, const LView& V,
     const double* Bm = V.at(c.y);
     const size_t ld = c.z;
     int k = 0;
-    for (; k + 3 <= c.w; k += 3) {   // 3 columns of loads in flight
+    for (; k + 6 <= c.w; k += 6) {   // 6 columns (one pose block) of loads in flight: one round trip
+      double av[6], bv[6][D];
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        av[u] = A[(k + u) * ld];
+#pragma unroll
+        for (int q = 0; q < D; ++q) bv[u][q] = Bm[(k + u) * ld + q];
+      }
+#pragma unroll
+      for (int u = 0; u < 6; ++u)
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[q] = fma(av[u], bv[u][q], acc[q]);
+    }
+    for (; k + 3 <= c.w; k += 3) {
       double av[3], bv[3][D];
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
@@ -1944,6 +1957,20 @@ __device__ __forceinline__ double pk_fwd_row_partial(const Pk& P, const LView& V
     const double* y = x + c.w;
     const size_t ld = c.y;
     int k = 0;
+    for (; k + 6 <= c.z; k += 6) {   // same accumulator assignment as two 3-column steps, loads hoisted
+      double av[6], yv[6];
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        av[u] = A[(k + u) * ld];
+        yv[u] = y[k + u];
+      }
+      s0 = fma(av[0], yv[0], s0);
+      s1 = fma(av[1], yv[1], s1);
+      s2 = fma(av[2], yv[2], s2);
+      s0 = fma(av[3], yv[3], s0);
+      s1 = fma(av[4], yv[4], s1);
+      s2 = fma(av[5], yv[5], s2);
+    }
     for (; k + 3 <= c.z; k += 3) {
       s0 = fma(A[k * ld], y[k], s0);
       s1 = fma(A[(k + 1) * ld], y[k + 1], s1);
