@@ -108,19 +108,22 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_oracle_step(topo, data, cfg, elements):
-    """Oracle fwd (K iterations + final factor) + implicit bwd on the listed elements."""
+def cpu_oracle_step(topo, data, cfg, elements, backward="implicit", eps=1e-3):
+    """Oracle fwd (K iterations [+ final factor]) + implicit or DLM bwd on the listed elements."""
+    from oracle import dlm as odlm
     from oracle import implicit as oimp
     from oracle import lie as olie
     from oracle import nls as onls
     G = "SE3" if cfg["dim"] == 3 else "SE2"
-    opt = onls.Options(optimizer=cfg["opt"], max_iterations=cfg["K"], implicit=True)
+    opt = onls.Options(optimizer=cfg["opt"], max_iterations=cfg["K"], implicit=(backward == "implicit"))
     v = np.ones(topo.num_poses * (6 if cfg["dim"] == 3 else 3))
     for b in elements:
         prob = onls.PGOProblem(G, topo.num_poses, topo.edges, topo.prior_vars, data["meas"][b],
                                data["prior_meas"][b], data["w_edge"], data["w_prior"])
         res = onls.optimize(prob, olie.to_homog(data["poses0"][b]), opt)
-        if res.L_final is not None:
+        if backward == "dlm":
+            odlm.dlm_weight_grads(prob, res.x, v, eps)
+        elif res.L_final is not None:
             oimp.implicit_weight_grads(prob, res.x, v, L_K=res.L_final)
 
 
@@ -131,16 +134,16 @@ def cores():
         return os.cpu_count()
 
 
-def cpu_baseline(cfg, n_elems):
+def cpu_baseline(cfg, n_elems, backward="implicit", eps=1e-3):
     import synth
     topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
     data = synth.cube_batch(topo, n_elems, seed=0)
     t0 = time.perf_counter()
-    cpu_oracle_step(topo, data, cfg, range(n_elems))
+    cpu_oracle_step(topo, data, cfg, range(n_elems), backward, eps)
     dt = time.perf_counter() - t0
     return {"value": n_elems * cfg["K"] / dt, "unit": UNIT, "cores": cores(), "kind": "oracle",
             "sample": f"{n_elems} element(s) of {cfg['desc'].split(':')[0]} (fwd K={cfg['K']} + final factor + "
-                      f"implicit bwd), {dt:.1f} s, numpy/OpenBLAS fp64 dense"}
+                      f"{backward} bwd), {dt:.1f} s, numpy/OpenBLAS fp64 dense"}
 
 
 def run_reference(args, cfg, rank):
@@ -184,6 +187,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-elements", type=int, default=4)
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--backward", default="implicit", choices=["implicit", "dlm"],
+                    help="backward mode timed in the step (dlm: PAPER.md:259-271, one augmented GN step)")
+    ap.add_argument("--epsilon", type=float, default=1e-3, help="DLM epsilon")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -225,7 +231,8 @@ def main():
     g = solver.graph
     st = solver.stats
     opt = solver.options
-    opt.backward_mode = D.BWD_IMPLICIT
+    dlm = args.backward == "dlm"
+    opt.backward_mode = D.BWD_NONE if dlm else D.BWD_IMPLICIT
     host = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in data.items() if k != "gt"}
     vgrad = torch.from_numpy(np.random.default_rng([1, rank]).standard_normal((B, topo.num_poses, d)))
     dv = {k: v.to(dev) for k, v in host.items()}
@@ -253,7 +260,10 @@ def main():
         if record is not None:
             b_.record(stream)
             record.append((a, b_))
-        D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws)
+        if dlm:
+            D.dnls_backward_dlm(g, B, prob, dvg, D.GRAD_TANGENT, args.epsilon, ge, gp, 0, ws)
+        else:
+            D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws)
         if world > 1:
             torch.sum(obj, dim=0, keepdim=True, out=red[E + P:])
             dist.all_reduce(red)
@@ -289,7 +299,7 @@ def main():
 
     # ---- roofline of the dominant kernel (k_forward): algorithmic bytes per launch / duration
     per_iter = st["bytes_linearize"] + st["bytes_factor"] + st["bytes_solve"] + st["bytes_update"]
-    alg_bytes = B * (K * per_iter + st["bytes_linearize"] + st["bytes_factor"])
+    alg_bytes = B * (K * per_iter + (0 if dlm else st["bytes_linearize"] + st["bytes_factor"]))
     peak, peak_src = load_peaks()
     achieved = alg_bytes / Tf / 1e9
     traffic = None
@@ -304,7 +314,8 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "k_forward", "peak_source": peak_src,
                 "alg_bytes_per_launch": alg_bytes, "kernel_ms": Tf * 1e3,
-                "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)+lin+factor) per SURVEY.md 8(d)"}
+                "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)" + ("" if dlm else "+lin+factor") +
+                        ") per SURVEY.md 8(d)"}
 
     # ---- e2e through the public API (PoseGraphSolver) with pinned host buffers
     e2e = None
@@ -323,9 +334,9 @@ def main():
                 dbuf[k].copy_(pin[k], non_blocking=True)
             dvg2.copy_(pvg, non_blocking=True)
             P_, o_, _, _ = solver.forward(dbuf["poses0"], dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"],
-                                          dbuf["w_prior"], implicit=True)
+                                          dbuf["w_prior"], implicit=not dlm)
             g1, g2 = solver.backward(P_, dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"], dbuf["w_prior"], dvg2,
-                                     D.GRAD_TANGENT)
+                                     D.GRAD_TANGENT, mode=args.backward, epsilon=args.epsilon)
             gg = torch.cat([g1, g2])
             if world > 1:
                 dist.all_reduce(gg)
@@ -355,7 +366,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.cpu_elements)
+        cpu = cpu_baseline(cfg, args.cpu_elements, args.backward, args.epsilon)
 
     if rank == 0:
         line = {
@@ -364,7 +375,7 @@ def main():
             "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "global_batch": total_elems, "batch_per_gpu": B,
                        "poses": cfg["N"], "edges": topo.num_edges, "iterations": K,
-                       "optimizer": cfg["opt"], "backward": "implicit",
+                       "optimizer": cfg["opt"], "backward": args.backward,
                        "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
                        "parallelism": f"dp{world}", "nnz_L": st["nnz_L"], "supernodes": st["num_supernodes"],
                        "levels": st["num_levels"]},

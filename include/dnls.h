@@ -200,6 +200,26 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
                                             int64_t grad_bstride, void* workspace, size_t ws_bytes,
                                             void* stream);
 
+/* DLM backward (direct loss minimisation, PAPER.md :259-271 and App. :897-934; DESIGN.md
+ * readings B1-B3):
+ *   theta_direct = argmin S(theta) + || eps delta - v/2 ||^2  (delta in the chart at theta*),
+ *   solved by ONE Gauss-Newton step from theta* (PAPER.md:934):
+ *       (J^T J + 2 eps^2 I) delta_a = J^T r - eps v,   theta_direct = theta* [+] (-delta_a)
+ *   (one extra factorisation of the augmented system), then
+ *       dL/dw_e ~= (1/eps) [ dS/dw_e(theta*) - dS/dw_e(theta_direct) ],  dS/dw_e = w_e ||c_e||^2
+ *   (and the same for the prior weight).  Approaches the implicit gradient as eps -> 0 at a
+ *   converged theta* ("lim eps->0").
+ * prob->poses: theta* (e.g. as returned by dnls_forward; any mode); grad_poses / grad_kind /
+ * grad_w_* / grad_bstride as for dnls_backward_implicit.  epsilon > 0 (finite).
+ * The call does not need a cached factor; it overwrites the factor storage of the workspace, so a
+ * later dnls_backward_implicit on it returns DNLS_E_STATE.  Elements whose augmented system is not
+ * SPD contribute zero gradient.  Errors: DNLS_E_INVALID (NULL grad_poses, bad kind, epsilon),
+ * DNLS_E_SHAPE, DNLS_E_WORKSPACE, DNLS_E_CUDA. */
+DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
+                                       const double* grad_poses, int32_t grad_kind, double epsilon,
+                                       double* grad_w_edge, double* grad_w_prior, int64_t grad_bstride,
+                                       void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- stage-level entry points (standalone solvers, "as standalone ... functions";
  *      SPEC.md:400).  They share the workspace layout of dnls_forward. ---- */
 

@@ -102,6 +102,10 @@ _SIGS = {
     "dnls_backward_implicit": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(DnlsProblem),
                                               ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "dnls_backward_dlm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(DnlsProblem),
+                                         ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
+                                         ctypes.c_void_p]),
     "dnls_linearize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(DnlsProblem), ctypes.c_void_p,
                                       ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "dnls_factorize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,

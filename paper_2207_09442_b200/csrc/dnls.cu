@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -368,6 +369,49 @@ __global__ void __launch_bounds__(NT, 1) k_solve(DevGraph g, DevWs ws, const dou
   }
 }
 
+// upstream gradient of pose o (original order) in right-tangent coordinates: given directly
+// (DNLS_GRAD_TANGENT) or projected from the Euclidean gradient on the matrix entries (App. D)
+template <int D>
+__device__ __forceinline__ void tangent_grad(const double* Tb, const double* gpose, int grad_kind, int b, int N,
+                                             int o, double (&v)[D]) {
+  constexpr int PS = GT<D>::PS;
+  if (grad_kind == DNLS_GRAD_TANGENT) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[a] = gpose[((size_t)b * N + o) * D + a];
+  } else {
+    // v_a = < dL/dT , T G_a >  (top rows), G_a the Lie-algebra generators
+    const double* G = gpose + ((size_t)b * N + o) * PS;
+    const double* T = Tb + (size_t)o * PS;
+    if (D == 6) {
+      // T G_a for translation generators: column 3 = R e_a ; rotation generators: R [e_a]x in the
+      // 3x3 block.   <G, R[e]x> = sum_ij G_ij (R[e]x)_ij
+#pragma unroll
+      for (int a = 0; a < 3; ++a) v[a] = G[0 * 4 + 3] * T[0 * 4 + a] + G[1 * 4 + 3] * T[1 * 4 + a] + G[2 * 4 + 3] * T[2 * 4 + a];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double e[3] = {0.0, 0.0, 0.0};
+        e[a] = 1.0;
+        // [e]x columns: col0 = (0, e2, -e1), col1 = (-e2, 0, e0), col2 = (e1, -e0, 0)
+        double Ex[3][3] = {{0.0, -e[2], e[1]}, {e[2], 0.0, -e[0]}, {-e[1], e[0], 0.0}};
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            double rex = T[i * 4 + 0] * Ex[0][j] + T[i * 4 + 1] * Ex[1][j] + T[i * 4 + 2] * Ex[2][j];
+            acc += G[i * 4 + j] * rex;
+          }
+        v[3 + a] = acc;
+      }
+    } else {
+      v[0] = G[2] * T[0] + G[5] * T[3];
+      v[1] = G[2] * T[1] + G[5] * T[4];
+      // rotation generator [[0,-1],[1,0]]: R*Gen = [[R01, -R00], [R11, -R10]]
+      v[2] = G[0] * T[1] - G[1] * T[0] + G[3] * T[4] - G[4] * T[3];
+    }
+  }
+}
+
 // implicit backward, per element: v -> lambda = H^-1 v (cached factor) -> per-slot weight grads
 template <int D>
 __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
@@ -386,41 +430,7 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
   // v (original order) -> permuted
   for (int o = threadIdx.x; o < g.N; o += NT) {
     double v[D];
-    if (grad_kind == DNLS_GRAD_TANGENT) {
-#pragma unroll
-      for (int a = 0; a < D; ++a) v[a] = gpose[((size_t)b * g.N + o) * D + a];
-    } else {
-      // v_a = < dL/dT , T G_a >  (top rows), G_a the Lie-algebra generators
-      const double* G = gpose + ((size_t)b * g.N + o) * PS;
-      const double* T = Tb + (size_t)o * PS;
-      if (D == 6) {
-        // T G_a for translation generators: column 3 = R e_a ; rotation generators: R [e_a]x in the
-        // 3x3 block.   <G, R[e]x> = sum_ij G_ij (R[e]x)_ij
-#pragma unroll
-        for (int a = 0; a < 3; ++a) v[a] = G[0 * 4 + 3] * T[0 * 4 + a] + G[1 * 4 + 3] * T[1 * 4 + a] + G[2 * 4 + 3] * T[2 * 4 + a];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          double e[3] = {0.0, 0.0, 0.0};
-          e[a] = 1.0;
-          // [e]x columns: col0 = (0, e2, -e1), col1 = (-e2, 0, e0), col2 = (e1, -e0, 0)
-          double Ex[3][3] = {{0.0, -e[2], e[1]}, {e[2], 0.0, -e[0]}, {-e[1], e[0], 0.0}};
-          double acc = 0.0;
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              double rex = T[i * 4 + 0] * Ex[0][j] + T[i * 4 + 1] * Ex[1][j] + T[i * 4 + 2] * Ex[2][j];
-              acc += G[i * 4 + j] * rex;
-            }
-          v[3 + a] = acc;
-        }
-      } else {
-        v[0] = G[2] * T[0] + G[5] * T[3];
-        v[1] = G[2] * T[1] + G[5] * T[4];
-        // rotation generator [[0,-1],[1,0]]: R*Gen = [[R01, -R00], [R11, -R10]]
-        v[2] = G[0] * T[1] - G[1] * T[0] + G[3] * T[4] - G[4] * T[3];
-      }
-    }
+    tangent_grad<D>(Tb, gpose, grad_kind, b, g.N, o, v);
 #pragma unroll
     for (int a = 0; a < D; ++a) x_b[(size_t)g.iperm[o] * D + a] = v[a];
   }
@@ -455,6 +465,63 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
       }
     }
     out_b[slot] = -2.0 * w * dot;
+  }
+}
+
+// DLM backward (PAPER.md :259-271, App. :897-934; readings B1-B3), per element:
+//   linearise at theta*, H_a = J^T J + 2 eps^2 I (identity damping), rhs = J^T r - eps v,
+//   factor + solve (one extra factorisation), theta_direct = theta* [+] (-delta_a)  (one GN step),
+//   per slot  g = (w / eps) (||c(theta*)||^2 - ||c(theta_direct)||^2)  -> k_reduce_wgrad.
+template <int D>
+__global__ void __launch_bounds__(NT, 1) k_backward_dlm(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
+                                                         int grad_kind, double eps) {
+  constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
+  const int b = blockIdx.x;
+  __shared__ double s_red[NT / 32];
+  __shared__ double sh_S, sh_max;
+  __shared__ int sh_fail;
+  const size_t slots = (size_t)g.E + g.P;
+  const double* Tb = pr.poses + (size_t)b * g.N * PS;
+  double* Tdir = ws.trial + (size_t)b * g.N * PS;
+  double* jac_b = ws.jac + (size_t)b * slots * JS;
+  double* cost_b = ws.cost + (size_t)b * slots;
+  double* Lg = ws.L + (size_t)b * g.storage;
+  Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  double* x_b = sm.x;
+  const LView L = full_view(g, Lg, sm);
+  linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, jac_b, 2.0 * eps * eps, DNLS_DAMP_IDENTITY, s_red);
+  finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+  for (int o = threadIdx.x; o < g.N; o += NT) {   // rhs = J^T r - eps v  (permuted order)
+    double v[D];
+    tangent_grad<D>(Tb, gpose, grad_kind, b, g.N, o, v);
+#pragma unroll
+    for (int a = 0; a < D; ++a) x_b[(size_t)g.iperm[o] * D + a] -= eps * v[a];
+  }
+  if (threadIdx.x == 0) sh_fail = 0;
+  __syncthreads();
+  factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, x_b, sm.pp);
+  __syncthreads();
+  const bool ok = sh_fail == 0;
+  if (ok) {
+    solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
+    retract_phase<D, NT>(g, Tb, Tdir, x_b, 1.0);
+  }
+  __syncthreads();
+  for (int slot = threadIdx.x; slot < (int)slots; slot += NT) {
+    double gw = 0.0;
+    if (ok) {
+      double c0[D], c1[D];
+      eval_slot<D>(g, pr, Tb, b, slot, c0, nullptr, nullptr, false);
+      eval_slot<D>(g, pr, Tdir, b, slot, c1, nullptr, nullptr, false);
+      double n0 = 0.0, n1 = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        n0 = fma(c0[a], c0[a], n0);
+        n1 = fma(c1[a], c1[a], n1);
+      }
+      gw = slot_weight<D>(g, pr, b, slot) * (n0 - n1) / eps;
+    }
+    cost_b[slot] = gw;
   }
 }
 
@@ -969,6 +1036,44 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
     k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
                                                         grad_w_prior, (long long)grad_bstride);
     if ((st = cuda_check("dnls_backward_implicit: k_reduce_wgrad launch"))) return st;
+  }
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
+                                       const double* grad_poses, int32_t grad_kind, double epsilon,
+                                       double* grad_w_edge, double* grad_w_prior, int64_t grad_bstride,
+                                       void* workspace, size_t ws_bytes, void* stream) {
+  dnls_status st = check_common("dnls_backward_dlm", g, batch, workspace, ws_bytes);
+  if (st) return st;
+  if ((st = check_problem("dnls_backward_dlm", g, prob))) return st;
+  if (!grad_poses && batch > 0) return fail(DNLS_E_INVALID, "dnls_backward_dlm: grad_poses is NULL");
+  if (grad_kind != DNLS_GRAD_TANGENT && grad_kind != DNLS_GRAD_MATRIX)
+    return fail(DNLS_E_INVALID, "dnls_backward_dlm: unknown grad_kind");
+  if (!(epsilon > 0.0) || !std::isfinite(epsilon))
+    return fail(DNLS_E_INVALID, "dnls_backward_dlm: epsilon must be finite and > 0");
+  if (grad_bstride < 0) return fail(DNLS_E_INVALID, "dnls_backward_dlm: grad_bstride < 0");
+  if (grad_bstride > 0 && grad_bstride < std::max(g->sym.E, g->sym.P))
+    return fail(DNLS_E_SHAPE, "dnls_backward_dlm: grad_bstride smaller than num_edges/num_priors");
+  {   // the augmented factorisation overwrites any implicit factor cached in this workspace
+    dnls_graph* gm = const_cast<dnls_graph*>(g);
+    std::lock_guard<std::mutex> lk(gm->mu);
+    if (gm->last_ws == workspace) {
+      gm->last_ws = nullptr;
+      gm->last_batch = -1;
+    }
+  }
+  if (batch == 0) return DNLS_OK;
+  WsLayout l = ws_layout(g->sym, batch);
+  DevWs ws = ws_views(l, workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward_dlm<DD>, smem_bytes(g->dg), "k_backward_dlm"))) return st; (k_backward_dlm<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind, epsilon)));
+  if ((st = cuda_check("dnls_backward_dlm: k_backward_dlm launch"))) return st;
+  const int slots = g->sym.E + g->sym.P;
+  if (slots > 0 && (grad_w_edge || grad_w_prior)) {
+    k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
+                                                        grad_w_prior, (long long)grad_bstride);
+    if ((st = cuda_check("dnls_backward_dlm: k_reduce_wgrad launch"))) return st;
   }
   return DNLS_OK;
 }

@@ -183,6 +183,15 @@ def dnls_backward_implicit(g: Graph, batch: int, prob: DnlsProblem, grad_poses: 
                                        workspace.numel(), _stream(stream)), "dnls_backward_implicit")
 
 
+def dnls_backward_dlm(g: Graph, batch: int, prob: DnlsProblem, grad_poses: torch.Tensor, grad_kind: int,
+                      epsilon: float, grad_w_edge, grad_w_prior, grad_bstride: int, workspace: torch.Tensor,
+                      stream=None):
+    check(lib().dnls_backward_dlm(g.handle, int(batch), ctypes.byref(prob), _f64(grad_poses, "grad_poses"),
+                                  int(grad_kind), float(epsilon), _f64(grad_w_edge, "grad_w_edge"),
+                                  _f64(grad_w_prior, "grad_w_prior"), int(grad_bstride), _ptr(workspace),
+                                  workspace.numel(), _stream(stream)), "dnls_backward_dlm")
+
+
 def dnls_linearize(g: Graph, batch: int, prob: DnlsProblem, lam, damping: int, workspace: torch.Tensor, stream=None):
     check(lib().dnls_linearize(g.handle, int(batch), ctypes.byref(prob), _f64(lam, "lambda"), int(damping),
                                _ptr(workspace), workspace.numel(), _stream(stream)), "dnls_linearize")

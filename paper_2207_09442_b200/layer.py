@@ -54,7 +54,10 @@ class PoseGraphSolver:
         return out, obj, st, it
 
     def backward(self, poses_K, meas, prior_meas, w_edge, w_prior, grad_poses, grad_kind=D.GRAD_MATRIX,
-                 per_element: bool = False):
+                 per_element: bool = False, mode: str = "implicit", epsilon: float = 1e-3):
+        """Weight gradients for the upstream pose gradient: mode "implicit" (Prop. 1, cached factor
+        of the last implicit forward) or "dlm" (direct loss minimisation, one
+        augmented GN step from poses_K; no cached factor needed)."""
         B = poses_K.shape[0]
         ws = self.workspace(B)
         E, P = self.graph.E, self.graph.P
@@ -68,8 +71,15 @@ class PoseGraphSolver:
             stride = 0
         prob = D.make_problem(poses_K, meas.contiguous(), prior_meas.contiguous(), w_edge.detach().contiguous(),
                               w_prior.detach().contiguous())
-        D.dnls_backward_implicit(self.graph, B, prob, grad_poses.contiguous(), grad_kind,
-                                 ge if E else None, gp if P else None, stride, ws)
+        if mode == "implicit":
+            D.dnls_backward_implicit(self.graph, B, prob, grad_poses.contiguous(), grad_kind,
+                                     ge if E else None, gp if P else None, stride, ws)
+        elif mode == "dlm":
+            D.dnls_backward_dlm(self.graph, B, prob, grad_poses.contiguous(), grad_kind, epsilon,
+                                ge if E else None, gp if P else None, stride, ws)
+            self.generation += 1   # the workspace factor was overwritten
+        else:
+            raise ValueError(f"unknown backward mode {mode!r} (implicit | dlm)")
         if per_element:
             return ge[:, :E], gp[:, :P]
         return ge, gp
@@ -77,9 +87,10 @@ class PoseGraphSolver:
 
 class _PoseGraphFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, solver, poses0, meas, prior_meas, w_edge, w_prior):
-        poses, obj, st, it = solver.forward(poses0, meas, prior_meas, w_edge, w_prior, implicit=True)
+    def forward(ctx, solver, poses0, meas, prior_meas, w_edge, w_prior, mode="implicit", epsilon=1e-3):
+        poses, obj, st, it = solver.forward(poses0, meas, prior_meas, w_edge, w_prior, implicit=(mode == "implicit"))
         ctx.solver = solver
+        ctx.mode, ctx.epsilon = mode, epsilon
         ctx.gen = solver.generation
         ctx.save_for_backward(poses, meas, prior_meas, w_edge, w_prior)
         ctx.mark_non_differentiable(obj, st, it)
@@ -88,22 +99,26 @@ class _PoseGraphFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g_poses, g_obj, g_st, g_it):
         solver = ctx.solver
-        if solver.generation != ctx.gen:
+        if ctx.mode == "implicit" and solver.generation != ctx.gen:
             raise RuntimeError("pose_graph_layer: the solver ran another forward since this one; its cached "
                                "factor is gone (DNLS_E_STATE)")
         poses, meas, prior_meas, w_edge, w_prior = ctx.saved_tensors
         if g_poses is None:
             g_poses = torch.zeros_like(poses)
         ge, gp = solver.backward(poses, meas, prior_meas, w_edge, w_prior, g_poses, D.GRAD_MATRIX,
-                                 per_element=(w_edge.dim() == 2))
+                                 per_element=(w_edge.dim() == 2), mode=ctx.mode, epsilon=ctx.epsilon)
         ge = ge if ctx.needs_input_grad[4] else None
         gp = gp if ctx.needs_input_grad[5] else None
-        return None, None, None, None, ge, gp
+        return None, None, None, None, ge, gp, None, None
 
 
-def pose_graph_layer(solver: PoseGraphSolver, poses0, meas, prior_meas, w_edge, w_prior):
-    """Differentiable solve (implicit backward).  Returns (poses*, objective, status, iterations)."""
+def pose_graph_layer(solver: PoseGraphSolver, poses0, meas, prior_meas, w_edge, w_prior, backward_mode="implicit",
+                     epsilon=1e-3):
+    """Differentiable solve.  backward_mode "implicit" (Prop. 1, factor reuse) or "dlm" (direct loss
+    minimisation with step eps).  Returns (poses*, objective, status, iterations)."""
+    if backward_mode not in ("implicit", "dlm"):
+        raise ValueError(f"unknown backward_mode {backward_mode!r}")
     if poses0.requires_grad or meas.requires_grad or prior_meas.requires_grad:
         raise ValueError("implicit backward gives no gradient for theta_init or measurements "
                          "(PAPER.md Table 6 :726); only w_edge / w_prior may require grad")
-    return _PoseGraphFn.apply(solver, poses0, meas, prior_meas, w_edge, w_prior)
+    return _PoseGraphFn.apply(solver, poses0, meas, prior_meas, w_edge, w_prior, backward_mode, epsilon)

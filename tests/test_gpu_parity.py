@@ -8,6 +8,7 @@ import torch
 
 from gpu_helpers import (DEV, TOL_GRAD, TOL_OBJ, TOL_POSE, D, graph_for, make_case, oimp, olie, onls,
                          oracle_problem, oracle_results, perm_matrix_indices, pose_err, rel_vec_err, to_dev)
+from paper_2207_09442_b200._lib import DnlsError
 from paper_2207_09442_b200.layer import PoseGraphSolver, pose_graph_layer
 
 pytestmark = pytest.mark.gpu
@@ -352,3 +353,59 @@ def test_forward_with_parallel_edges(dim):
     for b, r in enumerate(res):
         assert pose_err(P[b], r.x) <= TOL_POSE
         assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
+
+
+# ------------------------------------------------------------------ DLM backward
+@pytest.mark.parametrize("dim,kind,eps", [(3, D.GRAD_TANGENT, 1e-3), (3, D.GRAD_MATRIX, 1e-2),
+                                          (2, D.GRAD_TANGENT, 1e-4)])
+def test_dlm_backward_matches_oracle(dim, kind, eps):
+    """dnls_backward_dlm (one augmented GN step) vs oracle.dlm on the
+    oracle's own theta_K, per element and batch-summed, 1e-6 relative."""
+    from oracle import dlm as odlm
+    N, B, K = 36, 4, 8
+    topo, data = make_case(N, dim=dim, p=0.3, seed=11, B=B)
+    solver, t, poses, obj, st, it = run_forward(topo, data, max_iterations=K)
+    rng = np.random.default_rng(5)
+    d = 6 if dim == 3 else 3
+    res = oracle_results(topo, data, max_iterations=K)
+    if kind == D.GRAD_TANGENT:
+        v = rng.standard_normal((B, N, d))
+        gpose = torch.from_numpy(v).to(DEV)
+    else:
+        gm = rng.standard_normal(poses.shape)
+        gpose = torch.from_numpy(gm).to(DEV)
+        v = np.stack([oimp.tangent_from_matrix_grad(solver_group(dim), r.x, gm[b]) for b, r in enumerate(res)])
+    gep, gpp = solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"], gpose, kind,
+                               per_element=True, mode="dlm", epsilon=eps)
+    ge, gp = solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"], gpose, kind,
+                             mode="dlm", epsilon=eps)
+    torch.cuda.synchronize()
+    ref = np.zeros(topo.num_edges + 1)
+    for b, r in enumerate(res):
+        a, c, _ = odlm.dlm_weight_grads(oracle_problem(topo, data, b), r.x, v[b].reshape(-1), eps)
+        assert rel_vec_err(np.concatenate([gep[b].cpu().numpy(), gpp[b].cpu().numpy()]),
+                           np.concatenate([a, c])) <= TOL_GRAD
+        ref += np.concatenate([a, c])
+    assert rel_vec_err(np.concatenate([ge.cpu().numpy(), gp.cpu().numpy()]), ref) <= TOL_GRAD
+
+
+def test_dlm_invalidates_implicit_cache_and_layer_mode():
+    topo, data = make_case(30, dim=3, p=0.3, seed=3, B=2)
+    solver, t, poses, obj, st, it = run_forward(topo, data, implicit=True, max_iterations=6)
+    v = torch.zeros(2, 30, 6, dtype=torch.float64, device=DEV)
+    solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"], v, D.GRAD_TANGENT, mode="dlm")
+    with pytest.raises(DnlsError):
+        solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"], v, D.GRAD_TANGENT)
+    with pytest.raises(Exception):
+        solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"], v, D.GRAD_TANGENT,
+                        mode="dlm", epsilon=0.0)
+    # autograd layer in DLM mode: a gradient flows to the weights and matches the direct call
+    w = t["w_edge"].clone().requires_grad_(True)
+    from paper_2207_09442_b200.layer import pose_graph_layer
+    out, *_ = pose_graph_layer(solver, t["poses0"], t["meas"], t["prior_meas"], w, t["w_prior"],
+                               backward_mode="dlm", epsilon=1e-3)
+    gm = torch.from_numpy(np.random.default_rng(0).standard_normal(out.shape)).to(DEV)
+    (out * gm).sum().backward()
+    ge, _ = solver.backward(out.detach(), t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"], gm,
+                            D.GRAD_MATRIX, mode="dlm", epsilon=1e-3)
+    assert torch.allclose(w.grad, ge, rtol=0, atol=0)

@@ -1,0 +1,68 @@
+"""Pins for the oracle DLM backward (oracle/dlm.py; PAPER.md :259-271, App. :897-934;
+DESIGN.md readings B1-B3), -m "not gpu":
+ * closed form: one pose with a prior at its target (theta* = Z, c(theta* [+] u) = u exactly),
+   g_prior = -w eps |v|^2 / (w^2 + 2 eps^2)^2  -- pins the appended residual sqrt2 (eps d - v/2)
+   (the 2 eps^2 shift) and the eps scaling;
+ * the paper's limit ("grad L = lim_{eps->0} g_DLM"): on a converged pose graph
+   |g_DLM(eps) - g_implicit| shrinks linearly in eps (log-log slope ~ 1) -- pins the sign of
+   the -eps v term and of the retraction (a flipped sign converges to -g_implicit);
+ * zero upstream gradient at a converged theta*: g_DLM ~ 0."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import dlm, implicit, lie, nls
+
+
+@pytest.mark.parametrize("G", [lie.SE3, lie.SE2])
+@pytest.mark.parametrize("eps", [1e-1, 1e-3])
+def test_dlm_single_prior_closed_form(G, eps):
+    rng = np.random.default_rng(7)
+    d = G.d
+    Z = G.exp(0.3 * rng.standard_normal((1, d)))
+    w = 1.7
+    prob = nls.PGOProblem(G, 1, np.zeros((0, 2), dtype=np.int32), np.array([0], dtype=np.int32),
+                          np.zeros((0,) + lie.from_homog(Z).shape[1:]), lie.from_homog(Z), np.zeros(0),
+                          np.array([w]))
+    v = rng.standard_normal(d)
+    ge, gp, T_dir = dlm.dlm_weight_grads(prob, Z, v, eps)
+    expect = -w * eps * (v @ v) / (w * w + 2 * eps * eps) ** 2
+    assert ge.shape == (0,)
+    assert abs(gp[0] - expect) <= 1e-12 * abs(expect)
+    # theta_direct = Z Exp(eps v / (w^2 + 2 eps^2))
+    u = G.log(G.inv(Z) @ T_dir).reshape(-1)
+    assert np.allclose(u, eps * v / (w * w + 2 * eps * eps), rtol=1e-12, atol=1e-15)
+
+
+def converged_problem(dim, N, seed):
+    topo = synth.cube_topology(N, dim=dim, p=0.6, seed=seed)   # loop closures: S(theta*) > 0
+    data = synth.cube_batch(topo, 1, seed=seed)
+    G = lie.SE3 if dim == 3 else lie.SE2
+    w = 0.8 + 0.4 * np.random.default_rng(seed).random(topo.num_edges)
+    prob = nls.PGOProblem(G, N, topo.edges, topo.prior_vars, data["meas"][0], data["prior_meas"][0], w,
+                          np.array([1.2]))
+    T = nls.gauss_newton(prob, lie.to_homog(data["poses0"][0]), nls.Options(max_iterations=30)).x
+    return prob, T
+
+
+@pytest.mark.parametrize("dim,N", [(2, 12), (3, 10)])
+def test_dlm_converges_to_implicit_linearly_in_eps(dim, N):
+    prob, T = converged_problem(dim, N, seed=N)
+    v = np.random.default_rng(3).standard_normal(N * prob.d)
+    gi_e, gi_p, _ = implicit.implicit_weight_grads(prob, T, v)
+    gi = np.concatenate([gi_e, gi_p])
+    errs = []
+    epss = [1e-3, 1e-4, 1e-5]
+    for eps in epss:
+        ge, gp, _ = dlm.dlm_weight_grads(prob, T, v, eps)
+        errs.append(np.max(np.abs(np.concatenate([ge, gp]) - gi)) / np.max(np.abs(gi)))
+    slope = np.polyfit(np.log10(epss), np.log10(errs), 1)[0]
+    assert errs[-1] < 5e-3
+    assert 0.8 < slope < 1.2, (errs, slope)
+
+
+def test_dlm_zero_upstream_gradient():
+    prob, T = converged_problem(3, 10, seed=10)
+    assert prob.objective(T) > 1e-3
+    ge, gp, _ = dlm.dlm_weight_grads(prob, T, np.zeros(10 * 6), 1e-3)
+    assert np.max(np.abs(ge)) < 1e-8 and np.max(np.abs(gp)) < 1e-8
