@@ -108,7 +108,7 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_oracle_step(topo, data, cfg, elements, backward="implicit", eps=1e-3):
+def cpu_oracle_step(topo, data, cfg, elements, backward="implicit", eps=1e-3, radius=None):
     """Oracle fwd (K iterations [+ final factor]) + implicit or DLM bwd on the listed elements."""
     from oracle import dlm as odlm
     from oracle import implicit as oimp
@@ -119,7 +119,7 @@ def cpu_oracle_step(topo, data, cfg, elements, backward="implicit", eps=1e-3):
     v = np.ones(topo.num_poses * (6 if cfg["dim"] == 3 else 3))
     for b in elements:
         prob = onls.PGOProblem(G, topo.num_poses, topo.edges, topo.prior_vars, data["meas"][b],
-                               data["prior_meas"][b], data["w_edge"], data["w_prior"])
+                               data["prior_meas"][b], data["w_edge"], data["w_prior"], radius=radius)
         res = onls.optimize(prob, olie.to_homog(data["poses0"][b]), opt)
         if backward == "dlm":
             odlm.dlm_weight_grads(prob, res.x, v, eps)
@@ -134,12 +134,12 @@ def cores():
         return os.cpu_count()
 
 
-def cpu_baseline(cfg, n_elems, backward="implicit", eps=1e-3):
+def cpu_baseline(cfg, n_elems, backward="implicit", eps=1e-3, radius=None):
     import synth
     topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
     data = synth.cube_batch(topo, n_elems, seed=0)
     t0 = time.perf_counter()
-    cpu_oracle_step(topo, data, cfg, range(n_elems), backward, eps)
+    cpu_oracle_step(topo, data, cfg, range(n_elems), backward, eps, radius)
     dt = time.perf_counter() - t0
     return {"value": n_elems * cfg["K"] / dt, "unit": UNIT, "cores": cores(), "kind": "oracle",
             "sample": f"{n_elems} element(s) of {cfg['desc'].split(':')[0]} (fwd K={cfg['K']} + final factor + "
@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--backward", default="implicit", choices=["implicit", "dlm"],
                     help="backward mode timed in the step (dlm: PAPER.md:259-271, one augmented GN step)")
     ap.add_argument("--epsilon", type=float, default=1e-3, help="DLM epsilon")
+    ap.add_argument("--welsch", type=float, default=None,
+                    help="Welsch radius of the Between edges (PAPER.md:168 robust PGO); default: quadratic costs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -245,7 +247,10 @@ def main():
     red = torch.zeros(E + P + 1, dtype=torch.float64, device=dev)   # [grad_w_edge | grad_w_prior | loss]
     ge, gp = red[:E], red[E:E + P]
     ws = solver.workspace(B)
-    prob = D.make_problem(poses, dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"], obj, sts, its)
+    rad = None if args.welsch is None else torch.tensor([args.welsch], dtype=torch.float64, device=dev)
+    gr = None if rad is None else torch.zeros(1, dtype=torch.float64, device=dev)
+    prob = D.make_problem(poses, dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"], obj, sts, its,
+                          radius=rad)
     stream = torch.cuda.current_stream()
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -261,9 +266,9 @@ def main():
             b_.record(stream)
             record.append((a, b_))
         if dlm:
-            D.dnls_backward_dlm(g, B, prob, dvg, D.GRAD_TANGENT, args.epsilon, ge, gp, 0, ws)
+            D.dnls_backward_dlm(g, B, prob, dvg, D.GRAD_TANGENT, args.epsilon, ge, gp, 0, ws, grad_radius=gr)
         else:
-            D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws)
+            D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws, grad_radius=gr)
         if world > 1:
             torch.sum(obj, dim=0, keepdim=True, out=red[E + P:])
             dist.all_reduce(red)
@@ -323,7 +328,7 @@ def main():
         pin = {k: v.pin_memory() for k, v in host.items()}
         pvg = vgrad.pin_memory()
         out_obj = torch.empty(B, dtype=torch.float64).pin_memory()
-        out_g = torch.empty(E + P, dtype=torch.float64).pin_memory()
+        out_g = torch.empty(E + P + (0 if rad is None else 1), dtype=torch.float64).pin_memory()
         bi = sum(v.numel() * v.element_size() for v in pin.values()) + pvg.numel() * 8
         bo = out_obj.numel() * 8 + out_g.numel() * 8
         dbuf = {k: torch.empty_like(v, device=dev) for k, v in pin.items()}
@@ -334,10 +339,10 @@ def main():
                 dbuf[k].copy_(pin[k], non_blocking=True)
             dvg2.copy_(pvg, non_blocking=True)
             P_, o_, _, _ = solver.forward(dbuf["poses0"], dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"],
-                                          dbuf["w_prior"], implicit=not dlm)
-            g1, g2 = solver.backward(P_, dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"], dbuf["w_prior"], dvg2,
-                                     D.GRAD_TANGENT, mode=args.backward, epsilon=args.epsilon)
-            gg = torch.cat([g1, g2])
+                                          dbuf["w_prior"], implicit=not dlm, radius=rad)
+            gs = solver.backward(P_, dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"], dbuf["w_prior"], dvg2,
+                                 D.GRAD_TANGENT, mode=args.backward, epsilon=args.epsilon, radius=rad)
+            gg = torch.cat([g.reshape(-1) for g in gs])
             if world > 1:
                 dist.all_reduce(gg)
             out_g.copy_(gg, non_blocking=True)
@@ -366,7 +371,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.cpu_elements, args.backward, args.epsilon)
+        cpu = cpu_baseline(cfg, args.cpu_elements, args.backward, args.epsilon, args.welsch)
 
     if rank == 0:
         line = {
@@ -376,6 +381,7 @@ def main():
             "config": {"workload": cfg["desc"], "global_batch": total_elems, "batch_per_gpu": B,
                        "poses": cfg["N"], "edges": topo.num_edges, "iterations": K,
                        "optimizer": cfg["opt"], "backward": args.backward,
+                       "robust": "none" if args.welsch is None else f"welsch k={args.welsch}",
                        "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
                        "parallelism": f"dp{world}", "nnz_L": st["nnz_L"], "supernodes": st["num_supernodes"],
                        "levels": st["num_levels"]},

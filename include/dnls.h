@@ -102,6 +102,12 @@ typedef struct dnls_problem {
   double* objective;           /* out [B]: S(theta_K) = 1/2 sum ||w c||^2 (with the 1/2) */
   int32_t* status;             /* out [B]: DNLS_ST_* */
   int32_t* iterations;         /* out [B]: iterations executed (LM: accepted + rejected) */
+  /* Welsch robust kernel on every Between edge ("learn the radius of a Welsh robust
+   * cost function"; readings W1-W3): NULL = plain quadratic costs; else the radius k > 0,
+   * [1] shared (stride 0) or [B] per element.  An edge then costs rho_k(s) = k^2/2 (1 - e^{-s/k^2}),
+   * s = ||w c||^2, and the GN step is the IRLS step (J, r rescaled by sqrt(psi), psi = e^{-s/k^2}). */
+  const double* radius;
+  int64_t radius_bstride;
 } dnls_problem;
 
 typedef struct dnls_stats {
@@ -192,11 +198,14 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
  *   gradient on the pose matrices (DNLS_GRAD_MATRIX; projected on the device, App. D).
  * grad_w_edge / grad_w_prior: outputs, [E]/[P] summed over the batch in a fixed order when
  *   grad_bstride == 0, else per element with that stride (doubles).  Either may be NULL.
+ * grad_radius: output dL/dk of the Welsch radius (prob->radius != NULL), laid out like the radius:
+ *   [1] summed over the batch for a shared radius (radius_bstride == 0), else [B]; may be NULL.  With a robust kernel the weight
+ *   gradient is -2 w psi (1 - s/k^2) (C lambda) . c and dL/dk = -sum_e (2 s/k^3) psi w^2 (C lambda) . c.
  * prob->poses must hold theta_K as returned by that forward; weights/measurements unchanged.
  * Errors: DNLS_E_STATE if the workspace holds no implicit factor for (graph, batch). */
 DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
                                             const double* grad_poses, int32_t grad_kind,
-                                            double* grad_w_edge, double* grad_w_prior,
+                                            double* grad_w_edge, double* grad_w_prior, double* grad_radius,
                                             int64_t grad_bstride, void* workspace, size_t ws_bytes,
                                             void* stream);
 
@@ -210,15 +219,16 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
  *   (and the same for the prior weight).  Approaches the implicit gradient as eps -> 0 at a
  *   converged theta* ("lim eps->0").
  * prob->poses: theta* (e.g. as returned by dnls_forward; any mode); grad_poses / grad_kind /
- * grad_w_* / grad_bstride as for dnls_backward_implicit.  epsilon > 0 (finite).
+ * grad_w_* / grad_radius / grad_bstride as for dnls_backward_implicit (Welsch: dS/dw_e = psi w ||c||^2,
+ * dS/dk = k (1 - psi) - (s/k) psi).  epsilon > 0 (finite).
  * The call does not need a cached factor; it overwrites the factor storage of the workspace, so a
  * later dnls_backward_implicit on it returns DNLS_E_STATE.  Elements whose augmented system is not
  * SPD contribute zero gradient.  Errors: DNLS_E_INVALID (NULL grad_poses, bad kind, epsilon),
  * DNLS_E_SHAPE, DNLS_E_WORKSPACE, DNLS_E_CUDA. */
 DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
                                        const double* grad_poses, int32_t grad_kind, double epsilon,
-                                       double* grad_w_edge, double* grad_w_prior, int64_t grad_bstride,
-                                       void* workspace, size_t ws_bytes, void* stream);
+                                       double* grad_w_edge, double* grad_w_prior, double* grad_radius,
+                                       int64_t grad_bstride, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---- stage-level entry points (standalone solvers, "as standalone ... functions";
  *      SPEC.md:400).  They share the workspace layout of dnls_forward. ---- */

@@ -20,4 +20,4 @@ of the solve, zero-noise invariants, SE2-in-SE3 embedding, gauge invariance.
 Parity unpinned (self-consistency only): the LM damping schedule constants (our
 choice, SPEC.md:415 values) -- see DESIGN.md "Readings".
 """
-from . import lie, costs, linalg, nls, implicit, dlm  # noqa: F401
+from . import lie, costs, linalg, robust, nls, implicit, dlm  # noqa: F401

@@ -24,14 +24,15 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import linalg
+from . import linalg, robust
 from .nls import PGOProblem
 
 
 def weight_partials(prob: PGOProblem, T):
-    """dS/dw at fixed theta: w_e ||c_e(theta)||^2 per edge, w_p ||c_p||^2 per prior (B3)."""
+    """dS/dw at fixed theta: w_e ||c_e(theta)||^2 per edge (x psi_e with a Welsch kernel, W1-W2),
+    w_p ||c_p||^2 per prior (B3)."""
     c, _, _ = prob.edge_terms(T)
-    ge = prob.w * np.einsum("ea,ea->e", c, c)
+    ge = prob.irls_weights(c) * prob.w * np.einsum("ea,ea->e", c, c)
     gp = np.zeros(len(prob.prior_vars))
     if len(prob.prior_vars):
         cp, _ = prob.prior_terms(T)
@@ -53,3 +54,14 @@ def dlm_weight_grads(prob: PGOProblem, T_star, v, eps: float):
     ge0, gp0 = weight_partials(prob, T_star)
     ge1, gp1 = weight_partials(prob, T_dir)
     return (ge0 - ge1) / eps, (gp0 - gp1) / eps, T_dir
+
+
+def dlm_radius_grad(prob: PGOProblem, T_star, T_dir, eps: float):
+    """(1/eps) [dS/dk(theta*) - dS/dk(theta_direct)],  dS/dk = sum_e d rho_k(s_e)/dk  (W1)."""
+    if prob.radius is None:
+        return 0.0
+
+    def part(T):
+        c, _, _ = prob.edge_terms(T)
+        return float(np.sum(robust.drho_dk(np.sum((prob.w[:, None] * c) ** 2, axis=1), prob.radius)))
+    return (part(T_star) - part(T_dir)) / eps

@@ -19,19 +19,42 @@ from .nls import PGOProblem
 
 
 def _weight_vjp(prob: PGOProblem, T, lam):
-    """dL/dw = -2 w (C lambda) . c for every edge and prior (unweighted C, c)."""
+    """dL/dphi = -lambda^T D_phi g with g = grad S = sum_e psi_e w_e^2 C_e^T c_e + priors:
+    dL/dw_e = -2 w_e psi_e (1 - s_e/k^2) (C_e lambda_e) . c_e   (psi = 1, k = inf without kernel),
+    priors: -2 w_p (C_p lambda_p) . c_p (readings W1-W3; the radius: ``radius_vjp``)."""
     d = prob.d
     lam = np.asarray(lam).reshape(prob.n_vars, d)
     c, Ci, Cj = prob.edge_terms(T)
     e = prob.edges
     Cl = np.einsum("eab,eb->ea", Ci, lam[e[:, 0]]) + np.einsum("eab,eb->ea", Cj, lam[e[:, 1]])
-    g_edge = -2.0 * prob.w * np.einsum("ea,ea->e", Cl, c)
+    dot = np.einsum("ea,ea->e", Cl, c)
+    if prob.radius is None:
+        g_edge = -2.0 * prob.w * dot
+    else:
+        k = prob.radius
+        s = np.sum((prob.w[:, None] * c) ** 2, axis=1)
+        p = np.exp(-s / (k * k))
+        g_edge = -2.0 * prob.w * p * (1.0 - s / (k * k)) * dot
     g_prior = np.zeros(len(prob.prior_vars))
     if len(prob.prior_vars):
         cp, Cp = prob.prior_terms(T)
         Clp = np.einsum("pab,pb->pa", Cp, lam[prob.prior_vars])
         g_prior = -2.0 * prob.wp * np.einsum("pa,pa->p", Clp, cp)
     return g_edge, g_prior
+
+
+def radius_vjp(prob: PGOProblem, T, lam):
+    """dL/dk = -lambda^T D_k g = -sum_e (2 s_e / k^3) psi_e w_e^2 (C_e lambda_e) . c_e  (W1-W3)."""
+    if prob.radius is None:
+        return 0.0
+    lam = np.asarray(lam).reshape(prob.n_vars, prob.d)
+    c, Ci, Cj = prob.edge_terms(T)
+    e = prob.edges
+    Cl = np.einsum("eab,eb->ea", Ci, lam[e[:, 0]]) + np.einsum("eab,eb->ea", Cj, lam[e[:, 1]])
+    k = prob.radius
+    s = np.sum((prob.w[:, None] * c) ** 2, axis=1)
+    p = np.exp(-s / (k * k))
+    return float(-np.sum(2.0 * s / k ** 3 * p * prob.w ** 2 * np.einsum("ea,ea->e", Cl, c)))
 
 
 def implicit_weight_grads(prob: PGOProblem, T_K, v, L_K=None):

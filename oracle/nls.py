@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import costs, linalg
+from . import costs, linalg, robust
 from .lie import group, to_homog
 
 ST_OK, ST_CONVERGED, ST_NOT_SPD, ST_SATURATED = 0, 1, 2, 3
@@ -33,7 +33,9 @@ ST_OK, ST_CONVERGED, ST_NOT_SPD, ST_SATURATED = 0, 1, 2, 3
 class PGOProblem:
     """One batch element of a pose graph (poses are homogeneous matrices [N, m, m])."""
 
-    def __init__(self, G, num_vars, edges, prior_vars, meas, prior_meas, w_edge, w_prior):
+    def __init__(self, G, num_vars, edges, prior_vars, meas, prior_meas, w_edge, w_prior, radius=None):
+        """radius: Welsch radius k of the Between edges (oracle.robust, readings W1-W3) or None."""
+        self.radius = None if radius is None else float(radius)
         self.G = group(G) if not hasattr(G, "d") else G
         self.d = self.G.d
         self.n_vars = int(num_vars)
@@ -54,13 +56,29 @@ class PGOProblem:
         return costs.prior(self.G, T[self.prior_vars], self.Zp)
 
     def objective(self, T):
-        return costs.objective(self.G, T, self.edges, self.Z, self.w, self.prior_vars, self.Zp, self.wp)
+        if self.radius is None:
+            return costs.objective(self.G, T, self.edges, self.Z, self.w, self.prior_vars, self.Zp, self.wp)
+        c, _, _ = self.edge_terms(T)
+        s = np.sum((self.w[:, None] * c) ** 2, axis=1)
+        S = float(np.sum(robust.rho(s, self.radius)))
+        if len(self.prior_vars):
+            cp, _ = self.prior_terms(T)
+            S += 0.5 * float(np.sum((self.wp[:, None] * cp) ** 2))
+        return S
+
+    def irls_weights(self, c):
+        """psi_e = exp(-||w_e c_e||^2 / k^2) per edge (ones without a robust kernel)."""
+        if self.radius is None:
+            return np.ones(len(self.w))
+        return robust.psi(np.sum((self.w[:, None] * c) ** 2, axis=1), self.radius)
 
     def blocks(self, T):
+        """Weighted (and, with a robust kernel, IRLS-rescaled by sqrt(psi)) Jacobians / residuals."""
         c, Ci, Cj = self.edge_terms(T)
+        sq = np.sqrt(self.irls_weights(c))
         out = []
         for k, (i, j) in enumerate(self.edges):
-            w = self.w[k]
+            w = self.w[k] * sq[k]
             out.append(((int(i), int(j)), [w * Ci[k], w * Cj[k]], w * c[k]))
         if len(self.prior_vars):
             cp, Cp = self.prior_terms(T)
@@ -70,7 +88,7 @@ class PGOProblem:
 
     def linearize(self, T):
         blocks = self.blocks(T)
-        S = 0.5 * sum(float(r @ r) for _, _, r in blocks)
+        S = 0.5 * sum(float(r @ r) for _, _, r in blocks) if self.radius is None else self.objective(T)
         H, b = linalg.assemble(self.n_vars, self.d, blocks)
         return S, H, b
 
@@ -211,11 +229,12 @@ def optimize(prob, x0, opt: Options) -> Result:
 
 
 def solve_batch(G, num_vars, edges, prior_vars, poses0, meas, prior_meas, w_edge, w_prior,
-                opt: Options, elements=None):
+                opt: Options, elements=None, radius=None):
     """Run the oracle on batch elements (all, or the listed indices).
 
     poses0/meas/prior_meas are [B][..][r][r+1] top-row arrays; w_edge/w_prior are [E]/[P]
-    (shared) or [B][E]/[B][P].  Returns a list of Result (poses in homogeneous form).
+    (shared) or [B][E]/[B][P]; radius None, a scalar or [B] (Welsch kernel of the edges).
+    Returns a list of Result (poses in homogeneous form).
     """
     Gr = group(G) if not hasattr(G, "d") else G
     B = np.shape(poses0)[0]
@@ -224,7 +243,8 @@ def solve_batch(G, num_vars, edges, prior_vars, poses0, meas, prior_meas, w_edge
     for b in idx:
         we = np.asarray(w_edge)
         wp = np.asarray(w_prior)
+        rk = None if radius is None else float(np.asarray(radius).reshape(-1)[b if np.size(radius) > 1 else 0])
         prob = PGOProblem(Gr, num_vars, edges, prior_vars, meas[b], prior_meas[b],
-                          we[b] if we.ndim == 2 else we, wp[b] if wp.ndim == 2 else wp)
+                          we[b] if we.ndim == 2 else we, wp[b] if wp.ndim == 2 else wp, radius=rk)
         out.append(optimize(prob, to_homog(poses0[b]), opt))
     return out

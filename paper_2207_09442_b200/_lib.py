@@ -51,6 +51,8 @@ class DnlsProblem(ctypes.Structure):
         ("objective", ctypes.c_void_p),
         ("status", ctypes.c_void_p),
         ("iterations", ctypes.c_void_p),
+        ("radius", ctypes.c_void_p),
+        ("radius_bstride", ctypes.c_int64),
     ]
 
 
@@ -101,11 +103,12 @@ _SIGS = {
                                     ctypes.POINTER(DnlsProblem), ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "dnls_backward_implicit": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(DnlsProblem),
                                               ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
-                                              ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+                                              ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
+                                              ctypes.c_void_p]),
     "dnls_backward_dlm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(DnlsProblem),
                                          ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p,
-                                         ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
-                                         ctypes.c_void_p]),
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                         ctypes.c_size_t, ctypes.c_void_p]),
     "dnls_linearize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(DnlsProblem), ctypes.c_void_p,
                                       ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "dnls_factorize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,

@@ -56,7 +56,7 @@ struct dnls_graph {
 // ----------------------------------------------------------------------------- workspace layout
 namespace {
 struct WsLayout {
-  size_t L, x, jac, cost, trial, S, Sprev, lam, maxd, st, it, total;
+  size_t L, x, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, total;
 };
 WsLayout ws_layout(const Symbolic& s, int B) {
   const int D = s.D, PS = D == 6 ? 12 : 6, JS = D * (D + 1) + 2 * D + D * D;   // GT<D>::JS
@@ -67,6 +67,7 @@ WsLayout ws_layout(const Symbolic& s, int B) {
   w.x = o;     o = align_up(o + sizeof(double) * (size_t)B * n);
   w.jac = o;   o = align_up(o + sizeof(double) * (size_t)B * slots * JS);
   w.cost = o;  o = align_up(o + sizeof(double) * (size_t)B * slots);
+  w.rgrad = o; o = align_up(o + sizeof(double) * (size_t)B * slots);
   w.trial = o; o = align_up(o + sizeof(double) * (size_t)B * s.N * PS);
   w.S = o;     o = align_up(o + sizeof(double) * B);
   w.Sprev = o; o = align_up(o + sizeof(double) * B);
@@ -84,6 +85,7 @@ DevWs ws_views(const WsLayout& l, void* base) {
   w.x = (double*)(p + l.x);
   w.jac = (double*)(p + l.jac);
   w.cost = (double*)(p + l.cost);
+  w.rgrad = (double*)(p + l.rgrad);
   w.trial = (double*)(p + l.trial);
   w.S = (double*)(p + l.S);
   w.Sprev = (double*)(p + l.Sprev);
@@ -103,6 +105,8 @@ DevProb dev_prob(const dnls_problem* p) {
   d.we_bstride = p->w_edge_bstride;
   d.w_prior = p->w_prior;
   d.wp_bstride = p->w_prior_bstride;
+  d.radius = p->radius;
+  d.r_bstride = p->radius_bstride;
   return d;
 }
 }  // namespace
@@ -423,8 +427,9 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
   Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
   double* x_b = sm.x;
   double* out_b = ws.cost + (size_t)b * slots;
+  double* rg_b = ws.rgrad + (size_t)b * slots;
   if (ws.st[b] == DNLS_ST_NOT_SPD) {   // no valid factor: zero gradient contribution
-    for (int s = threadIdx.x; s < (int)slots; s += NT) out_b[s] = 0.0;
+    for (int s = threadIdx.x; s < (int)slots; s += NT) out_b[s] = rg_b[s] = 0.0;
     return;
   }
   // v (original order) -> permuted
@@ -464,7 +469,21 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
         dot += cl * c[r];
       }
     }
-    out_b[slot] = -2.0 * w * dot;
+    // Welsch edge (W1-W2): g_e = psi w^2 C^T c  =>  d/dw = 2 w psi (1 - s/k^2),  d/dk = (2 s/k^3) psi w^2
+    double n2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) n2 = fma(c[a], c[a], n2);
+    double psi;
+    const double sq = w * w * n2;
+    slot_cost(g, pr, b, slot, sq, psi);
+    double fw = 1.0, rg = 0.0;
+    if (pr.radius != nullptr && slot < g.E) {
+      const double k = pr.radius[(size_t)b * pr.r_bstride];
+      fw = psi * (1.0 - sq / (k * k));
+      rg = -2.0 * sq / (k * k * k) * psi * w * w * dot;
+    }
+    out_b[slot] = -2.0 * w * fw * dot;
+    rg_b[slot] = rg;
   }
 }
 
@@ -507,8 +526,9 @@ __global__ void __launch_bounds__(NT, 1) k_backward_dlm(DevGraph g, DevProb pr, 
     retract_phase<D, NT>(g, Tb, Tdir, x_b, 1.0);
   }
   __syncthreads();
+  double* rg_b = ws.rgrad + (size_t)b * slots;
   for (int slot = threadIdx.x; slot < (int)slots; slot += NT) {
-    double gw = 0.0;
+    double gw = 0.0, gr = 0.0;
     if (ok) {
       double c0[D], c1[D];
       eval_slot<D>(g, pr, Tb, b, slot, c0, nullptr, nullptr, false);
@@ -519,10 +539,40 @@ __global__ void __launch_bounds__(NT, 1) k_backward_dlm(DevGraph g, DevProb pr, 
         n0 = fma(c0[a], c0[a], n0);
         n1 = fma(c1[a], c1[a], n1);
       }
-      gw = slot_weight<D>(g, pr, b, slot) * (n0 - n1) / eps;
+      const double w = slot_weight<D>(g, pr, b, slot);
+      double p0, p1;   // dS/dw = psi w ||c||^2 (psi = 1 for quadratic costs)
+      slot_cost(g, pr, b, slot, w * w * n0, p0);
+      slot_cost(g, pr, b, slot, w * w * n1, p1);
+      gw = w * (p0 * n0 - p1 * n1) / eps;
+      if (pr.radius != nullptr && slot < g.E) {   // dS/dk = k (1 - psi) - (s/k) psi
+        const double k = pr.radius[(size_t)b * pr.r_bstride];
+        const double s0 = w * w * n0, s1 = w * w * n1;
+        const double d0 = -k * expm1(-s0 / (k * k)) - s0 / k * p0, d1 = -k * expm1(-s1 / (k * k)) - s1 / k * p1;
+        gr = (d0 - d1) / eps;
+      }
     }
     cost_b[slot] = gw;
+    rg_b[slot] = gr;
   }
+}
+
+// radius gradient: per element the fixed-order sum over edge slots, then, for a shared radius
+// (radius_bstride == 0), over the batch in order; per-element radii get per-element gradients; one warp
+__global__ void k_reduce_radius(int B, int E, int slots, const double* src, double* out, long long bstride) {
+  const int lane = threadIdx.x;
+  double tot = 0.0;
+  for (int b = 0; b < B; ++b) {
+    double s = 0.0;
+    for (int e = lane; e < E; e += 32) s += src[(size_t)b * slots + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (bstride > 0) {
+      if (lane == 0) out[b] = s;
+    } else {
+      tot += s;
+    }
+  }
+  if (bstride == 0 && lane == 0) out[0] = tot;
 }
 
 // fixed-order batch reduction (or per-element copy) of the per-slot weight gradients
@@ -931,7 +981,7 @@ dnls_status check_problem(const char* fn, const dnls_graph* g, const dnls_proble
     return fail(DNLS_E_INVALID, std::string(fn) + ": problem.meas / w_edge is NULL with num_edges > 0");
   if (g->sym.P > 0 && (!p->prior_meas || !p->w_prior))
     return fail(DNLS_E_INVALID, std::string(fn) + ": problem.prior_meas / w_prior is NULL with num_priors > 0");
-  if (p->prior_meas_bstride < 0 || p->w_edge_bstride < 0 || p->w_prior_bstride < 0)
+  if (p->prior_meas_bstride < 0 || p->w_edge_bstride < 0 || p->w_prior_bstride < 0 || p->radius_bstride < 0)
     return fail(DNLS_E_INVALID, std::string(fn) + ": negative batch stride");
   return DNLS_OK;
 }
@@ -1006,8 +1056,8 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
 
 DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
                                             const double* grad_poses, int32_t grad_kind, double* grad_w_edge,
-                                            double* grad_w_prior, int64_t grad_bstride, void* workspace,
-                                            size_t ws_bytes, void* stream) {
+                                            double* grad_w_prior, double* grad_radius, int64_t grad_bstride,
+                                            void* workspace, size_t ws_bytes, void* stream) {
   dnls_status st = check_common("dnls_backward_implicit", g, batch, workspace, ws_bytes);
   if (st) return st;
   if ((st = check_problem("dnls_backward_implicit", g, prob))) return st;
@@ -1037,13 +1087,17 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
                                                         grad_w_prior, (long long)grad_bstride);
     if ((st = cuda_check("dnls_backward_implicit: k_reduce_wgrad launch"))) return st;
   }
+  if (grad_radius && prob->radius) {
+    k_reduce_radius<<<1, 32, 0, s>>>(batch, g->sym.E, slots, ws.rgrad, grad_radius, (long long)prob->radius_bstride);
+    if ((st = cuda_check("dnls_backward_implicit: k_reduce_radius launch"))) return st;
+  }
   return DNLS_OK;
 }
 
 DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
                                        const double* grad_poses, int32_t grad_kind, double epsilon,
-                                       double* grad_w_edge, double* grad_w_prior, int64_t grad_bstride,
-                                       void* workspace, size_t ws_bytes, void* stream) {
+                                       double* grad_w_edge, double* grad_w_prior, double* grad_radius,
+                                       int64_t grad_bstride, void* workspace, size_t ws_bytes, void* stream) {
   dnls_status st = check_common("dnls_backward_dlm", g, batch, workspace, ws_bytes);
   if (st) return st;
   if ((st = check_problem("dnls_backward_dlm", g, prob))) return st;
@@ -1074,6 +1128,10 @@ DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const
     k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
                                                         grad_w_prior, (long long)grad_bstride);
     if ((st = cuda_check("dnls_backward_dlm: k_reduce_wgrad launch"))) return st;
+  }
+  if (grad_radius && prob->radius) {
+    k_reduce_radius<<<1, 32, 0, s>>>(batch, g->sym.E, slots, ws.rgrad, grad_radius, (long long)prob->radius_bstride);
+    if ((st = cuda_check("dnls_backward_dlm: k_reduce_radius launch"))) return st;
   }
   return DNLS_OK;
 }

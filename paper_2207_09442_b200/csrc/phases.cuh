@@ -103,6 +103,8 @@ struct DevProb {
   long long we_bstride;
   const double* w_prior;
   long long wp_bstride;
+  const double* radius;   // Welsch radius (nullptr: quadratic costs), readings W1-W3
+  long long r_bstride;
 };
 
 // per-call workspace views (device)
@@ -111,6 +113,7 @@ struct DevWs {
   double* x;      // [B][n]   rhs / solution (permuted order)
   double* jac;    // [B][E+P][JS]  weighted J_i, J_j, r per cost slot
   double* cost;   // [B][E+P]      1/2 |r|^2 per slot (or weight gradient in backward)
+  double* rgrad;  // [B][E+P]      per-slot radius gradient (backward with a Welsch kernel)
   double* trial;  // [B][N][PS]    LM trial poses
   double* S;      // [B] current objective
   double* Sprev;  // [B]
@@ -321,6 +324,21 @@ __device__ __forceinline__ double slot_weight(const DevGraph& g, const DevProb& 
                     : pr.w_prior[(size_t)b * pr.wp_bstride + (slot - g.E)];
 }
 
+// Cost of a slot from its weighted squared error s = ||w c||^2 (readings A6, W1-W2): returns the
+// slot's objective term and sets psi, the IRLS weight of its Jacobian/residual (1 if quadratic).
+//   quadratic: s / 2, psi = 1;   Welsch (edges, radius k): -k^2/2 expm1(-s/k^2), psi = e^{-s/k^2}
+__device__ __forceinline__ double slot_cost(const DevGraph& g, const DevProb& pr, int b, int slot, double s,
+                                            double& psi) {
+  if (pr.radius == nullptr || slot >= g.E) {
+    psi = 1.0;
+    return 0.5 * s;
+  }
+  const double k = pr.radius[(size_t)b * pr.r_bstride];
+  const double x = -s / (k * k);
+  psi = exp(x);
+  return -0.5 * k * k * expm1(x);
+}
+
 // deterministic CTA-wide sum of v[0..n) : warp 0 only, fixed summation order.  Returns the
 // value on every thread of warp 0 (callers use lane 0).
 __device__ __forceinline__ double warp0_sum(const double* v, int n) {
@@ -371,7 +389,8 @@ __device__ void objective_phase(const DevGraph& g, const DevProb& pr, const doub
     double n2 = 0.0;
 #pragma unroll
     for (int q = 0; q < D; ++q) n2 += (w * c[q]) * (w * c[q]);
-    cost_b[slot] = 0.5 * n2;
+    double psi;
+    cost_b[slot] = slot_cost(g, pr, b, slot, n2, psi);
   }
 }
 
@@ -744,7 +763,9 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
     double n2 = 0.0;
 #pragma unroll
     for (int q = 0; q < D; ++q) n2 = fma(J.c[q], J.c[q], n2);
-    cost_b[slot] = 0.5 * J.ww * n2;
+    double psi;
+    cost_b[slot] = slot_cost(g, pr, b, slot, J.ww * n2, psi);
+    J.ww *= psi;   // IRLS rescaling of the slot's H blocks and J^T r (W2)
     const int4 d0 = g.slot_desc[3 * slot], d1 = g.slot_desc[3 * slot + 1], d2 = g.slot_desc[3 * slot + 2];
     const bool edge = d0.y >= 0;
     double* o = scr + (size_t)slot * SC::SIZE;

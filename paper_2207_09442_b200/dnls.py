@@ -149,8 +149,10 @@ def alloc_workspace(g: Graph, batch: int, opt: DnlsOptions | None = None, device
     return ws
 
 
-def make_problem(poses, meas, prior_meas, w_edge, w_prior, objective=None, status=None, iterations=None):
-    """dnls_problem from tensors.  prior_meas / weights with no batch axis are shared (stride 0)."""
+def make_problem(poses, meas, prior_meas, w_edge, w_prior, objective=None, status=None, iterations=None,
+                 radius=None):
+    """dnls_problem from tensors.  prior_meas / weights with no batch axis are shared (stride 0).
+    radius: Welsch radius of the Between edges, [1] shared or [B] per element, or None (quadratic)."""
     pr = DnlsProblem()
     pr.poses = _f64(poses, "poses")
     pr.meas = _f64(meas, "meas")
@@ -167,6 +169,8 @@ def make_problem(poses, meas, prior_meas, w_edge, w_prior, objective=None, statu
         raise TypeError("iterations must be int32")
     pr.status = _ptr(status)
     pr.iterations = _ptr(iterations)
+    pr.radius = _f64(radius, "radius")
+    pr.radius_bstride = 1 if radius is not None and radius.numel() > 1 else 0
     return pr
 
 
@@ -176,20 +180,23 @@ def dnls_forward(g: Graph, batch: int, opt: DnlsOptions, prob: DnlsProblem, work
 
 
 def dnls_backward_implicit(g: Graph, batch: int, prob: DnlsProblem, grad_poses: torch.Tensor, grad_kind: int,
-                           grad_w_edge, grad_w_prior, grad_bstride: int, workspace: torch.Tensor, stream=None):
+                           grad_w_edge, grad_w_prior, grad_bstride: int, workspace: torch.Tensor, stream=None,
+                           grad_radius=None):
     check(lib().dnls_backward_implicit(g.handle, int(batch), ctypes.byref(prob), _f64(grad_poses, "grad_poses"),
                                        int(grad_kind), _f64(grad_w_edge, "grad_w_edge"),
-                                       _f64(grad_w_prior, "grad_w_prior"), int(grad_bstride), _ptr(workspace),
-                                       workspace.numel(), _stream(stream)), "dnls_backward_implicit")
+                                       _f64(grad_w_prior, "grad_w_prior"), _f64(grad_radius, "grad_radius"),
+                                       int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream)),
+          "dnls_backward_implicit")
 
 
 def dnls_backward_dlm(g: Graph, batch: int, prob: DnlsProblem, grad_poses: torch.Tensor, grad_kind: int,
                       epsilon: float, grad_w_edge, grad_w_prior, grad_bstride: int, workspace: torch.Tensor,
-                      stream=None):
+                      stream=None, grad_radius=None):
     check(lib().dnls_backward_dlm(g.handle, int(batch), ctypes.byref(prob), _f64(grad_poses, "grad_poses"),
                                   int(grad_kind), float(epsilon), _f64(grad_w_edge, "grad_w_edge"),
-                                  _f64(grad_w_prior, "grad_w_prior"), int(grad_bstride), _ptr(workspace),
-                                  workspace.numel(), _stream(stream)), "dnls_backward_dlm")
+                                  _f64(grad_w_prior, "grad_w_prior"), _f64(grad_radius, "grad_radius"),
+                                  int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream)),
+          "dnls_backward_dlm")
 
 
 def dnls_linearize(g: Graph, batch: int, prob: DnlsProblem, lam, damping: int, workspace: torch.Tensor, stream=None):

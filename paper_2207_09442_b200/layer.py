@@ -37,8 +37,9 @@ class PoseGraphSolver:
             self._ws_batch = batch
         return self._ws
 
-    def forward(self, poses, meas, prior_meas, w_edge, w_prior, implicit: bool = False, options=None):
-        """Solve in place on a copy of ``poses``.  Returns (poses_K, objective, status, iterations)."""
+    def forward(self, poses, meas, prior_meas, w_edge, w_prior, implicit: bool = False, options=None, radius=None):
+        """Solve in place on a copy of ``poses``.  Returns (poses_K, objective, status, iterations).
+        radius: Welsch radius tensor ([1] or [B]) of the Between edges, or None (quadratic costs)."""
         opt = options if options is not None else self.options
         opt.backward_mode = D.BWD_IMPLICIT if implicit else D.BWD_NONE
         B = poses.shape[0]
@@ -48,16 +49,18 @@ class PoseGraphSolver:
         it = torch.empty(B, dtype=torch.int32, device=poses.device)
         ws = self.workspace(B)
         prob = D.make_problem(out, meas.contiguous(), prior_meas.contiguous(), w_edge.detach().contiguous(),
-                              w_prior.detach().contiguous(), obj, st, it)
+                              w_prior.detach().contiguous(), obj, st, it,
+                              radius=None if radius is None else radius.detach().contiguous())
         D.dnls_forward(self.graph, B, opt, prob, ws)
         self.generation += 1
         return out, obj, st, it
 
     def backward(self, poses_K, meas, prior_meas, w_edge, w_prior, grad_poses, grad_kind=D.GRAD_MATRIX,
-                 per_element: bool = False, mode: str = "implicit", epsilon: float = 1e-3):
+                 per_element: bool = False, mode: str = "implicit", epsilon: float = 1e-3, radius=None):
         """Weight gradients for the upstream pose gradient: mode "implicit" (Prop. 1, cached factor
         of the last implicit forward) or "dlm" (direct loss minimisation, one
-        augmented GN step from poses_K; no cached factor needed)."""
+        augmented GN step from poses_K; no cached factor needed).  With a Welsch ``radius`` the
+        result is (grad_w_edge, grad_w_prior, grad_radius), else (grad_w_edge, grad_w_prior)."""
         B = poses_K.shape[0]
         ws = self.workspace(B)
         E, P = self.graph.E, self.graph.P
@@ -69,30 +72,38 @@ class PoseGraphSolver:
             ge = torch.zeros(E, dtype=torch.float64, device=poses_K.device)
             gp = torch.zeros(P, dtype=torch.float64, device=poses_K.device)
             stride = 0
+        rad = None if radius is None else radius.detach().contiguous()
+        gr = None
+        if rad is not None:   # laid out like the radius: shared [1] (batch sum) or per element [B]
+            gr = torch.zeros(rad.numel(), dtype=torch.float64, device=poses_K.device)
         prob = D.make_problem(poses_K, meas.contiguous(), prior_meas.contiguous(), w_edge.detach().contiguous(),
-                              w_prior.detach().contiguous())
+                              w_prior.detach().contiguous(), radius=rad)
         if mode == "implicit":
             D.dnls_backward_implicit(self.graph, B, prob, grad_poses.contiguous(), grad_kind,
-                                     ge if E else None, gp if P else None, stride, ws)
+                                     ge if E else None, gp if P else None, stride, ws, grad_radius=gr)
         elif mode == "dlm":
             D.dnls_backward_dlm(self.graph, B, prob, grad_poses.contiguous(), grad_kind, epsilon,
-                                ge if E else None, gp if P else None, stride, ws)
+                                ge if E else None, gp if P else None, stride, ws, grad_radius=gr)
             self.generation += 1   # the workspace factor was overwritten
         else:
             raise ValueError(f"unknown backward mode {mode!r} (implicit | dlm)")
         if per_element:
-            return ge[:, :E], gp[:, :P]
+            ge, gp = ge[:, :E], gp[:, :P]
+        if rad is not None:
+            return ge, gp, gr.reshape(rad.shape)
         return ge, gp
 
 
 class _PoseGraphFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, solver, poses0, meas, prior_meas, w_edge, w_prior, mode="implicit", epsilon=1e-3):
-        poses, obj, st, it = solver.forward(poses0, meas, prior_meas, w_edge, w_prior, implicit=(mode == "implicit"))
+    def forward(ctx, solver, poses0, meas, prior_meas, w_edge, w_prior, radius=None, mode="implicit", epsilon=1e-3):
+        poses, obj, st, it = solver.forward(poses0, meas, prior_meas, w_edge, w_prior, implicit=(mode == "implicit"),
+                                            radius=radius)
         ctx.solver = solver
         ctx.mode, ctx.epsilon = mode, epsilon
         ctx.gen = solver.generation
-        ctx.save_for_backward(poses, meas, prior_meas, w_edge, w_prior)
+        ctx.has_radius = radius is not None
+        ctx.save_for_backward(poses, meas, prior_meas, w_edge, w_prior, *([radius] if radius is not None else []))
         ctx.mark_non_differentiable(obj, st, it)
         return poses, obj, st, it
 
@@ -102,23 +113,27 @@ class _PoseGraphFn(torch.autograd.Function):
         if ctx.mode == "implicit" and solver.generation != ctx.gen:
             raise RuntimeError("pose_graph_layer: the solver ran another forward since this one; its cached "
                                "factor is gone (DNLS_E_STATE)")
-        poses, meas, prior_meas, w_edge, w_prior = ctx.saved_tensors
+        poses, meas, prior_meas, w_edge, w_prior, *rest = ctx.saved_tensors
+        radius = rest[0] if ctx.has_radius else None
         if g_poses is None:
             g_poses = torch.zeros_like(poses)
-        ge, gp = solver.backward(poses, meas, prior_meas, w_edge, w_prior, g_poses, D.GRAD_MATRIX,
-                                 per_element=(w_edge.dim() == 2), mode=ctx.mode, epsilon=ctx.epsilon)
+        out = solver.backward(poses, meas, prior_meas, w_edge, w_prior, g_poses, D.GRAD_MATRIX,
+                              per_element=(w_edge.dim() == 2), mode=ctx.mode, epsilon=ctx.epsilon, radius=radius)
+        ge, gp = out[0], out[1]
+        gr = out[2] if radius is not None and ctx.needs_input_grad[6] else None
         ge = ge if ctx.needs_input_grad[4] else None
         gp = gp if ctx.needs_input_grad[5] else None
-        return None, None, None, None, ge, gp, None, None
+        return None, None, None, None, ge, gp, gr, None, None
 
 
 def pose_graph_layer(solver: PoseGraphSolver, poses0, meas, prior_meas, w_edge, w_prior, backward_mode="implicit",
-                     epsilon=1e-3):
+                     epsilon=1e-3, radius=None):
     """Differentiable solve.  backward_mode "implicit" (Prop. 1, factor reuse) or "dlm" (direct loss
-    minimisation with step eps).  Returns (poses*, objective, status, iterations)."""
+    minimisation with step eps).  radius: learnable Welsch radius of the Between edges
+    (PAPER.md:168), [1] or [B], or None.  Returns (poses*, objective, status, iterations)."""
     if backward_mode not in ("implicit", "dlm"):
         raise ValueError(f"unknown backward_mode {backward_mode!r}")
     if poses0.requires_grad or meas.requires_grad or prior_meas.requires_grad:
         raise ValueError("implicit backward gives no gradient for theta_init or measurements "
                          "(PAPER.md Table 6 :726); only w_edge / w_prior may require grad")
-    return _PoseGraphFn.apply(solver, poses0, meas, prior_meas, w_edge, w_prior, backward_mode, epsilon)
+    return _PoseGraphFn.apply(solver, poses0, meas, prior_meas, w_edge, w_prior, radius, backward_mode, epsilon)

@@ -33,15 +33,18 @@ def oracle_results(topo, data, elements=None, **opt):
     G = "SE3" if topo.dim == 3 else "SE2"
     o = onls.Options(**opt)
     return onls.solve_batch(G, topo.num_poses, topo.edges, topo.prior_vars, data["poses0"], data["meas"],
-                            data["prior_meas"], data["w_edge"], data["w_prior"], o, elements=elements)
+                            data["prior_meas"], data["w_edge"], data["w_prior"], o, elements=elements,
+                            radius=data.get("radius"))
 
 
 def oracle_problem(topo, data, b):
     G = "SE3" if topo.dim == 3 else "SE2"
     we = data["w_edge"][b] if data["w_edge"].ndim == 2 else data["w_edge"]
     wp = data["w_prior"][b] if data["w_prior"].ndim == 2 else data["w_prior"]
+    r = data.get("radius")
+    rk = None if r is None else float(np.asarray(r).reshape(-1)[b if np.size(r) > 1 else 0])
     return onls.PGOProblem(G, topo.num_poses, topo.edges, topo.prior_vars, data["meas"][b], data["prior_meas"][b],
-                           we, wp)
+                           we, wp, radius=rk)
 
 
 def pose_err(P_gpu, T_oracle_homog):

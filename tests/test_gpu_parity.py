@@ -6,6 +6,8 @@ import numpy as np
 import pytest
 import torch
 
+import synth
+
 from gpu_helpers import (DEV, TOL_GRAD, TOL_OBJ, TOL_POSE, D, graph_for, make_case, oimp, olie, onls,
                          oracle_problem, oracle_results, perm_matrix_indices, pose_err, rel_vec_err, to_dev)
 from paper_2207_09442_b200._lib import DnlsError
@@ -409,3 +411,79 @@ def test_dlm_invalidates_implicit_cache_and_layer_mode():
     ge, _ = solver.backward(out.detach(), t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"], gm,
                             D.GRAD_MATRIX, mode="dlm", epsilon=1e-3)
     assert torch.allclose(w.grad, ge, rtol=0, atol=0)
+
+
+# ------------------------------------------------------------------ Welsch robust kernel
+def robust_case(dim, N=40, B=3, seed=21, radius=None):
+    topo, data = make_case(N, dim=dim, p=0.4, seed=seed, B=B)
+    topo = synth.cube_topology(N, dim=dim, p=0.4, seed=seed, outlier_ratio=0.3)
+    data = synth.cube_batch(topo, B, seed=seed)
+    data["radius"] = np.array([0.4]) if radius is None else np.asarray(radius, dtype=np.float64)
+    return topo, data
+
+
+@pytest.mark.parametrize("dim,opt,radius", [(3, "gn", None), (2, "gn", [0.3, 0.5, 0.8]), (3, "lm", None)])
+def test_welsch_forward_matches_oracle(dim, opt, radius):
+    topo, data = robust_case(dim, radius=radius)
+    group = D.SE3 if dim == 3 else D.SE2
+    solver = PoseGraphSolver(group, topo.num_poses, topo.edges, topo.prior_vars, device=0, max_iterations=8,
+                             optimizer=(D.LM if opt == "lm" else D.GN))
+    t = to_dev({k: v for k, v in data.items() if k != "gt"})
+    poses, obj, st, it = solver.forward(t["poses0"], t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
+                                        radius=t["radius"])
+    torch.cuda.synchronize()
+    res = oracle_results(topo, data, max_iterations=8, optimizer=opt)
+    P = poses.cpu().numpy()
+    for b, r in enumerate(res):
+        if opt == "lm" and lm_has_tie(r):
+            continue
+        assert pose_err(P[b], r.x) <= TOL_POSE
+        assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
+
+
+@pytest.mark.parametrize("mode,per_el_radius", [("implicit", False), ("implicit", True), ("dlm", False)])
+def test_welsch_backward_matches_oracle(mode, per_el_radius):
+    """Weight and radius gradients (implicit: Prop. 1 with the IRLS Hessian; dlm) vs the oracle."""
+    from oracle import dlm as odlm
+    B, N, dim = 3, 36, 3
+    topo, data = robust_case(dim, N=N, B=B, radius=[0.35, 0.5, 0.7] if per_el_radius else None)
+    group = D.SE3
+    solver = PoseGraphSolver(group, topo.num_poses, topo.edges, topo.prior_vars, device=0, max_iterations=8)
+    t = to_dev({k: v for k, v in data.items() if k != "gt"})
+    poses, obj, st, it = solver.forward(t["poses0"], t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
+                                        implicit=(mode == "implicit"), radius=t["radius"])
+    v = np.random.default_rng(9).standard_normal((B, N, 6))
+    ge, gp, gr = solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
+                                 torch.from_numpy(v).to(DEV), D.GRAD_TANGENT, mode=mode, epsilon=1e-3,
+                                 radius=t["radius"])
+    torch.cuda.synchronize()
+    res = oracle_results(topo, data, max_iterations=8, implicit=(mode == "implicit"))
+    ref_w = np.zeros(topo.num_edges + 1)
+    ref_r = np.zeros(B)
+    for b, r in enumerate(res):
+        prob = oracle_problem(topo, data, b)
+        if mode == "implicit":
+            a, c, lam = oimp.implicit_weight_grads(prob, r.x, v[b].reshape(-1), L_K=r.L_final)
+            ref_r[b] = oimp.radius_vjp(prob, r.x, lam)
+        else:
+            a, c, Td = odlm.dlm_weight_grads(prob, r.x, v[b].reshape(-1), 1e-3)
+            ref_r[b] = odlm.dlm_radius_grad(prob, r.x, Td, 1e-3)
+        ref_w += np.concatenate([a, c])
+    assert rel_vec_err(np.concatenate([ge.cpu().numpy(), gp.cpu().numpy()]), ref_w) <= TOL_GRAD
+    g_r = gr.cpu().numpy().reshape(-1)
+    if per_el_radius:
+        assert rel_vec_err(g_r, ref_r) <= TOL_GRAD
+    else:
+        assert rel_vec_err(g_r, [ref_r.sum()]) <= TOL_GRAD
+
+
+def test_welsch_layer_learnable_radius():
+    topo, data = robust_case(3, N=30, B=2)
+    solver = PoseGraphSolver(D.SE3, topo.num_poses, topo.edges, topo.prior_vars, device=0, max_iterations=6)
+    t = to_dev({k: v for k, v in data.items() if k != "gt"})
+    rad = t["radius"].clone().requires_grad_(True)
+    out, *_ = pose_graph_layer(solver, t["poses0"], t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
+                               radius=rad)
+    gt = torch.from_numpy(np.broadcast_to(data["gt"], out.shape).copy()).to(DEV)
+    ((out - gt) ** 2).sum().backward()
+    assert rad.grad is not None and rad.grad.shape == rad.shape and torch.isfinite(rad.grad).all()
