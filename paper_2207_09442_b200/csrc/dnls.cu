@@ -27,6 +27,10 @@ namespace {
 #define DNLS_NT 384
 #endif
 constexpr int NT = DNLS_NT;   // threads per CTA (one batch element per CTA)
+#ifndef DNLS_MINB
+#define DNLS_MINB 1
+#endif
+constexpr int MINB = DNLS_MINB;   // resident CTAs per SM the register allocation is sized for
 constexpr int64_t SMEM_BYTES = 190 * 1024;   // dynamic shared memory per CTA (x + resident + staging); the rest of the 256 KB unified L1 caches the global panels (measured optimum, tools/smem_sweep.sh)
 thread_local std::string g_err;
 
@@ -200,7 +204,7 @@ __device__ void finish_assembly(const DevGraph& g, const double* cost_b, double*
 }
 
 template <int D>
-__global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs ws, FwdParams fp) {
+__global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, DevWs ws, FwdParams fp) {
   constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
   const int b = blockIdx.x;
   __shared__ double s_red[NT / 32];
@@ -237,10 +241,12 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
     const bool ok = sh_fail == 0;
     __syncthreads();
     if (!fp.lm) {
+#ifndef DNLS_ABLATE   // development builds that skip a phase (timing ablation) must not stop early
       if (!ok) {
         status = DNLS_ST_NOT_SPD;
         break;
       }
+#endif
       solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
       DNLS_TRACE_POINT(400);
       retract_phase<D, NT>(g, Tb, Tb, x_b, fp.alpha);
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(NT, 1) k_forward(DevGraph g, DevProb pr, DevWs
 }
 
 template <int D>
-__global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, DevWs ws, const double* lam,
+__global__ void __launch_bounds__(NT, MINB) k_linearize(DevGraph g, DevProb pr, DevWs ws, const double* lam,
                                                       int damping, double* objective) {
   constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
   const int b = blockIdx.x;
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(NT, 1) k_linearize(DevGraph g, DevProb pr, Dev
 }
 
 template <int D>
-__global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* status) {
+__global__ void __launch_bounds__(NT, MINB) k_factorize(DevGraph g, DevWs ws, int* status) {
   const int b = blockIdx.x;
   __shared__ int sh_fail;
   if (threadIdx.x == 0) sh_fail = 0;
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(NT, 1) k_factorize(DevGraph g, DevWs ws, int* 
 
 // rhs/x in original order [B][N][D]
 template <int D>
-__global__ void __launch_bounds__(NT, 1) k_solve(DevGraph g, DevWs ws, const double* rhs, double* xout) {
+__global__ void __launch_bounds__(NT, MINB) k_solve(DevGraph g, DevWs ws, const double* rhs, double* xout) {
   const int b = blockIdx.x;
   Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
   double* x_b = sm.x;
@@ -418,7 +424,7 @@ __device__ __forceinline__ void tangent_grad(const double* Tb, const double* gpo
 
 // implicit backward, per element: v -> lambda = H^-1 v (cached factor) -> per-slot weight grads
 template <int D>
-__global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
+__global__ void __launch_bounds__(NT, MINB) k_backward(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
                                                      int grad_kind) {
   constexpr int PS = GT<D>::PS;
   const int b = blockIdx.x;
@@ -492,7 +498,7 @@ __global__ void __launch_bounds__(NT, 1) k_backward(DevGraph g, DevProb pr, DevW
 //   factor + solve (one extra factorisation), theta_direct = theta* [+] (-delta_a)  (one GN step),
 //   per slot  g = (w / eps) (||c(theta*)||^2 - ||c(theta_direct)||^2)  -> k_reduce_wgrad.
 template <int D>
-__global__ void __launch_bounds__(NT, 1) k_backward_dlm(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
+__global__ void __launch_bounds__(NT, MINB) k_backward_dlm(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
                                                          int grad_kind, double eps) {
   constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
   const int b = blockIdx.x;

@@ -1,11 +1,11 @@
-// Per-element device phases of one GN/LM iteration.  One CUDA block ("CTA") owns one batch
-// element; every phase below is executed cooperatively by the CTA's NT threads
-// (DESIGN.md "Kernels").  Phases:
-//   jac_phase       a1: per-cost residual + weighted Jacobians -> per-element scratch
-//   assemble_phase  a2: scatter-free H (+lambda damping) into the factor storage, b, S
-//   factor_phase    a3: supernodal left-looking Cholesky, level-synchronous
-//   solve_phase     a4: forward / backward substitution
+// Per-element device phases of one GN/LM iteration.  One CUDA block ("CTA"), or a cluster of CL
+// CTAs for few large problems, owns one batch element; every phase below is executed
+// cooperatively by its threads.  Phases:
+//   linearize_phase a1+a2: per-cost residual + compact Jacobian, single-writer assembly of H, b, S
+//   factor_phase    a3: supernodal left-looking Cholesky, level-synchronous (+ fused y = L^-1 b)
+//   solve_phase     a4: backward (and standalone forward) substitution
 //   retract_phase   a5: T <- T Exp(-alpha delta)
+//   objective_phase    S(theta) only (LM trial, final objective)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -350,34 +350,6 @@ __device__ __forceinline__ double warp0_sum(const double* v, int n) {
   return s;
 }
 
-// ============================================================================= a1: Jacobians
-template <int D, int NT>
-__device__ void jac_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, double* jac_b,
-                          double* cost_b) {
-  constexpr int JS = GT<D>::JS;
-  const int nslot = g.E + g.P;
-  for (int slot = threadIdx.x; slot < nslot; slot += NT) {
-    double c[D], Ci[D * D], Cj[D * D];
-    eval_slot<D>(g, pr, Tb, b, slot, c, Ci, Cj, true);
-    const double w = slot_weight<D>(g, pr, b, slot);
-    double* o = jac_b + (size_t)slot * JS;
-    double n2 = 0.0;
-#pragma unroll
-    for (int q = 0; q < D * D; ++q) o[q] = w * Ci[q];
-    if (slot < g.E) {
-#pragma unroll
-      for (int q = 0; q < D * D; ++q) o[D * D + q] = w * Cj[q];
-    }
-#pragma unroll
-    for (int q = 0; q < D; ++q) {
-      double r = w * c[q];
-      o[2 * D * D + q] = r;
-      n2 += r * r;
-    }
-    cost_b[slot] = 0.5 * n2;
-  }
-}
-
 // objective only (LM trial / final objective without implicit)
 template <int D, int NT>
 __device__ void objective_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, double* cost_b) {
@@ -392,183 +364,6 @@ __device__ void objective_phase(const DevGraph& g, const DevProb& pr, const doub
     double psi;
     cost_b[slot] = slot_cost(g, pr, b, slot, n2, psi);
   }
-}
-
-// ============================================================================= a2: assembly
-// Every d x d block of the factor storage is written exactly once (scatter-free, single writer,
-// fixed summation order over its contribution list).  Item = (block, row a) -> D outputs.
-// lam < 0: undamped.  damping 0: Marquardt (diag *= 1 + lam), 1: identity (diag += lam).
-template <int D, int NT>
-__device__ void assemble_phase(const DevGraph& g, LView L, const double* jac_b, double* x_b, double lam,
-                               int damping, double* s_red) {
-  constexpr int JS = GT<D>::JS;
-  double mymax = 0.0;
-  const int nitems = g.nblk * D;
-  for (int itm = threadIdx.x; itm < nitems; itm += NT) {
-    const int blk = itm / D, a = itm - blk * D;
-    double acc[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q) acc[q] = 0.0;
-    const int c0 = g.blk_cptr[blk], c1 = g.blk_cptr[blk + 1];
-    for (int ci = c0; ci < c1; ++ci) {
-      const int code = g.blk_con[ci];
-      const int slot = code >> 2, rs = (code >> 1) & 1, cs = code & 1;
-      const double* Jr = jac_b + (size_t)slot * JS + rs * D * D;
-      const double* Jc = jac_b + (size_t)slot * JS + cs * D * D;
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const double jra = Jr[k * D + a];
-#pragma unroll
-        for (int q = 0; q < D; ++q) acc[q] = fma(jra, Jc[k * D + q], acc[q]);
-      }
-    }
-    if (g.blk_kind[blk] == 1) {
-      double v = acc[a];
-      if (lam > 0.0) v = (damping == 0) ? v * (1.0 + lam) : v + lam;
-      acc[a] = v;
-      mymax = fmax(mymax, v);
-    }
-    double* T = L.at(g.blk_off[blk]);
-    const int ld = g.blk_ld[blk];
-#pragma unroll
-    for (int q = 0; q < D; ++q) T[(size_t)q * ld + a] = acc[q];
-  }
-  // b = J^T r (permuted order)
-  const int nb = g.N * D;
-  for (int itm = threadIdx.x; itm < nb; itm += NT) {
-    const int p = itm / D, a = itm - p * D;
-    double acc = 0.0;
-    for (int ci = g.bc_ptr[p]; ci < g.bc_ptr[p + 1]; ++ci) {
-      const int code = g.bc[ci];
-      const int slot = code >> 1, sd = code & 1;
-      const double* J = jac_b + (size_t)slot * JS + sd * D * D;
-      const double* r = jac_b + (size_t)slot * JS + 2 * D * D;
-#pragma unroll
-      for (int k = 0; k < D; ++k) acc = fma(J[k * D + a], r[k], acc);
-    }
-    x_b[itm] = acc;
-  }
-  // max diagonal (CTA reduce, max is order independent)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
-}
-
-// T (leading dim ld) += lower triangle of A^T B; all old values loaded before any store (the
-// target may be in global memory: one round trip instead of one per entry)
-template <int D>
-__device__ __forceinline__ void add_gram_lower(double* __restrict__ T, int ld, const double* A, const double* B) {
-  constexpr int NE = D * (D + 1) / 2;
-  double old[NE];
-  {
-    int e = 0;
-#pragma unroll
-    for (int q = 0; q < D; ++q)
-#pragma unroll
-      for (int a = q; a < D; ++a) old[e++] = T[(size_t)q * ld + a];
-  }
-  int e = 0;
-#pragma unroll
-  for (int q = 0; q < D; ++q)
-#pragma unroll
-    for (int a = q; a < D; ++a) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < D; k += 2) {
-        s0 = fma(A[k * D + a], B[k * D + q], s0);
-        if (k + 1 < D) s1 = fma(A[(k + 1) * D + a], B[(k + 1) * D + q], s1);
-      }
-      T[(size_t)q * ld + a] = old[e++] + (s0 + s1);
-    }
-}
-template <int D>
-__device__ __forceinline__ void add_gram_full(double* __restrict__ T, int ld, const double* A, const double* B) {
-#pragma unroll
-  for (int q = 0; q < D; ++q) {
-    double old[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) old[a] = T[(size_t)q * ld + a];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < D; k += 2) {
-        s0 = fma(A[k * D + a], B[k * D + q], s0);
-        if (k + 1 < D) s1 = fma(A[(k + 1) * D + a], B[(k + 1) * D + q], s1);
-      }
-      T[(size_t)q * ld + a] = old[a] + (s0 + s1);
-    }
-  }
-}
-template <int D>
-__device__ __forceinline__ void add_jtr(double* __restrict__ xb, const double* J, const double* r) {
-  double old[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) old[a] = xb[a];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    double s0 = 0.0;
-#pragma unroll
-    for (int k = 0; k < D; ++k) s0 = fma(J[k * D + a], r[k], s0);
-    xb[a] = old[a] + s0;
-  }
-}
-
-// Edge-coloured scatter assembly (replaces the gather assembly in the numeric kernels): zero the
-// factor storage and b, then for each colour class (no two slots of a class share a pose) every
-// slot adds J_i^T J_i, J_j^T J_j, J_i^T J_j (lower triangles of the diagonal blocks) and J^T r into
-// the storage (shared or global through L).  Classes run in a fixed order -> deterministic.
-// Then damping (lam > 0) and the max diagonal (s_red per warp).
-template <int D, int NT>
-__device__ void assemble_colored(const DevGraph& g, const LView& L, const double* jac_b, double* x_b, double lam,
-                                 int damping, double* s_red) {
-  constexpr int JS = GT<D>::JS;
-  for (int i = threadIdx.x; i < L.rlo; i += NT) L.g[i] = 0.0;
-  for (int i = L.rlo + threadIdx.x; i < g.storage; i += NT) L.r[i - L.rlo] = 0.0;
-  for (int i = threadIdx.x; i < g.n; i += NT) x_b[i] = 0.0;
-  __syncthreads();
-  for (int c = 0; c < g.ncls; ++c) {
-    for (int ii = g.cls_ptr[c] + threadIdx.x; ii < g.cls_ptr[c + 1]; ii += NT) {
-      const int slot = g.cls_slot[ii];
-      const int4 d0 = g.slot_desc[3 * slot], d1 = g.slot_desc[3 * slot + 1], d2 = g.slot_desc[3 * slot + 2];
-      const double* Jb = jac_b + (size_t)slot * JS;
-      double Ji[D * D], r[D];
-#pragma unroll
-      for (int q = 0; q < D * D; ++q) Ji[q] = Jb[q];
-#pragma unroll
-      for (int q = 0; q < D; ++q) r[q] = Jb[2 * D * D + q];
-      add_gram_lower<D>(L.at(d0.x), d1.x, Ji, Ji);
-      add_jtr<D>(x_b + (size_t)D * d2.x, Ji, r);
-      if (d0.y >= 0) {
-        double Jj[D * D];
-#pragma unroll
-        for (int q = 0; q < D * D; ++q) Jj[q] = Jb[D * D + q];
-        add_gram_lower<D>(L.at(d0.y), d1.y, Jj, Jj);
-        add_jtr<D>(x_b + (size_t)D * d2.y, Jj, r);
-        // off-diagonal block (row pose, col pose): J_row^T J_col
-        add_gram_full<D>(L.at(d0.z), d1.z, d0.w ? Jj : Ji, d0.w ? Ji : Jj);
-      }
-    }
-    __syncthreads();
-  }
-  // damping + max diagonal over the pose diagonal blocks
-  double mymax = 0.0;
-  for (int it = threadIdx.x; it < g.n; it += NT) {
-    const int p = it / D, a = it - p * D;
-    // diagonal entry (col, col) of pose p's panel, col = D (p - first) + a
-    const int s = g.pose_sn[p];
-    const int col = D * (p - g.sn_first[s]) + a;
-    double* T = L.at(g.sn_off[s] + col * g.sn_ld[s] + col);
-    double v = *T;
-    if (lam > 0.0) {
-      v = (damping == 0) ? v * (1.0 + lam) : v + lam;
-      *T = v;
-    }
-    mymax = fmax(mymax, v);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
 }
 
 // ---------------------------------------------------------------------------- fused linearisation
@@ -759,7 +554,12 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
   const int nslot = g.E + g.P;
   for (int slot = threadIdx.x; slot < nslot; slot += NT) {
     SlotJ<D> J;
+#ifndef DNLS_SKIP_JAC
     slot_jac<D>(g, pr, Tb, b, slot, J);
+#else
+    J = SlotJ<D>{};
+    J.ww = 1.0;
+#endif
     double n2 = 0.0;
 #pragma unroll
     for (int q = 0; q < D; ++q) n2 = fma(J.c[q], J.c[q], n2);
@@ -851,123 +651,6 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
-}
-
-// ============================================================================= a3: factorisation
-// A team is a warp, a group of warps synchronised by a named barrier, or the whole CTA.
-struct Team {
-  int rank, size, bar;
-  __device__ __forceinline__ void sync() const {
-    if (size == 32) __syncwarp();
-    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(size) : "memory");
-  }
-};
-
-// Dense right-looking Cholesky of one supernode panel P (m rows, w columns, column-major,
-// leading dim m), blocked by D columns.  Per D-column block: one thread factors the D x D
-// diagonal block (rsqrt pivots) and writes its inverse X = L_jj^-1 to the team scratch `xinv`;
-// the rows below are then an independent product a_r X^T per thread (no divisions, no chain);
-// the trailing columns of the panel get the rank-D update.  *fail set if a pivot <= tol.
-template <int D>
-__device__ void panel_factor(double* P, int m, int ld, int w, double tol, const Team& tm, int* fail, double* xinv) {
-  for (int c0 = 0; c0 < w; c0 += D) {
-    if (tm.rank == 0) {
-      double a[D][D];
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-#pragma unroll
-        for (int i = j; i < D; ++i) a[i][j] = P[(size_t)(c0 + j) * ld + c0 + i];
-      bool bad = false;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        double piv = a[j][j];
-#pragma unroll
-        for (int k = 0; k < j; ++k) piv = fma(-a[j][k], a[j][k], piv);
-        if (!(piv > tol)) {
-          bad = true;
-          piv = 1.0;
-        }
-        const double inv = rsqrt(piv);
-        xinv[j] = inv;
-        a[j][j] = piv * inv;
-#pragma unroll
-        for (int i = j + 1; i < D; ++i) {
-          double s = a[i][j];
-#pragma unroll
-          for (int k = 0; k < j; ++k) s = fma(-a[i][k], a[j][k], s);
-          a[i][j] = s * inv;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-#pragma unroll
-        for (int i = j; i < D; ++i) P[(size_t)(c0 + j) * ld + c0 + i] = a[i][j];
-      if (bad) *fail = 1;
-    }
-    tm.sync();
-    const int r0 = c0 + D;
-    if (r0 < m) {
-      // rows below: x L_jj^T = a  (forward substitution, inverse diagonal from the scratch)
-      double l[D][D], iv[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        iv[j] = xinv[j];
-#pragma unroll
-        for (int i = j + 1; i < D; ++i) l[i][j] = P[(size_t)(c0 + j) * ld + c0 + i];
-      }
-      for (int r = r0 + tm.rank; r < m; r += tm.size) {
-        double x[D];
-#pragma unroll
-        for (int q = 0; q < D; ++q) x[q] = P[(size_t)(c0 + q) * ld + r];
-#pragma unroll
-        for (int q = 0; q < D; ++q) {
-          double s = x[q];
-#pragma unroll
-          for (int k = 0; k < q; ++k) s = fma(-x[k], l[q][k], s);
-          x[q] = s * iv[q];
-        }
-#pragma unroll
-        for (int q = 0; q < D; ++q) P[(size_t)(c0 + q) * ld + r] = x[q];
-      }
-      tm.sync();
-      const int nc = w - r0;
-      if (nc > 0) {
-        const int nr = m - r0;
-        const int nit = nc * nr;
-        for (int it = tm.rank; it < nit; it += tm.size) {
-          const int ci = it / nr, ri = it - ci * nr;
-          if (ri < ci) continue;
-          const int c = r0 + ci, r = r0 + ri;
-          double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; k += 2) {
-            s0 = fma(P[(size_t)(c0 + k) * ld + r], P[(size_t)(c0 + k) * ld + c], s0);
-            if (k + 1 < D) s1 = fma(P[(size_t)(c0 + k + 1) * ld + r], P[(size_t)(c0 + k + 1) * ld + c], s1);
-          }
-          P[(size_t)c * ld + r] -= s0 + s1;
-        }
-        tm.sync();
-      }
-    }
-  }
-}
-
-// Split the CTA's warps into teams for `nsn` independent panels: warp per panel when there are
-// at least NW panels, otherwise power-of-two groups of warps (named barriers 1..NW).
-template <int NT>
-__device__ __forceinline__ void team_of(int nsn, Team& tm, int& team, int& nteams) {
-  constexpr int NW = NT / 32;
-  const int warp = threadIdx.x >> 5;
-  int tw = 1;
-  if (nsn < NW) {
-    tw = NW / nsn;
-    while (tw & (tw - 1)) tw &= tw - 1;   // round down to a power of two
-  }
-  nteams = NW / tw;
-  team = warp / tw;
-  tm.rank = threadIdx.x - team * tw * 32;
-  tm.size = tw * 32;
-  tm.bar = 1 + team;
 }
 
 // Warp-level dense triangular solves on a panel's w x w diagonal block (P column-major, leading
@@ -1064,128 +747,6 @@ __device__ __forceinline__ void group_reduce_var(double (&acc)[N], int G) {
   }
 }
 
-// partial row a of update task tk: acc[q] += sum_{k = lane mod G} A_k[a] B_k[q]
-template <int D>
-__device__ __forceinline__ void task_row_partial(const DevGraph& g, const LView& V, const int4 tk, int a, int lane,
-                                                 int G, double (&acc)[D]) {
-  int kb = 0;
-  for (int ci = tk.z; ci < tk.w; ++ci) {
-    const int4 c = g.con4[ci];
-    const double* A = V.at(c.x) + a;
-    const double* Bm = V.at(c.y);
-    int k = lane - kb % G;
-    if (k < 0) k += G;
-    for (; k < c.w; k += G) {
-      const double av = A[(size_t)k * c.z];
-      double bv[D];
-#pragma unroll
-      for (int q = 0; q < D; ++q) bv[q] = Bm[(size_t)k * c.z + q];
-#pragma unroll
-      for (int q = 0; q < D; ++q) acc[q] = fma(av, bv[q], acc[q]);
-    }
-    kb += c.w;
-  }
-}
-
-// partial forward-substitution sum of scalar row a of pose row p: sum_{k = lane mod G} A_k[a] y_k
-template <int D>
-__device__ __forceinline__ double fwd_row_partial(const DevGraph& g, const LView& V, const double* x, int p, int a,
-                                                  int lane, int G) {
-  double s0 = 0.0, s1 = 0.0;
-  int kb = 0;
-  const int c1 = g.fc_ptr[p + 1];
-  for (int ci = g.fc_ptr[p]; ci < c1; ++ci) {
-    const int4 c = g.fcon4[ci];
-    const double* A = V.at(c.x) + a;
-    const double* y = x + c.w;
-    int k = lane - kb % G;
-    if (k < 0) k += G;
-    for (; k + G < c.z; k += 2 * G) {
-      s0 = fma(A[(size_t)k * c.y], y[k], s0);
-      s1 = fma(A[(size_t)(k + G) * c.y], y[k + G], s1);
-    }
-    if (k < c.z) s0 = fma(A[(size_t)k * c.y], y[k], s0);
-    kb += c.z;
-  }
-  return s0 + s1;
-}
-
-// Gather-form Schur updates of one level (CTA-wide): item = (task t, row a), G = level_gu lanes.
-template <int D, int NT>
-__device__ void update_tasks(const DevGraph& g, const LView& V, int lv) {
-  const int G = g.level_gu[lv];
-  const int i0 = g.ut_level_ptr[lv] * D, i1 = g.ut_level_ptr[lv + 1] * D;
-  const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
-  for (int base = i0; base < i1; base += NT / G) {
-    const int item = base + grp;
-    const bool valid = item < i1;
-    const int t = valid ? item / D : 0, a = item - t * D;
-    double acc[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q) acc[q] = 0.0;
-    int4 tk = make_int4(0, 0, 0, 0);
-    if (valid) {
-      tk = g.task4[t];
-      task_row_partial<D>(g, V, tk, a, lane, G, acc);
-    }
-    group_reduce<D>(acc, G);
-    if (valid && lane == 0) {
-      double* T = V.at(tk.x) + a;
-#pragma unroll
-      for (int q = 0; q < D; ++q) T[(size_t)q * tk.y] -= acc[q];
-    }
-  }
-}
-
-// Forward-substitution gather of one level (CTA-wide, fused into the factorisation):
-// item = (pose row p of the level, component a), G = level_gf lanes.
-template <int D, int NT>
-__device__ void fwd_rows(const DevGraph& g, const LView& V, double* x, int lv) {
-  const int G = g.level_gf[lv];
-  const int i0 = g.lrow_ptr[lv] * D, i1 = g.lrow_ptr[lv + 1] * D;
-  const int grp = threadIdx.x / G, lane = threadIdx.x - grp * G;
-  for (int base = i0; base < i1; base += NT / G) {
-    const int item = base + grp;
-    const bool valid = item < i1;
-    const int r = valid ? item / D : i0 / D, a = item - r * D;
-    const int p = g.lrow[r];
-    double acc[1] = {valid ? fwd_row_partial<D>(g, V, x, p, a, lane, G) : 0.0};
-    group_reduce<1>(acc, G);
-    if (valid && lane == 0) x[(size_t)D * p + a] -= acc[0];
-  }
-}
-
-// Backward-substitution gather of one supernode by one warp: xs[c] -= sum over below rows of
-// L[r][c] x_r; G = 32 / w lanes (power of two) per column split the below pose rows.
-template <int D>
-__device__ __forceinline__ void bwd_gather_warp(const DevGraph& g, const double* P, int ld, int w, int s,
-                                                double* x, double* xs) {
-  const int lane = threadIdx.x & 31;
-  int G = 1;
-  while (G < 32 && G * 2 * w <= 32) G *= 2;
-  const int rb = g.snr_ptr[s], nbr = g.snr_ptr[s + 1] - rb;
-  const int cper = 32 / G;
-  for (int cb = 0; cb < w; cb += cper) {
-    const int c = cb + lane / G, sub = lane % G;
-    double acc[1] = {0.0};
-    if (c < w) {
-      const double* col = P + (size_t)c * ld + w;
-      double s0 = 0.0, s1 = 0.0;
-      for (int rr = sub; rr < nbr; rr += G) {
-        const double* xr = x + (size_t)D * g.snr[rb + rr];
-#pragma unroll
-        for (int a = 0; a < D; a += 2) {
-          s0 = fma(col[rr * D + a], xr[a], s0);
-          if (a + 1 < D) s1 = fma(col[rr * D + a + 1], xr[a + 1], s1);
-        }
-      }
-      acc[0] = s0 + s1;
-    }
-    group_reduce<1>(acc, G);
-    if (c < w && sub == 0) xs[c] -= acc[0];
-  }
-}
-
 // width-dispatched warp triangular solves (slots = ceil(w / 32) register rows per lane)
 template <int D>
 __device__ __forceinline__ void warp_trsv_lower_w(const double* P, int ld, int w, double* xs) {
@@ -1200,283 +761,6 @@ __device__ __forceinline__ void warp_trsv_upper_w(const double* P, int ld, int w
   else if (w <= 64) warp_trsv_upper<2>(P, ld, w, xs);
   else if (w <= 128) warp_trsv_upper<4>(P, ld, w, xs);
   else warp_trsv_upper<(64 * D + 31) / 32>(P, ld, w, xs);
-}
-
-// Supernodal left-looking Cholesky, level-synchronous.  Levels >= the resident boundary live
-// in shared memory for the whole solve; a lower level's prefix [level_off, level_stage_hi) is
-// bulk-loaded (TMA) into `stage`, updated (gather form, from descendant panels), factored by
-// teams, and written back.  `xinv` holds NT/32 team scratch blocks of D*D doubles.
-template <int D, int NT>
-__device__ void factor_levels(const DevGraph& g, const LView& L, double* stage, double tol, int* s_fail,
-                              uint64_t* mbar, uint32_t& phase, double* xinv, double* xf, int l0, int l1) {
-  for (int lv = l0; lv < l1; ++lv) {
-    const int lo = g.level_off[lv];
-    const bool resident = lo >= L.rlo;
-    const int hi = resident ? lo : g.level_stage_hi[lv];
-    DNLS_TRACE_POINT(1000 + lv);
-    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
-    DNLS_TRACE_POINT(1100 + lv);
-    const LView V = L.level(stage, lo, hi);
-    // (U) gather-form updates from descendants into this level's panels (+ forward rhs rows)
-    update_tasks<D, NT>(g, V, lv);
-    if (xf) fwd_rows<D, NT>(g, V, xf, lv);
-    __syncthreads();
-    DNLS_TRACE_POINT(1200 + lv);
-    // (F) dense factorisation of the level's panels by teams
-    const int s0 = g.level_ptr[lv], nsn = g.level_ptr[lv + 1] - s0;
-    Team tm;
-    int team, nteams;
-    team_of<NT>(nsn, tm, team, nteams);
-    for (int i = team; i < nsn; i += nteams) {
-      const int s = g.level_sn[s0 + i];
-      panel_factor<D>(V.at(g.sn_off[s]), g.sn_m[s], g.sn_ld[s], g.sn_w[s], tol, tm, s_fail, xinv + team * D * D);
-    }
-    __syncthreads();
-    if (xf) {   // fused forward substitution: y_s = L_ss^-1 t_s, warp per supernode
-      const int warp = threadIdx.x >> 5;
-      for (int i = warp; i < nsn; i += NT / 32) {
-        const int s = g.level_sn[s0 + i];
-        warp_trsv_lower_w<D>(V.at(g.sn_off[s]), g.sn_ld[s], g.sn_w[s], xf + (size_t)D * g.sn_first[s]);
-      }
-      __syncthreads();
-    }
-    DNLS_TRACE_POINT(1300 + lv);
-    if (!resident && hi > lo) {
-      copy_range<NT>(L.g + lo, stage, hi - lo);
-      __syncthreads();
-    }
-  }
-  DNLS_TRACE_POINT(1999);
-}
-
-// ============================================================================= a4: solves
-// x (permuted, length n; shared or global memory) holds b on entry and H^-1 b on exit.
-// Level ranges are staged into `stage` (read-only); warp per supernode.
-template <int D, int NT>
-__device__ void solve_levels(const DevGraph& g, const LView& L, double* stage, double* x, uint64_t* mbar,
-                             uint32_t& phase, bool forward, int bl0) {
-  constexpr int NW = NT / 32;
-  constexpr int MAXR = (64 * D + 31) / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // forward: L y = b, leaves to root (skipped when fused into the factorisation)
-  for (int lv = 0; lv < (forward ? g.L : 0); ++lv) {
-    const int lo = g.level_off[lv];
-    const bool resident = lo >= L.rlo;
-    const int hi = resident ? lo : g.level_stage_hi[lv];
-    DNLS_TRACE_POINT(2000 + lv);
-    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
-    DNLS_TRACE_POINT(2100 + lv);
-    const LView V = L.level(stage, lo, hi);
-    const int s0 = g.level_ptr[lv], s1 = g.level_ptr[lv + 1];
-    for (int i = s0 + warp; i < s1; i += NW) {
-      const int s = g.level_sn[i];
-      const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_ld[s];
-      const double* P = V.at(g.sn_off[s]);
-      double* xs = x + (size_t)D * f;
-      {
-        int G = 1;
-        while (G < 32 && G * 2 * w <= 32) G *= 2;
-        for (int rb0 = 0; rb0 < w; rb0 += 32 / G) {
-          const int r = rb0 + lane / G, sub = lane % G;
-          double acc[1] = {0.0};
-          if (r < w) acc[0] = fwd_row_partial<D>(g, V, x, f + r / D, r % D, sub, G);
-          group_reduce<1>(acc, G);
-          if (r < w && sub == 0) xs[r] -= acc[0];
-        }
-      }
-      __syncwarp();
-      warp_trsv_lower_w<D>(P, m, w, xs);
-    }
-    __syncthreads();
-  }
-  // backward: L^T x = y, root to leaves
-  for (int lv = g.L - 1; lv >= bl0; --lv) {
-    const int lo = g.level_off[lv];
-    const bool resident = lo >= L.rlo;
-    const int hi = resident ? lo : g.level_stage_hi[lv];
-    DNLS_TRACE_POINT(3000 + lv);
-    if (!resident) bulk_load<NT>(stage, L.g + lo, hi - lo, mbar, phase);
-    else __syncthreads();
-    DNLS_TRACE_POINT(3100 + lv);
-    const LView V = L.level(stage, lo, hi);
-    const int s0 = g.level_ptr[lv], s1 = g.level_ptr[lv + 1];
-    for (int i = s0 + warp; i < s1; i += NW) {
-      const int s = g.level_sn[i];
-      const int f = g.sn_first[s], w = g.sn_w[s], m = g.sn_ld[s];
-      const double* P = V.at(g.sn_off[s]);
-      double* xs = x + (size_t)D * f;
-      bwd_gather_warp<D>(g, P, m, w, s, x, xs);
-      __syncwarp();
-      warp_trsv_upper_w<D>(P, m, w, xs);
-    }
-    __syncthreads();
-  }
-}
-
-// ----------------------------------------------------------------------------- dataflow forest
-// Shared-memory scheduler state: pending child counts [S], ready queue [n_forest], head/tail.
-__device__ __forceinline__ int* sched_pending(int* sq) { return sq; }
-
-// one forest supernode, one warp: gather updates into its panel (staged into the warp's slice of
-// the staging buffer when the panel is not resident and fits), fused forward-substitution rows,
-// dense panel factorisation, y_s = L_ss^-1 t_s; write back.
-template <int D>
-__device__ void forest_factor_sn(const DevGraph& g, const LView& L, int s, double* slice, int slice_cap,
-                                 double tol, int* fail, double* xinv_w, double* xf) {
-  const int lane = threadIdx.x & 31;
-  const int off = g.sn_off[s], m = g.sn_m[s], ld = g.sn_ld[s], w = g.sn_w[s], f = g.sn_first[s];
-  const int size = (ld * w + 1) & ~1;
-  double* const Pg = L.at(off);
-  const bool staged = off < L.rlo && size <= slice_cap;
-  double* P = Pg;
-  if (staged) {
-    for (int i = lane; i < size; i += 32) slice[i] = Pg[i];
-    __syncwarp();
-    P = slice;
-  }
-  DNLS_TRACE_POINT(7001);
-  {
-    const int t0 = g.ut_sn_ptr[2 * s], t1 = g.ut_sn_ptr[2 * s + 1];
-    const int nitems = (t1 - t0) * D;
-    int G = 1;
-    while (G < 32 && G * 2 * nitems <= 32) G *= 2;
-    for (int ib = 0; ib < nitems; ib += 32 / G) {
-      const int item = ib + lane / G, sub = lane % G;
-      const bool valid = item < nitems;
-      const int t = t0 + (valid ? item / D : 0), a = valid ? item % D : 0;
-      double acc[D];
-#pragma unroll
-      for (int q = 0; q < D; ++q) acc[q] = 0.0;
-      int4 tk = make_int4(0, 0, 0, 0);
-      if (valid) {
-        tk = g.task4[t];
-        task_row_partial<D>(g, L, tk, a, sub, G, acc);
-      }
-      group_reduce<D>(acc, G);
-      if (valid && sub == 0) {
-        double* T = P + (tk.x - off) + a;
-#pragma unroll
-        for (int q = 0; q < D; ++q) T[(size_t)q * tk.y] -= acc[q];
-      }
-    }
-  }
-  DNLS_TRACE_POINT(7002);
-  if (xf) {
-    int G = 1;
-    while (G < 32 && G * 2 * w <= 32) G *= 2;
-    for (int rb0 = 0; rb0 < w; rb0 += 32 / G) {
-      const int r = rb0 + lane / G, sub = lane % G;
-      double acc[1] = {0.0};
-      if (r < w) acc[0] = fwd_row_partial<D>(g, L, xf, f + r / D, r % D, sub, G);
-      group_reduce<1>(acc, G);
-      if (r < w && sub == 0) xf[(size_t)D * f + r] -= acc[0];
-    }
-  }
-  __syncwarp();
-  DNLS_TRACE_POINT(7003);
-  panel_factor<D>(P, m, ld, w, tol, Team{lane, 32, 0}, fail, xinv_w);
-  __syncwarp();
-  DNLS_TRACE_POINT(7004);
-  if (xf) {
-    warp_trsv_lower_w<D>(P, ld, w, xf + (size_t)D * f);
-    __syncwarp();
-  }
-  DNLS_TRACE_POINT(7005);
-  if (staged) {
-    for (int i = lane; i < size; i += 32) Pg[i] = slice[i];
-    __syncwarp();
-  }
-}
-
-// Warp-level dataflow over the forest (supernodes below g.top_level): a supernode becomes ready
-// when all its children completed (shared-memory counters); warps pull ready supernodes from a
-// shared ready queue.  No CTA barrier inside.  `sq` = int scratch [S + n_forest + 2].
-template <int D, int NT>
-__device__ void forest_factor(const DevGraph& g, const LView& L, double* stage, int stage_cap, double tol,
-                              int* fail, double* xinv, double* xf, int* sq) {
-  constexpr int NW = NT / 32;
-  int* pending = sq;
-  int* queue = sq + g.S;
-  int* ctr = queue + g.n_forest;
-  for (int i = threadIdx.x; i < g.S; i += NT) pending[i] = g.child_ptr[i + 1] - g.child_ptr[i];
-  for (int i = threadIdx.x; i < g.n_forest; i += NT) queue[i] = i < g.n_leaves ? g.leaves[i] + 1 : 0;
-  if (threadIdx.x == 0) {
-    ctr[0] = 0;
-    ctr[1] = g.n_leaves;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slice_cap = (stage_cap / NW) & ~1;
-  double* slice = stage + (size_t)warp * slice_cap;
-  for (;;) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(&ctr[0], 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= g.n_forest) break;
-    int s = 0;
-    if (lane == 0) {
-      volatile int* vq = queue;
-      while ((s = vq[idx]) == 0) __nanosleep(32);
-    }
-    s = __shfl_sync(0xffffffffu, s, 0) - 1;
-    __threadfence_block();
-    DNLS_TRACE_POINT(5000 + s);
-    forest_factor_sn<D>(g, L, s, slice, slice_cap, tol, fail, xinv + warp * D * D, xf);
-    __threadfence_block();
-    DNLS_TRACE_POINT(6000 + s);
-    if (lane == 0) {
-      const int p = g.sn_parent[s];
-      if (p >= 0 && g.sn_sched[p] && atomicSub(&pending[p], 1) == 1) {
-        const int slot = atomicAdd(&ctr[1], 1);
-        atomicExch(&queue[slot], p + 1);
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// Backward substitution over the forest, top-down dataflow: a supernode is ready once its parent
-// is done; completion releases its children.
-template <int D, int NT>
-__device__ void forest_bsolve(const DevGraph& g, const LView& L, double* x, int* sq) {
-  int* queue = sq + g.S;
-  int* ctr = queue + g.n_forest;
-  for (int i = threadIdx.x; i < g.n_forest; i += NT) queue[i] = i < g.n_broots ? g.broots[i] + 1 : 0;
-  if (threadIdx.x == 0) {
-    ctr[0] = 0;
-    ctr[1] = g.n_broots;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(&ctr[0], 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= g.n_forest) break;
-    int s = 0;
-    if (lane == 0) {
-      volatile int* vq = queue;
-      while ((s = vq[idx]) == 0) __nanosleep(32);
-    }
-    s = __shfl_sync(0xffffffffu, s, 0) - 1;
-    __threadfence_block();
-    const int f = g.sn_first[s], w = g.sn_w[s], ld = g.sn_ld[s];
-    const double* P = L.at(g.sn_off[s]);
-    double* xs = x + (size_t)D * f;
-    bwd_gather_warp<D>(g, P, ld, w, s, x, xs);
-    __syncwarp();
-    warp_trsv_upper_w<D>(P, ld, w, xs);
-    __syncwarp();
-    __threadfence_block();
-    if (lane == 0) {
-      const int c0 = g.child_ptr[s], c1 = g.child_ptr[s + 1];
-      if (c1 > c0) {
-        const int slot = atomicAdd(&ctr[1], c1 - c0);
-        for (int c = c0; c < c1; ++c) atomicExch(&queue[slot + c - c0], g.child_idx[c] + 1);
-      }
-    }
-  }
-  __syncthreads();
 }
 
 // ----------------------------------------------------------------------------- packet-driven levels
@@ -1570,56 +854,6 @@ template <int D>
 __device__ __forceinline__ int ivpos(int c0, int j, int ld) {
   return j < D - 1 ? (c0 + j + 1) * ld + (c0 + j) : (c0 + D - 1) * ld + c0;
 }
-template <int D>
-__device__ __forceinline__ void chol_block(double* P, int ld, int c0, double tol, int* fail) {
-  double a[D][D];
-#pragma unroll
-  for (int j = 0; j < D; ++j)
-#pragma unroll
-    for (int i = j; i < D; ++i) a[i][j] = P[(size_t)(c0 + j) * ld + c0 + i];
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    double piv = a[j][j];
-#pragma unroll
-    for (int k = 0; k < j; ++k) piv = fma(-a[j][k], a[j][k], piv);
-    if (!(piv > tol)) {
-      bad = true;
-      piv = 1.0;
-    }
-    const double inv = rsqrt(piv);
-    P[ivpos<D>(c0, j, ld)] = inv;
-    a[j][j] = piv * inv;
-#pragma unroll
-    for (int i = j + 1; i < D; ++i) {
-      double s = a[i][j];
-#pragma unroll
-      for (int k = 0; k < j; ++k) s = fma(-a[i][k], a[j][k], s);
-      a[i][j] = s * inv;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < D; ++j)
-#pragma unroll
-    for (int i = j; i < D; ++i) P[(size_t)(c0 + j) * ld + c0 + i] = a[i][j];
-  if (bad) *fail = 1;
-}
-// row r below the diagonal block: x L_jj^T = a
-template <int D>
-__device__ __forceinline__ void trsm_row(double* P, int ld, int c0, int r) {
-  double x[D];
-#pragma unroll
-  for (int q = 0; q < D; ++q) x[q] = P[(size_t)(c0 + q) * ld + r];
-#pragma unroll
-  for (int q = 0; q < D; ++q) {
-    double s = x[q];
-#pragma unroll
-    for (int k = 0; k < q; ++k) s = fma(-x[k], P[(size_t)(c0 + k) * ld + c0 + q], s);
-    x[q] = s * P[ivpos<D>(c0, q, ld)];
-  }
-#pragma unroll
-  for (int q = 0; q < D; ++q) P[(size_t)(c0 + q) * ld + r] = x[q];
-}
 // single-block panel solves (w == D), one thread: forward y = L^-1 t / backward x = L^-T t
 template <int D>
 __device__ __forceinline__ void trsv_lower_block(const double* P, int ld, double* xs) {
@@ -1658,57 +892,11 @@ __device__ __forceinline__ int find_panel(const int* pre, int n, int it) {
   return lo;
 }
 
-// dense factorisation of all panels of a level: per D-column block, thread per panel for the
-// diagonal block, CTA-wide rows for the TRSM, CTA-wide trailing update of multi-block panels
-template <int D, int NT>
-__device__ void level_factor(const Pk& P, const LView& V, double tol, int* fail) {
-  for (int cb = 0; cb < P.maxb; ++cb) {
-    const int c0 = cb * D;
-    for (int i = threadIdx.x; i < P.nsn; i += NT) {
-      const int4 sa = P.sna[i];
-      if (c0 < sa.w) chol_block<D>(V.at(sa.x), sa.z, c0, tol, fail);
-    }
-    __syncthreads();
-    const int total = P.snm[P.nsn];
-    for (int it = threadIdx.x; it < total; it += NT) {
-      const int i = find_panel(P.snm, P.nsn, it);
-      const int4 sa = P.sna[i];
-      const int r = it - P.snm[i];
-      if (c0 < sa.w && r >= c0 + D) trsm_row<D>(V.at(sa.x), sa.z, c0, r);
-    }
-    __syncthreads();
-    if (cb + 1 < P.maxb) {
-      bool any = false;
-      for (int i = 0; i < P.nsn; ++i) {
-        const int4 sa = P.sna[i];
-        const int r0 = c0 + D;
-        if (sa.w <= r0) continue;
-        any = true;
-        double* Pn = V.at(sa.x);
-        const int ld = sa.z, nc = sa.w - r0, nr = sa.y - r0, nit = nc * nr;
-        for (int t = threadIdx.x; t < nit; t += NT) {
-          const int ci = t / nr, ri = t - ci * nr;
-          if (ri < ci) continue;
-          const int c = r0 + ci, r = r0 + ri;
-          double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; k += 2) {
-            s0 = fma(Pn[(size_t)(c0 + k) * ld + r], Pn[(size_t)(c0 + k) * ld + c], s0);
-            if (k + 1 < D) s1 = fma(Pn[(size_t)(c0 + k + 1) * ld + r], Pn[(size_t)(c0 + k + 1) * ld + c], s1);
-          }
-          Pn[(size_t)c * ld + r] -= s0 + s1;
-        }
-      }
-      if (any) __syncthreads();
-    }
-  }
-}
-
 // ---- team-wise level factorisation (replaces the CTA-phase version above on the hot path)
 // Redundant in-register Cholesky of the D x D diagonal block at (c0, c0): every lane of a team
 // loads the lower triangle (a shared-memory broadcast) and factors it, so no barrier separates
 // the diagonal factorisation from the TRSM rows that need it.  Same arithmetic and order as
-// chol_block (bitwise identical factor).  Returns true if a pivot <= tol.
+// the former chol_block (bitwise identical factor).  Returns true if a pivot <= tol.
 template <int D>
 __device__ __forceinline__ bool chol_regs(const double* P, int ld, int c0, double tol, double (&a)[D][D],
                                           double (&iv)[D]) {
@@ -1748,7 +936,7 @@ __device__ __forceinline__ void store_diag(double* P, int ld, int c0, const doub
 #pragma unroll
   for (int j = 0; j < D; ++j) P[ivpos<D>(c0, j, ld)] = iv[j];
 }
-// row r below the diagonal block, L_jj from registers (same arithmetic as trsm_row)
+// row r below the diagonal block, L_jj from registers (same arithmetic as the former trsm_row)
 template <int D>
 __device__ __forceinline__ void trsm_row_regs(double* P, int ld, int c0, int r, const double (&a)[D][D],
                                               const double (&iv)[D]) {
@@ -1810,10 +998,16 @@ __device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int*
     const int m = sa.y, ld = sa.z, w = sa.w;
     double* xs = x ? x + (size_t)D * P.snb[i].x : nullptr;
     if (w == D) {
+      // at most one warp factors redundantly and solves the TRSM rows (the fp64 pipe is shared);
+      // with a multi-warp team, lane 0 of the second warp stores L_jj and applies the forward
+      // substitution concurrently
+      const int Gr = G < 32 ? G : 32, sr = G >= 64 ? 32 : 0;
+      if (rank >= Gr && rank != sr) continue;
       double a[D][D], iv[D];
       const bool bad = chol_regs<D>(Pn, ld, 0, tol, a, iv);
-      for (int r = D + rank; r < m; r += G) trsm_row_regs<D>(Pn, ld, 0, r, a, iv);
-      if (rank == 0) {
+      if (rank < Gr)
+        for (int r = D + rank; r < m; r += Gr) trsm_row_regs<D>(Pn, ld, 0, r, a, iv);
+      if (rank == sr) {
         store_diag<D>(Pn, ld, 0, a, iv);
         if (bad) *fail = 1;
         if (xs) {
@@ -2049,7 +1243,9 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
 #pragma unroll
         for (int q = 0; q < D; ++q) acc[q] = 0.0;
         const int4 tk = P.ntasks > 0 ? P.task4[t] : make_int4(0, 0, 0, 0);
+#ifndef DNLS_SKIP_U
         if (valid) pk_task_row_partial<D>(P, V, tk, a, lane, G, acc);
+#endif
         group_reduce_var<D>(acc, G);
         if (valid && lane == 0) {
           double* T = V.at(tk.x) + a;
@@ -2061,11 +1257,15 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     DNLS_TRACE_POINT(1160 + lv);
     // forward-substitution rows read descendant panels and y of earlier levels only: no barrier
     // between them and the updates of this level's panels
+#ifndef DNLS_SKIP_FWD
     if (xf) pk_fwd_rows<D, NT>(P, V, xf);
+#endif
     __syncthreads();
     DNLS_TRACE_POINT(1200 + lv);
     // (F) dense factorisation of this packet's panels, level-wide
+#ifndef DNLS_SKIP_F
     level_factor_teams<D, NT>(P, V, tol, s_fail, xf);   // + fused y_s = L_ss^-1 t_s
+#endif
     __syncthreads();
     DNLS_TRACE_POINT(1300 + lv);
     if (P.last && !resident && hi > lo) copy_range<NT>(L.g + lo, stage, hi - lo);
@@ -2113,9 +1313,13 @@ __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, do
     if (P.last && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
     DNLS_TRACE_POINT(3100 + lv);
     const LView V = L.level(stage, lo, hi);
+#ifndef DNLS_SKIP_BS
     level_bwd_gather<D, NT>(P, V, x);
+#endif
     __syncthreads();
+#ifndef DNLS_SKIP_BS
     level_trsv_upper<D, NT>(P, V, x);
+#endif
     proxy_barrier();
     pk_issue(g, pp, k - 2);
   }
