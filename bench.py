@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--backward", default="implicit", choices=["implicit", "dlm"],
                     help="backward mode timed in the step (dlm: PAPER.md:259-271, one augmented GN step)")
     ap.add_argument("--epsilon", type=float, default=1e-3, help="DLM epsilon")
+    ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 8],
+                    help="CTAs per batch element in the forward (0 = automatic)")
     ap.add_argument("--welsch", type=float, default=None,
                     help="Welsch radius of the Between edges (PAPER.md:168 robust PGO); default: quadratic costs")
     args = ap.parse_args()
@@ -234,6 +236,7 @@ def main():
     st = solver.stats
     opt = solver.options
     dlm = args.backward == "dlm"
+    opt.cluster_ctas = args.cluster
     opt.backward_mode = D.BWD_NONE if dlm else D.BWD_IMPLICIT
     host = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in data.items() if k != "gt"}
     vgrad = torch.from_numpy(np.random.default_rng([1, rank]).standard_normal((B, topo.num_poses, d)))

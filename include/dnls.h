@@ -87,7 +87,9 @@ typedef struct dnls_options {
   double abs_tol;           /* early-stop tolerances, default 1e-10 / 1e-8 */
   double rel_tol;
   int32_t backward_mode;    /* dnls_backward: IMPLICIT keeps the undamped factor of H(theta_K) */
-  int32_t reserved;
+  int32_t cluster_ctas;     /* CTAs sharing one batch element in dnls_forward: 0 = automatic (a cluster
+                               of 2 CTAs when the batch leaves half the SMs idle and N >= 1024,
+                               DESIGN.md "few large problems"), else 1, 2 or 8 */
 } dnls_options;
 
 typedef struct dnls_problem {

@@ -34,7 +34,7 @@ class DnlsOptions(ctypes.Structure):
         ("abs_tol", ctypes.c_double),
         ("rel_tol", ctypes.c_double),
         ("backward_mode", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("cluster_ctas", ctypes.c_int32),
     ]
 
 

@@ -31,6 +31,7 @@ constexpr int NT = DNLS_NT;   // threads per CTA (one batch element per CTA)
 #define DNLS_MINB 1
 #endif
 constexpr int MINB = DNLS_MINB;   // resident CTAs per SM the register allocation is sized for
+constexpr int MAX_CL = 8;         // largest cluster (CTAs sharing one batch element)
 constexpr int64_t SMEM_BYTES = 190 * 1024;   // dynamic shared memory per CTA (x + resident + staging); the rest of the 256 KB unified L1 caches the global panels (measured optimum, tools/smem_sweep.sh)
 thread_local std::string g_err;
 
@@ -60,7 +61,7 @@ struct dnls_graph {
 // ----------------------------------------------------------------------------- workspace layout
 namespace {
 struct WsLayout {
-  size_t L, x, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, total;
+  size_t L, x, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, clred, total;
 };
 WsLayout ws_layout(const Symbolic& s, int B) {
   const int D = s.D, PS = D == 6 ? 12 : 6, JS = D * (D + 1) + 2 * D + D * D;   // GT<D>::JS
@@ -79,6 +80,7 @@ WsLayout ws_layout(const Symbolic& s, int B) {
   w.maxd = o;  o = align_up(o + sizeof(double) * B);
   w.st = o;    o = align_up(o + sizeof(int) * B);
   w.it = o;    o = align_up(o + sizeof(int) * B);
+  w.clred = o; o = align_up(o + sizeof(double) * B * 2 * MAX_CL);
   w.total = o;
   return w;
 }
@@ -97,6 +99,7 @@ DevWs ws_views(const WsLayout& l, void* base) {
   w.maxd = (double*)(p + l.maxd);
   w.st = (int*)(p + l.st);
   w.it = (int*)(p + l.it);
+  w.clred = (double*)(p + l.clred);
   return w;
 }
 DevProb dev_prob(const dnls_problem* p) {
@@ -122,6 +125,7 @@ size_t smem_bytes(const DevGraph& g) {
   return sizeof(double) * ((g.x_smem ? (size_t)g.n_pad : 0) + (size_t)g.res_n + (size_t)g.stage_n) +
          sizeof(int) * 2 * (size_t)g.pk_max;
 }
+size_t smem_bytes_grouped(const DevGraph& g) { return sizeof(int) * 2 * (size_t)g.pk_max; }
 
 template <class F>
 dnls_status set_smem(F* kernel, size_t bytes, const char* what) {
@@ -140,16 +144,19 @@ struct Smem {
   uint64_t* mbar;   // mbarrier of the bulk (TMA) loads
   uint32_t phase;
 };
-// must be called by every thread at kernel start (initialises the mbarrier, one barrier)
-__device__ __forceinline__ Smem smem_views(const DevGraph& g, double* xg) {
+// must be called by every thread at kernel start (initialises the mbarrier, one barrier).
+// grouped == true (a cluster shares the element): x, the factor and the staging stay in global
+// memory; shared memory holds only the descriptor packets.
+__device__ __forceinline__ Smem smem_views(const DevGraph& g, double* xg, bool grouped = false) {
   extern __shared__ __align__(16) double smem[];
   __shared__ uint64_t s_mbar, s_mbpk[2];
   __shared__ double s_xinv[(NT / 32) * 36];
   Smem v;
-  v.x = g.x_smem ? smem : xg;
-  v.res = smem + (g.x_smem ? g.n_pad : 0);
-  v.stage = v.res + g.res_n;
-  v.pp.buf[0] = reinterpret_cast<int*>(v.stage + g.stage_n);
+  const bool xs = g.x_smem && !grouped;
+  v.x = xs ? smem : xg;
+  v.res = smem + (xs ? g.n_pad : 0);
+  v.stage = v.res + (grouped ? 0 : g.res_n);
+  v.pp.buf[0] = reinterpret_cast<int*>(v.stage + (grouped ? 0 : g.stage_n));
   v.pp.buf[1] = v.pp.buf[0] + g.pk_max;
   v.pp.mb[0] = &s_mbpk[0];
   v.pp.mb[1] = &s_mbpk[1];
@@ -161,6 +168,7 @@ __device__ __forceinline__ Smem smem_views(const DevGraph& g, double* xg) {
     mbar_init(&s_mbar);
     mbar_init(&s_mbpk[0]);
     mbar_init(&s_mbpk[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");   // visible to the async proxy
   }
   __syncthreads();
   return v;
@@ -186,27 +194,56 @@ struct FwdParams {
   int* iterations;
 };
 
-// CTA-wide: S = sum(cost), maxdiag = max over warps.  Returns via shared variables.
-template <int D>
+// group-wide: S = sum(cost) (fixed order, identical in every CTA of the group), maxdiag = max
+// over warps (and over the group's CTAs through the global scratch clr[CL]).  Returns via shared
+// variables.
+template <int D, int CL = 1>
 __device__ void finish_assembly(const DevGraph& g, const double* cost_b, double* s_red, double* sh_S,
-                                double* sh_max) {
-  __syncthreads();
+                                double* sh_max, double* clr = nullptr) {
+  gsync<CL>();
   if (threadIdx.x < 32) {
     double s = warp0_sum(cost_b, g.E + g.P);
     if (threadIdx.x == 0) {
       double m = 0.0;
       for (int i = 0; i < NT / 32; ++i) m = fmax(m, s_red[i]);
       *sh_S = s;
+      if (CL > 1) clr[crank<CL>()] = m;
+      else *sh_max = m;
+    }
+  }
+  if (CL > 1) {
+    gsync<CL>();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int i = 0; i < CL; ++i) m = fmax(m, clr[i]);
       *sh_max = m;
     }
   }
   __syncthreads();
 }
+// group-wide OR of the per-CTA factorisation failure flags (after a group barrier)
+template <int CL>
+__device__ void group_fail(int* sh_fail, double* clr) {
+  if constexpr (CL > 1) {
+    if (threadIdx.x == 0) clr[CL + crank<CL>()] = (double)*sh_fail;
+    gsync<CL>();
+    if (threadIdx.x == 0) {
+      int f = 0;
+      for (int i = 0; i < CL; ++i) f |= clr[CL + i] != 0.0;
+      *sh_fail = f;
+    }
+  }
+  __syncthreads();
+}
 
-template <int D>
+// CL > 1: a cluster of CL CTAs shares element blockIdx.x / CL (few large problems)
+template <int D, int CL>
 __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, DevWs ws, FwdParams fp) {
   constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x / CL;
+  const int cr = crank<CL>();
+  const int gt = cr * NT + threadIdx.x;
+  double* clr = ws.clred + (size_t)b * 2 * CL;
   __shared__ double s_red[NT / 32];
   __shared__ double sh_S, sh_max, sh_Stry;
   __shared__ int sh_fail;
@@ -216,9 +253,9 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
   double* jac_b = ws.jac + (size_t)b * slots * JS;
   double* cost_b = ws.cost + (size_t)b * slots;
   double* Lg = ws.L + (size_t)b * g.storage;
-  Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  Smem sm = smem_views(g, ws.x + (size_t)b * g.n, CL > 1);
   double* x_b = sm.x;
-  const LView L = full_view(g, Lg, sm);
+  const LView L = CL > 1 ? global_view(g, Lg) : full_view(g, Lg, sm);
 
   int status = DNLS_ST_OK, iters = 0;
   double lam = fp.lam0, Sprev = 0.0;
@@ -227,8 +264,8 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
     // a1 + a2 at theta_k
     DNLS_TRACE_POINT(100);
     DNLS_TRACE_POINT(200);
-    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, jac_b, fp.lm ? lam : -1.0, fp.damping, s_red);
-    finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+    linearize_phase<D, NT, CL>(g, pr, Tb, b, L, x_b, cost_b, jac_b, fp.lm ? lam : -1.0, fp.damping, s_red);
+    finish_assembly<D, CL>(g, cost_b, s_red, &sh_S, &sh_max, clr);
     DNLS_TRACE_POINT(300);
     const double S = sh_S;
     if (fp.early_stop && have_prev && fabs(S - Sprev) < fp.abs_tol + fp.rel_tol * Sprev) {
@@ -237,7 +274,8 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
     }
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, x_b, sm.pp);
+    factor_phase<D, NT, CL>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, x_b, sm.pp);
+    group_fail<CL>(&sh_fail, clr);
     const bool ok = sh_fail == 0;
     __syncthreads();
     if (!fp.lm) {
@@ -247,10 +285,10 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
         break;
       }
 #endif
-      solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
+      solve_phase<D, NT, CL>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
       DNLS_TRACE_POINT(400);
-      retract_phase<D, NT>(g, Tb, Tb, x_b, fp.alpha);
-      __syncthreads();
+      retract_phase<D, NT, CL>(g, Tb, Tb, x_b, fp.alpha);
+      gsync<CL>();
       DNLS_TRACE_POINT(500);
       ++iters;
       Sprev = S;
@@ -259,11 +297,11 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
       ++iters;
       bool accept = false;
       if (ok) {
-        solve_phase<D, NT>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
-        retract_phase<D, NT>(g, Tb, Ttr, x_b, fp.alpha);
-        __syncthreads();
-        objective_phase<D, NT>(g, pr, Ttr, b, cost_b);
-        __syncthreads();
+        solve_phase<D, NT, CL>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
+        retract_phase<D, NT, CL>(g, Tb, Ttr, x_b, fp.alpha);
+        gsync<CL>();
+        objective_phase<D, NT, CL>(g, pr, Ttr, b, cost_b);
+        gsync<CL>();
         if (threadIdx.x < 32) {
           double s = warp0_sum(cost_b, g.E + g.P);
           if (threadIdx.x == 0) sh_Stry = s;
@@ -272,8 +310,8 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
         accept = sh_Stry < S;
       }
       if (accept) {
-        for (int i = threadIdx.x; i < g.N * PS; i += NT) Tb[i] = Ttr[i];
-        __syncthreads();
+        for (int i = gt; i < g.N * PS; i += CL * NT) Tb[i] = Ttr[i];
+        gsync<CL>();
         lam = fmax(lam / fp.lam_down, fp.lam_min);
         Sprev = S;
         have_prev = true;
@@ -289,25 +327,25 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
   __syncthreads();
   // final objective S(theta_K); implicit: undamped H(theta_K) and its factor stay in ws
   if (fp.implicit) {
-    linearize_phase<D, NT>(g, pr, Tb, b, L, x_b, cost_b, jac_b, -1.0, 0, s_red);
-    finish_assembly<D>(g, cost_b, s_red, &sh_S, &sh_max);
+    linearize_phase<D, NT, CL>(g, pr, Tb, b, L, x_b, cost_b, jac_b, -1.0, 0, s_red);
+    finish_assembly<D, CL>(g, cost_b, s_red, &sh_S, &sh_max, clr);
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
-    factor_phase<D, NT>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, nullptr, sm.pp);
-    __syncthreads();
+    factor_phase<D, NT, CL>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, nullptr, sm.pp);
+    group_fail<CL>(&sh_fail, clr);
     if (sh_fail && status == DNLS_ST_OK) status = DNLS_ST_NOT_SPD;
     // the cached factor must be complete in global memory for dnls_backward_implicit
-    copy_range<NT>(Lg + g.res_lo, sm.res, g.storage - g.res_lo);
+    if (CL == 1) copy_range<NT>(Lg + g.res_lo, sm.res, g.storage - g.res_lo);
   } else {
-    objective_phase<D, NT>(g, pr, Tb, b, cost_b);
-    __syncthreads();
+    objective_phase<D, NT, CL>(g, pr, Tb, b, cost_b);
+    gsync<CL>();
     if (threadIdx.x < 32) {
       double s = warp0_sum(cost_b, g.E + g.P);
       if (threadIdx.x == 0) sh_S = s;
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && cr == 0) {
     if (fp.objective) fp.objective[b] = sh_S;
     if (fp.status) fp.status[b] = status;
     if (fp.iterations) fp.iterations[b] = iters;
@@ -680,6 +718,43 @@ __global__ void k_export_rhs(DevGraph g, DevWs ws, double* out) {
 }  // namespace
 
 // ============================================================================= C ABI
+namespace {
+// CTAs per batch element for dnls_forward: a cluster when the
+// batch leaves most SMs idle and the graph has enough work per level to share
+int forward_cluster(const dnls_graph* g, int batch, int req) {
+  if (req == 1 || req == 2 || req == 8) return req;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // measured on C3 (4096 poses, B = 16): 1 CTA 2.18k, 2 CTAs 2.53k, 8 CTAs 1.62k problem-iter/s --
+  // the cluster barriers and the all-global working set outweigh the wider levels beyond 2
+  if (g->sym.N < 1024) return 1;
+  if (batch * 2 <= sms) return 2;
+  return 1;
+}
+template <int CL, class K>
+dnls_status launch_grouped(K* kernel, const dnls_graph* g, int batch, cudaStream_t s, DevProb pr, DevWs ws,
+                           FwdParams fp) {
+  const size_t smem = smem_bytes_grouped(g->dg);
+  dnls_status st = set_smem(kernel, smem, "k_forward (cluster)");
+  if (st) return st;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * CL));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kernel, g->dg, pr, ws, fp) != cudaSuccess)
+    return fail(DNLS_E_CUDA, std::string("dnls_forward: cluster launch: ") + cudaGetErrorString(cudaGetLastError()));
+  return DNLS_OK;
+}
+}  // namespace
+
 extern "C" {
 
 DNLS_API const char* dnls_version_string(void) {
@@ -1001,6 +1076,7 @@ dnls_status check_problem(const char* fn, const dnls_graph* g, const dnls_proble
   }
 }  // namespace
 
+
 DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls_options* opt,
                                   const dnls_problem* prob, void* workspace, size_t ws_bytes, void* stream) {
   dnls_status st = check_common("dnls_forward", g, batch, workspace, ws_bytes);
@@ -1021,6 +1097,8 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
     return fail(DNLS_E_INVALID, "dnls_forward: invalid LM damping schedule");
   if (opt->damping != DNLS_DAMP_MARQUARDT && opt->damping != DNLS_DAMP_IDENTITY)
     return fail(DNLS_E_INVALID, "dnls_forward: unknown damping");
+  if (opt->cluster_ctas != 0 && opt->cluster_ctas != 1 && opt->cluster_ctas != 2 && opt->cluster_ctas != 8)
+    return fail(DNLS_E_INVALID, "dnls_forward: cluster_ctas must be 0 (automatic), 1, 2 or 8");
   dnls_graph* gm = const_cast<dnls_graph*>(g);
   {
     std::lock_guard<std::mutex> lk(gm->mu);
@@ -1050,7 +1128,14 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   fp.status = prob->status;
   fp.iterations = prob->iterations;
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
+  const int cl = forward_cluster(g, batch, opt->cluster_ctas);
+  if (cl == 1) {
+    DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD, 1>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD, 1><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
+  } else if (cl == 2) {
+    DISPATCH_D(g->sym.D, if ((st = launch_grouped<2>(k_forward<DD, 2>, g, batch, s, dev_prob(prob), ws, fp))) return st);
+  } else {
+    DISPATCH_D(g->sym.D, if ((st = launch_grouped<8>(k_forward<DD, 8>, g, batch, s, dev_prob(prob), ws, fp))) return st);
+  }
   if ((st = cuda_check("dnls_forward: k_forward launch"))) return st;
   if (fp.implicit) {
     std::lock_guard<std::mutex> lk(gm->mu);

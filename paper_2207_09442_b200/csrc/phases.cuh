@@ -93,6 +93,43 @@ __device__ __forceinline__ DevGraph remap_graph(const DevGraph& g, const int* sb
   return r;
 }
 
+// ---- CTA groups: CL CTAs of one thread-block cluster share one batch element (CL == 1: the CTA
+// alone).  Item loops run over the group's CL * NT threads; gsync<CL>() is the group barrier
+// (a cluster barrier with release/acquire semantics orders the global-memory writes of all its
+// CTAs, few large problems).
+template <int CL>
+__device__ __forceinline__ int crank() {
+  if constexpr (CL == 1) {
+    return 0;
+  } else {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return (int)r;
+  }
+}
+// The non-.aligned barrier form tolerates warps that have not reconverged after divergent item
+// loops (the compiler does not reconverge around inline asm); the cluster-scope fence after the
+// wait invalidates this SM's L1 (CCTL.IVALL) so global data written by the other CTAs is re-read.
+template <int CL>
+__device__ __forceinline__ void gsync() {
+  if constexpr (CL == 1) {
+    __syncthreads();
+  } else {
+#ifdef DNLS_STRONG_GSYNC
+    __threadfence();
+#endif
+#ifndef DNLS_NO_CLUSTER_FENCE
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;\n\tfence.acq_rel.cluster;" :::
+                 "memory");
+#else
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+#endif
+#ifdef DNLS_STRONG_GSYNC
+    __threadfence();
+#endif
+  }
+}
+
 // problem inputs (see dnls_problem)
 struct DevProb {
   double* poses;
@@ -114,6 +151,7 @@ struct DevWs {
   double* jac;    // [B][E+P][JS]  weighted J_i, J_j, r per cost slot
   double* cost;   // [B][E+P]      1/2 |r|^2 per slot (or weight gradient in backward)
   double* rgrad;  // [B][E+P]      per-slot radius gradient (backward with a Welsch kernel)
+  double* clred;  // [B][2 * CL]   cross-CTA exchange of a cluster (max diagonal, failure flags)
   double* trial;  // [B][N][PS]    LM trial poses
   double* S;      // [B] current objective
   double* Sprev;  // [B]
@@ -351,10 +389,10 @@ __device__ __forceinline__ double warp0_sum(const double* v, int n) {
 }
 
 // objective only (LM trial / final objective without implicit)
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void objective_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, double* cost_b) {
   const int nslot = g.E + g.P;
-  for (int slot = threadIdx.x; slot < nslot; slot += NT) {
+  for (int slot = crank<CL>() * NT + threadIdx.x; slot < nslot; slot += CL * NT) {
     double c[D];
     eval_slot<D>(g, pr, Tb, b, slot, c, nullptr, nullptr, false);
     const double w = slot_weight<D>(g, pr, b, slot);
@@ -542,17 +580,18 @@ struct Scr {   // per-slot scratch layout (doubles)
   static constexpr int H0 = 0, H1 = NL, B0 = 2 * NL, B1 = 2 * NL + D, HIJ = 2 * NL + 2 * D;
   static constexpr int SIZE = HIJ + D * D;
 };
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, const LView& L,
                                 double* x_b, double* cost_b, double* scr, double lam, int damping, double* s_red) {
   using SC = Scr<D>;
-  constexpr int NL = SC::NL;
-  for (int i = threadIdx.x; i < L.rlo; i += NT) L.g[i] = 0.0;
-  for (int i = L.rlo + threadIdx.x; i < g.storage; i += NT) L.r[i - L.rlo] = 0.0;
-  __syncthreads();
+  constexpr int NL = SC::NL, GN = CL * NT;
+  const int gt = crank<CL>() * NT + threadIdx.x;
+  for (int i = gt; i < L.rlo; i += GN) L.g[i] = 0.0;
+  for (int i = L.rlo + gt; i < g.storage; i += GN) L.r[i - L.rlo] = 0.0;
+  gsync<CL>();
   DNLS_TRACE_POINT(210);
   const int nslot = g.E + g.P;
-  for (int slot = threadIdx.x; slot < nslot; slot += NT) {
+  for (int slot = gt; slot < nslot; slot += GN) {
     SlotJ<D> J;
 #ifndef DNLS_SKIP_JAC
     slot_jac<D>(g, pr, Tb, b, slot, J);
@@ -594,10 +633,10 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
         for (int a = 0; a < D; ++a) O[(size_t)q * ld + a] = blk<D>(J, which2, a, q);
     }
   }
-  __syncthreads();
+  gsync<CL>();
   DNLS_TRACE_POINT(220);
   double mymax = 0.0;
-  for (int p = threadIdx.x; p < g.N; p += NT) {
+  for (int p = gt; p < g.N; p += GN) {
     double h[NL], r[D];
 #pragma unroll
     for (int i = 0; i < NL; ++i) h[i] = 0.0;
@@ -631,7 +670,7 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
 #pragma unroll
     for (int a = 0; a < D; ++a) x_b[(size_t)D * p + a] = r[a];
   }
-  for (int k = threadIdx.x; k < g.ndup; k += NT) {   // off-diagonal blocks shared by several edges
+  for (int k = gt; k < g.ndup; k += GN) {   // off-diagonal blocks shared by several edges
     const int bk = g.dup_blk[k];
     double h[D * D];
 #pragma unroll
@@ -969,30 +1008,33 @@ struct TeamSync {
 // one team barrier.  Single-block panels (the common case) need no barrier at all.  x != nullptr
 // fuses the forward substitution of the panel's diagonal block (y_s = L_ss^-1 t_s).
 // The caller places a CTA barrier after this function.
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int* fail, double* x) {
   constexpr int NW = NT / 32;
   const int nsn = P.nsn;
   if (nsn <= 0) return;
+  const int nsc = (nsn + CL - 1) / CL;   // panels per CTA of the group
   int G;
-  if (nsn >= NT) {
+  if (nsc >= NT) {
     G = 1;
-  } else if (nsn > NW) {
-    G = NT / nsn;
+  } else if (nsc > NW) {
+    G = NT / nsc;
     while (G & (G - 1)) G &= G - 1;
     if (G > 32) G = 32;
   } else {
-    int tw = NW / nsn;
+    int tw = NW / nsc;
     while (tw & (tw - 1)) tw &= tw - 1;
     G = 32 * tw;
   }
   const int nteams = NT / G;
+  const int cr = crank<CL>();
+  if (threadIdx.x >= nteams * G) return;   // NT need not be a multiple of G (384 = 256 + 128)
   const int team = threadIdx.x / G, rank = threadIdx.x - team * G;
   TeamSync ts;
   ts.size = G;
   ts.bar = 1 + team;
   ts.mask = G >= 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
-  for (int i = team; i < nsn; i += nteams) {
+  for (int i = team + cr * nteams; i < nsn; i += nteams * CL) {
     const int4 sa = P.sna[i];
     double* Pn = V.at(sa.x);
     const int m = sa.y, ld = sa.z, w = sa.w;
@@ -1081,22 +1123,22 @@ __device__ void level_trsv_lower(const Pk& P, const LView& V, double* x) {
     if (sa.w > D) warp_trsv_lower_w<D>(V.at(sa.x), sa.z, sa.w, x + (size_t)D * P.snb[i].x);
   }
 }
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void level_trsv_upper(const Pk& P, const LView& V, double* x) {
-  for (int i = threadIdx.x; i < P.nsn; i += NT) {
+  for (int i = crank<CL>() * NT + threadIdx.x; i < P.nsn; i += CL * NT) {
     const int4 sa = P.sna[i];
     if (sa.w == D) trsv_upper_block<D>(V.at(sa.x), sa.z, x + (size_t)D * P.snb[i].x);
   }
-  for (int i = threadIdx.x >> 5; i < P.nsn; i += NT / 32) {
+  for (int i = crank<CL>() * (NT / 32) + (threadIdx.x >> 5); i < P.nsn; i += CL * (NT / 32)) {
     const int4 sa = P.sna[i];
     if (sa.w > D) warp_trsv_upper_w<D>(V.at(sa.x), sa.z, sa.w, x + (size_t)D * P.snb[i].x);
   }
 }
 // backward gather of a level: item (panel, column c): x_c -= sum over below rows L[r][c] x_r
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void level_bwd_gather(const Pk& P, const LView& V, double* x) {
   const int total = P.snw[P.nsn];
-  for (int it = threadIdx.x; it < total; it += NT) {
+  for (int it = crank<CL>() * NT + threadIdx.x; it < total; it += CL * NT) {
     const int i = find_panel(P.snw, P.nsn, it);
     const int4 sa = P.sna[i], sb = P.snb[i];
     const int c = it - P.snw[i];
@@ -1198,9 +1240,9 @@ __device__ __forceinline__ double pk_fwd_row_partial(const Pk& P, const LView& V
 
 // forward-substitution gather of a level's pose rows (CTA-wide): x_pa -= sum L_d[p_a,:] y_d.
 // Lane map (packet): each (row, component) item owns an aligned group of G lanes.
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void pk_fwd_rows(const Pk& P, const LView& V, double* x) {
-  for (int base = 0; base < P.nfl; base += NT) {
+  for (int base = crank<CL>() * NT; base < P.nfl; base += CL * NT) {
     const int L = base + threadIdx.x;
     const int e = L < P.nfl ? P.flane[L] : -1;
     const int G = e >= 0 ? 1 << ((e >> 5) & 7) : 1, sub = e >= 0 ? (e & 31) : 0;
@@ -1215,7 +1257,7 @@ __device__ void pk_fwd_rows(const Pk& P, const LView& V, double* x) {
 
 // Full numeric factorisation, level-synchronous with packet prefetch.  xf != nullptr fuses the
 // forward substitution (y = L^-1 x in place).
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, double tol, int* s_fail,
                              uint64_t* mbar, uint32_t& phase, double* xinv, double* xf, PkPipe& pp) {
   proxy_barrier();
@@ -1226,13 +1268,13 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     const int lv = P.level;
     const int lo = g.level_off[lv];
     const bool resident = lo >= L.rlo;
-    const int hi = resident ? lo : g.level_stage_hi[lv];
+    const int hi = (resident || CL > 1) ? lo : g.level_stage_hi[lv];   // groups work in global memory
     DNLS_TRACE_POINT(1000 + lv);
     if (P.first && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
     DNLS_TRACE_POINT(1100 + lv);
     const LView V = L.level(stage, lo, hi);
     {   // (U) gather-form updates: item = (task, row a) owns an aligned group of G lanes (lane map)
-      for (int base = 0; base < P.nul; base += NT) {
+      for (int base = crank<CL>() * NT; base < P.nul; base += CL * NT) {
         const int Ln = base + threadIdx.x;
         const int e = Ln < P.nul ? P.ulane[Ln] : -1;
         const bool valid = e >= 0;
@@ -1258,15 +1300,15 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     // forward-substitution rows read descendant panels and y of earlier levels only: no barrier
     // between them and the updates of this level's panels
 #ifndef DNLS_SKIP_FWD
-    if (xf) pk_fwd_rows<D, NT>(P, V, xf);
+    if (xf) pk_fwd_rows<D, NT, CL>(P, V, xf);
 #endif
-    __syncthreads();
+    gsync<CL>();
     DNLS_TRACE_POINT(1200 + lv);
     // (F) dense factorisation of this packet's panels, level-wide
 #ifndef DNLS_SKIP_F
-    level_factor_teams<D, NT>(P, V, tol, s_fail, xf);   // + fused y_s = L_ss^-1 t_s
+    level_factor_teams<D, NT, CL>(P, V, tol, s_fail, xf);   // + fused y_s = L_ss^-1 t_s
 #endif
-    __syncthreads();
+    gsync<CL>();
     DNLS_TRACE_POINT(1300 + lv);
     if (P.last && !resident && hi > lo) copy_range<NT>(L.g + lo, stage, hi - lo);
     proxy_barrier();
@@ -1277,7 +1319,7 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
 
 // Solve with the factor: forward (unless fused into the factorisation) and backward
 // substitution, level-synchronous with packet prefetch; warp per supernode for the dense parts.
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, double* x, uint64_t* mbar,
                             uint32_t& phase, PkPipe& pp, bool forward = true) {
   if (forward) {
@@ -1308,30 +1350,30 @@ __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, do
     const int lv = P.level;
     const int lo = g.level_off[lv];
     const bool resident = lo >= L.rlo;
-    const int hi = resident ? lo : g.level_stage_hi[lv];
+    const int hi = (resident || CL > 1) ? lo : g.level_stage_hi[lv];
     DNLS_TRACE_POINT(3000 + lv);
     if (P.last && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
     DNLS_TRACE_POINT(3100 + lv);
     const LView V = L.level(stage, lo, hi);
 #ifndef DNLS_SKIP_BS
-    level_bwd_gather<D, NT>(P, V, x);
+    level_bwd_gather<D, NT, CL>(P, V, x);
 #endif
-    __syncthreads();
+    gsync<CL>();
 #ifndef DNLS_SKIP_BS
-    level_trsv_upper<D, NT>(P, V, x);
+    level_trsv_upper<D, NT, CL>(P, V, x);
 #endif
-    proxy_barrier();
+    gsync<CL>();   // also orders the packet buffer reuse (proxy barrier)
     pk_issue(g, pp, k - 2);
   }
 }
 
 // ============================================================================= a5: retraction
 // Tout[o] = Tin[o] Exp(-alpha delta_o), delta in permuted order
-template <int D, int NT>
+template <int D, int NT, int CL = 1>
 __device__ void retract_phase(const DevGraph& g, const double* Tin, double* Tout, const double* x, double alpha) {
   constexpr int PS = GT<D>::PS;
   using namespace dev;
-  for (int o = threadIdx.x; o < g.N; o += NT) {
+  for (int o = crank<CL>() * NT + threadIdx.x; o < g.N; o += CL * NT) {
     const double* dl = x + (size_t)D * g.iperm[o];
     double xi[D];
 #pragma unroll

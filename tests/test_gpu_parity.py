@@ -487,3 +487,37 @@ def test_welsch_layer_learnable_radius():
     gt = torch.from_numpy(np.broadcast_to(data["gt"], out.shape).copy()).to(DEV)
     ((out - gt) ** 2).sum().backward()
     assert rad.grad is not None and rad.grad.shape == rad.shape and torch.isfinite(rad.grad).all()
+
+
+# ------------------------------------------------------------------ cluster path (few large problems)
+@pytest.mark.parametrize("cl", [2, 8])
+@pytest.mark.parametrize("N,dim,opt,B", [(64, 3, "gn", 3), (40, 2, "lm", 3), (150, 3, "gn", 2), (30, 3, "gn", 1)])
+def test_forward_cluster_matches_oracle(cl, N, dim, opt, B):
+    """dnls_forward with a cluster of cl CTAs per element (global-memory factor, cluster barriers)
+    vs the oracle; then the implicit backward on the factor the cluster left in the workspace."""
+    topo, data = make_case(N, dim=dim, p=0.3, seed=N + cl, B=B)
+    K = 8
+    solver, t, poses, obj, st, it = run_forward(topo, data, implicit=True, max_iterations=K, cluster_ctas=cl,
+                                                optimizer=(D.LM if opt == "lm" else D.GN))
+    res = oracle_results(topo, data, max_iterations=K, optimizer=opt, implicit=True)
+    P = poses.cpu().numpy()
+    d = 6 if dim == 3 else 3
+    v = np.random.default_rng(4).standard_normal((B, N, d))
+    ge, gp = solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
+                             torch.from_numpy(v).to(DEV), D.GRAD_TANGENT, per_element=True)
+    torch.cuda.synchronize()
+    for b, r in enumerate(res):
+        if opt == "lm" and lm_has_tie(r):
+            continue
+        assert pose_err(P[b], r.x) <= TOL_POSE
+        assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
+        assert st[b].item() == r.status and it[b].item() == r.iterations
+        a, c, _ = oimp.implicit_weight_grads(oracle_problem(topo, data, b), r.x, v[b].reshape(-1), L_K=r.L_final)
+        assert rel_vec_err(np.concatenate([ge[b].cpu().numpy(), gp[b].cpu().numpy()]),
+                           np.concatenate([a, c])) <= TOL_GRAD
+
+
+def test_cluster_option_validation():
+    topo, data = make_case(20, dim=3, B=1)
+    with pytest.raises(DnlsError):
+        run_forward(topo, data, max_iterations=2, cluster_ctas=3)
