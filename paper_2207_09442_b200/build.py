@@ -6,7 +6,8 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", "dnls.cu"), os.path.join(HERE, "csrc", "symbolic.cpp")]
+SRC = [os.path.join(HERE, "csrc", "dnls.cu"), os.path.join(HERE, "csrc", "dnls_cluster.cu"),
+       os.path.join(HERE, "csrc", "symbolic.cpp")]
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("phases.cuh", "lie.cuh", "symbolic.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "dnls.h")]
 OUT = os.path.join(HERE, "lib", "libdnls.so")

@@ -119,6 +119,27 @@ DevProb dev_prob(const dnls_problem* p) {
 }  // namespace
 
 // ============================================================================= kernels
+namespace dnls {
+struct FwdParams {
+  int K;
+  int lm;
+  double alpha;
+  double lam0, lam_min, lam_max, lam_down, lam_up;
+  int damping;
+  int early_stop;
+  double abs_tol, rel_tol;
+  int implicit;
+  double* objective;
+  int* status;
+  int* iterations;
+};
+// k_forward with clusters of CL CTAs per element, compiled in its own translation unit
+// (dnls_cluster.cu: instantiating it here changes the inlining of the shared device phases and
+// makes the one-CTA kernel spill).  Returns the launch error.
+cudaError_t launch_forward_cluster(int CL, int D, const DevGraph& g, DevProb pr, DevWs ws, FwdParams fp, int batch,
+                                   cudaStream_t s);
+}  // namespace dnls
+
 namespace {
 
 size_t smem_bytes(const DevGraph& g) {
@@ -180,19 +201,6 @@ __device__ __forceinline__ LView global_view(const DevGraph& g, double* Lg) {
   return LView{Lg, nullptr, g.storage, nullptr, 0, 0};
 }
 
-struct FwdParams {
-  int K;
-  int lm;
-  double alpha;
-  double lam0, lam_min, lam_max, lam_down, lam_up;
-  int damping;
-  int early_stop;
-  double abs_tol, rel_tol;
-  int implicit;
-  double* objective;
-  int* status;
-  int* iterations;
-};
 
 // group-wide: S = sum(cost) (fixed order, identical in every CTA of the group), maxdiag = max
 // over warps (and over the group's CTAs through the global scratch clr[CL]).  Returns via shared
@@ -242,8 +250,7 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
   constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
   const int b = blockIdx.x / CL;
   const int cr = crank<CL>();
-  const int gt = cr * NT + threadIdx.x;
-  double* clr = ws.clred + (size_t)b * 2 * CL;
+  double* const clr = CL > 1 ? ws.clred + (size_t)b * 2 * CL : nullptr;   // no live register at CL == 1
   __shared__ double s_red[NT / 32];
   __shared__ double sh_S, sh_max, sh_Stry;
   __shared__ int sh_fail;
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
         accept = sh_Stry < S;
       }
       if (accept) {
-        for (int i = gt; i < g.N * PS; i += CL * NT) Tb[i] = Ttr[i];
+        for (int i = cr * NT + threadIdx.x; i < g.N * PS; i += CL * NT) Tb[i] = Ttr[i];
         gsync<CL>();
         lam = fmax(lam / fp.lam_down, fp.lam_min);
         Sprev = S;
@@ -356,6 +363,7 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
   }
 }
 
+#ifndef DNLS_CLUSTER_TU
 template <int D>
 __global__ void __launch_bounds__(NT, MINB) k_linearize(DevGraph g, DevProb pr, DevWs ws, const double* lam,
                                                       int damping, double* objective) {
@@ -715,28 +723,15 @@ __global__ void k_export_rhs(DevGraph g, DevWs ws, double* out) {
   }
 }
 
+#endif  // !DNLS_CLUSTER_TU
 }  // namespace
 
 // ============================================================================= C ABI
-namespace {
-// CTAs per batch element for dnls_forward (DESIGN.md "few large problems"): a cluster when the
-// batch leaves most SMs idle and the graph has enough work per level to share
-int forward_cluster(const dnls_graph* g, int batch, int req) {
-  if (req == 1 || req == 2 || req == 8) return req;
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // measured on C3 (4096 poses, B = 16): 1 CTA 2.18k, 2 CTAs 2.53k, 8 CTAs 1.62k problem-iter/s --
-  // the cluster barriers and the all-global working set outweigh the wider levels beyond 2
-  if (g->sym.N < 1024) return 1;
-  if (batch * 2 <= sms) return 2;
-  return 1;
-}
-template <int CL, class K>
-dnls_status launch_grouped(K* kernel, const dnls_graph* g, int batch, cudaStream_t s, DevProb pr, DevWs ws,
-                           FwdParams fp) {
-  const size_t smem = smem_bytes_grouped(g->dg);
-  dnls_status st = set_smem(kernel, smem, "k_forward (cluster)");
-  if (st) return st;
+#ifdef DNLS_CLUSTER_TU
+namespace dnls {
+cudaError_t launch_forward_cluster(int CL, int D, const DevGraph& g, DevProb pr, DevWs ws, FwdParams fp, int batch,
+                                   cudaStream_t s) {
+  const size_t smem = smem_bytes_grouped(g);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * CL));
   cfg.blockDim = dim3(NT);
@@ -749,9 +744,35 @@ dnls_status launch_grouped(K* kernel, const dnls_graph* g, int batch, cudaStream
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kernel, g->dg, pr, ws, fp) != cudaSuccess)
-    return fail(DNLS_E_CUDA, std::string("dnls_forward: cluster launch: ") + cudaGetErrorString(cudaGetLastError()));
-  return DNLS_OK;
+#define DNLS_LAUNCH_CL(DD, CC)                                                                         \
+  {                                                                                                  \
+    cudaError_t e = cudaFuncSetAttribute(k_forward<DD, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         (int)smem);                                                 \
+    if (e != cudaSuccess) return e;                                                                  \
+    return cudaLaunchKernelEx(&cfg, k_forward<DD, CC>, g, pr, ws, fp);                               \
+  }
+  if (D == 6 && CL == 2) DNLS_LAUNCH_CL(6, 2)
+  if (D == 6 && CL == 8) DNLS_LAUNCH_CL(6, 8)
+  if (D == 3 && CL == 2) DNLS_LAUNCH_CL(3, 2)
+  if (D == 3 && CL == 8) DNLS_LAUNCH_CL(3, 8)
+#undef DNLS_LAUNCH_CL
+  return cudaErrorInvalidValue;
+}
+}  // namespace dnls
+#else  // the main translation unit: host API
+
+namespace {
+// CTAs per batch element for dnls_forward (DESIGN.md "few large problems"): a cluster when the
+// batch leaves most SMs idle and the graph has enough work per level to share
+int forward_cluster(const dnls_graph* g, int batch, int req) {
+  if (req == 1 || req == 2 || req == 8) return req;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // measured on C3 (4096 poses, B = 16): 1 CTA 2.18k, 2 CTAs 2.53k, 8 CTAs 1.62k problem-iter/s --
+  // the cluster barriers and the all-global working set outweigh the wider levels beyond 2
+  if (g->sym.N < 1024) return 1;
+  if (batch * 2 <= sms) return 2;
+  return 1;
 }
 }  // namespace
 
@@ -1131,10 +1152,8 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   const int cl = forward_cluster(g, batch, opt->cluster_ctas);
   if (cl == 1) {
     DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD, 1>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD, 1><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
-  } else if (cl == 2) {
-    DISPATCH_D(g->sym.D, if ((st = launch_grouped<2>(k_forward<DD, 2>, g, batch, s, dev_prob(prob), ws, fp))) return st);
-  } else {
-    DISPATCH_D(g->sym.D, if ((st = launch_grouped<8>(k_forward<DD, 8>, g, batch, s, dev_prob(prob), ws, fp))) return st);
+  } else if (launch_forward_cluster(cl, g->sym.D, g->dg, dev_prob(prob), ws, fp, batch, s) != cudaSuccess) {
+    return fail(DNLS_E_CUDA, std::string("dnls_forward: cluster launch: ") + cudaGetErrorString(cudaGetLastError()));
   }
   if ((st = cuda_check("dnls_forward: k_forward launch"))) return st;
   if (fp.implicit) {
@@ -1303,3 +1322,4 @@ DNLS_API dnls_status dnls_export_rhs(const dnls_graph* g, int32_t batch, const v
 }
 
 }  // extern "C"
+#endif  // DNLS_CLUSTER_TU

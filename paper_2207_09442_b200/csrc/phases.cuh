@@ -1028,13 +1028,14 @@ __device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int*
   }
   const int nteams = NT / G;
   const int cr = crank<CL>();
-  if (threadIdx.x >= nteams * G) return;   // NT need not be a multiple of G (384 = 256 + 128)
+
   const int team = threadIdx.x / G, rank = threadIdx.x - team * G;
   TeamSync ts;
   ts.size = G;
   ts.bar = 1 + team;
   ts.mask = G >= 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
-  for (int i = team + cr * nteams; i < nsn; i += nteams * CL) {
+  // threads of a partial last team (NT need not be a multiple of G: 384 = 256 + 128) take no panel
+  for (int i = (team < nteams ? team + cr * nteams : nsn); i < nsn; i += nteams * CL) {
     const int4 sa = P.sna[i];
     double* Pn = V.at(sa.x);
     const int m = sa.y, ld = sa.z, w = sa.w;
