@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--backward", default="implicit", choices=["implicit", "dlm"],
                     help="backward mode timed in the step (dlm: PAPER.md:259-271, one augmented GN step)")
     ap.add_argument("--epsilon", type=float, default=1e-3, help="DLM epsilon")
+    ap.add_argument("--optimizer", default=None, choices=["gn", "lm", "dogleg"],
+                    help="override the config's inner optimizer (dogleg: PAPER.md:153 trust region)")
     ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 8],
                     help="CTAs per batch element in the forward (0 = automatic)")
     ap.add_argument("--welsch", type=float, default=None,
@@ -197,7 +199,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.optimizer:
+        cfg["opt"] = args.optimizer
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -231,7 +235,7 @@ def main():
     group = D.SE3 if cfg["dim"] == 3 else D.SE2
     K = cfg["K"]
     solver = PoseGraphSolver(group, topo.num_poses, topo.edges, topo.prior_vars, device=local_rank,
-                             max_iterations=K, optimizer=(D.LM if cfg["opt"] == "lm" else D.GN))
+                             max_iterations=K, optimizer={"gn": D.GN, "lm": D.LM, "dogleg": D.DOGLEG}[cfg["opt"]])
     g = solver.graph
     st = solver.stats
     opt = solver.options

@@ -62,7 +62,7 @@ typedef enum {
 } dnls_status;
 
 typedef enum { DNLS_SE2 = 3, DNLS_SE3 = 6 } dnls_group;          /* value = tangent dimension d */
-typedef enum { DNLS_GN = 0, DNLS_LM = 1 } dnls_optimizer;
+typedef enum { DNLS_GN = 0, DNLS_LM = 1, DNLS_DOGLEG = 2 } dnls_optimizer;
 typedef enum { DNLS_BWD_NONE = 0, DNLS_BWD_IMPLICIT = 1 } dnls_backward;
 typedef enum { DNLS_DAMP_MARQUARDT = 0, DNLS_DAMP_IDENTITY = 1 } dnls_damping;
 typedef enum { DNLS_GRAD_TANGENT = 0, DNLS_GRAD_MATRIX = 1 } dnls_grad_kind;
@@ -90,6 +90,14 @@ typedef struct dnls_options {
   int32_t cluster_ctas;     /* CTAs sharing one batch element in dnls_forward: 0 = automatic (a cluster
                                of 2 CTAs when the batch leaves half the SMs idle and N >= 1024,
                                DESIGN.md "few large problems"), else 1, 2 or 8 */
+  /* Dogleg trust region (reading DL1): initial, maximum and
+   * minimum radius of the tangent step, defaults 1, 1e4, 1e-10.  Step: the GN point if it lies in
+   * the radius, else the scaled gradient (Cauchy point outside) or the dogleg interpolation;
+   * gain ratio rho: accept iff rho > 0, rho > 0.75 doubles, rho < 0.25 halves the radius; a
+   * rejection below the minimum radius freezes the element (status DNLS_ST_SATURATED). */
+  double trust_radius0;
+  double trust_radius_max;
+  double trust_radius_min;
 } dnls_options;
 
 typedef struct dnls_problem {

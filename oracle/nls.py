@@ -119,7 +119,7 @@ class EuclidProblem:
 
 @dataclass
 class Options:
-    optimizer: str = "gn"          # "gn" | "lm"
+    optimizer: str = "gn"          # "gn" | "lm" | "dogleg"
     max_iterations: int = 10
     step_size: float = 1.0
     lambda0: float = 1e-3
@@ -132,6 +132,9 @@ class Options:
     abs_tol: float = 1e-10
     rel_tol: float = 1e-8
     implicit: bool = False
+    delta0: float = 1.0            # Dogleg trust radius: initial, max, min (reading DL1)
+    delta_max: float = 1e4
+    delta_min: float = 1e-10
 
 
 @dataclass
@@ -207,6 +210,66 @@ def levenberg_marquardt(prob, x0, opt: Options) -> Result:
     return res
 
 
+def dogleg(prob, x0, opt: Options) -> Result:
+    """Powell's dogleg trust-region step ("Dogleg"; reading DL1).
+    With b = J^T r (the gradient of S), H = J^T J and our sign convention theta <- theta [+] (-d):
+      d_gn = H^-1 b;  if |d_gn| <= Delta: d = d_gn
+      else d_c = (b.b / b.Hb) b;  if |d_c| >= Delta: d = (Delta / |b|) b
+      else d = d_c + tau (d_gn - d_c), tau in [0, 1] with |d| = Delta;
+    predicted decrease b.d - 1/2 d.Hd, gain ratio rho = (S - S(theta [+] -d)) / predicted;
+    accept iff rho > 0; rho > 0.75: Delta <- min(2 Delta, Delta_max); rho < 0.25: Delta <- Delta / 2;
+    a rejection with Delta < Delta_min marks the element (status 3, trust region collapsed)."""
+    x = np.array(x0, dtype=np.float64, copy=True)
+    status, iters = ST_OK, 0
+    Delta = opt.delta0
+    hist, trials = [], []
+    S, H, b = prob.linearize(x)
+    S_prev = None
+    for k in range(opt.max_iterations):
+        if opt.early_stop and S_prev is not None and abs(S - S_prev) < opt.abs_tol + opt.rel_tol * S_prev:
+            status = ST_CONVERGED
+            break
+        hist.append(S)
+        iters += 1
+        L, ok = linalg.cholesky(H)
+        if not ok:
+            status = ST_NOT_SPD
+            break
+        d_gn = linalg.chol_solve(L, b)
+        if np.linalg.norm(d_gn) <= Delta:
+            d, kind = d_gn, "gn"
+        else:
+            bb = float(b @ b)
+            d_c = (bb / float(b @ H @ b)) * b
+            if np.linalg.norm(d_c) >= Delta:
+                d, kind = (Delta / np.sqrt(bb)) * b, "sd"
+            else:
+                u = d_gn - d_c
+                qa, qb, qc = float(u @ u), 2.0 * float(d_c @ u), float(d_c @ d_c) - Delta * Delta
+                tau = (-qb + np.sqrt(qb * qb - 4.0 * qa * qc)) / (2.0 * qa)
+                d, kind = d_c + tau * u, "dogleg"
+        pred = float(b @ d) - 0.5 * float(d @ H @ d)
+        x_try = prob.retract(x, -d)
+        S_try = prob.objective(x_try)
+        rho = (S - S_try) / pred if pred > 0 else 0.0
+        accept = rho > 0
+        trials.append((S, S_try, accept, rho, Delta, kind, float(np.linalg.norm(d_gn))))
+        if rho > 0.75:
+            Delta = min(2.0 * Delta, opt.delta_max)
+        elif rho < 0.25:
+            Delta = 0.5 * Delta
+        if accept:
+            x = x_try
+            S_prev = S
+            S, H, b = prob.linearize(x)
+        elif Delta < opt.delta_min:
+            status = ST_SATURATED
+            break
+    res = _finish(prob, x, status, iters, hist, Delta, opt)
+    res.trials = trials
+    return res
+
+
 def _finish(prob, x, status, iters, hist, lam, opt) -> Result:
     res = Result(x=x, objective=prob.objective(x), status=status, iterations=iters,
                  history=hist, lam=lam)
@@ -225,6 +288,8 @@ def optimize(prob, x0, opt: Options) -> Result:
         return gauss_newton(prob, x0, opt)
     if opt.optimizer == "lm":
         return levenberg_marquardt(prob, x0, opt)
+    if opt.optimizer == "dogleg":
+        return dogleg(prob, x0, opt)
     raise ValueError(opt.optimizer)
 
 

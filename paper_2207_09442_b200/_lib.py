@@ -35,6 +35,9 @@ class DnlsOptions(ctypes.Structure):
         ("rel_tol", ctypes.c_double),
         ("backward_mode", ctypes.c_int32),
         ("cluster_ctas", ctypes.c_int32),
+        ("trust_radius0", ctypes.c_double),
+        ("trust_radius_max", ctypes.c_double),
+        ("trust_radius_min", ctypes.c_double),
     ]
 
 

@@ -61,7 +61,7 @@ struct dnls_graph {
 // ----------------------------------------------------------------------------- workspace layout
 namespace {
 struct WsLayout {
-  size_t L, x, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, clred, total;
+  size_t L, x, bsave, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, clred, total;
 };
 WsLayout ws_layout(const Symbolic& s, int B) {
   const int D = s.D, PS = D == 6 ? 12 : 6, JS = D * (D + 1) + 2 * D + D * D;   // GT<D>::JS
@@ -70,6 +70,7 @@ WsLayout ws_layout(const Symbolic& s, int B) {
   size_t o = 0;
   w.L = o;     o = align_up(o + sizeof(double) * (size_t)B * s.storage);
   w.x = o;     o = align_up(o + sizeof(double) * (size_t)B * n);
+  w.bsave = o; o = align_up(o + sizeof(double) * (size_t)B * n);
   w.jac = o;   o = align_up(o + sizeof(double) * (size_t)B * slots * JS);
   w.cost = o;  o = align_up(o + sizeof(double) * (size_t)B * slots);
   w.rgrad = o; o = align_up(o + sizeof(double) * (size_t)B * slots);
@@ -89,6 +90,7 @@ DevWs ws_views(const WsLayout& l, void* base) {
   DevWs w;
   w.L = (double*)(p + l.L);
   w.x = (double*)(p + l.x);
+  w.bsave = (double*)(p + l.bsave);
   w.jac = (double*)(p + l.jac);
   w.cost = (double*)(p + l.cost);
   w.rgrad = (double*)(p + l.rgrad);
@@ -129,6 +131,8 @@ struct FwdParams {
   int early_stop;
   double abs_tol, rel_tol;
   int implicit;
+  int dogleg;
+  double dl0, dl_max, dl_min;   // trust radius
   double* objective;
   int* status;
   int* iterations;
@@ -244,6 +248,58 @@ __device__ void group_fail(int* sh_fail, double* clr) {
   __syncthreads();
 }
 
+// CTA-wide deterministic sum (fixed shuffle tree, warps summed in order); every thread gets it
+__device__ __forceinline__ double cta_sum(double v, double* s_tmp) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_tmp[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < NT / 32; ++i) t += s_tmp[i];
+  __syncthreads();
+  return t;
+}
+// packed lower-triangular quadratic form u^T H u (H symmetric, lower triangle packed column-wise)
+template <int D>
+__device__ __forceinline__ double quad_lower(const double* h, const double* u) {
+  double v = 0.0;
+  int e = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = q; a < D; ++a) {
+      const double t = h[e++] * u[a] * u[q];
+      v += (a == q) ? t : 2.0 * t;
+    }
+  return v;
+}
+// b^T H_s b of one cost slot from its H contributions (scratch diagonal parts, the off-diagonal
+// block in the factor storage -- before the factorisation overwrites it -- or in the scratch for
+// parallel edges).  x_b holds b (permuted order).  Dogleg's Cauchy point needs sum_s b^T H_s b.
+template <int D>
+__device__ double slot_bHb(const DevGraph& g, const LView& L, const double* x_b, const double* scr, int slot) {
+  using SC = Scr<D>;
+  const int4 d0 = g.slot_desc[3 * slot], d1 = g.slot_desc[3 * slot + 1], d2 = g.slot_desc[3 * slot + 2];
+  const double* o = scr + (size_t)slot * SC::SIZE;
+  const double* bi = x_b + (size_t)D * d2.x;
+  double v = quad_lower<D>(o + SC::H0, bi);
+  if (d0.y >= 0) {
+    const double* bj = x_b + (size_t)D * d2.y;
+    v += quad_lower<D>(o + SC::H1, bj);
+    const double* O = d2.z ? L.at(d0.z) : o + SC::HIJ;
+    const int ld = d2.z ? d1.z : D;
+    const double* br = d0.w ? bj : bi;   // block rows: pose P (j if d0.w), columns: the other pose
+    const double* bc = d0.w ? bi : bj;
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int a = 0; a < D; ++a) t += br[a] * O[(size_t)q * ld + a] * bc[q];
+    v += 2.0 * t;
+  }
+  return v;
+}
+
 // CL > 1: a cluster of CL CTAs shares element blockIdx.x / CL (few large problems)
 template <int D, int CL>
 __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, DevWs ws, FwdParams fp) {
@@ -266,12 +322,18 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
 
   int status = DNLS_ST_OK, iters = 0;
   double lam = fp.lam0, Sprev = 0.0;
+  // Dogleg state in shared memory (not live in registers across the factorisation):
+  // [0] trust radius, [1] b.b, [2] b.Hb, [3] y.y
+  __shared__ double s_tmp[NT / 32], sh_dl[4];
+  if (threadIdx.x == 0) sh_dl[0] = fp.dl0;
   bool have_prev = false;
   for (int k = 0; k < fp.K; ++k) {
     // a1 + a2 at theta_k
     DNLS_TRACE_POINT(100);
     DNLS_TRACE_POINT(200);
+#ifndef DNLS_SKIP_LIN
     linearize_phase<D, NT, CL>(g, pr, Tb, b, L, x_b, cost_b, jac_b, fp.lm ? lam : -1.0, fp.damping, s_red);
+#endif
     finish_assembly<D, CL>(g, cost_b, s_red, &sh_S, &sh_max, clr);
     DNLS_TRACE_POINT(300);
     const double S = sh_S;
@@ -279,13 +341,90 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
       status = DNLS_ST_CONVERGED;
       break;
     }
+    if (CL == 1 && fp.dogleg) {   // b = J^T r (saved), b.b and b.Hb before the factor overwrites H
+      double* bs = ws.bsave + (size_t)b * g.n;
+      double pb = 0.0, ph = 0.0;
+      for (int i = threadIdx.x; i < g.n; i += NT) {
+        const double v = x_b[i];
+        bs[i] = v;
+        pb = fma(v, v, pb);
+      }
+      for (int sl = threadIdx.x; sl < g.E + g.P; sl += NT) ph += slot_bHb<D>(g, L, x_b, jac_b, sl);
+      const double bb = cta_sum(pb, s_tmp), bHb = cta_sum(ph, s_tmp);
+      if (threadIdx.x == 0) {
+        sh_dl[1] = bb;
+        sh_dl[2] = bHb;
+      }
+    }
     if (threadIdx.x == 0) sh_fail = 0;
     __syncthreads();
     factor_phase<D, NT, CL>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, x_b, sm.pp);
     group_fail<CL>(&sh_fail, clr);
     const bool ok = sh_fail == 0;
     __syncthreads();
-    if (!fp.lm) {
+    if (CL == 1 && fp.dogleg && ok) {   // y = L^-1 b: b^T H^-1 b = y.y
+      double py = 0.0;
+      for (int i = threadIdx.x; i < g.n; i += NT) py = fma(x_b[i], x_b[i], py);
+      const double yy = cta_sum(py, s_tmp);
+      if (threadIdx.x == 0) sh_dl[3] = yy;
+    }
+    if (CL == 1 && fp.dogleg) {   // Powell's dogleg (reading DL1)
+      ++iters;
+      if (!ok) {
+        status = DNLS_ST_NOT_SPD;
+        break;
+      }
+      solve_phase<D, NT, CL>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);   // x_b = d_gn = H^-1 b
+      double pg = 0.0;
+      for (int i = threadIdx.x; i < g.n; i += NT) pg = fma(x_b[i], x_b[i], pg);
+      const double gg = cta_sum(pg, s_tmp);
+      const double delta = sh_dl[0], bb = sh_dl[1], bHb = sh_dl[2], yy = sh_dl[3];
+      const double* bs = ws.bsave + (size_t)b * g.n;
+      // step d = alpha b + beta d_gn; scalars from H d_gn = b, d_gn.b = y.y (identical in all threads)
+      double alpha, beta;
+      if (sqrt(gg) <= delta) {
+        alpha = 0.0;
+        beta = 1.0;
+      } else {
+        const double kappa = bb / bHb;   // Cauchy point d_c = kappa b
+        if (kappa * sqrt(bb) >= delta) {
+          alpha = delta / sqrt(bb);
+          beta = 0.0;
+        } else {   // |d_c + tau (d_gn - d_c)| = delta
+          const double uu = gg - 2.0 * kappa * yy + kappa * kappa * bb;
+          const double qb = 2.0 * (kappa * yy - kappa * kappa * bb), qc = kappa * kappa * bb - delta * delta;
+          const double tau = (-qb + sqrt(qb * qb - 4.0 * uu * qc)) / (2.0 * uu);
+          alpha = (1.0 - tau) * kappa;
+          beta = tau;
+        }
+      }
+      const double pred = (alpha * bb + beta * yy) - 0.5 * (alpha * alpha * bHb + 2.0 * alpha * beta * bb +
+                                                            beta * beta * yy);
+      for (int i = threadIdx.x; i < g.n; i += NT) x_b[i] = alpha * bs[i] + beta * x_b[i];
+      __syncthreads();
+      retract_phase<D, NT, CL>(g, Tb, Ttr, x_b, 1.0);
+      __syncthreads();
+      objective_phase<D, NT, CL>(g, pr, Ttr, b, cost_b);
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const double st = warp0_sum(cost_b, g.E + g.P);
+        if (threadIdx.x == 0) sh_Stry = st;
+      }
+      __syncthreads();
+      const double rho = pred > 0.0 ? (S - sh_Stry) / pred : 0.0;
+      const double delta_new = rho > 0.75 ? fmin(2.0 * delta, fp.dl_max) : (rho < 0.25 ? 0.5 * delta : delta);
+      __syncthreads();
+      if (threadIdx.x == 0) sh_dl[0] = delta_new;
+      if (rho > 0.0) {
+        for (int i = threadIdx.x; i < g.N * PS; i += NT) Tb[i] = Ttr[i];
+        __syncthreads();
+        Sprev = S;
+        have_prev = true;
+      } else if (delta_new < fp.dl_min) {
+        status = DNLS_ST_SATURATED;
+        break;
+      }
+    } else if (!fp.lm) {
 #ifndef DNLS_ABLATE   // development builds that skip a phase (timing ablation) must not stop early
       if (!ok) {
         status = DNLS_ST_NOT_SPD;
@@ -357,7 +496,7 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
     if (fp.status) fp.status[b] = status;
     if (fp.iterations) fp.iterations[b] = iters;
     ws.S[b] = sh_S;
-    ws.lam[b] = lam;
+    ws.lam[b] = fp.dogleg ? sh_dl[0] : lam;
     ws.st[b] = status;
     ws.it[b] = iters;
   }
@@ -819,6 +958,9 @@ DNLS_API void dnls_options_default(dnls_options* o) {
   o->abs_tol = 1e-10;
   o->rel_tol = 1e-8;
   o->backward_mode = DNLS_BWD_NONE;
+  o->trust_radius0 = 1.0;
+  o->trust_radius_max = 1e4;
+  o->trust_radius_min = 1e-10;
 }
 
 DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t num_edges,
@@ -1104,7 +1246,7 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   if (st) return st;
   if (!opt) return fail(DNLS_E_INVALID, "dnls_forward: options is NULL");
   if ((st = check_problem("dnls_forward", g, prob))) return st;
-  if (opt->optimizer != DNLS_GN && opt->optimizer != DNLS_LM)
+  if (opt->optimizer != DNLS_GN && opt->optimizer != DNLS_LM && opt->optimizer != DNLS_DOGLEG)
     return fail(DNLS_E_INVALID, "dnls_forward: unknown optimizer " + std::to_string(opt->optimizer));
   if (opt->max_iterations < 0) return fail(DNLS_E_INVALID, "dnls_forward: max_iterations < 0");
   if (!(opt->step_size > 0.0 && opt->step_size <= 1.0))
@@ -1116,6 +1258,9 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
       !(opt->lambda0 > 0 && opt->lambda_min > 0 && opt->lambda_max >= opt->lambda_min && opt->lambda_down > 1 &&
         opt->lambda_up > 1))
     return fail(DNLS_E_INVALID, "dnls_forward: invalid LM damping schedule");
+  if (opt->optimizer == DNLS_DOGLEG &&
+      !(opt->trust_radius0 > 0 && opt->trust_radius_min > 0 && opt->trust_radius_max >= opt->trust_radius0))
+    return fail(DNLS_E_INVALID, "dnls_forward: invalid Dogleg trust radii");
   if (opt->damping != DNLS_DAMP_MARQUARDT && opt->damping != DNLS_DAMP_IDENTITY)
     return fail(DNLS_E_INVALID, "dnls_forward: unknown damping");
   if (opt->cluster_ctas != 0 && opt->cluster_ctas != 1 && opt->cluster_ctas != 2 && opt->cluster_ctas != 8)
@@ -1145,11 +1290,15 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   fp.abs_tol = opt->abs_tol;
   fp.rel_tol = opt->rel_tol;
   fp.implicit = opt->backward_mode == DNLS_BWD_IMPLICIT;
+  fp.dogleg = opt->optimizer == DNLS_DOGLEG;
+  fp.dl0 = opt->trust_radius0;
+  fp.dl_max = opt->trust_radius_max;
+  fp.dl_min = opt->trust_radius_min;
   fp.objective = prob->objective;
   fp.status = prob->status;
   fp.iterations = prob->iterations;
   cudaStream_t s = (cudaStream_t)stream;
-  const int cl = forward_cluster(g, batch, opt->cluster_ctas);
+  const int cl = opt->optimizer == DNLS_DOGLEG ? 1 : forward_cluster(g, batch, opt->cluster_ctas);
   if (cl == 1) {
     DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD, 1>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD, 1><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
   } else if (launch_forward_cluster(cl, g->sym.D, g->dg, dev_prob(prob), ws, fp, batch, s) != cudaSuccess) {

@@ -148,6 +148,7 @@ struct DevProb {
 struct DevWs {
   double* L;      // [B][storage]
   double* x;      // [B][n]   rhs / solution (permuted order)
+  double* bsave;  // [B][n]   Dogleg: the gradient b = J^T r of the current linearisation
   double* jac;    // [B][E+P][JS]  weighted J_i, J_j, r per cost slot
   double* cost;   // [B][E+P]      1/2 |r|^2 per slot (or weight gradient in backward)
   double* rgrad;  // [B][E+P]      per-slot radius gradient (backward with a Welsch kernel)
@@ -886,6 +887,20 @@ __device__ __forceinline__ void stage_in(double* __restrict__ dst, const double*
   __syncthreads();
 }
 
+// staging of a level's contiguous panel range: TMA bulk copy (one thread issues, the copy engine
+// moves the range; the panels were written by generic stores, hence the proxy fence in bulk_load)
+// or plain vector loads
+template <int NT>
+__device__ __forceinline__ void stage_level(double* dst, const double* src, int n, uint64_t* mbar, uint32_t& phase) {
+#ifdef DNLS_TMA_STAGE
+  if ((n & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    bulk_load<NT>(dst, src, n, mbar, phase);
+    return;
+  }
+#endif
+  stage_in<NT>(dst, src, n);
+}
+
 // ---- level-wide dense kernels (all panels of a level at once)
 // inverse pivots 1/L_jj of the D x D diagonal block at (c0, c0) live in its unused strict upper
 // triangle: (c0+j, c0+j+1) for j < D-1 and (c0, c0+D-1) for j = D-1
@@ -1271,8 +1286,10 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
     const bool resident = lo >= L.rlo;
     const int hi = (resident || CL > 1) ? lo : g.level_stage_hi[lv];   // groups work in global memory
     DNLS_TRACE_POINT(1000 + lv);
-    if (P.first && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
+#ifndef DNLS_SKIP_STAGE
+    if (P.first && !resident) stage_level<NT>(stage, L.g + lo, hi - lo, mbar, phase);
     DNLS_TRACE_POINT(1100 + lv);
+#endif
     const LView V = L.level(stage, lo, hi);
     {   // (U) gather-form updates: item = (task, row a) owns an aligned group of G lanes (lane map)
       for (int base = crank<CL>() * NT; base < P.nul; base += CL * NT) {
@@ -1311,7 +1328,9 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
 #endif
     gsync<CL>();
     DNLS_TRACE_POINT(1300 + lv);
+#ifndef DNLS_SKIP_STAGE
     if (P.last && !resident && hi > lo) copy_range<NT>(L.g + lo, stage, hi - lo);
+#endif
     proxy_barrier();
     pk_issue(g, pp, k + 2);
   }
@@ -1353,7 +1372,9 @@ __device__ void solve_phase(const DevGraph& g, const LView& L, double* stage, do
     const bool resident = lo >= L.rlo;
     const int hi = (resident || CL > 1) ? lo : g.level_stage_hi[lv];
     DNLS_TRACE_POINT(3000 + lv);
-    if (P.last && !resident) stage_in<NT>(stage, L.g + lo, hi - lo);
+#ifndef DNLS_SKIP_STAGE
+    if (P.last && !resident) stage_level<NT>(stage, L.g + lo, hi - lo, mbar, phase);
+#endif
     DNLS_TRACE_POINT(3100 + lv);
     const LView V = L.level(stage, lo, hi);
 #ifndef DNLS_SKIP_BS

@@ -15,7 +15,7 @@ import torch
 from ._lib import DnlsOptions, DnlsProblem, DnlsStats, check, lib
 
 SE2, SE3 = 3, 6
-GN, LM = 0, 1
+GN, LM, DOGLEG = 0, 1, 2
 BWD_NONE, BWD_IMPLICIT = 0, 1
 DAMP_MARQUARDT, DAMP_IDENTITY = 0, 1
 GRAD_TANGENT, GRAD_MATRIX = 0, 1

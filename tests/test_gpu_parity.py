@@ -521,3 +521,50 @@ def test_cluster_option_validation():
     topo, data = make_case(20, dim=3, B=1)
     with pytest.raises(DnlsError):
         run_forward(topo, data, max_iterations=2, cluster_ctas=3)
+
+
+# ------------------------------------------------------------------ Dogleg
+def dogleg_tie(r):
+    """Decisions that can flip between two correct implementations (rounding, reading DL1 / the
+    LM caveat A13): a gain ratio at a threshold, a GN point on the radius, or an actual decrease at
+    rounding level (converged element: rho is then noise).  Such elements are compared on the
+    converged iterate (1e-7) instead of the exact iterate."""
+    for (S, S_try, acc, rho, Delta, kind, ngn) in r.trials:
+        if min(abs(rho), abs(rho - 0.25), abs(rho - 0.75)) < 1e-7 or abs(ngn - Delta) <= 1e-9 * Delta:
+            return True
+        if S_try is not None and abs(S - S_try) <= 1e-10 * S:
+            return True
+    return False
+
+
+@pytest.mark.parametrize("N,dim,B,delta0", [(40, 3, 4, 0.3), (30, 2, 4, 0.1), (64, 3, 3, 5.0)])
+def test_forward_dogleg_matches_oracle(N, dim, B, delta0):
+    noise = dict(init_sigma_t=0.4, init_sigma_r=0.2) if delta0 < 1.0 else {}   # far init: the radius binds
+    topo, data = make_case(N, dim=dim, p=0.3, seed=N, B=B, **noise)
+    K = 10 if delta0 < 1.0 else 3   # (GN-like steps converge to rounding level after ~4 iterations)
+    solver, t, poses, obj, st, it = run_forward(topo, data, implicit=True, max_iterations=K, optimizer=D.DOGLEG,
+                                                trust_radius0=delta0)
+    res = oracle_results(topo, data, max_iterations=K, optimizer="dogleg", delta0=delta0, implicit=True)
+    P = poses.cpu().numpy()
+    d = 6 if dim == 3 else 3
+    v = np.random.default_rng(8).standard_normal((B, N, d))
+    ge, gp = solver.backward(poses, t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
+                             torch.from_numpy(v).to(DEV), D.GRAD_TANGENT, per_element=True)
+    torch.cuda.synchronize()
+    kinds = set()
+    compared = 0
+    for b, r in enumerate(res):
+        kinds |= {tr[5] for tr in r.trials}
+        if dogleg_tie(r):
+            assert pose_err(P[b], r.x) <= 1e-7
+            continue
+        compared += 1
+        assert pose_err(P[b], r.x) <= TOL_POSE
+        assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
+        assert st[b].item() == r.status and it[b].item() == r.iterations
+        a, c, _ = oimp.implicit_weight_grads(oracle_problem(topo, data, b), r.x, v[b].reshape(-1), L_K=r.L_final)
+        assert rel_vec_err(np.concatenate([ge[b].cpu().numpy(), gp[b].cpu().numpy()]),
+                           np.concatenate([a, c])) <= TOL_GRAD
+    assert compared >= 1
+    if delta0 < 1.0:
+        assert kinds & {"sd", "dogleg"}   # the trust region was active
