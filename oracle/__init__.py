@@ -16,8 +16,10 @@ the ad-series, coefficient functions vs mpmath, Jacobians vs central finite
 differences, App. B curve fit (v0=1 -> v1=3), GN one-step exactness on affine
 residuals, hand 2x2 Cholesky/solve examples, brute force vs
 scipy.optimize.least_squares on tiny graphs, implicit gradient vs finite differences
-of the solve, zero-noise invariants, SE2-in-SE3 embedding, gauge invariance.
+of the solve, zero-noise invariants, SE2-in-SE3 embedding, gauge invariance; DLM
+(oracle/dlm.py) closed form and eps -> 0 limit; Welsch (oracle/robust.py) SPEC values and
+finite differences; Dogleg (nls.dogleg) SPEC hand geometry and GN limit.
 Parity unpinned (self-consistency only): the LM damping schedule constants (our
-choice, SPEC.md:415 values) -- see DESIGN.md "Readings".
+choice, SPEC.md:415 values) and the Dogleg radius constants -- see DESIGN.md "Readings".
 """
 from . import lie, costs, linalg, robust, nls, implicit, dlm  # noqa: F401
