@@ -251,11 +251,12 @@ def main():
     sts = torch.empty(B, dtype=torch.int32, device=dev)
     its = torch.empty(B, dtype=torch.int32, device=dev)
     E, P = topo.num_edges, int(topo.prior_vars.shape[0])
-    red = torch.zeros(E + P + 1, dtype=torch.float64, device=dev)   # [grad_w_edge | grad_w_prior | loss]
+    # [grad_w_edge | grad_w_prior | loss | grad_radius (Welsch)]: ONE all_reduce per step for G > 1
+    red = torch.zeros(E + P + 1 + (0 if args.welsch is None else 1), dtype=torch.float64, device=dev)
     ge, gp = red[:E], red[E:E + P]
     ws = solver.workspace(B)
     rad = None if args.welsch is None else torch.tensor([args.welsch], dtype=torch.float64, device=dev)
-    gr = None if rad is None else torch.zeros(1, dtype=torch.float64, device=dev)
+    gr = None if rad is None else red[E + P + 1:]
     prob = D.make_problem(poses, dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"], obj, sts, its,
                           radius=rad)
     stream = torch.cuda.current_stream()

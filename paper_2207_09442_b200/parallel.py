@@ -32,6 +32,20 @@ def allreduce_weight_grads(grad_w_edge: torch.Tensor, grad_w_prior: torch.Tensor
     return buf[:E].clone(), buf[E:E + P].clone(), buf[E + P:].clone()
 
 
+def allreduce_shared_grads(*grads: torch.Tensor, group=None) -> list[torch.Tensor]:
+    """Sum any set of gradients of parameters shared by the batch (weights, a shared Welsch radius,
+    the loss) over ranks with ONE all_reduce of their concatenation (fixed order)."""
+    sizes = [g.numel() for g in grads]
+    buf = torch.cat([g.reshape(-1) for g in grads])
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    out, o = [], 0
+    for g, n in zip(grads, sizes):
+        out.append(buf[o:o + n].clone().reshape(g.shape))
+        o += n
+    return out
+
+
 def max_over_ranks(value: float, device=None, group=None) -> float:
     """Max of a scalar over ranks (timings are reported as the slowest rank)."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:

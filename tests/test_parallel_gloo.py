@@ -93,3 +93,55 @@ def test_two_rank_gloo_matches_single_rank():
         assert abs(g2[0] - gp[0]) <= 1e-12 * abs(gp[0]) + 1e-300
         assert abs(l - loss) <= 1e-12 * loss
         assert t == 1.0                                              # max over ranks
+
+
+def shard_compute_robust(b0, b1, radius=0.4, eps=1e-3):
+    """Welsch kernel (shared learnable radius) + DLM backward per element: weight and radius
+    gradients of the shard."""
+    from oracle import dlm as odlm
+    topo = synth.cube_topology(N, dim=2, p=0.7, seed=5, outlier_ratio=0.3)
+    data = synth.cube_batch(topo, b1 - b0, seed=5, b_start=b0)
+    res = onls.solve_batch("SE2", N, topo.edges, topo.prior_vars, data["poses0"], data["meas"], data["prior_meas"],
+                           data["w_edge"], data["w_prior"], onls.Options(max_iterations=K), radius=radius)
+    ge, gp, gr = np.zeros(topo.num_edges), np.zeros(1), np.zeros(1)
+    for bl, r in enumerate(res):
+        prob = onls.PGOProblem("SE2", N, topo.edges, topo.prior_vars, data["meas"][bl], data["prior_meas"][bl],
+                               data["w_edge"], data["w_prior"], radius=radius)
+        v = np.random.default_rng([9, b0 + bl]).standard_normal(N * 3)
+        a, c, Td = odlm.dlm_weight_grads(prob, r.x, v, eps)
+        ge += a
+        gp += c
+        gr += odlm.dlm_radius_grad(prob, r.x, Td, eps)
+    return ge, gp, gr
+
+
+def _worker_robust(rank, world, port, out):
+    from paper_2207_09442_b200.parallel import allreduce_shared_grads
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b0, b1 = shard_range(GB, world, rank)
+    ge, gp, gr = shard_compute_robust(b0, b1)
+    g1, g2, g3 = allreduce_shared_grads(torch.from_numpy(ge), torch.from_numpy(gp), torch.from_numpy(gr))
+    out[rank] = (g1.numpy(), g2.numpy(), g3.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_shared_radius_and_dlm():
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_robust, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    ge, gp, gr = shard_compute_robust(0, GB)
+    for r in range(2):
+        g1, g2, g3 = out[r]
+        assert np.max(np.abs(g1 - ge)) <= 1e-12 * np.max(np.abs(ge))
+        assert abs(g2[0] - gp[0]) <= 1e-12 * abs(gp[0]) + 1e-300
+        assert abs(g3[0] - gr[0]) <= 1e-12 * abs(gr[0]) + 1e-300
