@@ -278,7 +278,7 @@ def main():
         else:
             D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws, grad_radius=gr)
         if world > 1:
-            torch.sum(obj, dim=0, keepdim=True, out=red[E + P:])
+            torch.sum(obj, dim=0, keepdim=True, out=red[E + P:E + P + 1])
             dist.all_reduce(red)
 
     for _ in range(args.warmup):
