@@ -212,7 +212,10 @@ __device__ __forceinline__ LView global_view(const DevGraph& g, double* Lg) {
 template <int D, int CL = 1>
 __device__ void finish_assembly(const DevGraph& g, const double* cost_b, double* s_red, double* sh_S,
                                 double* sh_max, double* clr = nullptr) {
+  DNLS_PROBE_NOW(q0);
   gsync<CL>();
+  DNLS_PROBE_NOW(q1);
+  DNLS_PROBE_ADD(4, q0, q1);
   if (threadIdx.x < 32) {
     double s = warp0_sum(cost_b, g.E + g.P);
     if (threadIdx.x == 0) {
@@ -232,6 +235,8 @@ __device__ void finish_assembly(const DevGraph& g, const double* cost_b, double*
     }
   }
   __syncthreads();
+  DNLS_PROBE_NOW(q2);
+  DNLS_PROBE_ADD(5, q1, q2);
 }
 // group-wide OR of the per-CTA factorisation failure flags (after a group barrier)
 template <int CL>
@@ -941,6 +946,17 @@ DNLS_API dnls_status dnls_debug_trace(int64_t* out, int32_t capacity, int32_t* c
   return fail(DNLS_E_UNSUPPORTED, "dnls_debug_trace: library built without -DDNLS_TRACE");
 #endif
 }
+
+#ifdef DNLS_LIN_PROBE
+DNLS_API int dnls_debug_probe(unsigned long long* out8, int reset) {
+  if (cudaMemcpyFromSymbol(out8, g_probe, sizeof(unsigned long long) * 8) != cudaSuccess) return 7;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_probe, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 DNLS_API void dnls_options_default(dnls_options* o) {
   if (!o) return;

@@ -37,6 +37,18 @@ __device__ int g_trace_n;
   } while (0)
 #endif
 
+// -DDNLS_LIN_PROBE: thread 0 of block 0 accumulates the cycles of linearisation segments into
+// g_probe (clock deltas kept in registers -- no dependent global reads on the measured path)
+#ifdef DNLS_LIN_PROBE
+__device__ unsigned long long g_probe[8];
+#define DNLS_PROBE_NOW(v) const long long v = clock64()
+#define DNLS_PROBE_ADD(i, a, b) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_probe[i], (unsigned long long)((b) - (a)))
+#else
+#define DNLS_PROBE_NOW(v)
+#define DNLS_PROBE_ADD(i, a, b)
+#endif
+
 // device view of the symbolic analysis (all arrays int32, uploaded once per graph)
 struct DevGraph {
   int D, N, E, P, S, L, storage, nblk, n;
@@ -581,15 +593,56 @@ struct Scr {   // per-slot scratch layout (doubles)
   static constexpr int H0 = 0, H1 = NL, B0 = 2 * NL, B1 = 2 * NL + D, HIJ = 2 * NL + 2 * D;
   static constexpr int SIZE = HIJ + D * D;
 };
+
+// the slot's scratch contributions (lower triangles packed column-wise, then J^T r parts)
+template <int D, class JT>
+__device__ __forceinline__ void slot_blocks_edge(const JT& J, double* o) {
+  using SC = Scr<D>;
+  int e = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = q; a < D; ++a) {
+      o[SC::H0 + e] = blk<D>(J, 1, a, q);
+      o[SC::H1 + e] = blk<D>(J, 0, a, q);
+      ++e;
+    }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    o[SC::B0 + a] = rhs<D>(J, 1, a);
+    o[SC::B1 + a] = rhs<D>(J, 0, a);
+  }
+}
+template <int D, class JT>
+__device__ __forceinline__ void slot_blocks_prior(const JT& J, double* o) {
+  using SC = Scr<D>;
+  int e = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = q; a < D; ++a) o[SC::H0 + e++] = blk<D>(J, 0, a, q);
+#pragma unroll
+  for (int a = 0; a < D; ++a) o[SC::B0 + a] = rhs<D>(J, 0, a);
+}
+template <int D, int WHICH, class JT>
+__device__ __forceinline__ void slot_offdiag(const JT& J, double* O, int ld) {
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = 0; a < D; ++a) O[(size_t)q * ld + a] = blk<D>(J, WHICH, a, q);
+}
 template <int D, int NT, int CL = 1>
 __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, const LView& L,
                                 double* x_b, double* cost_b, double* scr, double lam, int damping, double* s_red) {
   using SC = Scr<D>;
   constexpr int NL = SC::NL, GN = CL * NT;
   const int gt = crank<CL>() * NT + threadIdx.x;
+  DNLS_PROBE_NOW(p0);
   for (int i = gt; i < L.rlo; i += GN) L.g[i] = 0.0;
   for (int i = L.rlo + gt; i < g.storage; i += GN) L.r[i - L.rlo] = 0.0;
   gsync<CL>();
+  DNLS_PROBE_NOW(p1);
+  DNLS_PROBE_ADD(0, p0, p1);
   DNLS_TRACE_POINT(210);
   const int nslot = g.E + g.P;
   for (int slot = gt; slot < nslot; slot += GN) {
@@ -609,32 +662,24 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
     const int4 d0 = g.slot_desc[3 * slot], d1 = g.slot_desc[3 * slot + 1], d2 = g.slot_desc[3 * slot + 2];
     const bool edge = d0.y >= 0;
     double* o = scr + (size_t)slot * SC::SIZE;
-    // side 0 = endpoint i (a prior's pose: its Jacobian has the C_j form, block 0 / rhs 0)
-    int e = 0;
-#pragma unroll
-    for (int q = 0; q < D; ++q)
-#pragma unroll
-      for (int a = q; a < D; ++a) {
-        o[SC::H0 + e] = blk<D>(J, edge ? 1 : 0, a, q);
-        if (edge) o[SC::H1 + e] = blk<D>(J, 0, a, q);
-        ++e;
-      }
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      o[SC::B0 + a] = rhs<D>(J, edge ? 1 : 0, a);
-      if (edge) o[SC::B1 + a] = rhs<D>(J, 0, a);
-    }
-    if (edge) {   // off-diagonal block at (row pose, col pose): C_i^T C_j if the row pose is i, else C_j^T C_i
-      const int which2 = d0.w ? 3 : 2;
-      double* O = d2.z ? L.at(d0.z) + 0 : o + SC::HIJ;
+    // side 0 = endpoint i (a prior's pose: its Jacobian has the C_j form, block 0 / rhs 0).  The
+    // block kinds are compile-time in every branch (a runtime `which` made the compiler evaluate
+    // the four block formulas with predication)
+    if (edge) {
+      slot_blocks_edge<D>(J, o);
+      double* O = d2.z ? L.at(d0.z) : o + SC::HIJ;
       const int ld = d2.z ? d1.z : D;
-#pragma unroll
-      for (int q = 0; q < D; ++q)
-#pragma unroll
-        for (int a = 0; a < D; ++a) O[(size_t)q * ld + a] = blk<D>(J, which2, a, q);
+      if (d0.w) slot_offdiag<D, 3>(J, O, ld);   // row pose is j: C_j^T C_i
+      else slot_offdiag<D, 2>(J, O, ld);        // row pose is i: C_i^T C_j
+    } else {
+      slot_blocks_prior<D>(J, o);
     }
   }
+  DNLS_PROBE_NOW(p2);
+  DNLS_PROBE_ADD(1, p1, p2);
   gsync<CL>();
+  DNLS_PROBE_NOW(p3);
+  DNLS_PROBE_ADD(2, p2, p3);
   DNLS_TRACE_POINT(220);
   double mymax = 0.0;
   for (int p = gt; p < g.N; p += GN) {
@@ -691,6 +736,8 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mymax = fmax(mymax, __shfl_xor_sync(0xffffffffu, mymax, o));
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mymax;
+  DNLS_PROBE_NOW(p4);
+  DNLS_PROBE_ADD(3, p3, p4);
 }
 
 // Warp-level dense triangular solves on a panel's w x w diagonal block (P column-major, leading
@@ -892,7 +939,7 @@ __device__ __forceinline__ void stage_in(double* __restrict__ dst, const double*
 // or plain vector loads
 template <int NT>
 __device__ __forceinline__ void stage_level(double* dst, const double* src, int n, uint64_t* mbar, uint32_t& phase) {
-#ifdef DNLS_TMA_STAGE
+#ifndef DNLS_NO_TMA_STAGE
   if ((n & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
     bulk_load<NT>(dst, src, n, mbar, phase);
     return;
