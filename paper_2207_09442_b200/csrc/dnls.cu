@@ -64,7 +64,7 @@ struct WsLayout {
   size_t L, x, bsave, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, clred, total;
 };
 WsLayout ws_layout(const Symbolic& s, int B) {
-  const int D = s.D, PS = D == 6 ? 12 : 6, JS = D * (D + 1) + 2 * D + D * D;   // GT<D>::JS
+  const int D = s.D, PS = D == 6 ? 12 : 6, JS = D == 6 ? Scr<6>::SIZE : Scr<3>::SIZE;   // GT<D>::JS
   const size_t n = (size_t)s.N * D, slots = (size_t)s.E + s.P;
   WsLayout w{};
   size_t o = 0;

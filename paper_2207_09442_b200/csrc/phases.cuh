@@ -174,10 +174,13 @@ struct DevWs {
   int* it;        // [B] iterations
 };
 
+__host__ __device__ constexpr int pad4(int x) { return (x + 3) & ~3; }
+template <int D>
+struct Scr;
 template <int D>
 struct GT {
   static constexpr int PS = (D == 6) ? 12 : 6;   // doubles per pose
-  static constexpr int JS = D * (D + 1) + 2 * D + D * D;   // scratch doubles per cost slot (Scr<D>)
+  static constexpr int JS = Scr<D>::SIZE;   // scratch doubles per cost slot
 };
 
 // Factor storage view.  Offsets >= rlo (the top elimination-tree levels) are RESIDENT in
@@ -588,41 +591,73 @@ __device__ __forceinline__ double rhs(const JT& J, int side, int a) {
 //     atomics), damped (lam > 0; damping 0: Marquardt diag *= 1 + lam, 1: diag += lam) and written
 //     once; shared off-diagonal blocks are summed the same way.  Max diagonal -> s_red per warp.
 template <int D>
-struct Scr {   // per-slot scratch layout (doubles)
+struct Scr {   // per-slot scratch layout (doubles); every field starts on a 32-byte boundary so a
+               // slot writes it with 256-bit stores (one L1 wavefront per 4 doubles instead of one
+               // per double: the slots of a warp are 800 B apart, so every store is uncoalesced)
   static constexpr int NL = D * (D + 1) / 2;
-  static constexpr int H0 = 0, H1 = NL, B0 = 2 * NL, B1 = 2 * NL + D, HIJ = 2 * NL + 2 * D;
-  static constexpr int SIZE = HIJ + D * D;
+  static constexpr int H0 = 0, H1 = pad4(NL), B0 = 2 * pad4(NL), B1 = B0 + pad4(D), HIJ = B1 + pad4(D);
+  static constexpr int SIZE = pad4(HIJ + D * D);
 };
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
+}
+// (q, a) of entry e of a packed lower triangle (column-major, a >= q); folds for constant e
+__device__ __forceinline__ void lower_qa(int e, int D, int& q, int& a) {
+  int qq = 0, rem = e;
+  while (rem >= D - qq) {
+    rem -= D - qq;
+    ++qq;
+  }
+  q = qq;
+  a = qq + rem;
+}
+template <int D, int WHICH, class JT>
+__device__ __forceinline__ void store_lower_v4(const JT& J, double* o) {
+  // nested constant-bound loops (fully unrolled: the J entries are indexed by constants, so J stays
+  // in registers), flushed every four entries
+  double buf[4] = {0.0, 0.0, 0.0, 0.0};
+  int nb = 0, e0 = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = q; a < D; ++a) {
+      buf[nb++] = blk<D>(J, WHICH, a, q);
+      if (nb == 4) {
+        st_v4(o + e0, buf[0], buf[1], buf[2], buf[3]);
+        e0 += 4;
+        nb = 0;
+      }
+    }
+  if (nb > 0) st_v4(o + e0, buf[0], nb > 1 ? buf[1] : 0.0, nb > 2 ? buf[2] : 0.0, 0.0);
+}
+template <int D, int SIDE, class JT>
+__device__ __forceinline__ void store_rhs_v4(const JT& J, double* o) {
+#pragma unroll
+  for (int a0 = 0; a0 < D; a0 += 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (a0 + u < D) ? rhs<D>(J, SIDE, a0 + u) : 0.0;
+    st_v4(o + a0, v[0], v[1], v[2], v[3]);
+  }
+}
 
 // the slot's scratch contributions (lower triangles packed column-wise, then J^T r parts)
 template <int D, class JT>
 __device__ __forceinline__ void slot_blocks_edge(const JT& J, double* o) {
   using SC = Scr<D>;
-  int e = 0;
-#pragma unroll
-  for (int q = 0; q < D; ++q)
-#pragma unroll
-    for (int a = q; a < D; ++a) {
-      o[SC::H0 + e] = blk<D>(J, 1, a, q);
-      o[SC::H1 + e] = blk<D>(J, 0, a, q);
-      ++e;
-    }
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    o[SC::B0 + a] = rhs<D>(J, 1, a);
-    o[SC::B1 + a] = rhs<D>(J, 0, a);
-  }
+  store_lower_v4<D, 1>(J, o + SC::H0);
+  store_lower_v4<D, 0>(J, o + SC::H1);
+  store_rhs_v4<D, 1>(J, o + SC::B0);
+  store_rhs_v4<D, 0>(J, o + SC::B1);
 }
 template <int D, class JT>
 __device__ __forceinline__ void slot_blocks_prior(const JT& J, double* o) {
   using SC = Scr<D>;
-  int e = 0;
-#pragma unroll
-  for (int q = 0; q < D; ++q)
-#pragma unroll
-    for (int a = q; a < D; ++a) o[SC::H0 + e++] = blk<D>(J, 0, a, q);
-#pragma unroll
-  for (int a = 0; a < D; ++a) o[SC::B0 + a] = rhs<D>(J, 0, a);
+  store_lower_v4<D, 0>(J, o + SC::H0);
+  store_rhs_v4<D, 0>(J, o + SC::B0);
 }
 template <int D, int WHICH, class JT>
 __device__ __forceinline__ void slot_offdiag(const JT& J, double* O, int ld) {
@@ -681,22 +716,41 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
   DNLS_PROBE_NOW(p3);
   DNLS_PROBE_ADD(2, p2, p3);
   DNLS_TRACE_POINT(220);
+  // thread per pose: its diagonal block and b segment are the sums of its slots' scratch fields
+  // (256-bit loads: every field is 32-byte aligned), fixed order of the symbolic list bc
   double mymax = 0.0;
   for (int p = gt; p < g.N; p += GN) {
-    double h[NL], r[D];
+    constexpr int NH = pad4(NL), NR = pad4(D);
+    double h[NH], r[NR];
 #pragma unroll
-    for (int i = 0; i < NL; ++i) h[i] = 0.0;
+    for (int i = 0; i < NH; ++i) h[i] = 0.0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) r[a] = 0.0;
+    for (int a = 0; a < NR; ++a) r[a] = 0.0;
     const int c0 = g.bc_ptr[p], c1 = g.bc_ptr[p + 1];
     for (int c = c0; c < c1; ++c) {
       const int code = g.bc[c];
       const double* o = scr + (size_t)(code >> 1) * SC::SIZE;
       const int side = code & 1;
+      const double* oh = o + (side ? SC::H1 : SC::H0);
+      const double* orh = o + (side ? SC::B1 : SC::B0);
 #pragma unroll
-      for (int i = 0; i < NL; ++i) h[i] += o[side * NL + i];
+      for (int i = 0; i < NH; i += 4) {
+        double v0, v1, v2, v3;
+        ld_v4(oh + i, v0, v1, v2, v3);
+        h[i] += v0;
+        h[i + 1] += v1;
+        h[i + 2] += v2;
+        h[i + 3] += v3;
+      }
 #pragma unroll
-      for (int a = 0; a < D; ++a) r[a] += o[SC::B0 + side * D + a];
+      for (int a = 0; a < NR; a += 4) {
+        double v0, v1, v2, v3;
+        ld_v4(orh + a, v0, v1, v2, v3);
+        r[a] += v0;
+        r[a + 1] += v1;
+        r[a + 2] += v2;
+        r[a + 3] += v3;
+      }
     }
     const int s = g.pose_sn[p], ld = g.sn_ld[s];
     const int cc = D * (p - g.sn_first[s]);
