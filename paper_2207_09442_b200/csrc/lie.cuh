@@ -143,8 +143,19 @@ struct SE3 {
   double t[3];
 };
 
+// Poses and measurements live in global memory, one pose per thread: a warp's accesses are 96 B
+// apart, so each row [R_i0 R_i1 R_i2 t_i] (32 B) is moved with one 256-bit access when aligned.
 __device__ __forceinline__ SE3 se3_load(const double* p) {
   SE3 T;
+  if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(T.R[i][0]), "=d"(T.R[i][1]), "=d"(T.R[i][2]), "=d"(T.t[i])
+                   : "l"(p + 4 * i)
+                   : "memory");
+    return T;
+  }
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     T.R[i][0] = p[4 * i + 0];
@@ -155,6 +166,14 @@ __device__ __forceinline__ SE3 se3_load(const double* p) {
   return T;
 }
 __device__ __forceinline__ void se3_store(const SE3& T, double* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p + 4 * i), "d"(T.R[i][0]), "d"(T.R[i][1]),
+                   "d"(T.R[i][2]), "d"(T.t[i])
+                   : "memory");
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     p[4 * i + 0] = T.R[i][0];
