@@ -35,13 +35,30 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, varia
         return out
     os.makedirs(os.path.dirname(out), exist_ok=True)
     tmp = out + ".tmp"
-    cmd = [NVCC] + FLAGS + (["-DDNLS_TRACE"] if trace else []) + [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    extra = (["-DDNLS_TRACE"] if trace else []) + [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else [])
+    # the translation units compile in parallel (-c), then one nvcc link step
+    tag = os.path.basename(out).replace(".so", "")
+    objs = [os.path.join(os.path.dirname(out), f".{tag}.{os.path.basename(src)}.o") for src in SRC]
+    cflags = [f for f in FLAGS if f not in ("-shared",)]
+    procs = [subprocess.Popen([NVCC] + cflags + extra + ["-c", "-o", o, src], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for src, o in zip(SRC, objs)]
+    errs = []
+    for pr in procs:
+        so, se = pr.communicate()
+        if pr.returncode != 0:
+            errs.append(so + se)
+        elif verbose:
+            sys.stderr.write(se)
+    if errs:
+        sys.stderr.write("".join(errs))
+        raise RuntimeError("nvcc failed building libdnls.so")
+    r = subprocess.run([NVCC] + FLAGS + ["-o", tmp] + objs, capture_output=True, text=True)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libdnls.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libdnls.so")
     os.replace(tmp, out)
     return out
 
