@@ -396,7 +396,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": (3 + (0 if args.welsch is None else 1)) * args.steps,   # forward, backward, weight-grad (+ radius) reductions
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
