@@ -673,7 +673,13 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
   constexpr int NL = SC::NL, GN = CL * NT;
   const int gt = crank<CL>() * NT + threadIdx.x;
   DNLS_PROBE_NOW(p0);
-  for (int i = gt; i < L.rlo; i += GN) L.g[i] = 0.0;
+  {   // zero the global part with 256-bit stores (32-byte aligned body, scalar head / tail)
+    const int head = min((int)(((32 - (reinterpret_cast<uintptr_t>(L.g) & 31)) & 31) >> 3), L.rlo);
+    const int nbody = (L.rlo - head) >> 2;
+    if (gt < head) L.g[gt] = 0.0;
+    for (int i = gt; i < nbody; i += GN) st_v4(L.g + head + 4 * i, 0.0, 0.0, 0.0, 0.0);
+    for (int i = head + 4 * nbody + gt; i < L.rlo; i += GN) L.g[i] = 0.0;
+  }
   for (int i = L.rlo + gt; i < g.storage; i += GN) L.r[i - L.rlo] = 0.0;
   gsync<CL>();
   DNLS_PROBE_NOW(p1);
