@@ -216,12 +216,22 @@ __device__ void finish_assembly(const DevGraph& g, const double* cost_b, double*
   gsync<CL>();
   DNLS_PROBE_NOW(q1);
   DNLS_PROBE_ADD(4, q0, q1);
-  if (threadIdx.x < 32) {
-    double s = warp0_sum(cost_b, g.E + g.P);
+  {   // S: every thread one strided share, fixed shuffle tree, warps in order (deterministic and
+      // identical in every CTA of a group, which all sum the whole array)
+    __shared__ double s_part[NT / 32];
+    double part = 0.0;
+    for (int i = threadIdx.x; i < g.E + g.P; i += NT) part += cost_b[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
+    __syncthreads();
     if (threadIdx.x == 0) {
-      double m = 0.0;
-      for (int i = 0; i < NT / 32; ++i) m = fmax(m, s_red[i]);
-      *sh_S = s;
+      double sum = 0.0, m = 0.0;
+      for (int i = 0; i < NT / 32; ++i) {
+        sum += s_part[i];
+        m = fmax(m, s_red[i]);
+      }
+      *sh_S = sum;
       if (CL > 1) clr[crank<CL>()] = m;
       else *sh_max = m;
     }
