@@ -274,6 +274,13 @@ __device__ __forceinline__ double cta_sum(double v, double* s_tmp) {
   __syncthreads();
   return t;
 }
+// CTA-wide deterministic sum of v[0..n): strided per-thread shares, fixed shuffle tree, warps in
+// order; every thread of the CTA gets the value (identical in every CTA of a group)
+__device__ __forceinline__ double cta_sum_array(const double* v, int n, double* s_tmp) {
+  double part = 0.0;
+  for (int i = threadIdx.x; i < n; i += NT) part += v[i];
+  return cta_sum(part, s_tmp);
+}
 // packed lower-triangular quadratic form u^T H u (H symmetric, lower triangle packed column-wise)
 template <int D>
 __device__ __forceinline__ double quad_lower(const double* h, const double* u) {
@@ -421,8 +428,8 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
       __syncthreads();
       objective_phase<D, NT, CL>(g, pr, Ttr, b, cost_b);
       __syncthreads();
-      if (threadIdx.x < 32) {
-        const double st = warp0_sum(cost_b, g.E + g.P);
+      {
+        const double st = cta_sum_array(cost_b, g.E + g.P, s_tmp);
         if (threadIdx.x == 0) sh_Stry = st;
       }
       __syncthreads();
@@ -463,9 +470,9 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
         gsync<CL>();
         objective_phase<D, NT, CL>(g, pr, Ttr, b, cost_b);
         gsync<CL>();
-        if (threadIdx.x < 32) {
-          double s = warp0_sum(cost_b, g.E + g.P);
-          if (threadIdx.x == 0) sh_Stry = s;
+        {
+          const double st = cta_sum_array(cost_b, g.E + g.P, s_tmp);
+          if (threadIdx.x == 0) sh_Stry = st;
         }
         __syncthreads();
         accept = sh_Stry < S;
@@ -500,9 +507,9 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
   } else {
     objective_phase<D, NT, CL>(g, pr, Tb, b, cost_b);
     gsync<CL>();
-    if (threadIdx.x < 32) {
-      double s = warp0_sum(cost_b, g.E + g.P);
-      if (threadIdx.x == 0) sh_S = s;
+    {
+      const double st = cta_sum_array(cost_b, g.E + g.P, s_tmp);
+      if (threadIdx.x == 0) sh_S = st;
     }
     __syncthreads();
   }
