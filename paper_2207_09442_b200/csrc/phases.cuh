@@ -661,10 +661,25 @@ __device__ __forceinline__ void slot_blocks_prior(const JT& J, double* o) {
 }
 template <int D, int WHICH, class JT>
 __device__ __forceinline__ void slot_offdiag(const JT& J, double* O, int ld) {
+  // each block column is D contiguous doubles: 128-bit stores where 16-byte aligned (the odd
+  // leading dimensions alternate the alignment of consecutive columns)
 #pragma unroll
-  for (int q = 0; q < D; ++q)
+  for (int q = 0; q < D; ++q) {
+    double v[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) O[(size_t)q * ld + a] = blk<D>(J, WHICH, a, q);
+    for (int a = 0; a < D; ++a) v[a] = blk<D>(J, WHICH, a, q);
+    double* c = O + (size_t)q * ld;
+    if ((reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+#pragma unroll
+      for (int a = 0; a + 1 < D; a += 2) *reinterpret_cast<double2*>(c + a) = make_double2(v[a], v[a + 1]);
+      if (D & 1) c[D - 1] = v[D - 1];
+    } else {
+      c[0] = v[0];
+#pragma unroll
+      for (int a = 1; a + 1 < D; a += 2) *reinterpret_cast<double2*>(c + a) = make_double2(v[a], v[a + 1]);
+      if (!(D & 1)) c[D - 1] = v[D - 1];
+    }
+  }
 }
 template <int D, int NT, int CL = 1>
 __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const double* Tb, int b, const LView& L,
