@@ -776,18 +776,34 @@ __device__ void linearize_phase(const DevGraph& g, const DevProb& pr, const doub
     const int s = g.pose_sn[p], ld = g.sn_ld[s];
     const int cc = D * (p - g.sn_first[s]);
     double* T = L.at(g.sn_off[s] + cc * ld + cc);
-    int e = 0;
+    // damping / max on the diagonal, then each lower column (D - q contiguous doubles) with 128-bit
+    // stores where 16-byte aligned
 #pragma unroll
-    for (int q = 0; q < D; ++q)
+    for (int q = 0, e = 0; q < D; e += D - q, ++q) {
+      double v = h[e];
+      if (lam > 0.0) v = (damping == 0) ? v * (1.0 + lam) : v + lam;
+      mymax = fmax(mymax, v);
+      h[e] = v;
+    }
 #pragma unroll
-      for (int a = q; a < D; ++a) {
-        double v = h[e++];
-        if (a == q) {
-          if (lam > 0.0) v = (damping == 0) ? v * (1.0 + lam) : v + lam;
-          mymax = fmax(mymax, v);
+    for (int q = 0, e = 0; q < D; e += D - q, ++q) {
+      double* c = T + (size_t)q * ld + q;
+      const int n = D - q;
+      if ((reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+#pragma unroll
+        for (int k = 0; k < n; k += 2) {
+          if (k + 1 < n) *reinterpret_cast<double2*>(c + k) = make_double2(h[e + k], h[e + k + 1]);
+          else c[k] = h[e + k];
         }
-        T[(size_t)q * ld + a] = v;
+      } else {
+        c[0] = h[e];
+#pragma unroll
+        for (int k = 1; k < n; k += 2) {
+          if (k + 1 < n) *reinterpret_cast<double2*>(c + k) = make_double2(h[e + k], h[e + k + 1]);
+          else c[k] = h[e + k];
+        }
       }
+    }
 #pragma unroll
     for (int a = 0; a < D; ++a) x_b[(size_t)D * p + a] = r[a];
   }
