@@ -66,3 +66,67 @@ def test_dlm_zero_upstream_gradient():
     assert prob.objective(T) > 1e-3
     ge, gp, _ = dlm.dlm_weight_grads(prob, T, np.zeros(10 * 6), 1e-3)
     assert np.max(np.abs(ge)) < 1e-8 and np.max(np.abs(gp)) < 1e-8
+
+
+# ---- Welsch kernel (readings W1-W3 and B3): the psi branch of weight_partials and
+# dlm_radius_grad are pinned by the paper's eps -> 0 limit against the implicit VJPs,
+# which are themselves pinned by FD of the converged solve (tests/test_oracle_robust.py).  A wrong
+# psi factor, a dropped (s/k) psi term of d rho/dk or a flipped sign makes the error plateau (slope 0)
+# or converge to the negated gradient instead of shrinking linearly in eps.
+def welsch_converged_problem(dim, N, seed, k):
+    topo = synth.cube_topology(N, dim=dim, p=0.6, seed=seed, outlier_ratio=0.3)
+    data = synth.cube_batch(topo, 1, seed=seed)
+    G = lie.SE3 if dim == 3 else lie.SE2
+    w = 0.8 + 0.4 * np.random.default_rng(seed).random(topo.num_edges)
+    prob = nls.PGOProblem(G, N, topo.edges, topo.prior_vars, data["meas"][0], data["prior_meas"][0], w,
+                          np.array([1.2]), radius=k)
+    T = nls.gauss_newton(prob, lie.to_homog(data["poses0"][0]), nls.Options(max_iterations=80)).x
+    _, _, b = prob.linearize(T)
+    assert np.max(np.abs(b)) < 1e-10   # IRLS fixed point: the robust gradient vanishes
+    return prob, T
+
+
+@pytest.mark.parametrize("dim,N,k", [(2, 12, 0.4), (3, 10, 0.6)])
+def test_dlm_welsch_weight_and_radius_grads_converge_to_implicit(dim, N, k):
+    prob, T = welsch_converged_problem(dim, N, seed=N + 1, k=k)
+    # the kernel must be active: some edges far from the quadratic regime (psi well below 1)
+    c, _, _ = prob.edge_terms(T)
+    psi = prob.irls_weights(c)
+    assert psi.min() < 0.9
+    v = np.random.default_rng(5).standard_normal(N * prob.d)
+    gi_e, gi_p, lam = implicit.implicit_weight_grads(prob, T, v)
+    gi_k = implicit.radius_vjp(prob, T, lam)
+    gi = np.concatenate([gi_e, gi_p])
+    errs_w, errs_k = [], []
+    epss = [1e-3, 1e-4, 1e-5]
+    for eps in epss:
+        ge, gp, T_dir = dlm.dlm_weight_grads(prob, T, v, eps)
+        gk = dlm.dlm_radius_grad(prob, T, T_dir, eps)
+        errs_w.append(np.max(np.abs(np.concatenate([ge, gp]) - gi)) / np.max(np.abs(gi)))
+        errs_k.append(abs(gk - gi_k) / abs(gi_k))
+    for errs in (errs_w, errs_k):
+        slope = np.polyfit(np.log10(epss), np.log10(errs), 1)[0]
+        assert errs[-1] < 5e-3, errs
+        assert 0.8 < slope < 1.2, (errs, slope)
+
+
+def test_weight_partials_psi_branch_is_dS_dw():
+    """dS/dw_e of the robust objective (B3 with W1: psi_e w_e ||c_e||^2) against central differences
+    of the oracle objective over w_e at fixed theta."""
+    prob, T = welsch_converged_problem(3, 8, seed=3, k=0.5)
+    ge, gp = dlm.weight_partials(prob, T)
+    h = 1e-6
+    for e in (0, 2, prob.edges.shape[0] - 1):
+        wp_, wm_ = prob.w.copy(), prob.w.copy()
+        wp_[e] += h
+        wm_[e] -= h
+        mk = lambda w: nls.PGOProblem(prob.G, prob.n_vars, prob.edges, prob.prior_vars, prob.Z, prob.Zp, w,
+                                      prob.wp, radius=prob.radius)
+        fd = (mk(wp_).objective(T) - mk(wm_).objective(T)) / (2 * h)
+        assert abs(ge[e] - fd) <= 1e-7 * max(1.0, abs(fd)), (e, ge[e], fd)
+    # prior weight (quadratic, W1)
+    fdp = (nls.PGOProblem(prob.G, prob.n_vars, prob.edges, prob.prior_vars, prob.Z, prob.Zp, prob.w,
+                          prob.wp + h, radius=prob.radius).objective(T) -
+           nls.PGOProblem(prob.G, prob.n_vars, prob.edges, prob.prior_vars, prob.Z, prob.Zp, prob.w,
+                          prob.wp - h, radius=prob.radius).objective(T)) / (2 * h)
+    assert abs(gp[0] - fdp) <= 1e-7 * max(1.0, abs(fdp))
