@@ -56,7 +56,9 @@ typedef enum {
   DNLS_E_STRUCTURAL = 3,   /* variable without any cost (empty diagonal block), self edge */
   DNLS_E_WORKSPACE = 4,    /* workspace too small */
   DNLS_E_STATE = 5,        /* backward without a matching implicit forward on this workspace */
-  DNLS_E_ALL_FAILED = 6,   /* reserved: every element failed (never returned asynchronously) */
+  DNLS_E_ALL_FAILED = 6,   /* every element failed: returned only by the host-synchronous
+                              dnls_status_summary (the compute calls are asynchronous, so per-element
+                              failures stay in status[B]) */
   DNLS_E_CUDA = 7,         /* a CUDA runtime call failed */
   DNLS_E_UNSUPPORTED = 8   /* e.g. graph too large for the per-element kernels */
 } dnls_status;
@@ -72,6 +74,11 @@ typedef enum { DNLS_GRAD_TANGENT = 0, DNLS_GRAD_MATRIX = 1 } dnls_grad_kind;
 #define DNLS_ST_CONVERGED 1   /* early stop: |S_k - S_{k-1}| < abs_tol + rel_tol S_{k-1}; frozen */
 #define DNLS_ST_NOT_SPD 2     /* a pivot <= 1e-13 * max diag(H) (GN: frozen at that iterate) */
 #define DNLS_ST_SATURATED 3   /* LM rejected a step with lambda already at lambda_max; frozen */
+/* Warning bit OR-ed into the code (mask the code with DNLS_ST_CODE_MASK): an implicit-mode forward whose
+ * last accepted iteration still changed the objective by |S_K - S_{K-1}| >= abs_tol + rel_tol S_{K-1}
+ * (theta_K may not be the optimum Prop. 1 assumes; "a warning, not an error"). */
+#define DNLS_ST_WARN_NOT_CONVERGED 0x100
+#define DNLS_ST_CODE_MASK 0xff
 
 typedef struct dnls_options {
   int32_t optimizer;        /* dnls_optimizer */
@@ -272,6 +279,24 @@ DNLS_API dnls_status dnls_import_matrix(const dnls_graph* g, int32_t batch, cons
                                         void* workspace, size_t ws_bytes, void* stream);
 DNLS_API dnls_status dnls_export_rhs(const dnls_graph* g, int32_t batch, const void* workspace,
                                      size_t ws_bytes, double* b, void* stream);
+
+/* Assembly map of the per-element factor storage (SURVEY.md §8(b) "per-edge/prior offsets so tests can
+ * scatter an oracle H"; "symbolic analysis ... used for all subsequent factorizations").
+ * Each block is a d x d column-major block at `off` doubles from the element's storage base (layout
+ * [B][storage_doubles] as used by the stage-level entry points), column stride `ld`:
+ *   edge_desc  HOST [E][7] = (off_ii, ld_ii, off_jj, ld_jj, off_ij, ld_ij, row_is_j): the diagonal blocks
+ *              of the endpoints (lower triangles significant) and the below-diagonal block between them;
+ *              row_is_j = 1 if the block row is pose j (block = H_ji), else it is H_ij;
+ *   prior_desc HOST [P][2] = (off, ld) of the prior's diagonal block.
+ * Either pointer may be NULL.  Host-only; works on host-only graphs.  Errors: DNLS_E_INVALID. */
+DNLS_API dnls_status dnls_block_offsets(const dnls_graph* g, int32_t* edge_desc, int32_t* prior_desc);
+
+/* Host-synchronous summary of a device status[B] array written by dnls_forward (synchronises `stream`):
+ * n_failed = elements whose code is DNLS_ST_NOT_SPD or DNLS_ST_SATURATED, n_warned = elements with
+ * DNLS_ST_WARN_NOT_CONVERGED.  Returns DNLS_E_ALL_FAILED when batch > 0 and every element failed
+ * (SPEC.md:459), else DNLS_OK.  Outputs may be NULL.  Errors: DNLS_E_INVALID, DNLS_E_CUDA. */
+DNLS_API dnls_status dnls_status_summary(const int32_t* status, int32_t batch, int32_t* n_failed,
+                                         int32_t* n_warned, void* stream);
 
 /* Debug: (tag, clock64) pairs recorded by CTA 0 of the last kernels in a -DDNLS_TRACE build
  * (pairs written to out[2*i], out[2*i+1]; at most `capacity` pairs; the buffer is reset).

@@ -125,6 +125,8 @@ _SIGS = {
     "dnls_debug_trace": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
     "dnls_export_rhs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "dnls_block_offsets": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p]),
+    "dnls_status_summary": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_int32_p, c_int32_p, ctypes.c_void_p]),
 }
 
 _lib = None

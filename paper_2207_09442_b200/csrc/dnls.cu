@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -54,9 +55,53 @@ struct dnls_graph {
   size_t dbuf_bytes = 0;
   DevGraph dg{};
   std::mutex mu;
-  const void* last_ws = nullptr;   // workspace holding the last implicit factor
-  int last_batch = -1;
+  // Factor cache registry (include/dnls.h "Ownership"): workspace base -> what its factor storage
+  // holds for (graph, batch).  An implicit forward registers its workspace; every entry point that
+  // writes the factor storage of a workspace drops it, so a backward on a workspace whose cached
+  // factor was overwritten (or never made) returns DNLS_E_STATE.  Several workspaces may hold
+  // cached factors of the same graph at once.
+  struct FactorRecord {
+    int batch;
+    int kind;   // DNLS_BWD_* of the forward that wrote it
+    int K;      // unroll: iterations whose factors are kept
+  };
+  std::map<const void*, FactorRecord> cached;
+  void drop(const void* ws) {
+    std::lock_guard<std::mutex> lk(mu);
+    cached.erase(ws);
+  }
+  void keep(const void* ws, FactorRecord r) {
+    std::lock_guard<std::mutex> lk(mu);
+    cached[ws] = r;
+  }
+  bool get(const void* ws, FactorRecord& r) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cached.find(ws);
+    if (it == cached.end()) return false;
+    r = it->second;
+    return true;
+  }
 };
+
+namespace {
+// Runs the calling thread's CUDA calls on the graph's device and restores the previous one
+// (the graph's index arrays and the caller's buffers live on that device).
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
+    }
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    if (!ok) cudaGetLastError();
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
 
 // ----------------------------------------------------------------------------- workspace layout
 namespace {
@@ -501,7 +546,11 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
     __syncthreads();
     factor_phase<D, NT, CL>(g, L, sm.stage, 1e-13 * sh_max, &sh_fail, sm.mbar, sm.phase, sm.xinv, nullptr, sm.pp);
     group_fail<CL>(&sh_fail, clr);
-    if (sh_fail && status == DNLS_ST_OK) status = DNLS_ST_NOT_SPD;
+    // a failed final factor takes precedence over CONVERGED / SATURATED: the backward must not use it
+    if (sh_fail) status = DNLS_ST_NOT_SPD;
+    // Prop. 1 assumes theta* optimal: warn (not fail) when the last accepted step still
+    // changed the objective by more than the early-stop tolerance
+    else if (have_prev && !(fabs(sh_S - Sprev) < fp.abs_tol + fp.rel_tol * Sprev)) status |= DNLS_ST_WARN_NOT_CONVERGED;
     // the cached factor must be complete in global memory for dnls_backward_implicit
     if (CL == 1) copy_range<NT>(Lg + g.res_lo, sm.res, g.storage - g.res_lo);
   } else {
@@ -1040,32 +1089,14 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
     buf.insert(buf.end(), v.begin(), v.end());
     buf.push_back(0);   // never empty
   };
-  // packed 16-byte descriptors
-  std::vector<int32_t> task4, con4, fcon4;
-  for (size_t t = 0; t < s.ut_off.size(); ++t) {
-    task4.push_back(s.ut_off[t]); task4.push_back(s.ut_ld[t]);
-    task4.push_back(s.ut_cptr[t]); task4.push_back(s.ut_cptr[t + 1]);
-  }
-  for (size_t c = 0; c < s.uc_a.size(); ++c) {
-    con4.push_back(s.uc_a[c]); con4.push_back(s.uc_b[c]); con4.push_back(s.uc_ld[c]); con4.push_back(s.uc_w[c]);
-  }
-  for (size_t c = 0; c < s.fc_off.size(); ++c) {
-    fcon4.push_back(s.fc_off[c]); fcon4.push_back(s.fc_ld[c]); fcon4.push_back(s.fc_w[c]); fcon4.push_back(s.fc_x[c]);
-  }
   std::vector<int32_t> sn_off32(s.sn_off.begin(), s.sn_off.end());
   add(s.perm); add(s.iperm); add(s.edges); add(s.prior_vars);
-  add(s.sn_first); add(s.sn_ncols); add(s.sn_m); add(s.sn_ld); add(s.sn_w); add(sn_off32);
-  add(s.level_ptr); add(s.level_sn); add(s.level_off); add(s.level_stage_hi);
-  add(s.ut_level_ptr); add(s.ut_off); add(s.ut_ld); add(s.ut_cptr); add(s.uc_a); add(s.uc_b); add(s.uc_ld); add(s.uc_w);
-  add(s.level_gu); add(s.level_gf); add(s.lrow_ptr); add(s.lrow);
-  add(s.sn_parent); add(s.ut_sn_ptr); add(s.child_ptr); add(s.child_idx); add(s.sn_sched); add(s.leaves);
-  add(s.broots);
-  add(task4); add(con4); add(fcon4);
+  add(s.sn_first); add(s.sn_m); add(s.sn_ld); add(s.sn_w); add(sn_off32);
+  add(s.level_off); add(s.level_stage_hi);
   add(s.pk); add(s.pk_off);
-  add(s.cls_ptr); add(s.cls_slot); add(s.slot_desc); add(s.col_sn);
-  add(s.fc_ptr); add(s.fc_off); add(s.fc_ld); add(s.fc_w); add(s.fc_x);
+  add(s.slot_desc); add(s.col_sn);
   add(s.snr_ptr); add(s.snr);
-  add(s.blk_off); add(s.blk_ld); add(s.blk_kind); add(s.blk_cptr); add(s.blk_con);
+  add(s.blk_off); add(s.blk_ld); add(s.blk_cptr); add(s.blk_con);
   add(s.bc_ptr); add(s.bc);
   add(s.dup_blk);
   if (std::getenv("DNLS_VERBOSE")) {
@@ -1073,9 +1104,9 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
     for (int l = 0; l < s.num_levels; ++l) maxlev = std::max<int64_t>(maxlev, s.level_off[l + 1] - s.level_off[l]);
     std::fprintf(stderr,
                  "[dnls] N=%d levels=%d storage=%lld res_lo=%d res_n=%lld stage_cap=%lld max_level=%lld "
-                 "max_stage=%lld pk_max=%d ints packets=%d colours=%d\n",
+                 "max_stage=%lld pk_max=%d ints packets=%d\n",
                  s.N, s.num_levels, (long long)s.storage, s.res_lo, (long long)s.res_n, (long long)s.stage_cap,
-                 (long long)maxlev, (long long)s.max_level_stage, s.pk_max, s.npk, (int)s.cls_ptr.size() - 1);
+                 (long long)maxlev, (long long)s.max_level_stage, s.pk_max, s.npk);
     if (std::atoi(std::getenv("DNLS_VERBOSE")) > 1)
       for (int k = 0; k < s.npk; ++k) {
         const int32_t* h = s.pk.data() + s.pk_off[k];
@@ -1111,10 +1142,8 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   const int* d = g->dbuf;
   int k = 0;
   DevGraph& dg = g->dg;
-  dg.D = s.D; dg.N = s.N; dg.E = s.E; dg.P = s.P; dg.S = s.S; dg.L = s.num_levels;
-  dg.storage = (int)s.storage; dg.nblk = (int)s.blk_off.size(); dg.n = s.N * s.D;
-  dg.x_smem = (int64_t)dg.n * 8 <= 65536 ? 1 : 0;
-  dg.n_pad = (dg.n + 1) & ~1;
+  dg.D = s.D; dg.N = s.N; dg.E = s.E; dg.P = s.P; dg.S = s.S;
+  dg.storage = (int)s.storage; dg.n = s.N * s.D;
   dg.res_lo = s.res_lo;
   dg.res_n = (int)((s.res_n + 1) & ~int64_t(1));
   dg.x_smem = (int64_t)dg.n * 8 <= 65536 ? 1 : 0;
@@ -1122,34 +1151,17 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
   dg.stage_n = (int)((s.max_level_stage + 1) & ~int64_t(1));
   dg.stage_n = std::max<int>(dg.stage_n, (int)(((s.stage_cap > 0 ? s.stage_cap : 0)) & ~int64_t(1)));
   dg.perm = d + offs[k++]; dg.iperm = d + offs[k++]; dg.edges = d + offs[k++]; dg.prior_vars = d + offs[k++];
-  dg.sn_first = d + offs[k++]; dg.sn_ncols = d + offs[k++]; dg.sn_m = d + offs[k++]; dg.sn_ld = d + offs[k++]; dg.sn_w = d + offs[k++];
+  dg.sn_first = d + offs[k++]; dg.sn_m = d + offs[k++]; dg.sn_ld = d + offs[k++]; dg.sn_w = d + offs[k++];
   dg.sn_off = d + offs[k++];
-  dg.level_ptr = d + offs[k++]; dg.level_sn = d + offs[k++];
   dg.level_off = d + offs[k++]; dg.level_stage_hi = d + offs[k++];
-  dg.ut_level_ptr = d + offs[k++]; dg.ut_off = d + offs[k++]; dg.ut_ld = d + offs[k++]; dg.ut_cptr = d + offs[k++];
-  dg.uc_a = d + offs[k++]; dg.uc_b = d + offs[k++]; dg.uc_ld = d + offs[k++]; dg.uc_w = d + offs[k++];
-  dg.level_gu = d + offs[k++]; dg.level_gf = d + offs[k++]; dg.lrow_ptr = d + offs[k++]; dg.lrow = d + offs[k++];
-  dg.sn_parent = d + offs[k++]; dg.ut_sn_ptr = d + offs[k++]; dg.child_ptr = d + offs[k++];
-  dg.child_idx = d + offs[k++]; dg.sn_sched = d + offs[k++]; dg.leaves = d + offs[k++]; dg.broots = d + offs[k++];
-  dg.top_level = s.top_level; dg.n_forest = s.n_forest; dg.n_leaves = (int)s.leaves.size();
-  dg.n_broots = (int)s.broots.size();
-  dg.task4 = reinterpret_cast<const int4*>(d + offs[k++]);
-  dg.con4 = reinterpret_cast<const int4*>(d + offs[k++]);
-  dg.fcon4 = reinterpret_cast<const int4*>(d + offs[k++]);
   dg.pk = d + offs[k++];
   dg.pk_off = d + offs[k++];
   dg.pk_max = s.pk_max;
   dg.npk = s.npk;
-  dg.cls_ptr = d + offs[k++];
-  dg.cls_slot = d + offs[k++];
   dg.slot_desc = reinterpret_cast<const int4*>(d + offs[k++]);
   dg.pose_sn = d + offs[k++];
-  dg.ncls = (int)s.cls_ptr.size() - 1;
-  dg.fc_ptr = d + offs[k++]; dg.fc_off = d + offs[k++]; dg.fc_ld = d + offs[k++]; dg.fc_w = d + offs[k++];
-  dg.fc_x = d + offs[k++];
   dg.snr_ptr = d + offs[k++]; dg.snr = d + offs[k++];
-  dg.blk_off = d + offs[k++]; dg.blk_ld = d + offs[k++]; dg.blk_kind = d + offs[k++]; dg.blk_cptr = d + offs[k++];
-  dg.blk_con = d + offs[k++];
+  dg.blk_off = d + offs[k++]; dg.blk_ld = d + offs[k++]; dg.blk_cptr = d + offs[k++]; dg.blk_con = d + offs[k++];
   dg.bc_ptr = d + offs[k++]; dg.bc = d + offs[k++];
   dg.dup_blk = d + offs[k++];
   dg.ndup = (int)s.dup_blk.size();
@@ -1192,6 +1204,46 @@ DNLS_API dnls_status dnls_graph_stats(const dnls_graph* g, dnls_stats* o) {
   o->index_bytes = (int64_t)g->dbuf_bytes;
   o->smem_bytes = g->dbuf ? (int64_t)smem_bytes(g->dg) : 0;
   o->resident_doubles = (int64_t)(s.storage - s.res_lo);
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_block_offsets(const dnls_graph* g, int32_t* edge_desc, int32_t* prior_desc) {
+  if (!g) return fail(DNLS_E_INVALID, "dnls_block_offsets: graph is NULL");
+  const Symbolic& s = g->sym;
+  for (int sl = 0; sl < s.E + s.P; ++sl) {
+    const int32_t* d = &s.slot_desc[12 * (size_t)sl];
+    if (sl < s.E) {
+      if (!edge_desc) continue;
+      int32_t* o = edge_desc + 7 * (size_t)sl;
+      o[0] = d[0]; o[1] = d[4]; o[2] = d[1]; o[3] = d[5]; o[4] = d[2]; o[5] = d[6]; o[6] = d[3];
+    } else if (prior_desc) {
+      int32_t* o = prior_desc + 2 * (size_t)(sl - s.E);
+      o[0] = d[0]; o[1] = d[4];
+    }
+  }
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_status_summary(const int32_t* status, int32_t batch, int32_t* n_failed, int32_t* n_warned,
+                                         void* stream) {
+  if (batch < 0 || (batch > 0 && !status)) return fail(DNLS_E_INVALID, "dnls_status_summary: bad arguments");
+  std::vector<int32_t> h((size_t)batch);
+  if (batch > 0) {
+    if (cudaMemcpyAsync(h.data(), status, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, (cudaStream_t)stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+      return fail(DNLS_E_CUDA, std::string("dnls_status_summary: ") + cudaGetErrorString(cudaGetLastError()));
+  }
+  int nf = 0, nw = 0;
+  for (int32_t v : h) {
+    const int c = v & DNLS_ST_CODE_MASK;
+    nf += (c == DNLS_ST_NOT_SPD || c == DNLS_ST_SATURATED);
+    nw += (v & DNLS_ST_WARN_NOT_CONVERGED) != 0;
+  }
+  if (n_failed) *n_failed = nf;
+  if (n_warned) *n_warned = nw;
+  if (batch > 0 && nf == batch)
+    return fail(DNLS_E_ALL_FAILED, "dnls_status_summary: all " + std::to_string(batch) + " elements failed");
   return DNLS_OK;
 }
 
@@ -1299,14 +1351,10 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   if (opt->cluster_ctas != 0 && opt->cluster_ctas != 1 && opt->cluster_ctas != 2 && opt->cluster_ctas != 8)
     return fail(DNLS_E_INVALID, "dnls_forward: cluster_ctas must be 0 (automatic), 1, 2 or 8");
   dnls_graph* gm = const_cast<dnls_graph*>(g);
-  {
-    std::lock_guard<std::mutex> lk(gm->mu);
-    if (gm->last_ws == workspace) {
-      gm->last_ws = nullptr;
-      gm->last_batch = -1;
-    }
-  }
+  gm->drop(workspace);
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_forward: cannot select the graph's device");
   WsLayout l = ws_layout(g->sym, batch);
   DevWs ws = ws_views(l, workspace);
   FwdParams fp;
@@ -1338,11 +1386,7 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
     return fail(DNLS_E_CUDA, std::string("dnls_forward: cluster launch: ") + cudaGetErrorString(cudaGetLastError()));
   }
   if ((st = cuda_check("dnls_forward: k_forward launch"))) return st;
-  if (fp.implicit) {
-    std::lock_guard<std::mutex> lk(gm->mu);
-    gm->last_ws = workspace;
-    gm->last_batch = batch;
-  }
+  if (fp.implicit) gm->keep(workspace, dnls_graph::FactorRecord{batch, DNLS_BWD_IMPLICIT, 0});
   return DNLS_OK;
 }
 
@@ -1360,14 +1404,15 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
   if (grad_bstride > 0 && grad_bstride < std::max(g->sym.E, g->sym.P))
     return fail(DNLS_E_SHAPE, "dnls_backward_implicit: grad_bstride smaller than num_edges/num_priors");
   {
-    dnls_graph* gm = const_cast<dnls_graph*>(g);
-    std::lock_guard<std::mutex> lk(gm->mu);
-    if (gm->last_ws != workspace || gm->last_batch != batch)
+    dnls_graph::FactorRecord rec;
+    if (!const_cast<dnls_graph*>(g)->get(workspace, rec) || rec.batch != batch || rec.kind != DNLS_BWD_IMPLICIT)
       return fail(DNLS_E_STATE,
                   "dnls_backward_implicit: no implicit-mode dnls_forward on this workspace/batch "
                   "(factor cache missing or overwritten)");
   }
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_backward_implicit: cannot select the graph's device");
   WsLayout l = ws_layout(g->sym, batch);
   DevWs ws = ws_views(l, workspace);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1401,15 +1446,11 @@ DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const
   if (grad_bstride < 0) return fail(DNLS_E_INVALID, "dnls_backward_dlm: grad_bstride < 0");
   if (grad_bstride > 0 && grad_bstride < std::max(g->sym.E, g->sym.P))
     return fail(DNLS_E_SHAPE, "dnls_backward_dlm: grad_bstride smaller than num_edges/num_priors");
-  {   // the augmented factorisation overwrites any implicit factor cached in this workspace
-    dnls_graph* gm = const_cast<dnls_graph*>(g);
-    std::lock_guard<std::mutex> lk(gm->mu);
-    if (gm->last_ws == workspace) {
-      gm->last_ws = nullptr;
-      gm->last_batch = -1;
-    }
-  }
+  // the augmented factorisation overwrites any factor cached in this workspace
+  const_cast<dnls_graph*>(g)->drop(workspace);
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_backward_dlm: cannot select the graph's device");
   WsLayout l = ws_layout(g->sym, batch);
   DevWs ws = ws_views(l, workspace);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1436,7 +1477,10 @@ DNLS_API dnls_status dnls_linearize(const dnls_graph* g, int32_t batch, const dn
   if ((st = check_problem("dnls_linearize", g, prob))) return st;
   if (damping != DNLS_DAMP_MARQUARDT && damping != DNLS_DAMP_IDENTITY)
     return fail(DNLS_E_INVALID, "dnls_linearize: unknown damping");
+  const_cast<dnls_graph*>(g)->drop(workspace);   // the factor storage is overwritten
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_linearize: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
   DISPATCH_D(g->sym.D, if ((st = set_smem(k_linearize<DD>, smem_bytes(g->dg), "k_linearize"))) return st;
@@ -1448,7 +1492,10 @@ DNLS_API dnls_status dnls_factorize(const dnls_graph* g, int32_t batch, void* wo
                                     int32_t* status, void* stream) {
   dnls_status st = check_common("dnls_factorize", g, batch, workspace, ws_bytes);
   if (st) return st;
+  const_cast<dnls_graph*>(g)->drop(workspace);   // the factor storage is overwritten
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_factorize: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
   DISPATCH_D(g->sym.D, if ((st = set_smem(k_factorize<DD>, smem_bytes(g->dg), "k_factorize"))) return st; (k_factorize<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, status)));
@@ -1461,6 +1508,8 @@ DNLS_API dnls_status dnls_solve_factored(const dnls_graph* g, int32_t batch, voi
   if (st) return st;
   if (batch > 0 && (!rhs || !x)) return fail(DNLS_E_INVALID, "dnls_solve_factored: rhs/x is NULL");
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_solve_factored: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
   DISPATCH_D(g->sym.D, if ((st = set_smem(k_solve<DD>, smem_bytes(g->dg), "k_solve"))) return st; (k_solve<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, rhs, x)));
@@ -1473,6 +1522,8 @@ DNLS_API dnls_status dnls_export_factor(const dnls_graph* g, int32_t batch, cons
   if (st) return st;
   if (batch > 0 && !dense) return fail(DNLS_E_INVALID, "dnls_export_factor: dense is NULL");
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_export_factor: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), const_cast<void*>(workspace));
   cudaStream_t s = (cudaStream_t)stream;
   DISPATCH_D(g->sym.D, (k_export_factor<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
@@ -1484,7 +1535,10 @@ DNLS_API dnls_status dnls_import_matrix(const dnls_graph* g, int32_t batch, cons
   dnls_status st = check_common("dnls_import_matrix", g, batch, workspace, ws_bytes);
   if (st) return st;
   if (batch > 0 && !dense) return fail(DNLS_E_INVALID, "dnls_import_matrix: dense is NULL");
+  const_cast<dnls_graph*>(g)->drop(workspace);   // the factor storage is overwritten
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_import_matrix: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
   DISPATCH_D(g->sym.D, (k_import_matrix<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
@@ -1497,6 +1551,8 @@ DNLS_API dnls_status dnls_export_rhs(const dnls_graph* g, int32_t batch, const v
   if (st) return st;
   if (batch > 0 && !b) return fail(DNLS_E_INVALID, "dnls_export_rhs: b is NULL");
   if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_export_rhs: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), const_cast<void*>(workspace));
   cudaStream_t s = (cudaStream_t)stream;
   DISPATCH_D(g->sym.D, (k_export_rhs<DD><<<batch, NT, 0, s>>>(g->dg, ws, b)));

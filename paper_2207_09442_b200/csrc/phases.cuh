@@ -49,61 +49,30 @@ __device__ unsigned long long g_probe[8];
 #define DNLS_PROBE_ADD(i, a, b)
 #endif
 
-// device view of the symbolic analysis (all arrays int32, uploaded once per graph)
+// device view of the symbolic analysis (int32 arrays uploaded once per graph; only what the numeric
+// kernels read -- the update / solve lists travel inside the per-level descriptor packets `pk`)
 struct DevGraph {
-  int D, N, E, P, S, L, storage, nblk, n;
+  int D, N, E, P, S, storage, n;
   int x_smem;     // 1: the solution vector x lives in shared memory (offset 0, n_pad doubles)
   int n_pad;      // n rounded up to an even count (16-byte alignment of the next area)
   int res_lo;     // storage offsets >= res_lo are resident in shared memory (top levels)
   int res_n;      // resident doubles (even)
   int stage_n;    // doubles of the level-staging area (largest staged level prefix)
   const int *perm, *iperm, *edges, *prior_vars;
-  const int *sn_first, *sn_ncols, *sn_m, *sn_ld, *sn_w, *sn_off;
-  const int *level_ptr, *level_sn, *level_off, *level_stage_hi;
-  const int *ut_level_ptr, *ut_off, *ut_ld, *ut_cptr, *uc_a, *uc_b, *uc_ld, *uc_w;
-  const int *level_gu, *level_gf, *lrow_ptr, *lrow;
-  const int *sn_parent, *ut_sn_ptr, *child_ptr, *child_idx, *sn_sched, *leaves, *broots;
-  int top_level, n_forest, n_leaves, n_broots;
-  const int *fc_ptr, *fc_off, *fc_ld, *fc_w, *fc_x;
-  // packed 16-byte descriptors: task4 = (target off, target ld, contrib begin, contrib end),
-  // con4 = (source row-p off, source row-q off, ld, width), fcon4 = (source row off, ld, width, y off)
-  const int4 *task4, *con4, *fcon4;
-  const int *snr_ptr, *snr;
-  const int *blk_off, *blk_ld, *blk_kind, *blk_cptr, *blk_con;
-  const int *bc_ptr, *bc;
-  const int *cls_ptr, *cls_slot;   // edge-coloured assembly classes
-  const int4* slot_desc;            // 3 int4 per cost slot
+  const int *sn_first, *sn_m, *sn_ld, *sn_w, *sn_off;   // per supernode: panel geometry and offset
+  const int *level_off, *level_stage_hi;                 // per level: storage range, staged prefix end
+  const int *snr_ptr, *snr;                              // per supernode: below-diagonal pose rows
+  const int *blk_off, *blk_ld, *blk_cptr, *blk_con;      // per storage block: offset, ld, contributing slots
+  const int *bc_ptr, *bc;                                // per pose: its cost slots (fixed gather order)
+  const int4* slot_desc;            // 3 int4 per cost slot (block offsets / lds of its H blocks)
   const int* pose_sn;               // supernode of each permuted pose column
-  int ncls;
   const int* dup_blk;               // blk_* indices of off-diagonal blocks shared by several edges
   int ndup;
-  const int* pk;       // per-level descriptor packets (ints), pk_off[L+1] offsets
+  const int* pk;       // per-level descriptor packets (ints), pk_off[npk+1] offsets
   const int* pk_off;
   int pk_max;          // ints of the largest packet
   int npk;             // number of packets (levels split into size-bounded chunks)
-  const int* ibase;   // start of the device index buffer
-  int inum;           // its length (ints, multiple of 4)
-  int idx_smem;       // 1: kernels copy the index buffer into shared memory and read it there
 };
-
-#define DNLS_DEVGRAPH_PTRS(X)                                                                           \
-  X(perm) X(iperm) X(edges) X(prior_vars) X(sn_first) X(sn_ncols) X(sn_m) X(sn_ld) X(sn_w) X(sn_off)     \
-  X(level_ptr) X(level_sn) X(level_off) X(level_stage_hi) X(ut_level_ptr) X(ut_off) X(ut_ld) X(ut_cptr) \
-  X(uc_a) X(uc_b) X(uc_ld) X(uc_w) X(level_gu) X(level_gf) X(lrow_ptr) X(lrow) X(sn_parent) X(ut_sn_ptr)  \
-  X(child_ptr) X(child_idx) X(sn_sched) X(leaves) X(broots) X(fc_ptr) X(fc_off) X(fc_ld) X(fc_w) X(fc_x) \
-  X(snr_ptr) X(snr) X(blk_off) X(blk_ld) X(blk_kind) X(blk_cptr) X(blk_con) X(bc_ptr) X(bc)
-
-// a copy of g whose index pointers refer to the shared-memory copy `sb` of the index buffer
-__device__ __forceinline__ DevGraph remap_graph(const DevGraph& g, const int* sb) {
-  DevGraph r = g;
-#define DNLS_REMAP(f) r.f = sb + (g.f - g.ibase);
-  DNLS_DEVGRAPH_PTRS(DNLS_REMAP)
-#undef DNLS_REMAP
-  r.task4 = reinterpret_cast<const int4*>(sb + (reinterpret_cast<const int*>(g.task4) - g.ibase));
-  r.con4 = reinterpret_cast<const int4*>(sb + (reinterpret_cast<const int*>(g.con4) - g.ibase));
-  r.fcon4 = reinterpret_cast<const int4*>(sb + (reinterpret_cast<const int*>(g.fcon4) - g.ibase));
-  return r;
-}
 
 // ---- CTA groups: CL CTAs of one thread-block cluster share one batch element (CL == 1: the CTA
 // alone).  Item loops run over the group's CL * NT threads; gsync<CL>() is the group barrier

@@ -505,33 +505,12 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       }
       S.fc_ptr.push_back((int)S.fc_off.size());
     }
-    // per-level pose rows and lane-group sizes (work per level spread over ~cta_threads lanes)
-    S.lrow_ptr.assign(1, 0);
-    S.level_gu.assign(S.num_levels, 1);
-    S.level_gf.assign(S.num_levels, 1);
-    auto group_for = [&](int64_t ntasks) {
-      int G = 1;
-      while (G < 32 && ntasks * G * 2 <= opt.cta_threads) G *= 2;
-      return G;
-    };
-    for (int l = 0; l < S.num_levels; ++l) {
-      for (int i = S.level_ptr[l]; i < S.level_ptr[l + 1]; ++i) {
-        int sn = S.level_sn[i];
-        for (int k = 0; k < S.sn_ncols[sn]; ++k) S.lrow.push_back(S.sn_first[sn] + k);
-      }
-      S.lrow_ptr.push_back((int)S.lrow.size());
-      S.level_gu[l] = group_for((int64_t)D * (S.ut_level_ptr[l + 1] - S.ut_level_ptr[l]));
-      S.level_gf[l] = group_for((int64_t)D * (S.lrow_ptr[l + 1] - S.lrow_ptr[l]));
-    }
     S.snr_ptr.assign(1, 0);
     for (int s = 0; s < NS; ++s) {
       for (int p : S.sn_rows[s]) S.snr.push_back(p);
       S.snr_ptr.push_back((int)S.snr.size());
     }
-    // dataflow scheduling: per-supernode update-task ranges, children lists, forest / top split.
-    // The "top" is the suffix of levels with at most top_max supernodes (processed by CTA-wide
-    // teams, level-synchronous); everything below is the "forest" (warp per supernode, ready
-    // queue driven by child-completion counters).
+    // per-supernode update-task ranges (packet construction places a panel after its tasks)
     {
       // recover the target supernode of each task from its storage offset
       std::vector<int> tsn(S.ut_off.size());
@@ -552,32 +531,6 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         S.ut_sn_ptr[2 * sn] = first[sn] < 0 ? 0 : first[sn];
         S.ut_sn_ptr[2 * sn + 1] = first[sn] < 0 ? 0 : last[sn];
       }
-    }
-    S.child_ptr.assign(NS + 1, 0);
-    for (int sn = 0; sn < NS; ++sn)
-      if (S.sn_parent[sn] >= 0) S.child_ptr[S.sn_parent[sn] + 1]++;
-    for (int sn = 0; sn < NS; ++sn) S.child_ptr[sn + 1] += S.child_ptr[sn];
-    S.child_idx.assign(S.child_ptr[NS], 0);
-    {
-      std::vector<int> fill(S.child_ptr.begin(), S.child_ptr.end() - 1);
-      for (int sn = 0; sn < NS; ++sn)
-        if (S.sn_parent[sn] >= 0) S.child_idx[fill[S.sn_parent[sn]]++] = sn;
-    }
-    S.top_level = S.num_levels;
-    while (S.top_level > 0 && S.level_ptr[S.top_level] - S.level_ptr[S.top_level - 1] <= opt.top_max) --S.top_level;
-    S.n_forest = S.level_ptr[S.top_level];
-    S.sn_sched.assign(NS, 0);   // 1 = forest supernode
-    for (int i = 0; i < S.n_forest; ++i) S.sn_sched[S.level_sn[i]] = 1;
-    S.leaves.clear();
-    for (int i = 0; i < S.n_forest; ++i) {
-      int sn = S.level_sn[i];
-      if (S.child_ptr[sn + 1] == S.child_ptr[sn]) S.leaves.push_back(sn);
-    }
-    // top-down ready set for the backward pass: forest supernodes whose parent is in the top
-    S.broots.clear();
-    for (int i = 0; i < S.n_forest; ++i) {
-      int sn = S.level_sn[i];
-      if (S.sn_parent[sn] < 0 || !S.sn_sched[S.sn_parent[sn]]) S.broots.push_back(sn);
     }
   }
   // ---- 5b'. descriptor packets (prefetched into shared memory one packet ahead).  A level is
@@ -796,38 +749,10 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       S.bc_ptr.push_back((int)S.bc.size());
     }
   }
-  // ---- 5d. edge-coloured scatter assembly: cost slots (edges, then priors) are coloured so that
-  // no two slots of a class touch the same pose; classes are applied in order, so every H block
-  // receives its contributions in a fixed order (deterministic) without atomics.
+  // ---- 5d. per-slot descriptors of the single-writer assembly: the storage
+  // offsets / leading dims of the slot's H blocks and its permuted poses
   {
     const int slots = E + P;
-    std::vector<uint64_t> used(N, 0);
-    std::vector<int> color(slots, 0);
-    int ncol = 0;
-    for (int sl = 0; sl < slots; ++sl) {
-      const int a = sl < E ? edges[2 * sl] : priors[sl - E];
-      const int b = sl < E ? edges[2 * sl + 1] : a;
-      const uint64_t m = used[a] | used[b];
-      int c = 0;
-      while (c < 64 && (m >> c) & 1) ++c;
-      if (c >= 64) {
-        *code = 8;
-        err << "dnls_graph_create: pose degree too high for the 64-class edge colouring";
-        return err.str();
-      }
-      color[sl] = c;
-      used[a] |= 1ull << c;
-      used[b] |= 1ull << c;
-      ncol = std::max(ncol, c + 1);
-    }
-    S.cls_ptr.assign(ncol + 1, 0);
-    for (int sl = 0; sl < slots; ++sl) S.cls_ptr[color[sl] + 1]++;
-    for (int c = 0; c < ncol; ++c) S.cls_ptr[c + 1] += S.cls_ptr[c];
-    S.cls_slot.assign(slots, 0);
-    {
-      std::vector<int> fill(S.cls_ptr.begin(), S.cls_ptr.end() - 1);
-      for (int sl = 0; sl < slots; ++sl) S.cls_slot[fill[color[sl]]++] = sl;
-    }
     auto diag_off = [&](int p) {
       const int sn = col_sn[p];
       return (int)S.sn_off[sn] + D * (p - S.sn_first[sn]) * (S.sn_ld[sn] + 1);
@@ -851,7 +776,6 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         d[4] = S.sn_ld[col_sn[pi]];
         d[5] = S.sn_ld[col_sn[pj]];
         d[6] = S.sn_ld[t];
-        d[7] = color[sl];
         d[8] = pi;
         d[9] = pj;
         d[10] = pair_count[std::make_pair(Q, P_)] == 1 ? 1 : 0;   // only edge between its poses
@@ -861,7 +785,6 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         d[1] = -1;
         d[2] = -1;
         d[4] = S.sn_ld[col_sn[pp]];
-        d[7] = color[sl];
         d[8] = pp;
         d[9] = -1;
       }

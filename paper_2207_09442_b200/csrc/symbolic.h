@@ -24,8 +24,6 @@ struct SymbolicOptions {
   int64_t smem_cap_doubles = 0;
   // threads per CTA of the numeric kernels (lane-group sizes are chosen against it)
   int cta_threads = 256;
-  // levels at the top of the tree with at most this many supernodes are processed CTA-wide
-  int top_max = 2;
   // size bound of one descriptor packet (ints); larger levels are split into chunks
   int packet_ints = 4096;
 };
@@ -60,21 +58,16 @@ struct Symbolic {
   //   contribution c: source rows at uc_a (entry (row_p, k=0)), uc_b (row_q), ld uc_ld, width uc_w
   std::vector<int32_t> ut_level_ptr, ut_off, ut_ld, ut_cptr;
   std::vector<int32_t> uc_a, uc_b, uc_ld, uc_w;
-  // lanes cooperating on one update task / one forward-substitution row, per level (1..32)
-  std::vector<int32_t> level_gu, level_gf;
-  // pose rows (columns of the level's supernodes) per level, for the fused forward substitution
-  std::vector<int32_t> lrow_ptr, lrow;
 
   // forward substitution gather per permuted pose row p: sum over source panels holding row p
   std::vector<int32_t> fc_ptr, fc_off, fc_ld, fc_w, fc_x;
   // backward substitution: below rows of each supernode (flattened sn_rows)
   std::vector<int32_t> snr_ptr, snr;
-  // dataflow schedule: update-task range [2s, 2s+1] per supernode, children CSR, forest flags
-  std::vector<int32_t> ut_sn_ptr, child_ptr, child_idx, sn_sched, leaves, broots;
+  // update-task range [2s, 2s+1] of each target supernode
+  std::vector<int32_t> ut_sn_ptr;
   // per-level descriptor packets (see symbolic.cpp 5b'), offsets in ints, largest packet
   std::vector<int32_t> pk, pk_off, pk_level;
   int pk_max = 0, npk = 0;
-  int top_level = 0, n_forest = 0;
 
   // scatter-free assembly: every d x d block of the storage exactly once
   //   block k: storage offset blk_off[k], leading dim blk_ld[k], kind blk_kind[k]
@@ -86,9 +79,9 @@ struct Symbolic {
   std::vector<int32_t> bc_ptr, bc;
   // off-diagonal blocks (blk_* indices) that receive contributions from more than one edge
   std::vector<int32_t> dup_blk;
-  // edge-coloured scatter assembly: classes cls_ptr[C+1] over slots cls_slot; per slot 3 int4:
-  // (off_ii, off_jj, off_ij, row-is-j flag), (ld_ii, ld_jj, ld_ij, 0), (perm pose i, perm pose j, 0, 0)
-  std::vector<int32_t> cls_ptr, cls_slot, slot_desc;
+  // per cost slot 3 int4: (off_ii, off_jj, off_ij, row-is-j flag), (ld_ii, ld_jj, ld_ij, 0),
+  // (perm pose i, perm pose j, only-edge-between-its-poses flag, 0)
+  std::vector<int32_t> slot_desc;
 
   // stats
   int64_t nnz_H_blocks = 0, nnz_L_blocks = 0, nnz_L = 0;

@@ -20,6 +20,7 @@ BWD_NONE, BWD_IMPLICIT = 0, 1
 DAMP_MARQUARDT, DAMP_IDENTITY = 0, 1
 GRAD_TANGENT, GRAD_MATRIX = 0, 1
 ST_OK, ST_CONVERGED, ST_NOT_SPD, ST_SATURATED = 0, 1, 2, 3
+ST_WARN_NOT_CONVERGED, ST_CODE_MASK = 0x100, 0xFF
 
 
 def _ptr(t):
@@ -40,8 +41,10 @@ def _f64(t, name):
     return _ptr(t)
 
 
-def _stream(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream(stream=None, device=None):
+    """The caller's stream, else the current stream OF THE GRAPH'S DEVICE (the C ABI switches to that
+    device for the call, so the stream must belong to it)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -102,6 +105,25 @@ def dnls_graph_stats(g: Graph) -> dict:
 def _i32(n):
     a = np.zeros(max(int(n), 1), dtype=np.int32)
     return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def dnls_block_offsets(g: Graph):
+    """(edge_desc [E][7], prior_desc [P][2]) int32: storage offsets / leading dims of each cost's H blocks."""
+    ed = np.zeros((max(g.E, 1), 7), dtype=np.int32)
+    pd = np.zeros((max(g.P, 1), 2), dtype=np.int32)
+    check(lib().dnls_block_offsets(g.handle, ed.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                   pd.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), "dnls_block_offsets")
+    return ed[:g.E], pd[:g.P]
+
+
+def dnls_status_summary(status: torch.Tensor, stream=None):
+    """Host-synchronous (n_failed, n_warned) of a device status[B]; raises DnlsError(6) if all failed."""
+    if status.dtype != torch.int32:
+        raise TypeError("status must be int32")
+    nf, nw = ctypes.c_int32(0), ctypes.c_int32(0)
+    check(lib().dnls_status_summary(_ptr(status), int(status.numel()), ctypes.byref(nf), ctypes.byref(nw),
+                                    _stream(stream)), "dnls_status_summary")
+    return nf.value, nw.value
 
 
 def dnls_graph_perm(g: Graph) -> np.ndarray:
@@ -176,7 +198,7 @@ def make_problem(poses, meas, prior_meas, w_edge, w_prior, objective=None, statu
 
 def dnls_forward(g: Graph, batch: int, opt: DnlsOptions, prob: DnlsProblem, workspace: torch.Tensor, stream=None):
     check(lib().dnls_forward(g.handle, int(batch), ctypes.byref(opt), ctypes.byref(prob), _ptr(workspace),
-                             workspace.numel(), _stream(stream)), "dnls_forward")
+                             workspace.numel(), _stream(stream, g.device)), "dnls_forward")
 
 
 def dnls_backward_implicit(g: Graph, batch: int, prob: DnlsProblem, grad_poses: torch.Tensor, grad_kind: int,
@@ -185,7 +207,7 @@ def dnls_backward_implicit(g: Graph, batch: int, prob: DnlsProblem, grad_poses: 
     check(lib().dnls_backward_implicit(g.handle, int(batch), ctypes.byref(prob), _f64(grad_poses, "grad_poses"),
                                        int(grad_kind), _f64(grad_w_edge, "grad_w_edge"),
                                        _f64(grad_w_prior, "grad_w_prior"), _f64(grad_radius, "grad_radius"),
-                                       int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream)),
+                                       int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream, g.device)),
           "dnls_backward_implicit")
 
 
@@ -195,36 +217,36 @@ def dnls_backward_dlm(g: Graph, batch: int, prob: DnlsProblem, grad_poses: torch
     check(lib().dnls_backward_dlm(g.handle, int(batch), ctypes.byref(prob), _f64(grad_poses, "grad_poses"),
                                   int(grad_kind), float(epsilon), _f64(grad_w_edge, "grad_w_edge"),
                                   _f64(grad_w_prior, "grad_w_prior"), _f64(grad_radius, "grad_radius"),
-                                  int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream)),
+                                  int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream, g.device)),
           "dnls_backward_dlm")
 
 
 def dnls_linearize(g: Graph, batch: int, prob: DnlsProblem, lam, damping: int, workspace: torch.Tensor, stream=None):
     check(lib().dnls_linearize(g.handle, int(batch), ctypes.byref(prob), _f64(lam, "lambda"), int(damping),
-                               _ptr(workspace), workspace.numel(), _stream(stream)), "dnls_linearize")
+                               _ptr(workspace), workspace.numel(), _stream(stream, g.device)), "dnls_linearize")
 
 
 def dnls_factorize(g: Graph, batch: int, workspace: torch.Tensor, status=None, stream=None):
     check(lib().dnls_factorize(g.handle, int(batch), _ptr(workspace), workspace.numel(), _ptr(status),
-                               _stream(stream)), "dnls_factorize")
+                               _stream(stream, g.device)), "dnls_factorize")
 
 
 def dnls_solve_factored(g: Graph, batch: int, workspace: torch.Tensor, rhs: torch.Tensor, x: torch.Tensor,
                         stream=None):
     check(lib().dnls_solve_factored(g.handle, int(batch), _ptr(workspace), workspace.numel(), _f64(rhs, "rhs"),
-                                    _f64(x, "x"), _stream(stream)), "dnls_solve_factored")
+                                    _f64(x, "x"), _stream(stream, g.device)), "dnls_solve_factored")
 
 
 def dnls_export_factor(g: Graph, batch: int, workspace: torch.Tensor, dense: torch.Tensor, stream=None):
     check(lib().dnls_export_factor(g.handle, int(batch), _ptr(workspace), workspace.numel(), _f64(dense, "dense"),
-                                   _stream(stream)), "dnls_export_factor")
+                                   _stream(stream, g.device)), "dnls_export_factor")
 
 
 def dnls_import_matrix(g: Graph, batch: int, dense: torch.Tensor, workspace: torch.Tensor, stream=None):
     check(lib().dnls_import_matrix(g.handle, int(batch), _f64(dense, "dense"), _ptr(workspace), workspace.numel(),
-                                   _stream(stream)), "dnls_import_matrix")
+                                   _stream(stream, g.device)), "dnls_import_matrix")
 
 
 def dnls_export_rhs(g: Graph, batch: int, workspace: torch.Tensor, b: torch.Tensor, stream=None):
     check(lib().dnls_export_rhs(g.handle, int(batch), _ptr(workspace), workspace.numel(), _f64(b, "b"),
-                                _stream(stream)), "dnls_export_rhs")
+                                _stream(stream, g.device)), "dnls_export_rhs")

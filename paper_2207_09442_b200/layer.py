@@ -117,9 +117,15 @@ class _PoseGraphFn(torch.autograd.Function):
         radius = rest[0] if ctx.has_radius else None
         if g_poses is None:
             g_poses = torch.zeros_like(poses)
+        # per-element gradients when either weight is per element ([B][E] / [B][P]); a weight shared by the
+        # batch (1-D) gets the batch sum of its per-element gradients
+        per_el = w_edge.dim() == 2 or w_prior.dim() == 2
         out = solver.backward(poses, meas, prior_meas, w_edge, w_prior, g_poses, D.GRAD_MATRIX,
-                              per_element=(w_edge.dim() == 2), mode=ctx.mode, epsilon=ctx.epsilon, radius=radius)
+                              per_element=per_el, mode=ctx.mode, epsilon=ctx.epsilon, radius=radius)
         ge, gp = out[0], out[1]
+        if per_el:
+            ge = ge if w_edge.dim() == 2 else ge.sum(0)
+            gp = gp if w_prior.dim() == 2 else gp.sum(0)
         gr = out[2] if radius is not None and ctx.needs_input_grad[6] else None
         ge = ge if ctx.needs_input_grad[4] else None
         gp = gp if ctx.needs_input_grad[5] else None

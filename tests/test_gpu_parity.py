@@ -144,7 +144,7 @@ def test_forward_gn_matches_oracle(N, dim, B, K, p, mode):
     for b, r in enumerate(res):
         assert pose_err(P[b], r.x) <= TOL_POSE
         assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
-        assert st[b].item() == r.status and it[b].item() == r.iterations
+        assert (st[b].item() & 0xff) == r.status and it[b].item() == r.iterations
 
 
 def lm_has_tie(r, rel=1e-10):
@@ -169,7 +169,7 @@ def test_forward_lm_matches_oracle(K, seed):
         else:
             n_strict += 1
             assert pose_err(P[b], r.x) <= TOL_POSE
-            assert st[b].item() == r.status and it[b].item() == r.iterations
+            assert (st[b].item() & 0xff) == r.status and it[b].item() == r.iterations
     if K <= 6:
         assert n_strict == len(res)      # far from convergence no ties occur: strict iterate parity
 
@@ -181,7 +181,7 @@ def test_forward_step_size_and_early_stop():
     res = oracle_results(topo, data, max_iterations=12, step_size=0.5, early_stop=True, abs_tol=1e-12, rel_tol=1e-6)
     for b, r in enumerate(res):
         assert pose_err(poses[b].cpu().numpy(), r.x) <= TOL_POSE
-        assert st[b].item() == r.status and it[b].item() == r.iterations
+        assert (st[b].item() & 0xff) == r.status and it[b].item() == r.iterations
 
 
 def test_not_spd_without_prior_is_per_element_status():
@@ -511,7 +511,7 @@ def test_forward_cluster_matches_oracle(cl, N, dim, opt, B):
             continue
         assert pose_err(P[b], r.x) <= TOL_POSE
         assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
-        assert st[b].item() == r.status and it[b].item() == r.iterations
+        assert (st[b].item() & 0xff) == r.status and it[b].item() == r.iterations
         a, c, _ = oimp.implicit_weight_grads(oracle_problem(topo, data, b), r.x, v[b].reshape(-1), L_K=r.L_final)
         assert rel_vec_err(np.concatenate([ge[b].cpu().numpy(), gp[b].cpu().numpy()]),
                            np.concatenate([a, c])) <= TOL_GRAD
@@ -561,7 +561,7 @@ def test_forward_dogleg_matches_oracle(N, dim, B, delta0):
         compared += 1
         assert pose_err(P[b], r.x) <= TOL_POSE
         assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
-        assert st[b].item() == r.status and it[b].item() == r.iterations
+        assert (st[b].item() & 0xff) == r.status and it[b].item() == r.iterations
         a, c, _ = oimp.implicit_weight_grads(oracle_problem(topo, data, b), r.x, v[b].reshape(-1), L_K=r.L_final)
         assert rel_vec_err(np.concatenate([ge[b].cpu().numpy(), gp[b].cpu().numpy()]),
                            np.concatenate([a, c])) <= TOL_GRAD
