@@ -1,22 +1,27 @@
 #!/usr/bin/env python
-"""Benchmark: batched SE3 pose-graph GN iterations/sec (fwd + implicit bwd) -- BASELINE.json metric.
+"""Benchmark: batched SE3 pose-graph GN iterations/sec (fwd + implicit bwd) at 1/2/4/8 B200 --
+BASELINE.json's metric, on the configuration it is quoted on.
 
-One STEP = the whole hot path on one batch: reset poses to theta_0, dnls_forward (K GN
-iterations + the final undamped linearise+factor at theta_K, implicit mode), then
+One STEP = the whole hot path on one batch: reset poses to theta_0, dnls_forward
+(K GN iterations + the final undamped linearise+factor at theta_K, implicit mode), then
 dnls_backward_implicit (adjoint solve on the cached factor + weight-gradient contraction +
-fixed-order batch reduction), and for N > 1 GPUs the NCCL all-reduce of [grad_w_edge,
-grad_w_prior, loss].  value = (batch elements of all ranks) * K / T_step.
+fixed-order batch reduction), and for N > 1 GPUs ONE all_reduce of [grad_w_edge | grad_w_prior |
+loss] (paper_2207_09442_b200.parallel.allreduce_shared_grads).
+value = (batch elements of all ranks) * K / T, T = device time of the K timed steps, max over ranks.
 
-Default workload (N = 1): BASELINE.json configs[1] = C2, SE3 Cube graph, 256 poses, batch 128 per
-GPU, GN K = 10, implicit backward (weak scaling: 128 per GPU at every N).
+Default workload: BASELINE.json configs[4] = C5, SE3 Cube graph, 1024 poses, global batch 2048 split
+over the N GPUs (strong scaling: 2048 at N=1, 256 per GPU at N=8), GN K = 10, implicit backward.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
 
---impl reference times the fp64 CPU oracle (the reference arm of this tier) on a bounded sample.
+--gpus N > 1 without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks (one per GPU, NCCL).  --impl reference times the fp64 CPU oracle (the reference arm of this
+tier) on a bounded sample.
 """
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -31,6 +36,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "batched SE3 pose-graph GN iterations/sec (fwd+implicit bwd) at 1/2/4/8 B200"
 UNIT = "problem-iterations/s"
+L2_BYTES = 126 * 1024 * 1024
 
 CONFIGS = {
     "C1": dict(N=16, dim=2, B=4, K=10, opt="gn", p=0.2, mode="local", scaling="weak",
@@ -39,6 +45,8 @@ CONFIGS = {
                desc="C2: SE3 cube pose graph, 256 poses, batch 128 per GPU, GN K=10 + implicit backward"),
     "C3": dict(N=4096, dim=3, B=16, K=10, opt="lm", p=0.2, mode="local", scaling="weak",
                desc="C3: SE3 pose graph, 4096 poses, batch 16 per GPU, LM K=10 + implicit backward"),
+    "C3r": dict(N=4096, dim=3, B=16, K=10, opt="lm", p=0.2, mode="random", scaling="weak",
+                desc="C3r: SE3 pose graph, 4096 poses, random loop closures (large supernodes), batch 16, LM K=10"),
     "C4": dict(N=1024, dim=3, B=256, K=10, opt="gn", p=0.2, mode="local", scaling="weak",
                desc="C4: SE3 pose graph, 1024 poses, batch 256 per GPU, GN K=10 + implicit backward (learnable w)"),
     "C5": dict(N=1024, dim=3, B=2048, K=10, opt="gn", p=0.2, mode="local", scaling="strong",
@@ -108,14 +116,34 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_oracle_step(topo, data, cfg, elements, backward="implicit", eps=1e-3, radius=None):
+# ----------------------------------------------------------------------------- host-side step wiring
+def shard(cfg: dict, world: int, rank: int) -> tuple[int, int]:
+    """[b0, b1) of the global batch solved by `rank`: strong scaling splits the
+    config's batch, weak scaling gives every rank the config's batch (global indices continue)."""
+    from paper_2207_09442_b200.parallel import shard_range
+    if cfg["scaling"] == "weak":
+        return rank * cfg["B"], (rank + 1) * cfg["B"]
+    return shard_range(cfg["B"], world, rank)
+
+
+def reduce_step(ge, gp, obj, extra=()):
+    """The step's only exchange: ONE all_reduce(SUM) of [grad_w_edge | grad_w_prior | loss | extra]
+    (parallel.allreduce_shared_grads; identity on one rank).  Returns the reduced tensors."""
+    from paper_2207_09442_b200.parallel import allreduce_shared_grads
+    return allreduce_shared_grads(ge, gp, obj.sum().reshape(1), *extra)
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+def cpu_oracle_step(topo, data, cfg, elements, backward="implicit", eps=1e-3, radius=None, K=None):
     """Oracle fwd (K iterations [+ final factor]) + implicit or DLM bwd on the listed elements."""
     from oracle import dlm as odlm
     from oracle import implicit as oimp
     from oracle import lie as olie
     from oracle import nls as onls
     G = "SE3" if cfg["dim"] == 3 else "SE2"
-    opt = onls.Options(optimizer=cfg["opt"], max_iterations=cfg["K"], implicit=(backward == "implicit"))
+    K = cfg["K"] if K is None else K
+    with_bwd = backward in ("implicit", "dlm")
+    opt = onls.Options(optimizer=cfg["opt"], max_iterations=K, implicit=(backward == "implicit"))
     v = np.ones(topo.num_poses * (6 if cfg["dim"] == 3 else 3))
     for b in elements:
         prob = onls.PGOProblem(G, topo.num_poses, topo.edges, topo.prior_vars, data["meas"][b],
@@ -123,7 +151,7 @@ def cpu_oracle_step(topo, data, cfg, elements, backward="implicit", eps=1e-3, ra
         res = onls.optimize(prob, olie.to_homog(data["poses0"][b]), opt)
         if backward == "dlm":
             odlm.dlm_weight_grads(prob, res.x, v, eps)
-        elif res.L_final is not None:
+        elif with_bwd and res.L_final is not None:
             oimp.implicit_weight_grads(prob, res.x, v, L_K=res.L_final)
 
 
@@ -134,6 +162,14 @@ def cores():
         return os.cpu_count()
 
 
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"), default=None)
+    except Exception:
+        return None
+
+
 def cpu_baseline(cfg, n_elems, backward="implicit", eps=1e-3, radius=None):
     import synth
     topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
@@ -141,12 +177,17 @@ def cpu_baseline(cfg, n_elems, backward="implicit", eps=1e-3, radius=None):
     t0 = time.perf_counter()
     cpu_oracle_step(topo, data, cfg, range(n_elems), backward, eps, radius)
     dt = time.perf_counter() - t0
-    return {"value": n_elems * cfg["K"] / dt, "unit": UNIT, "cores": cores(), "kind": "oracle",
+    return {"value": n_elems * cfg["K"] / dt, "unit": UNIT, "cores": cores(), "blas_threads": blas_threads(),
+            "kind": "oracle",
             "sample": f"{n_elems} element(s) of {cfg['desc'].split(':')[0]} (fwd K={cfg['K']} + final factor + "
-                      f"{backward} bwd), {dt:.1f} s, numpy/OpenBLAS fp64 dense"}
+                      f"{backward} bwd), {dt:.1f} s, numpy/OpenBLAS fp64 dense n={cfg['N'] * (6 if cfg['dim'] == 3 else 3)}"}
 
 
 def run_reference(args, cfg, rank):
+    """Reference arm of this tier: the fp64 CPU oracle as it stands.  One step = ONE GN iteration
+    (dense linearise, dense Cholesky, solve, retraction, objective) of one batch element of the
+    workload; the implicit backward's extra factorisation (1/K of the work) is not included, so the
+    value is an upper bound of the oracle's rate."""
     if rank != 0:
         return
     import synth
@@ -154,39 +195,69 @@ def run_reference(args, cfg, rank):
     n_el = 1
     data = synth.cube_batch(topo, n_el, seed=0)
     for _ in range(args.warmup):
-        cpu_oracle_step(topo, data, cfg, range(n_el))
+        cpu_oracle_step(topo, data, cfg, range(n_el), backward="none", K=1)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        cpu_oracle_step(topo, data, cfg, range(n_el))
+        cpu_oracle_step(topo, data, cfg, range(n_el), backward="none", K=1)
         ts.append(time.perf_counter() - t0)
     T = sum(ts) / len(ts)
-    val = n_el * cfg["K"] / T
+    val = n_el * 1 / T
+    sample = (f"one GN iteration of {n_el} batch element per step (dense n={topo.num_poses * (6 if cfg['dim'] == 3 else 3)}"
+              f" linearise + Cholesky + solve + retraction), fp64 NumPy/OpenBLAS oracle; the implicit backward's "
+              f"extra factorisation is not timed (upper bound of the oracle's rate)")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": cfg["scaling"],
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "sample": f"{n_el} batch element per step (bounded CPU sample)",
-                   "poses": cfg["N"], "edges": topo.num_edges, "iterations": cfg["K"]},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores(), "kind": "oracle",
-                         "sample": f"{n_el} element per step, fp64 NumPy dense oracle"},
+        "config": {"workload": cfg["desc"], "sample": sample, "poses": cfg["N"], "edges": topo.num_edges,
+                   "iterations": cfg["K"]},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores(), "blas_threads": blas_threads(),
+                         "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- launcher
+def relaunch_distributed(args):
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run, N ranks."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def nccl_init_summary():
+    """nRanks / NVLS lines NCCL wrote during communicator init (NCCL_DEBUG=INFO to a file)."""
+    out = []
+    for f in sorted(glob.glob("/tmp/dnls_nccl.*.log")):
+        try:
+            for ln in open(f):
+                if "nRanks" in ln or "NVLS" in ln or "comm 0x" in ln and "Init COMPLETE" in ln:
+                    out.append(ln.strip()[-160:])
+        except Exception:
+            pass
+    return out[:8]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="dnls", choices=["dnls", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-elements", type=int, default=4)
-    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-factor-roofline", action="store_true")
+    ap.add_argument("--cpu-elements", type=int, default=None)
+    ap.add_argument("--flush", choices=["auto", "always", "never"], default="auto",
+                    help="flush L2 between timed steps (auto: only when the step's working set is < 2x L2)")
     ap.add_argument("--backward", default="implicit", choices=["implicit", "dlm"],
                     help="backward mode timed in the step (dlm: PAPER.md:259-271, one augmented GN step)")
     ap.add_argument("--epsilon", type=float, default=1e-3, help="DLM epsilon")
@@ -196,15 +267,26 @@ def main():
                     help="CTAs per batch element in the forward (0 = automatic)")
     ap.add_argument("--welsch", type=float, default=None,
                     help="Welsch radius of the Between edges (PAPER.md:168 robust PGO); default: quadratic costs")
+    ap.add_argument("--batch", type=int, default=None, help="override the config's (global) batch")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo + --share-gpu: multi-rank wiring test on one GPU)")
+    ap.add_argument("--share-gpu", action="store_true", help="every rank uses cuda:0 (testing on a 1-GPU box)")
+    ap.add_argument("--dump-shard", default=None, help="write this rank's theta_K / grads to <path>.rank<r>.npz")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
     if args.optimizer:
         cfg["opt"] = args.optimizer
+    if args.batch:
+        cfg["B"] = args.batch
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch_distributed(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         run_reference(args, cfg, rank)
@@ -217,25 +299,30 @@ def main():
     from paper_2207_09442_b200 import dnls as D
     from paper_2207_09442_b200.layer import PoseGraphSolver
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = 0 if args.share_gpu else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/dnls_nccl.%h.%p.log")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     # ---- data: per-rank shard of the global batch (per-element seeds -> shard independent)
-    if cfg["scaling"] == "weak":
-        B = cfg["B"]
-    else:
-        assert cfg["B"] % world == 0
-        B = cfg["B"] // world
-    b_start = rank * B
+    b0, b1 = shard(cfg, world, rank)
+    B = b1 - b0
     topo = synth.cube_topology(cfg["N"], dim=cfg["dim"], p=cfg["p"], mode=cfg["mode"], seed=0)
-    data = synth.cube_batch(topo, B, seed=0, b_start=b_start)
+    data = synth.cube_batch(topo, B, seed=0, b_start=b0)
     d = 6 if cfg["dim"] == 3 else 3
     group = D.SE3 if cfg["dim"] == 3 else D.SE2
     K = cfg["K"]
-    solver = PoseGraphSolver(group, topo.num_poses, topo.edges, topo.prior_vars, device=local_rank,
+    t_sym = time.perf_counter()
+    solver = PoseGraphSolver(group, topo.num_poses, topo.edges, topo.prior_vars, device=dev_index,
                              max_iterations=K, optimizer={"gn": D.GN, "lm": D.LM, "dogleg": D.DOGLEG}[cfg["opt"]])
+    t_sym = time.perf_counter() - t_sym
     g = solver.graph
     st = solver.stats
     opt = solver.options
@@ -243,7 +330,8 @@ def main():
     opt.cluster_ctas = args.cluster
     opt.backward_mode = D.BWD_NONE if dlm else D.BWD_IMPLICIT
     host = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in data.items() if k != "gt"}
-    vgrad = torch.from_numpy(np.random.default_rng([1, rank]).standard_normal((B, topo.num_poses, d)))
+    vgrad = torch.from_numpy(np.stack([np.random.default_rng([1, b]).standard_normal((topo.num_poses, d))
+                                       for b in range(b0, b1)]))
     dv = {k: v.to(dev) for k, v in host.items()}
     dvg = vgrad.to(dev)
     poses = torch.empty_like(dv["poses0"])
@@ -251,18 +339,19 @@ def main():
     sts = torch.empty(B, dtype=torch.int32, device=dev)
     its = torch.empty(B, dtype=torch.int32, device=dev)
     E, P = topo.num_edges, int(topo.prior_vars.shape[0])
-    # [grad_w_edge | grad_w_prior | loss | grad_radius (Welsch)]: ONE all_reduce per step for G > 1
-    red = torch.zeros(E + P + 1 + (0 if args.welsch is None else 1), dtype=torch.float64, device=dev)
-    ge, gp = red[:E], red[E:E + P]
+    ge = torch.zeros(E, dtype=torch.float64, device=dev)
+    gp = torch.zeros(P, dtype=torch.float64, device=dev)
     ws = solver.workspace(B)
     rad = None if args.welsch is None else torch.tensor([args.welsch], dtype=torch.float64, device=dev)
-    gr = None if rad is None else red[E + P + 1:]
+    gr = None if rad is None else torch.zeros(1, dtype=torch.float64, device=dev)
     prob = D.make_problem(poses, dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"], obj, sts, its,
                           radius=rad)
     stream = torch.cuda.current_stream()
-    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-
-    ev_f = []
+    # the step's working set: factor storage + per-slot scratch of the workspace, poses, measurements
+    ws_bytes = ws.numel() + sum(v.numel() * v.element_size() for v in dv.values())
+    flush_on = args.flush == "always" or (args.flush == "auto" and ws_bytes < 2 * L2_BYTES)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev) if flush_on else None
+    reduced = [None]
 
     def step(record=None):
         poses.copy_(dv["poses0"])
@@ -277,17 +366,18 @@ def main():
             D.dnls_backward_dlm(g, B, prob, dvg, D.GRAD_TANGENT, args.epsilon, ge, gp, 0, ws, grad_radius=gr)
         else:
             D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws, grad_radius=gr)
-        if world > 1:
-            torch.sum(obj, dim=0, keepdim=True, out=red[E + P:E + P + 1])
-            dist.all_reduce(red)
+        reduced[0] = reduce_step(ge, gp, obj, () if gr is None else (gr,))
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local_rank).start()
-    times = []
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev_index).start()
+    ev_f, per_step = [], []
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
     for _ in range(args.steps):
         if flush is not None:
             flush.fill_(1)
@@ -295,20 +385,28 @@ def main():
         e0.record(stream)
         step(ev_f)
         e1.record(stream)
-        times.append((e0, e1))
+        per_step.append((e0, e1))
+    t1.record(stream)
     torch.cuda.synchronize()
-    clocks = sampler.stop()
     if world > 1:
         dist.barrier()
-    T = sum(a.elapsed_time(b) for a, b in times) / 1e3          # seconds, K steps
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    steps_ms = [a.elapsed_time(b) for a, b in per_step]
+    # the timed region: the K steps end to end (with a flush the flush writes are excluded: sum of steps)
+    T = (sum(steps_ms) if flush is not None else t0.elapsed_time(t1)) / 1e3
     Tf = sum(a.elapsed_time(b) for a, b in ev_f) / 1e3 / args.steps
     if world > 1:
         tt = torch.tensor([T, Tf], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         T, Tf = tt.tolist()
-    total_elems = B * world
+    total_elems = cfg["B"] if cfg["scaling"] == "strong" else B * world
     value = total_elems * K * args.steps / T
     ms_per_step = T / args.steps * 1e3
+
+    if args.dump_shard:
+        np.savez(f"{args.dump_shard}.rank{rank}.npz", poses=poses.cpu().numpy(), obj=obj.cpu().numpy(),
+                 grads=torch.cat([r.reshape(-1) for r in reduced[0]]).cpu().numpy(), b0=b0, b1=b1)
 
     # ---- roofline of the dominant kernel (k_forward): algorithmic bytes per launch / duration
     per_iter = st["bytes_linearize"] + st["bytes_factor"] + st["bytes_solve"] + st["bytes_update"]
@@ -320,25 +418,51 @@ def main():
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            if tj.get("config") == args.config:
-                traffic = tj.get("dram_bytes_per_launch")
+            ent = tj.get(args.config) if isinstance(tj.get(args.config), dict) else None
+            if ent and ent.get("batch") == B:
+                traffic = ent.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "k_forward", "peak_source": peak_src,
                 "alg_bytes_per_launch": alg_bytes, "kernel_ms": Tf * 1e3,
                 "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)" + ("" if dlm else "+lin+factor") +
-                        ") per SURVEY.md 8(d)"}
+                        ") per SURVEY.md 8(d); traffic = ncu dram read+write of one launch (profiles/ncu_traffic.json)"}
 
-    # ---- e2e through the public API (PoseGraphSolver) with pinned host buffers
+    # ---- factor-only roofline (north_star: "the numeric-factorisation kernel"): dnls_factorize on the
+    # assembled H(theta_0) of the same batch, 16 nnz(L) B algorithmic bytes per launch
+    if not args.no_factor_roofline:
+        fprob = D.make_problem(dv["poses0"], dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"])
+        fts = []
+        for r in range(args.warmup + args.steps):
+            D.dnls_linearize(g, B, fprob, None, D.DAMP_MARQUARDT, ws)
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            D.dnls_factorize(g, B, ws, sts)
+            b_.record(stream)
+            if r >= args.warmup:
+                fts.append((a, b_))
+        torch.cuda.synchronize()
+        fms = [a.elapsed_time(b) for a, b in fts]
+        tfac = statistics.median(fms) / 1e3
+        fbytes = 16.0 * st["nnz_L"] * B
+        roofline["factor"] = {"kernel": "k_factorize", "bound": "hbm", "achieved": fbytes / tfac / 1e9,
+                              "peak": peak, "unit": "GB/s", "frac": fbytes / tfac / 1e9 / peak,
+                              "alg_bytes_per_launch": fbytes, "kernel_ms_median": tfac * 1e3,
+                              "kernel_ms_min": min(fms), "flops_per_launch": st["factor_flops"] * B,
+                              "note": "16 nnz(L) B per launch (SURVEY.md 8(d) a3), standalone dnls_factorize"}
+
+    # ---- e2e through the public API (PoseGraphSolver) with pinned host buffers: H2D of the step's inputs,
+    # D2H of theta_K, the objective and the (reduced) gradients
     e2e = None
     if not args.no_e2e:
         pin = {k: v.pin_memory() for k, v in host.items()}
         pvg = vgrad.pin_memory()
         out_obj = torch.empty(B, dtype=torch.float64).pin_memory()
-        out_g = torch.empty(E + P + (0 if rad is None else 1), dtype=torch.float64).pin_memory()
+        out_pose = torch.empty(host["poses0"].shape, dtype=torch.float64).pin_memory()
+        out_g = torch.empty(E + P + 1 + (0 if rad is None else 1), dtype=torch.float64).pin_memory()
         bi = sum(v.numel() * v.element_size() for v in pin.values()) + pvg.numel() * 8
-        bo = out_obj.numel() * 8 + out_g.numel() * 8
+        bo = out_obj.numel() * 8 + out_g.numel() * 8 + out_pose.numel() * 8
         dbuf = {k: torch.empty_like(v, device=dev) for k, v in pin.items()}
         dvg2 = torch.empty_like(pvg, device=dev)
 
@@ -350,15 +474,16 @@ def main():
                                           dbuf["w_prior"], implicit=not dlm, radius=rad)
             gs = solver.backward(P_, dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"], dbuf["w_prior"], dvg2,
                                  D.GRAD_TANGENT, mode=args.backward, epsilon=args.epsilon, radius=rad)
-            gg = torch.cat([g.reshape(-1) for g in gs])
-            if world > 1:
-                dist.all_reduce(gg)
-            out_g.copy_(gg, non_blocking=True)
+            red = reduce_step(gs[0], gs[1], o_, tuple(gs[2:]))
+            out_g.copy_(torch.cat([r.reshape(-1) for r in red]), non_blocking=True)
             out_obj.copy_(o_, non_blocking=True)
+            out_pose.copy_(P_, non_blocking=True)
 
         for _ in range(args.warmup):
             e2e_step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         ts = []
         for _ in range(args.steps):
             if flush is not None:
@@ -375,11 +500,14 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             Te = tt.item()
         e2e = {"value": total_elems * K * args.steps / Te, "unit": UNIT, "h2d_bytes_per_step": int(bi),
-               "d2h_bytes_per_step": int(bo), "ms_per_step": Te / args.steps * 1e3}
+               "d2h_bytes_per_step": int(bo), "ms_per_step": Te / args.steps * 1e3,
+               "note": "pinned host inputs -> device, PoseGraphSolver.forward/backward, all_reduce, "
+                       "theta_K + objective + gradients -> host, every step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.cpu_elements, args.backward, args.epsilon, args.welsch)
+        n_el = args.cpu_elements if args.cpu_elements else (1 if cfg["N"] >= 1024 else 4)
+        cpu = cpu_baseline(cfg, n_el, args.backward, args.epsilon, args.welsch)
 
     if rank == 0:
         line = {
@@ -390,15 +518,22 @@ def main():
                        "poses": cfg["N"], "edges": topo.num_edges, "iterations": K,
                        "optimizer": cfg["opt"], "backward": args.backward,
                        "robust": "none" if args.welsch is None else f"welsch k={args.welsch}",
-                       "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
+                       "l2": ("flushed between timed steps (256 MB write)" if flush is not None else
+                              f"not flushed: the step's working set ({ws_bytes / 2**30:.2f} GiB per GPU) is larger "
+                              f"than L2"),
                        "parallelism": f"dp{world}", "nnz_L": st["nnz_L"], "supernodes": st["num_supernodes"],
-                       "levels": st["num_levels"]},
+                       "levels": st["num_levels"], "symbolic_ms": t_sym * 1e3},
+            "step_ms": {"median": statistics.median(steps_ms), "min": min(steps_ms), "max": max(steps_ms)},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (3 + (0 if args.welsch is None else 1)) * args.steps,   # forward, backward, weight-grad (+ radius) reductions
+            # k_forward, k_backward / k_backward_dlm, k_reduce_wgrad (+ k_reduce_radius) per timed step
+            "gpu_launches": (3 + (0 if args.welsch is None else 1)) * args.steps,
             "clocks": clocks,
         }
+        if world > 1:
+            line["dist"] = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                            "nccl_init": nccl_init_summary() if args.dist_backend == "nccl" else None}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

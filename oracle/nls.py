@@ -278,7 +278,7 @@ def _finish(prob, x, status, iters, hist, lam, opt) -> Result:
         _, H, _ = prob.linearize(x)
         L, ok = linalg.cholesky(H)
         res.H_final, res.L_final = H, (L if ok else None)
-        if not ok and res.status == ST_OK:
+        if not ok:   # a failed final factor takes precedence: the implicit gradient is unavailable
             res.status = ST_NOT_SPD
     return res
 

@@ -145,3 +145,40 @@ def test_two_rank_gloo_shared_radius_and_dlm():
         assert np.max(np.abs(g1 - ge)) <= 1e-12 * np.max(np.abs(ge))
         assert abs(g2[0] - gp[0]) <= 1e-12 * abs(gp[0]) + 1e-300
         assert abs(g3[0] - gr[0]) <= 1e-12 * abs(gr[0]) + 1e-300
+
+
+# ---- bench.py's own step wiring (shard() + reduce_step(), the code the timed step runs), 2 ranks over gloo
+def _bench_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    cfg = dict(bench.CONFIGS["C5"])
+    b0, b1 = bench.shard(cfg, world, rank)
+    cfgw = dict(bench.CONFIGS["C2"])
+    w0, w1 = bench.shard(cfgw, world, rank)
+    poses, ge, gp, loss = shard_compute(*shard_range(GB, world, rank))
+    obj = torch.tensor([loss, 0.0], dtype=torch.float64)   # reduce_step sums the per-element objectives
+    red = bench.reduce_step(torch.from_numpy(ge), torch.from_numpy(gp), obj)
+    out[rank] = ((b0, b1), (w0, w1), [r.numpy().copy() for r in red])
+    dist.destroy_process_group()
+
+
+def test_bench_step_wiring_two_ranks():
+    import bench
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_bench_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    # strong scaling (C5): contiguous halves of the 2048 global elements; weak (C2): 128 per rank
+    assert out[0][0] == (0, 1024) and out[1][0] == (1024, 2048)
+    assert out[0][1] == (0, 128) and out[1][1] == (128, 256)
+    assert bench.shard(dict(bench.CONFIGS["C5"]), 1, 0) == (0, 2048)
+    # the reduced gradients / loss equal the single-rank full-batch values (both ranks hold the same)
+    _, ge1, gp1, l1 = shard_compute(0, GB)
+    for r in range(world):
+        ge, gp, loss = out[r][2]
+        assert np.max(np.abs(ge - ge1)) <= 1e-12 * np.max(np.abs(ge1))
+        assert np.max(np.abs(gp - gp1)) <= 1e-12 * np.max(np.abs(gp1))
+        assert abs(loss[0] - l1) <= 1e-12 * l1
+    assert all(np.array_equal(a, b) for a, b in zip(out[0][2], out[1][2]))
