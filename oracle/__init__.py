@@ -22,4 +22,4 @@ finite differences; Dogleg (nls.dogleg) SPEC hand geometry and GN limit.
 Parity unpinned (self-consistency only): the LM damping schedule constants (our
 choice, SPEC.md:415 values) and the Dogleg radius constants -- see DESIGN.md "Readings".
 """
-from . import lie, costs, linalg, robust, nls, implicit, dlm  # noqa: F401
+from . import lie, costs, linalg, robust, nls, implicit, dlm, unroll  # noqa: F401

@@ -29,7 +29,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import linalg
+from . import costs, linalg
 from .nls import PGOProblem
 
 FD_STEP = 1e-5
@@ -53,16 +53,12 @@ def gn_history(prob: PGOProblem, T0, K: int, alpha: float = 1.0):
     return T, Ts, ds, Ls
 
 
-def _jac_at(prob: PGOProblem, T, kind, k, poses):
-    """Unweighted Jacobian blocks of cost term (kind, k) with its pose(s) replaced by `poses`."""
-    G = prob.G
+def _jac_at(prob: PGOProblem, kind, k, poses):
+    """Unweighted Jacobian blocks of cost term (kind, k) evaluated at the given pose(s)."""
     if kind == "edge":
-        Ti, Tj = poses
-        _, Ci, Cj = G and __import__("oracle.costs", fromlist=["between"]).between(
-            G, Ti[None], Tj[None], prob.Z[k][None])
+        _, Ci, Cj = costs.between(prob.G, poses[0][None], poses[1][None], prob.Z[k][None])
         return [Ci[0], Cj[0]]
-    Tp = poses[0]
-    _, Cp = __import__("oracle.costs", fromlist=["prior"]).prior(G, Tp[None], prob.Zp[k][None])
+    _, Cp = costs.prior(prob.G, poses[0][None], prob.Zp[k][None])
     return [Cp[0]]
 
 
@@ -82,9 +78,7 @@ def unroll_step_vjp(prob: PGOProblem, T, delta, L, v, alpha: float = 1.0, h: flo
     gw = np.zeros(len(prob.w))
     gp = np.zeros(len(prob.wp))
     terms = [("edge", k, (int(i), int(j)), prob.w[k]) for k, (i, j) in enumerate(prob.edges)]
-    if len(prob.prior_vars):
-        cp, _ = prob.prior_terms(T)
-        terms += [("prior", k, (int(p),), prob.wp[k]) for k, p in enumerate(prob.prior_vars)]
+    terms += [("prior", k, (int(p),), prob.wp[k]) for k, p in enumerate(prob.prior_vars)]
     c_e, Ci_e, Cj_e = prob.edge_terms(T)
     if len(prob.prior_vars):
         c_p, C_p = prob.prior_terms(T)
@@ -113,7 +107,7 @@ def unroll_step_vjp(prob: PGOProblem, T, delta, L, v, alpha: float = 1.0, h: flo
                 for sgn in (1.0, -1.0):
                     poses = [T[b] for b in vars_]
                     poses[slot] = poses[slot] @ G.exp((sgn * e)[None])[0]
-                    Cn = _jac_at(prob, T, kind, k, poses)
+                    Cn = _jac_at(prob, kind, k, poses)
                     vals.append(sum(C @ x for C, x in zip(Cn, lam_e)) @ p -
                                 sum(C @ x for C, x in zip(Cn, del_e)) @ q)
                 grad[t] += (vals[0] - vals[1]) / (2.0 * h)
