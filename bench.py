@@ -258,8 +258,11 @@ def main():
     ap.add_argument("--cpu-elements", type=int, default=None)
     ap.add_argument("--flush", choices=["auto", "always", "never"], default="auto",
                     help="flush L2 between timed steps (auto: only when the step's working set is < 2x L2)")
-    ap.add_argument("--backward", default="implicit", choices=["implicit", "dlm"],
-                    help="backward mode timed in the step (dlm: PAPER.md:259-271, one augmented GN step)")
+    ap.add_argument("--backward", default="implicit", choices=["implicit", "dlm", "unroll", "truncated"],
+                    help="backward mode timed in the step (dlm: PAPER.md:259-271, one augmented GN step; "
+                         "unroll / truncated: PAPER.md:235-239, backprop through the recorded GN iterations)")
+    ap.add_argument("--trunc-steps", type=int, default=5, help="truncated backward: iterations differentiated")
+    ap.add_argument("--iters", type=int, default=None, help="override the config's K")
     ap.add_argument("--epsilon", type=float, default=1e-3, help="DLM epsilon")
     ap.add_argument("--optimizer", default=None, choices=["gn", "lm", "dogleg"],
                     help="override the config's inner optimizer (dogleg: PAPER.md:153 trust region)")
@@ -280,6 +283,8 @@ def main():
         cfg["opt"] = args.optimizer
     if args.batch:
         cfg["B"] = args.batch
+    if args.iters is not None:
+        cfg["K"] = args.iters
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         relaunch_distributed(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -327,8 +332,11 @@ def main():
     st = solver.stats
     opt = solver.options
     dlm = args.backward == "dlm"
+    unroll = args.backward in ("unroll", "truncated")
     opt.cluster_ctas = args.cluster
-    opt.backward_mode = D.BWD_NONE if dlm else D.BWD_IMPLICIT
+    opt.backward_mode = {"implicit": D.BWD_IMPLICIT, "dlm": D.BWD_NONE, "unroll": D.BWD_UNROLL,
+                         "truncated": D.BWD_TRUNCATED}[args.backward]
+    opt.backward_steps = args.trunc_steps
     host = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in data.items() if k != "gt"}
     vgrad = torch.from_numpy(np.stack([np.random.default_rng([1, b]).standard_normal((topo.num_poses, d))
                                        for b in range(b0, b1)]))
@@ -341,7 +349,7 @@ def main():
     E, P = topo.num_edges, int(topo.prior_vars.shape[0])
     ge = torch.zeros(E, dtype=torch.float64, device=dev)
     gp = torch.zeros(P, dtype=torch.float64, device=dev)
-    ws = solver.workspace(B)
+    ws = solver.workspace(B, opt)
     rad = None if args.welsch is None else torch.tensor([args.welsch], dtype=torch.float64, device=dev)
     gr = None if rad is None else torch.zeros(1, dtype=torch.float64, device=dev)
     prob = D.make_problem(poses, dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"], obj, sts, its,
@@ -364,6 +372,8 @@ def main():
             record.append((a, b_))
         if dlm:
             D.dnls_backward_dlm(g, B, prob, dvg, D.GRAD_TANGENT, args.epsilon, ge, gp, 0, ws, grad_radius=gr)
+        elif unroll:
+            D.dnls_backward_unroll(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws)
         else:
             D.dnls_backward_implicit(g, B, prob, dvg, D.GRAD_TANGENT, ge, gp, 0, ws, grad_radius=gr)
         reduced[0] = reduce_step(ge, gp, obj, () if gr is None else (gr,))
@@ -410,7 +420,7 @@ def main():
 
     # ---- roofline of the dominant kernel (k_forward): algorithmic bytes per launch / duration
     per_iter = st["bytes_linearize"] + st["bytes_factor"] + st["bytes_solve"] + st["bytes_update"]
-    alg_bytes = B * (K * per_iter + (0 if dlm else st["bytes_linearize"] + st["bytes_factor"]))
+    alg_bytes = B * (K * per_iter + (0 if (dlm or unroll) else st["bytes_linearize"] + st["bytes_factor"]))
     peak, peak_src = load_peaks()
     achieved = alg_bytes / Tf / 1e9
     traffic = None
@@ -426,7 +436,7 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "k_forward", "peak_source": peak_src,
                 "alg_bytes_per_launch": alg_bytes, "kernel_ms": Tf * 1e3,
-                "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)" + ("" if dlm else "+lin+factor") +
+                "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)" + ("" if (dlm or unroll) else "+lin+factor") +
                         ") per SURVEY.md 8(d); traffic = ncu dram read+write of one launch (profiles/ncu_traffic.json)"}
 
     # ---- factor-only roofline (north_star: "the numeric-factorisation kernel"): dnls_factorize on the
@@ -471,9 +481,11 @@ def main():
                 dbuf[k].copy_(pin[k], non_blocking=True)
             dvg2.copy_(pvg, non_blocking=True)
             P_, o_, _, _ = solver.forward(dbuf["poses0"], dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"],
-                                          dbuf["w_prior"], implicit=not dlm, radius=rad)
+                                          dbuf["w_prior"], radius=rad, backward_mode=opt.backward_mode,
+                                          backward_steps=args.trunc_steps)
             gs = solver.backward(P_, dbuf["meas"], dbuf["prior_meas"], dbuf["w_edge"], dbuf["w_prior"], dvg2,
-                                 D.GRAD_TANGENT, mode=args.backward, epsilon=args.epsilon, radius=rad)
+                                 D.GRAD_TANGENT, mode="unroll" if unroll else args.backward, epsilon=args.epsilon,
+                                 radius=rad)
             red = reduce_step(gs[0], gs[1], o_, tuple(gs[2:]))
             out_g.copy_(torch.cat([r.reshape(-1) for r in red]), non_blocking=True)
             out_obj.copy_(o_, non_blocking=True)
@@ -505,7 +517,7 @@ def main():
                        "theta_K + objective + gradients -> host, every step"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not unroll:
         n_el = args.cpu_elements if args.cpu_elements else (1 if cfg["N"] >= 1024 else 4)
         cpu = cpu_baseline(cfg, n_el, args.backward, args.epsilon, args.welsch)
 
@@ -517,6 +529,8 @@ def main():
             "config": {"workload": cfg["desc"], "global_batch": total_elems, "batch_per_gpu": B,
                        "poses": cfg["N"], "edges": topo.num_edges, "iterations": K,
                        "optimizer": cfg["opt"], "backward": args.backward,
+                       "backward_steps": args.trunc_steps if args.backward == "truncated" else None,
+                       "workspace_bytes": int(ws.numel()),
                        "robust": "none" if args.welsch is None else f"welsch k={args.welsch}",
                        "l2": ("flushed between timed steps (256 MB write)" if flush is not None else
                               f"not flushed: the step's working set ({ws_bytes / 2**30:.2f} GiB per GPU) is larger "

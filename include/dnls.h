@@ -65,7 +65,10 @@ typedef enum {
 
 typedef enum { DNLS_SE2 = 3, DNLS_SE3 = 6 } dnls_group;          /* value = tangent dimension d */
 typedef enum { DNLS_GN = 0, DNLS_LM = 1, DNLS_DOGLEG = 2 } dnls_optimizer;
-typedef enum { DNLS_BWD_NONE = 0, DNLS_BWD_IMPLICIT = 1 } dnls_backward;
+/* backward modes (§4.3 :232-271): IMPLICIT keeps the factor of H(theta_K) (Prop. 1); UNROLL /
+ * TRUNCATED keep theta_k, delta_k and the factor of every (of the last backward_steps) GN iteration for
+ * dnls_backward_unroll ("necessary ... for unrolling"). */
+typedef enum { DNLS_BWD_NONE = 0, DNLS_BWD_IMPLICIT = 1, DNLS_BWD_UNROLL = 2, DNLS_BWD_TRUNCATED = 3 } dnls_backward;
 typedef enum { DNLS_DAMP_MARQUARDT = 0, DNLS_DAMP_IDENTITY = 1 } dnls_damping;
 typedef enum { DNLS_GRAD_TANGENT = 0, DNLS_GRAD_MATRIX = 1 } dnls_grad_kind;
 
@@ -105,6 +108,12 @@ typedef struct dnls_options {
   double trust_radius0;
   double trust_radius_max;
   double trust_radius_min;
+  /* DNLS_BWD_TRUNCATED: number T >= 1 of final GN iterations the backward differentiates through
+   * (TBPTT); the workspace keeps min(T, K) iterations.  Ignored by the other modes. */
+  int32_t backward_steps;
+  /* Batch elements processed in lockstep by one CTA of dnls_forward (DESIGN.md "batch-interleaved
+   * path"): 0 = automatic, 1 = one element per CTA.  Larger values are chosen by the library only. */
+  int32_t batch_interleave;
 } dnls_options;
 
 typedef struct dnls_problem {
@@ -194,7 +203,9 @@ DNLS_API dnls_status dnls_graph_supernodes(const dnls_graph* g, int32_t* first, 
                                            int32_t* level);
 
 /* Bytes of device workspace for `batch` elements (factor storage, vectors, per-edge Jacobian
- * scratch, per-element optimiser state).  256-byte aligned base required. */
+ * scratch, per-element optimiser state; with opt->backward_mode UNROLL / TRUNCATED also the per-iteration
+ * history of min(K, T) iterations: poses, steps and factors).  opt may be NULL (no history).
+ * 256-byte aligned base required. */
 DNLS_API dnls_status dnls_workspace_bytes(const dnls_graph* g, int32_t batch, const dnls_options* opt,
                                           size_t* bytes);
 
@@ -246,6 +257,28 @@ DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const
                                        const double* grad_poses, int32_t grad_kind, double epsilon,
                                        double* grad_w_edge, double* grad_w_prior, double* grad_radius,
                                        int64_t grad_bstride, void* workspace, size_t ws_bytes, void* stream);
+
+/* Unroll / Truncated backward (§4.3 :235-239 "unrolled optimization", "truncated
+ * backpropagation through time"; linear-solve gradients :224; reading U1):
+ * the exact reverse-mode chain rule through the GN iterations recorded by the last dnls_forward with
+ * backward_mode DNLS_BWD_UNROLL (every iteration) or DNLS_BWD_TRUNCATED (the last backward_steps) on
+ * this workspace: per iteration k (in reverse), with v = dL/dtheta_{k+1},
+ *   u_m = -alpha Jr(-alpha delta_m)^T v_m,  lambda = H_k^-1 u  (the iteration's cached factor),
+ *   dL/dw_e += 2 w_e (C lambda).(c - C delta),
+ *   dL/dtheta_k = Ad(Exp(alpha delta))^T v + sum_e w_e^2 [C^T C lambda + grad_eta((C lambda).(c - C delta) - (C delta).(C lambda))]
+ * (the gradient of the two contractions of the Jacobian C with fixed vectors by central differences of
+ * the analytic Jacobian, step 1e-5 in the chart: ~1e-10 relative, reading U1).
+ * Gauss-Newton with quadratic costs only (the forward returns DNLS_E_UNSUPPORTED for LM / Dogleg /
+ * a Welsch kernel in these modes).
+ * grad_poses / grad_kind / grad_w_edge / grad_w_prior / grad_bstride as for dnls_backward_implicit.
+ * grad_poses0: out [B][N][d] dL/dtheta_0 in right-tangent coordinates (zero when truncated to fewer
+ *   iterations than were executed), or NULL.
+ * Elements whose forward stopped on a non-SPD system differentiate through the iterations they executed.
+ * Errors: DNLS_E_STATE (no unroll/truncated forward on this workspace/batch), DNLS_E_INVALID, DNLS_E_SHAPE. */
+DNLS_API dnls_status dnls_backward_unroll(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
+                                          const double* grad_poses, int32_t grad_kind, double* grad_w_edge,
+                                          double* grad_w_prior, double* grad_poses0, int64_t grad_bstride,
+                                          void* workspace, size_t ws_bytes, void* stream);
 
 /* ---- stage-level entry points (standalone solvers, "as standalone ... functions";
  *      SPEC.md:400).  They share the workspace layout of dnls_forward. ---- */

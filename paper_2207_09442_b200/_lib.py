@@ -38,6 +38,8 @@ class DnlsOptions(ctypes.Structure):
         ("trust_radius0", ctypes.c_double),
         ("trust_radius_max", ctypes.c_double),
         ("trust_radius_min", ctypes.c_double),
+        ("backward_steps", ctypes.c_int32),
+        ("batch_interleave", ctypes.c_int32),
     ]
 
 
@@ -125,6 +127,10 @@ _SIGS = {
     "dnls_debug_trace": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
     "dnls_export_rhs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "dnls_backward_unroll": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(DnlsProblem),
+                                            ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
+                                            ctypes.c_void_p]),
     "dnls_block_offsets": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p]),
     "dnls_status_summary": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_int32_p, c_int32_p, ctypes.c_void_p]),
 }

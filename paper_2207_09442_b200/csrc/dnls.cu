@@ -64,6 +64,7 @@ struct dnls_graph {
     int batch;
     int kind;   // DNLS_BWD_* of the forward that wrote it
     int K;      // unroll: iterations whose factors are kept
+    double alpha = 1.0;   // unroll: the GN step size of the recorded forward
   };
   std::map<const void*, FactorRecord> cached;
   void drop(const void* ws) {
@@ -106,9 +107,11 @@ struct DeviceGuard {
 // ----------------------------------------------------------------------------- workspace layout
 namespace {
 struct WsLayout {
-  size_t L, x, bsave, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, clred, total;
+  size_t L, x, bsave, jac, cost, rgrad, trial, S, Sprev, lam, maxd, st, it, clred, hT, hd, hL, total;
+  int keep;
 };
-WsLayout ws_layout(const Symbolic& s, int B) {
+// keep > 0: room for the unroll / truncated history of `keep` GN iterations per element
+WsLayout ws_layout(const Symbolic& s, int B, int keep = 0) {
   const int D = s.D, PS = D == 6 ? 12 : 6, JS = D == 6 ? Scr<6>::SIZE : Scr<3>::SIZE;   // GT<D>::JS
   const size_t n = (size_t)s.N * D, slots = (size_t)s.E + s.P;
   WsLayout w{};
@@ -127,8 +130,20 @@ WsLayout ws_layout(const Symbolic& s, int B) {
   w.st = o;    o = align_up(o + sizeof(int) * B);
   w.it = o;    o = align_up(o + sizeof(int) * B);
   w.clred = o; o = align_up(o + sizeof(double) * B * 2 * MAX_CL);
+  w.keep = keep;
+  w.hT = o;    o = align_up(o + sizeof(double) * (size_t)B * keep * s.N * PS);
+  w.hd = o;    o = align_up(o + sizeof(double) * (size_t)B * keep * n);
+  w.hL = o;    o = align_up(o + sizeof(double) * (size_t)B * keep * s.storage);
   w.total = o;
   return w;
+}
+// iterations an unroll / truncated forward records (0 for the other modes)
+int history_keep(const dnls_options* opt) {
+  if (!opt) return 0;
+  if (opt->backward_mode == DNLS_BWD_UNROLL) return std::max(0, (int)opt->max_iterations);
+  if (opt->backward_mode == DNLS_BWD_TRUNCATED)
+    return std::max(0, std::min((int)opt->max_iterations, (int)opt->backward_steps));
+  return 0;
 }
 DevWs ws_views(const WsLayout& l, void* base) {
   char* p = (char*)base;
@@ -147,6 +162,10 @@ DevWs ws_views(const WsLayout& l, void* base) {
   w.st = (int*)(p + l.st);
   w.it = (int*)(p + l.it);
   w.clred = (double*)(p + l.clred);
+  w.keep = l.keep;
+  w.hT = (double*)(p + l.hT);
+  w.hd = (double*)(p + l.hd);
+  w.hL = (double*)(p + l.hL);
   return w;
 }
 DevProb dev_prob(const dnls_problem* p) {
@@ -500,6 +519,17 @@ __global__ void __launch_bounds__(NT, MINB) k_forward(DevGraph g, DevProb pr, De
 #endif
       solve_phase<D, NT, CL>(g, L, sm.stage, x_b, sm.mbar, sm.phase, sm.pp, false);
       DNLS_TRACE_POINT(400);
+      if (CL == 1 && ws.keep > 0) {   // unroll / truncated history: theta_k, delta_k, the factor of H(theta_k)
+        const size_t hs = (size_t)b * ws.keep + (k % ws.keep);
+        double* hT = ws.hT + hs * g.N * PS;
+        for (int i = threadIdx.x; i < g.N * PS; i += NT) hT[i] = Tb[i];
+        double* hd = ws.hd + hs * g.n;
+        for (int i = threadIdx.x; i < g.n; i += NT) hd[i] = x_b[i];
+        double* hL = ws.hL + hs * g.storage;
+        copy_range<NT>(hL, Lg, g.res_lo);
+        copy_range<NT>(hL + g.res_lo, sm.res, g.storage - g.res_lo);
+        __syncthreads();
+      }
       retract_phase<D, NT, CL>(g, Tb, Tb, x_b, fp.alpha);
       gsync<CL>();
       DNLS_TRACE_POINT(500);
@@ -816,6 +846,224 @@ __global__ void __launch_bounds__(NT, MINB) k_backward_dlm(DevGraph g, DevProb p
     cost_b[slot] = gw;
     rg_b[slot] = gr;
   }
+}
+
+// ---------------------------------------------------------------------------- unroll / truncated backward
+// Retraction adjoint of theta_{k+1} = theta_k Exp(-alpha delta) for one pose (oracle/unroll.py):
+//   u = -alpha Jr(-alpha delta)^T v  (dL/d delta),   v <- Ad(Exp(alpha delta))^T v  (direct part).
+__device__ __forceinline__ void retract_adjoint(const double* dl, double alpha, double* v, double* u, dev::SE3*) {
+  using namespace dev;
+  double x[6], y[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) x[a] = -alpha * dl[a];
+  // Jr(x) = [[Jr(w), Q], [0, Jr(w)]] = inverse of Jr^-1(x) = [[Ji, U], [0, Ji]]:  Jr(w) = Ji^-1, Q = -Jr(w) U Jr(w)
+  M3 Ji, U;
+  se3_jr_inv(x, Ji, U);
+  const double th = sqrt(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+  const Coef k = coefs(th);
+  const M3 Jw = poly_hat(1.0, -k.B, k.C, x + 3);   // Jr(w) = Jl(-w) = I - B W + C W^2
+  const M3 Q0 = mul(mul(Jw, U), Jw);
+  // Jr^T v = (Jw^T v_r, -Q0^T v_r + Jw^T v_w)
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    y[a] = Jw.m[0][a] * v[0] + Jw.m[1][a] * v[1] + Jw.m[2][a] * v[2];
+    y[3 + a] = -(Q0.m[0][a] * v[0] + Q0.m[1][a] * v[1] + Q0.m[2][a] * v[2]) +
+               Jw.m[0][a] * v[3] + Jw.m[1][a] * v[4] + Jw.m[2][a] * v[5];
+  }
+#pragma unroll
+  for (int a = 0; a < 6; ++a) u[a] = -alpha * y[a];
+  // Ad(T)^T v with T = Exp(alpha delta) = [R | t]:  (R^T v_r, -R^T (t x v_r) + R^T v_w)
+#pragma unroll
+  for (int a = 0; a < 6; ++a) x[a] = alpha * dl[a];
+  const SE3 T = se3_exp(x);
+  const double tx[3] = {T.t[1] * v[2] - T.t[2] * v[1], T.t[2] * v[0] - T.t[0] * v[2], T.t[0] * v[1] - T.t[1] * v[0]};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    y[a] = T.R[0][a] * v[0] + T.R[1][a] * v[1] + T.R[2][a] * v[2];
+    y[3 + a] = -(T.R[0][a] * tx[0] + T.R[1][a] * tx[1] + T.R[2][a] * tx[2]) +
+               T.R[0][a] * v[3] + T.R[1][a] * v[4] + T.R[2][a] * v[5];
+  }
+#pragma unroll
+  for (int a = 0; a < 6; ++a) v[a] = y[a];
+}
+__device__ __forceinline__ void retract_adjoint(const double* dl, double alpha, double* v, double* u, dev::SE2*) {
+  using namespace dev;
+  // Jr(x) = [[A, wB, wC r1 - B r2], [-wB, A, B r1 + wC r2], [0, 0, 1]] at x = -alpha delta
+  const double r1 = -alpha * dl[0], r2 = -alpha * dl[1], w = -alpha * dl[2];
+  const Coef k = coefs(fabs(w));
+  const double a = k.A, bb = w * k.B, v0 = w * k.C * r1 - k.B * r2, v1 = k.B * r1 + w * k.C * r2;
+  u[0] = -alpha * (a * v[0] - bb * v[1]);
+  u[1] = -alpha * (bb * v[0] + a * v[1]);
+  u[2] = -alpha * (v0 * v[0] + v1 * v[1] + v[2]);
+  // Ad(T)^T v, T = Exp(alpha delta) = [R | t], Ad = [[R, (t_y, -t_x)^T], [0, 1]]
+  double x[3] = {alpha * dl[0], alpha * dl[1], alpha * dl[2]};
+  const SE2 T = se2_exp(x);
+  const double y0 = T.R[0][0] * v[0] + T.R[1][0] * v[1], y1 = T.R[0][1] * v[0] + T.R[1][1] * v[1];
+  const double y2 = T.t[1] * v[0] - T.t[0] * v[1] + v[2];
+  v[0] = y0;
+  v[1] = y1;
+  v[2] = y2;
+}
+__device__ __forceinline__ dev::SE3 pose_retract(const dev::SE3& T, const double* e) { return dev::se3_mul(T, dev::se3_exp(e)); }
+__device__ __forceinline__ dev::SE2 pose_retract(const dev::SE2& T, const double* e) { return dev::se2_mul(T, dev::se2_exp(e)); }
+
+// (C(theta) lam).p - (C(theta) del).q of one cost term at the given poses (reading U1's contraction)
+template <int D, class PT>
+__device__ __forceinline__ double jac_contract(bool edge, const PT& Ti, const PT& Tj, const PT& Z, const double* li,
+                                               const double* lj, const double* di, const double* dj, const double* p,
+                                               const double* q) {
+  double c[D], Ci[D * D], Cj[D * D];
+  if (edge) edge_eval(Ti, Tj, Z, c, Ci, Cj, true);
+  else prior_eval(Ti, Z, c, Ci, true);
+  double v = 0.0;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    double cl = 0.0, cd = 0.0;
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+      cl = fma(Ci[r * D + t], li[t], cl);
+      cd = fma(Ci[r * D + t], di[t], cd);
+      if (edge) {
+        cl = fma(Cj[r * D + t], lj[t], cl);
+        cd = fma(Cj[r * D + t], dj[t], cd);
+      }
+    }
+    v += cl * p[r] - cd * q[r];
+  }
+  return v;
+}
+
+constexpr double UNROLL_FD_STEP = 1e-5;   // reading U1 (oracle/unroll.py FD_STEP)
+
+// Unroll / Truncated backward, one CTA per element (oracle/unroll.py, dnls.h dnls_backward_unroll):
+// reverse the recorded GN iterations k = it-1 .. it-Tw.  v (original pose order) lives in ws.bsave, the
+// per-slot weight gradients accumulate in ws.cost, the per-slot pose-gradient contributions go to the slot
+// scratch and are gathered per pose in the fixed order of the symbolic list bc (deterministic).
+template <int D>
+__global__ void __launch_bounds__(NT, MINB) k_backward_unroll(DevGraph g, DevProb pr, DevWs ws, const double* gpose,
+                                                            int grad_kind, int Tw, double alpha, double* gpose0) {
+  constexpr int PS = GT<D>::PS, JS = GT<D>::JS;
+  using PT = typename PoseT<D>::T;
+  const int b = blockIdx.x;
+  const size_t slots = (size_t)g.E + g.P;
+  Smem sm = smem_views(g, ws.x + (size_t)b * g.n);
+  double* x_b = sm.x;
+  double* v = ws.bsave + (size_t)b * g.n;
+  double* gw = ws.cost + (size_t)b * slots;
+  double* pg = ws.jac + (size_t)b * slots * JS;
+  const double* TK = pr.poses + (size_t)b * g.N * PS;
+  const int iters = ws.it[b];
+  for (int o = threadIdx.x; o < g.N; o += NT) {
+    double vv[D];
+    tangent_grad<D>(TK, gpose, grad_kind, b, g.N, o, vv);
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[(size_t)o * D + a] = vv[a];
+  }
+  for (int sl = threadIdx.x; sl < (int)slots; sl += NT) gw[sl] = 0.0;
+  __syncthreads();
+  const int kend = max(0, iters - Tw);
+  for (int k = iters - 1; k >= kend; --k) {
+    const size_t hs = (size_t)b * ws.keep + (k % ws.keep);
+    const double* Tk = ws.hT + hs * g.N * PS;
+    const double* dk = ws.hd + hs * g.n;
+    double* Lk = ws.hL + hs * g.storage;
+    // (a) retraction adjoint: rhs u (permuted order) and the direct part of v
+    for (int o = threadIdx.x; o < g.N; o += NT) {
+      const int pp = g.iperm[o];
+      double u[D];
+      retract_adjoint(dk + (size_t)D * pp, alpha, v + (size_t)o * D, u, (PT*)nullptr);
+#pragma unroll
+      for (int a = 0; a < D; ++a) x_b[(size_t)D * pp + a] = u[a];
+    }
+    // (b) lambda = H_k^-1 u on the iteration's cached factor
+    bulk_load<NT>(sm.res, Lk + g.res_lo, g.storage - g.res_lo, sm.mbar, sm.phase);
+    solve_phase<D, NT>(g, full_view(g, Lk, sm), sm.stage, x_b, sm.mbar, sm.phase, sm.pp);
+    __syncthreads();
+    // (c) per cost term: weight gradient and the pose-gradient contributions
+    for (int slot = threadIdx.x; slot < (int)slots; slot += NT) {
+      const bool edge = slot < g.E;
+      const int vi = edge ? g.edges[2 * slot] : g.prior_vars[slot - g.E];
+      const int vj = edge ? g.edges[2 * slot + 1] : vi;
+      const double* li = x_b + (size_t)D * g.iperm[vi];
+      const double* lj = x_b + (size_t)D * g.iperm[vj];
+      const double* di = dk + (size_t)D * g.iperm[vi];
+      const double* dj = dk + (size_t)D * g.iperm[vj];
+      double c[D], Ci[D * D], Cj[D * D];
+      eval_slot<D>(g, pr, Tk, b, slot, c, Ci, Cj, true);
+      const double w = slot_weight<D>(g, pr, b, slot);
+      double q[D], p[D], qc = 0.0, qd = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double cl = 0.0, cd = 0.0;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+          cl = fma(Ci[r * D + t], li[t], cl);
+          cd = fma(Ci[r * D + t], di[t], cd);
+          if (edge) {
+            cl = fma(Cj[r * D + t], lj[t], cl);
+            cd = fma(Cj[r * D + t], dj[t], cd);
+          }
+        }
+        q[r] = cl;
+        p[r] = c[r] - cd;
+        qc = fma(cl, c[r], qc);
+        qd = fma(cl, cd, qd);
+      }
+      gw[slot] += 2.0 * w * (qc - qd);
+      // w^2 [C_s^T q + grad_eta contraction] for each endpoint s
+      const PT Ti = PoseT<D>::load(Tk + (size_t)vi * PS);
+      const PT Tj = PoseT<D>::load(Tk + (size_t)vj * PS);
+      const PT Z = edge ? PoseT<D>::load(pr.meas + ((size_t)b * g.E + slot) * PS)
+                        : PoseT<D>::load(pr.prior_meas + (size_t)b * pr.pm_bstride + (size_t)(slot - g.E) * PS);
+      for (int side = 0; side < (edge ? 2 : 1); ++side) {
+        const double* Cs = side == 0 ? Ci : Cj;
+        double gr[D];
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+          double a = 0.0;
+#pragma unroll
+          for (int r = 0; r < D; ++r) a = fma(Cs[r * D + t], q[r], a);
+          gr[t] = a;
+        }
+        for (int t = 0; t < D; ++t) {
+          double e[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) e[a] = a == t ? UNROLL_FD_STEP : 0.0;
+          const PT Tp = pose_retract(side == 0 ? Ti : Tj, e);
+#pragma unroll
+          for (int a = 0; a < D; ++a) e[a] = -e[a];
+          const PT Tm = pose_retract(side == 0 ? Ti : Tj, e);
+          const double fp_ = side == 0 ? jac_contract<D>(edge, Tp, Tj, Z, li, lj, di, dj, p, q)
+                                       : jac_contract<D>(edge, Ti, Tp, Z, li, lj, di, dj, p, q);
+          const double fm_ = side == 0 ? jac_contract<D>(edge, Tm, Tj, Z, li, lj, di, dj, p, q)
+                                       : jac_contract<D>(edge, Ti, Tm, Z, li, lj, di, dj, p, q);
+          gr[t] += (fp_ - fm_) / (2.0 * UNROLL_FD_STEP);
+        }
+        double* o = pg + (size_t)slot * JS + side * 8;
+#pragma unroll
+        for (int t = 0; t < D; ++t) o[t] = w * w * gr[t];
+      }
+    }
+    __syncthreads();
+    // (d) v_o += sum of its slots' contributions (fixed order of bc)
+    for (int pp = threadIdx.x; pp < g.N; pp += NT) {
+      double acc[D];
+      const int o = g.perm[pp];
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc[a] = v[(size_t)o * D + a];
+      for (int cidx = g.bc_ptr[pp]; cidx < g.bc_ptr[pp + 1]; ++cidx) {
+        const int code = g.bc[cidx];
+        const double* src = pg + (size_t)(code >> 1) * JS + (code & 1) * 8;
+#pragma unroll
+        for (int a = 0; a < D; ++a) acc[a] += src[a];
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) v[(size_t)o * D + a] = acc[a];
+    }
+    __syncthreads();
+  }
+  if (gpose0)
+    for (int i = threadIdx.x; i < g.n; i += NT) gpose0[(size_t)b * g.n + i] = kend == 0 ? v[i] : 0.0;
 }
 
 // radius gradient: per element the fixed-order sum over edge slots, then, for a shared radius
@@ -1283,21 +1531,21 @@ DNLS_API dnls_status dnls_graph_supernodes(const dnls_graph* g, int32_t* first, 
 
 DNLS_API dnls_status dnls_workspace_bytes(const dnls_graph* g, int32_t batch, const dnls_options* opt,
                                           size_t* bytes) {
-  (void)opt;
   if (!g || !bytes) return fail(DNLS_E_INVALID, "dnls_workspace_bytes: NULL argument");
   if (batch < 0) return fail(DNLS_E_SHAPE, "dnls_workspace_bytes: batch < 0");
-  *bytes = ws_layout(g->sym, batch).total;
+  *bytes = ws_layout(g->sym, batch, history_keep(opt)).total;
   return DNLS_OK;
 }
 
 namespace {
-dnls_status check_common(const char* fn, const dnls_graph* g, int32_t batch, const void* ws, size_t ws_bytes) {
+dnls_status check_common(const char* fn, const dnls_graph* g, int32_t batch, const void* ws, size_t ws_bytes,
+                         int keep = 0) {
   if (!g) return fail(DNLS_E_INVALID, std::string(fn) + ": graph is NULL");
   if (!g->dbuf) return fail(DNLS_E_INVALID, std::string(fn) + ": graph was created host-only (device < 0)");
   if (batch < 0) return fail(DNLS_E_SHAPE, std::string(fn) + ": batch < 0");
   if (!ws && batch > 0) return fail(DNLS_E_INVALID, std::string(fn) + ": workspace is NULL");
   if (((uintptr_t)ws) % 256) return fail(DNLS_E_INVALID, std::string(fn) + ": workspace not 256-byte aligned");
-  size_t need = ws_layout(g->sym, batch).total;
+  size_t need = ws_layout(g->sym, batch, keep).total;
   if (ws_bytes < need)
     return fail(DNLS_E_WORKSPACE, std::string(fn) + ": workspace has " + std::to_string(ws_bytes) +
                                       " bytes, needs " + std::to_string(need));
@@ -1327,18 +1575,24 @@ dnls_status check_problem(const char* fn, const dnls_graph* g, const dnls_proble
 
 DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls_options* opt,
                                   const dnls_problem* prob, void* workspace, size_t ws_bytes, void* stream) {
-  dnls_status st = check_common("dnls_forward", g, batch, workspace, ws_bytes);
-  if (st) return st;
   if (!opt) return fail(DNLS_E_INVALID, "dnls_forward: options is NULL");
+  const int keep = history_keep(opt);
+  dnls_status st = check_common("dnls_forward", g, batch, workspace, ws_bytes, keep);
+  if (st) return st;
   if ((st = check_problem("dnls_forward", g, prob))) return st;
   if (opt->optimizer != DNLS_GN && opt->optimizer != DNLS_LM && opt->optimizer != DNLS_DOGLEG)
     return fail(DNLS_E_INVALID, "dnls_forward: unknown optimizer " + std::to_string(opt->optimizer));
   if (opt->max_iterations < 0) return fail(DNLS_E_INVALID, "dnls_forward: max_iterations < 0");
   if (!(opt->step_size > 0.0 && opt->step_size <= 1.0))
     return fail(DNLS_E_INVALID, "dnls_forward: step_size must be in (0, 1]");
-  if (opt->backward_mode != DNLS_BWD_NONE && opt->backward_mode != DNLS_BWD_IMPLICIT)
-    return fail(DNLS_E_UNSUPPORTED, "dnls_forward: backward_mode " + std::to_string(opt->backward_mode) +
-                                        " not supported (NONE or IMPLICIT)");
+  if (opt->backward_mode < DNLS_BWD_NONE || opt->backward_mode > DNLS_BWD_TRUNCATED)
+    return fail(DNLS_E_INVALID, "dnls_forward: unknown backward_mode " + std::to_string(opt->backward_mode));
+  const bool unroll = opt->backward_mode == DNLS_BWD_UNROLL || opt->backward_mode == DNLS_BWD_TRUNCATED;
+  if (unroll && (opt->optimizer != DNLS_GN || prob->radius != nullptr))
+    return fail(DNLS_E_UNSUPPORTED, "dnls_forward: UNROLL / TRUNCATED backward modes support Gauss-Newton with "
+                                    "quadratic costs only");
+  if (opt->backward_mode == DNLS_BWD_TRUNCATED && opt->backward_steps < 1)
+    return fail(DNLS_E_INVALID, "dnls_forward: TRUNCATED needs backward_steps >= 1");
   if (opt->optimizer == DNLS_LM &&
       !(opt->lambda0 > 0 && opt->lambda_min > 0 && opt->lambda_max >= opt->lambda_min && opt->lambda_down > 1 &&
         opt->lambda_up > 1))
@@ -1355,7 +1609,7 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   if (batch == 0) return DNLS_OK;
   DeviceGuard dguard(g->device);
   if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_forward: cannot select the graph's device");
-  WsLayout l = ws_layout(g->sym, batch);
+  WsLayout l = ws_layout(g->sym, batch, keep);
   DevWs ws = ws_views(l, workspace);
   FwdParams fp;
   fp.K = opt->max_iterations;
@@ -1379,7 +1633,7 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   fp.status = prob->status;
   fp.iterations = prob->iterations;
   cudaStream_t s = (cudaStream_t)stream;
-  const int cl = opt->optimizer == DNLS_DOGLEG ? 1 : forward_cluster(g, batch, opt->cluster_ctas);
+  const int cl = (opt->optimizer == DNLS_DOGLEG || unroll) ? 1 : forward_cluster(g, batch, opt->cluster_ctas);
   if (cl == 1) {
     DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD, 1>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD, 1><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
   } else if (launch_forward_cluster(cl, g->sym.D, g->dg, dev_prob(prob), ws, fp, batch, s) != cudaSuccess) {
@@ -1387,6 +1641,7 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   }
   if ((st = cuda_check("dnls_forward: k_forward launch"))) return st;
   if (fp.implicit) gm->keep(workspace, dnls_graph::FactorRecord{batch, DNLS_BWD_IMPLICIT, 0});
+  if (unroll && keep > 0) gm->keep(workspace, dnls_graph::FactorRecord{batch, opt->backward_mode, keep, opt->step_size});
   return DNLS_OK;
 }
 
@@ -1465,6 +1720,45 @@ DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const
   if (grad_radius && prob->radius) {
     k_reduce_radius<<<1, 32, 0, s>>>(batch, g->sym.E, slots, ws.rgrad, grad_radius, (long long)prob->radius_bstride);
     if ((st = cuda_check("dnls_backward_dlm: k_reduce_radius launch"))) return st;
+  }
+  return DNLS_OK;
+}
+
+DNLS_API dnls_status dnls_backward_unroll(const dnls_graph* g, int32_t batch, const dnls_problem* prob,
+                                          const double* grad_poses, int32_t grad_kind, double* grad_w_edge,
+                                          double* grad_w_prior, double* grad_poses0, int64_t grad_bstride,
+                                          void* workspace, size_t ws_bytes, void* stream) {
+  if (!g) return fail(DNLS_E_INVALID, "dnls_backward_unroll: graph is NULL");
+  dnls_graph::FactorRecord rec{};
+  if (!const_cast<dnls_graph*>(g)->get(workspace, rec) || rec.batch != batch ||
+      (rec.kind != DNLS_BWD_UNROLL && rec.kind != DNLS_BWD_TRUNCATED))
+    return fail(DNLS_E_STATE, "dnls_backward_unroll: no unroll/truncated dnls_forward on this workspace/batch "
+                              "(history missing or overwritten)");
+  dnls_status st = check_common("dnls_backward_unroll", g, batch, workspace, ws_bytes, rec.K);
+  if (st) return st;
+  if ((st = check_problem("dnls_backward_unroll", g, prob))) return st;
+  if (!grad_poses && batch > 0) return fail(DNLS_E_INVALID, "dnls_backward_unroll: grad_poses is NULL");
+  if (grad_kind != DNLS_GRAD_TANGENT && grad_kind != DNLS_GRAD_MATRIX)
+    return fail(DNLS_E_INVALID, "dnls_backward_unroll: unknown grad_kind");
+  if (grad_bstride < 0) return fail(DNLS_E_INVALID, "dnls_backward_unroll: grad_bstride < 0");
+  if (grad_bstride > 0 && grad_bstride < std::max(g->sym.E, g->sym.P))
+    return fail(DNLS_E_SHAPE, "dnls_backward_unroll: grad_bstride smaller than num_edges/num_priors");
+  if (batch == 0) return DNLS_OK;
+  DeviceGuard dguard(g->device);
+  if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_backward_unroll: cannot select the graph's device");
+  DevWs ws = ws_views(ws_layout(g->sym, batch, rec.K), workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  // UNROLL differentiates every recorded iteration; TRUNCATED the last rec.K (= min(T, K)) of them
+  const int Tw = rec.K;
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward_unroll<DD>, smem_bytes(g->dg), "k_backward_unroll"))) return st;
+             (k_backward_unroll<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses,
+                                                                         grad_kind, Tw, rec.alpha, grad_poses0)));
+  if ((st = cuda_check("dnls_backward_unroll: k_backward_unroll launch"))) return st;
+  const int slots = g->sym.E + g->sym.P;
+  if (slots > 0 && (grad_w_edge || grad_w_prior)) {
+    k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
+                                                        grad_w_prior, (long long)grad_bstride);
+    if ((st = cuda_check("dnls_backward_unroll: k_reduce_wgrad launch"))) return st;
   }
   return DNLS_OK;
 }

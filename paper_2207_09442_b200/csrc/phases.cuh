@@ -141,6 +141,12 @@ struct DevWs {
   double* maxd;   // [B] max diagonal of the matrix last assembled/imported
   int* st;        // [B] status
   int* it;        // [B] iterations
+  // unroll / truncated history (backward_mode UNROLL / TRUNCATED), `keep` iterations per element in a
+  // ring (iteration k in slot k % keep), element-major:
+  int keep;
+  double* hT;     // [B][keep][N][PS]   theta_k
+  double* hd;     // [B][keep][n]       delta_k (permuted order)
+  double* hL;     // [B][keep][storage] the factor of H(theta_k)
 };
 
 __host__ __device__ constexpr int pad4(int x) { return (x + 3) & ~3; }
@@ -237,107 +243,118 @@ __device__ __forceinline__ void bulk_load(double* dst, const double* src, int nd
 }
 
 // ============================================================================= cost evaluation
+// Unweighted cost c and Jacobians of a Between edge / prior from poses held in registers
+// (SURVEY.md §8(a) a1): c = Log(Z^-1 T_i^-1 T_j), C_j = Jr^-1(c), C_i = -Jr^-1(c) Ad(T_j^-1 T_i);
+// prior c = Log(Z^-1 T), C = Jr^-1(c).  Ci/Cj row-major D x D.
+__device__ __forceinline__ void edge_eval(const dev::SE3& Ti, const dev::SE3& Tj, const dev::SE3& Z, double* c,
+                                          double* Ci, double* Cj, bool need_jac) {
+  using namespace dev;
+  SE3 X = se3_between(Ti, Tj);
+  se3_log(se3_between(Z, X), c);
+  if (!need_jac) return;
+  M3 Ji, U;
+  se3_jr_inv(c, Ji, U);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      Cj[r * 6 + q] = Ji.m[r][q];
+      Cj[r * 6 + q + 3] = U.m[r][q];
+      Cj[(r + 3) * 6 + q] = 0.0;
+      Cj[(r + 3) * 6 + q + 3] = Ji.m[r][q];
+    }
+  // Ci = -Jr^-1(c) Ad(Tj^-1 Ti),  Ad(M) = [[R, t^ R], [0, R]]
+  SE3 M = se3_between(Tj, Ti);
+  M3 R, tR;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) R.m[r][q] = M.R[r][q];
+  tR = mul(hat(M.t), R);
+  M3 JR = mul(Ji, R);
+  M3 JtR = mul(Ji, tR);
+  M3 UR = mul(U, R);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      Ci[r * 6 + q] = -JR.m[r][q];
+      Ci[r * 6 + q + 3] = -(JtR.m[r][q] + UR.m[r][q]);
+      Ci[(r + 3) * 6 + q] = 0.0;
+      Ci[(r + 3) * 6 + q + 3] = -JR.m[r][q];
+    }
+}
+__device__ __forceinline__ void prior_eval(const dev::SE3& T, const dev::SE3& Z, double* c, double* C, bool need_jac) {
+  using namespace dev;
+  se3_log(se3_between(Z, T), c);
+  if (!need_jac) return;
+  M3 Ji, U;
+  se3_jr_inv(c, Ji, U);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      C[r * 6 + q] = Ji.m[r][q];
+      C[r * 6 + q + 3] = U.m[r][q];
+      C[(r + 3) * 6 + q] = 0.0;
+      C[(r + 3) * 6 + q + 3] = Ji.m[r][q];
+    }
+}
+__device__ __forceinline__ void edge_eval(const dev::SE2& Ti, const dev::SE2& Tj, const dev::SE2& Z, double* c,
+                                          double* Ci, double* Cj, bool need_jac) {
+  using namespace dev;
+  se2_log(se2_between(Z, se2_between(Ti, Tj)), c);
+  if (!need_jac) return;
+  double J[3][3];
+  se2_jr_inv(c, J);
+  SE2 M = se2_between(Tj, Ti);
+  // Ad(M) = [[R, (t_y, -t_x)^T], [0, 1]]
+  double Ad[3][3] = {{M.R[0][0], M.R[0][1], M.t[1]}, {M.R[1][0], M.R[1][1], -M.t[0]}, {0.0, 0.0, 1.0}};
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      Cj[r * 3 + q] = J[r][q];
+      Ci[r * 3 + q] = -(J[r][0] * Ad[0][q] + J[r][1] * Ad[1][q] + J[r][2] * Ad[2][q]);
+    }
+}
+__device__ __forceinline__ void prior_eval(const dev::SE2& T, const dev::SE2& Z, double* c, double* C, bool need_jac) {
+  using namespace dev;
+  se2_log(se2_between(Z, T), c);
+  if (!need_jac) return;
+  double J[3][3];
+  se2_jr_inv(c, J);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) C[r * 3 + q] = J[r][q];
+}
+template <int D>
+struct PoseT {
+  using T = dev::SE3;
+  static __device__ __forceinline__ T load(const double* p) { return dev::se3_load(p); }
+};
+template <>
+struct PoseT<3> {
+  using T = dev::SE2;
+  static __device__ __forceinline__ T load(const double* p) { return dev::se2_load(p); }
+};
+
 // Unweighted cost c and Jacobians of slot `slot` (edge e < E, else prior slot - E) at poses Tb.
 // Ci/Cj are row-major D x D.  For priors only Ci is written.
 template <int D>
 __device__ __forceinline__ void eval_slot(const DevGraph& g, const DevProb& pr, const double* Tb, int b,
                                           int slot, double* c, double* Ci, double* Cj, bool need_jac) {
   constexpr int PS = GT<D>::PS;
-  using namespace dev;
-  if (D == 6) {
-    SE3 Eerr;
-    if (slot < g.E) {
-      const int i = g.edges[2 * slot], j = g.edges[2 * slot + 1];
-      SE3 Ti = se3_load(Tb + (size_t)i * PS), Tj = se3_load(Tb + (size_t)j * PS);
-      SE3 Z = se3_load(pr.meas + ((size_t)b * g.E + slot) * PS);
-      SE3 X = se3_between(Ti, Tj);
-      Eerr = se3_between(Z, X);
-      se3_log(Eerr, c);
-      if (!need_jac) return;
-      M3 Ji, U;
-      se3_jr_inv(c, Ji, U);
-      // Cj = Jr^-1(c) = [[Ji, U], [0, Ji]]
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          Cj[r * 6 + q] = Ji.m[r][q];
-          Cj[r * 6 + q + 3] = U.m[r][q];
-          Cj[(r + 3) * 6 + q] = 0.0;
-          Cj[(r + 3) * 6 + q + 3] = Ji.m[r][q];
-        }
-      // Ci = -Jr^-1(c) Ad(Tj^-1 Ti),  Ad(M) = [[R, t^ R], [0, R]]
-      SE3 M = se3_between(Tj, Ti);
-      M3 R, tR;
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) R.m[r][q] = M.R[r][q];
-      tR = mul(hat(M.t), R);
-      M3 JR = mul(Ji, R);
-      M3 JtR = mul(Ji, tR);
-      M3 UR = mul(U, R);
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          Ci[r * 6 + q] = -JR.m[r][q];
-          Ci[r * 6 + q + 3] = -(JtR.m[r][q] + UR.m[r][q]);
-          Ci[(r + 3) * 6 + q] = 0.0;
-          Ci[(r + 3) * 6 + q + 3] = -JR.m[r][q];
-        }
-    } else {
-      const int k = slot - g.E;
-      SE3 T = se3_load(Tb + (size_t)g.prior_vars[k] * PS);
-      SE3 Z = se3_load(pr.prior_meas + (size_t)b * pr.pm_bstride + (size_t)k * PS);
-      Eerr = se3_between(Z, T);
-      se3_log(Eerr, c);
-      if (!need_jac) return;
-      M3 Ji, U;
-      se3_jr_inv(c, Ji, U);
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          Ci[r * 6 + q] = Ji.m[r][q];
-          Ci[r * 6 + q + 3] = U.m[r][q];
-          Ci[(r + 3) * 6 + q] = 0.0;
-          Ci[(r + 3) * 6 + q + 3] = Ji.m[r][q];
-        }
-    }
+  using P = PoseT<D>;
+  if (slot < g.E) {
+    const int i = g.edges[2 * slot], j = g.edges[2 * slot + 1];
+    edge_eval(P::load(Tb + (size_t)i * PS), P::load(Tb + (size_t)j * PS),
+              P::load(pr.meas + ((size_t)b * g.E + slot) * PS), c, Ci, Cj, need_jac);
   } else {
-    if (slot < g.E) {
-      const int i = g.edges[2 * slot], j = g.edges[2 * slot + 1];
-      SE2 Ti = se2_load(Tb + (size_t)i * PS), Tj = se2_load(Tb + (size_t)j * PS);
-      SE2 Z = se2_load(pr.meas + ((size_t)b * g.E + slot) * PS);
-      SE2 Eerr = se2_between(Z, se2_between(Ti, Tj));
-      se2_log(Eerr, c);
-      if (!need_jac) return;
-      double J[3][3];
-      se2_jr_inv(c, J);
-      SE2 M = se2_between(Tj, Ti);
-      // Ad(M) = [[R, (t_y, -t_x)^T], [0, 1]]
-      double Ad[3][3] = {{M.R[0][0], M.R[0][1], M.t[1]}, {M.R[1][0], M.R[1][1], -M.t[0]}, {0.0, 0.0, 1.0}};
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          Cj[r * 3 + q] = J[r][q];
-          Ci[r * 3 + q] = -(J[r][0] * Ad[0][q] + J[r][1] * Ad[1][q] + J[r][2] * Ad[2][q]);
-        }
-    } else {
-      const int k = slot - g.E;
-      SE2 T = se2_load(Tb + (size_t)g.prior_vars[k] * PS);
-      SE2 Z = se2_load(pr.prior_meas + (size_t)b * pr.pm_bstride + (size_t)k * PS);
-      se2_log(se2_between(Z, T), c);
-      if (!need_jac) return;
-      double J[3][3];
-      se2_jr_inv(c, J);
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) Ci[r * 3 + q] = J[r][q];
-    }
+    const int k = slot - g.E;
+    prior_eval(P::load(Tb + (size_t)g.prior_vars[k] * PS),
+               P::load(pr.prior_meas + (size_t)b * pr.pm_bstride + (size_t)k * PS), c, Ci, need_jac);
   }
 }
 

@@ -16,7 +16,7 @@ from ._lib import DnlsOptions, DnlsProblem, DnlsStats, check, lib
 
 SE2, SE3 = 3, 6
 GN, LM, DOGLEG = 0, 1, 2
-BWD_NONE, BWD_IMPLICIT = 0, 1
+BWD_NONE, BWD_IMPLICIT, BWD_UNROLL, BWD_TRUNCATED = 0, 1, 2, 3
 DAMP_MARQUARDT, DAMP_IDENTITY = 0, 1
 GRAD_TANGENT, GRAD_MATRIX = 0, 1
 ST_OK, ST_CONVERGED, ST_NOT_SPD, ST_SATURATED = 0, 1, 2, 3
@@ -219,6 +219,16 @@ def dnls_backward_dlm(g: Graph, batch: int, prob: DnlsProblem, grad_poses: torch
                                   _f64(grad_w_prior, "grad_w_prior"), _f64(grad_radius, "grad_radius"),
                                   int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream, g.device)),
           "dnls_backward_dlm")
+
+
+def dnls_backward_unroll(g: Graph, batch: int, prob: DnlsProblem, grad_poses: torch.Tensor, grad_kind: int,
+                         grad_w_edge, grad_w_prior, grad_bstride: int, workspace: torch.Tensor, stream=None,
+                         grad_poses0=None):
+    check(lib().dnls_backward_unroll(g.handle, int(batch), ctypes.byref(prob), _f64(grad_poses, "grad_poses"),
+                                     int(grad_kind), _f64(grad_w_edge, "grad_w_edge"),
+                                     _f64(grad_w_prior, "grad_w_prior"), _f64(grad_poses0, "grad_poses0"),
+                                     int(grad_bstride), _ptr(workspace), workspace.numel(), _stream(stream, g.device)),
+          "dnls_backward_unroll")
 
 
 def dnls_linearize(g: Graph, batch: int, prob: DnlsProblem, lam, damping: int, workspace: torch.Tensor, stream=None):

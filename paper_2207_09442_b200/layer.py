@@ -31,23 +31,30 @@ class PoseGraphSolver:
     def group(self):
         return self.graph.group
 
-    def workspace(self, batch: int) -> torch.Tensor:
-        if self._ws is None or self._ws_batch != batch:
-            self._ws = D.alloc_workspace(self.graph, batch, self.options, self.device)
+    def workspace(self, batch: int, opt=None) -> torch.Tensor:
+        nbytes = D.dnls_workspace_bytes(self.graph, batch, opt if opt is not None else self.options)
+        if self._ws is None or self._ws_batch != batch or self._ws.numel() < nbytes:
+            self._ws = D.alloc_workspace(self.graph, batch, opt if opt is not None else self.options, self.device)
             self._ws_batch = batch
         return self._ws
 
-    def forward(self, poses, meas, prior_meas, w_edge, w_prior, implicit: bool = False, options=None, radius=None):
+    def forward(self, poses, meas, prior_meas, w_edge, w_prior, implicit: bool = False, options=None, radius=None,
+                backward_mode=None, backward_steps: int = 0):
         """Solve in place on a copy of ``poses``.  Returns (poses_K, objective, status, iterations).
-        radius: Welsch radius tensor ([1] or [B]) of the Between edges, or None (quadratic costs)."""
+        radius: Welsch radius tensor ([1] or [B]) of the Between edges, or None (quadratic costs).
+        backward_mode: D.BWD_* (overrides ``implicit``); UNROLL / TRUNCATED record the per-iteration history
+        (TRUNCATED: the last ``backward_steps`` iterations) for ``backward(mode="unroll")``."""
         opt = options if options is not None else self.options
-        opt.backward_mode = D.BWD_IMPLICIT if implicit else D.BWD_NONE
+        if backward_mode is None:
+            backward_mode = D.BWD_IMPLICIT if implicit else D.BWD_NONE
+        opt.backward_mode = backward_mode
+        opt.backward_steps = int(backward_steps)
         B = poses.shape[0]
         out = poses.detach().clone().contiguous()
         obj = torch.empty(B, dtype=torch.float64, device=poses.device)
         st = torch.empty(B, dtype=torch.int32, device=poses.device)
         it = torch.empty(B, dtype=torch.int32, device=poses.device)
-        ws = self.workspace(B)
+        ws = self.workspace(B, opt)
         prob = D.make_problem(out, meas.contiguous(), prior_meas.contiguous(), w_edge.detach().contiguous(),
                               w_prior.detach().contiguous(), obj, st, it,
                               radius=None if radius is None else radius.detach().contiguous())
@@ -56,7 +63,8 @@ class PoseGraphSolver:
         return out, obj, st, it
 
     def backward(self, poses_K, meas, prior_meas, w_edge, w_prior, grad_poses, grad_kind=D.GRAD_MATRIX,
-                 per_element: bool = False, mode: str = "implicit", epsilon: float = 1e-3, radius=None):
+                 per_element: bool = False, mode: str = "implicit", epsilon: float = 1e-3, radius=None,
+                 grad_poses0=None):
         """Weight gradients for the upstream pose gradient: mode "implicit" (Prop. 1, cached factor
         of the last implicit forward) or "dlm" (direct loss minimisation, one
         augmented GN step from poses_K; no cached factor needed).  With a Welsch ``radius`` the
@@ -81,12 +89,15 @@ class PoseGraphSolver:
         if mode == "implicit":
             D.dnls_backward_implicit(self.graph, B, prob, grad_poses.contiguous(), grad_kind,
                                      ge if E else None, gp if P else None, stride, ws, grad_radius=gr)
+        elif mode == "unroll":   # unroll / truncated: the history recorded by the last forward
+            D.dnls_backward_unroll(self.graph, B, prob, grad_poses.contiguous(), grad_kind,
+                                   ge if E else None, gp if P else None, stride, ws, grad_poses0=grad_poses0)
         elif mode == "dlm":
             D.dnls_backward_dlm(self.graph, B, prob, grad_poses.contiguous(), grad_kind, epsilon,
                                 ge if E else None, gp if P else None, stride, ws, grad_radius=gr)
             self.generation += 1   # the workspace factor was overwritten
         else:
-            raise ValueError(f"unknown backward mode {mode!r} (implicit | dlm)")
+            raise ValueError(f"unknown backward mode {mode!r} (implicit | dlm | unroll)")
         if per_element:
             ge, gp = ge[:, :E], gp[:, :P]
         if rad is not None:
@@ -96,9 +107,12 @@ class PoseGraphSolver:
 
 class _PoseGraphFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, solver, poses0, meas, prior_meas, w_edge, w_prior, radius=None, mode="implicit", epsilon=1e-3):
-        poses, obj, st, it = solver.forward(poses0, meas, prior_meas, w_edge, w_prior, implicit=(mode == "implicit"),
-                                            radius=radius)
+    def forward(ctx, solver, poses0, meas, prior_meas, w_edge, w_prior, radius=None, mode="implicit", epsilon=1e-3,
+                steps=0):
+        bmode = {"implicit": D.BWD_IMPLICIT, "dlm": D.BWD_NONE, "unroll": D.BWD_UNROLL,
+                 "truncated": D.BWD_TRUNCATED}[mode]
+        poses, obj, st, it = solver.forward(poses0, meas, prior_meas, w_edge, w_prior, radius=radius,
+                                            backward_mode=bmode, backward_steps=steps)
         ctx.solver = solver
         ctx.mode, ctx.epsilon = mode, epsilon
         ctx.gen = solver.generation
@@ -110,7 +124,7 @@ class _PoseGraphFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g_poses, g_obj, g_st, g_it):
         solver = ctx.solver
-        if ctx.mode == "implicit" and solver.generation != ctx.gen:
+        if ctx.mode != "dlm" and solver.generation != ctx.gen:
             raise RuntimeError("pose_graph_layer: the solver ran another forward since this one; its cached "
                                "factor is gone (DNLS_E_STATE)")
         poses, meas, prior_meas, w_edge, w_prior, *rest = ctx.saved_tensors
@@ -121,7 +135,8 @@ class _PoseGraphFn(torch.autograd.Function):
         # batch (1-D) gets the batch sum of its per-element gradients
         per_el = w_edge.dim() == 2 or w_prior.dim() == 2
         out = solver.backward(poses, meas, prior_meas, w_edge, w_prior, g_poses, D.GRAD_MATRIX,
-                              per_element=per_el, mode=ctx.mode, epsilon=ctx.epsilon, radius=radius)
+                              per_element=per_el, mode="unroll" if ctx.mode == "truncated" else ctx.mode,
+                              epsilon=ctx.epsilon, radius=radius)
         ge, gp = out[0], out[1]
         if per_el:
             ge = ge if w_edge.dim() == 2 else ge.sum(0)
@@ -129,17 +144,20 @@ class _PoseGraphFn(torch.autograd.Function):
         gr = out[2] if radius is not None and ctx.needs_input_grad[6] else None
         ge = ge if ctx.needs_input_grad[4] else None
         gp = gp if ctx.needs_input_grad[5] else None
-        return None, None, None, None, ge, gp, gr, None, None
+        return None, None, None, None, ge, gp, gr, None, None, None
 
 
 def pose_graph_layer(solver: PoseGraphSolver, poses0, meas, prior_meas, w_edge, w_prior, backward_mode="implicit",
-                     epsilon=1e-3, radius=None):
-    """Differentiable solve.  backward_mode "implicit" (Prop. 1, factor reuse) or "dlm" (direct loss
-    minimisation with step eps).  radius: learnable Welsch radius of the Between edges
-    (PAPER.md:168), [1] or [B], or None.  Returns (poses*, objective, status, iterations)."""
-    if backward_mode not in ("implicit", "dlm"):
+                     epsilon=1e-3, radius=None, backward_steps=0):
+    """Differentiable solve.  backward_mode "implicit" (Prop. 1, factor reuse), "dlm" (direct loss
+    minimisation with step eps), "unroll" (backprop through every GN iteration) or
+    "truncated" (through the last ``backward_steps``).  radius: learnable Welsch radius of
+    the Between edges, [1] or [B], or None.  Returns (poses*, objective, status, iterations).
+    theta_init gradients of the unroll modes are available from PoseGraphSolver.backward(grad_poses0=...)."""
+    if backward_mode not in ("implicit", "dlm", "unroll", "truncated"):
         raise ValueError(f"unknown backward_mode {backward_mode!r}")
     if poses0.requires_grad or meas.requires_grad or prior_meas.requires_grad:
         raise ValueError("implicit backward gives no gradient for theta_init or measurements "
                          "(PAPER.md Table 6 :726); only w_edge / w_prior may require grad")
-    return _PoseGraphFn.apply(solver, poses0, meas, prior_meas, w_edge, w_prior, radius, backward_mode, epsilon)
+    return _PoseGraphFn.apply(solver, poses0, meas, prior_meas, w_edge, w_prior, radius, backward_mode, epsilon,
+                              backward_steps)
