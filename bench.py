@@ -271,6 +271,9 @@ def main():
     ap.add_argument("--welsch", type=float, default=None,
                     help="Welsch radius of the Between edges (PAPER.md:168 robust PGO); default: quadratic costs")
     ap.add_argument("--batch", type=int, default=None, help="override the config's (global) batch")
+    ap.add_argument("--interleave", type=int, default=0, choices=[0, 1, 32],
+                    help="dnls_options.batch_interleave: 0 automatic, 1 one CTA per element, 32 batch-interleaved "
+                         "level-major path")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo + --share-gpu: multi-rank wiring test on one GPU)")
     ap.add_argument("--share-gpu", action="store_true", help="every rank uses cuda:0 (testing on a 1-GPU box)")
@@ -334,6 +337,7 @@ def main():
     dlm = args.backward == "dlm"
     unroll = args.backward in ("unroll", "truncated")
     opt.cluster_ctas = args.cluster
+    opt.batch_interleave = args.interleave
     opt.backward_mode = {"implicit": D.BWD_IMPLICIT, "dlm": D.BWD_NONE, "unroll": D.BWD_UNROLL,
                          "truncated": D.BWD_TRUNCATED}[args.backward]
     opt.backward_steps = args.trunc_steps
@@ -439,6 +443,29 @@ def main():
                 "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)" + ("" if (dlm or unroll) else "+lin+factor") +
                         ") per SURVEY.md 8(d); traffic = ncu dram read+write of one launch (profiles/ncu_traffic.json)"}
 
+    # ---- batch-interleaved path: the factorisation phases of one forward (CUDA events around each of the
+    # K + 1 factorisations, DNLS_PHASE_TIMING) give the factor-kernel roofline of the configuration timed above
+    os.environ["DNLS_PHASE_TIMING"] = "1"
+    poses.copy_(dv["poses0"])
+    D.dnls_forward(g, B, opt, prob, ws)
+    del os.environ["DNLS_PHASE_TIMING"]
+    phases = D.dnls_debug_phase_times(g)
+    path = "batch-interleaved level-major (bl.cuh)" if phases else "one CTA per element (k_forward)"
+    if phases:
+        fbytes = 16.0 * st["nnz_L"] * B
+        pm = statistics.median(phases)
+        roofline["kernel"] = "bl_update + bl_factor (one factorisation: all levels)"
+        roofline["kernel_ms"] = pm
+        roofline["alg_bytes_per_launch"] = fbytes
+        roofline["achieved"] = fbytes / (pm / 1e3) / 1e9
+        roofline["frac"] = roofline["achieved"] / peak
+        roofline["note"] = ("batch-interleaved path: the dominant phase is the factorisation (per-level update + "
+                            "factor launches); algorithmic bytes 16 nnz(L) B per factorisation (SURVEY.md 8(d) a3), "
+                            "median over the K+1 factorisations of one forward, CUDA events on the stream")
+        roofline["factorisations_ms"] = phases
+        roofline["forward_alg_bytes_per_launch"] = alg_bytes
+        roofline["forward_frac"] = alg_bytes / Tf / 1e9 / peak
+
     # ---- factor-only roofline (north_star: "the numeric-factorisation kernel"): dnls_factorize on the
     # assembled H(theta_0) of the same batch, 16 nnz(L) B algorithmic bytes per launch
     if not args.no_factor_roofline:
@@ -535,7 +562,7 @@ def main():
                        "l2": ("flushed between timed steps (256 MB write)" if flush is not None else
                               f"not flushed: the step's working set ({ws_bytes / 2**30:.2f} GiB per GPU) is larger "
                               f"than L2"),
-                       "parallelism": f"dp{world}", "nnz_L": st["nnz_L"], "supernodes": st["num_supernodes"],
+                       "parallelism": f"dp{world}", "path": path, "nnz_L": st["nnz_L"], "supernodes": st["num_supernodes"],
                        "levels": st["num_levels"], "symbolic_ms": t_sym * 1e3},
             "step_ms": {"median": statistics.median(steps_ms), "min": min(steps_ms), "max": max(steps_ms)},
             "roofline": roofline,

@@ -336,6 +336,11 @@ DNLS_API dnls_status dnls_status_summary(const int32_t* status, int32_t batch, i
  * Host-synchronous.  Returns DNLS_E_UNSUPPORTED in the production build. */
 DNLS_API dnls_status dnls_debug_trace(int64_t* out, int32_t capacity, int32_t* count);
 
+/* Debug: device times (ms) of the factorisation phases of the last batch-interleaved dnls_forward on this
+ * graph when the process runs with DNLS_PHASE_TIMING=1 (CUDA events around every factorisation; used for
+ * the factor-kernel roofline in bench.py).  Host-synchronous; clears the record.  count = phases written. */
+DNLS_API dnls_status dnls_debug_phase_times(const dnls_graph* g, double* ms, int32_t capacity, int32_t* count);
+
 #ifdef __cplusplus
 }
 #endif

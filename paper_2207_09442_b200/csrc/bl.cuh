@@ -1,0 +1,1000 @@
+// Batch-interleaved, level-major path ("BL") for many problems per GPU
+// (BASELINE.json C4 / C5: 1024 poses x 256..2048 problems).  Included by dnls.cu inside its anonymous
+// namespace (it reuses the per-cost device math of phases.cuh and the helpers of dnls.cu).
+//
+// The one-CTA-per-element kernel (k_forward) runs the elimination tree of ONE element level by level, so
+// every level costs a barrier-separated latency chain while the SM is mostly idle.  Here the batch is the
+// innermost dimension instead:
+//   * storage is element-interleaved: entry i of the factor of element b lives at L[i * Bp + b]
+//     (Bp = B rounded up to 32), so the 32 lanes of a warp -- 32 consecutive elements doing the SAME
+//     item -- move 256 contiguous bytes per access (fully coalesced, no divergence, no shuffles);
+//   * the factorisation is pose-level left-looking block Cholesky (every block d x d, stored column-major
+//     36 / 9 doubles): per elimination-tree level one launch gathers the updates of the level's target
+//     blocks (T_pk -= sum_s L_ps L_ks^T, one thread per (element, target block)) and the forward-substitution
+//     rows, one launch factors the level's columns (redundant register Cholesky of L_kk per thread, one
+//     TRSM block row per thread, fused y_k = L_kk^-1 x_k);
+//   * every phase of the GN iteration (linearise, assemble, factor, solve, retract) is a grid of
+//     (element, item) threads; the host enqueues the launches of all K iterations on the stream.
+// Same arithmetic as the per-element path up to summation order (parity against the oracle, tests).
+// Gauss-Newton (and the implicit backward) with quadratic or Welsch costs; LM / Dogleg / DLM / unroll
+// use the per-element path.
+
+constexpr int BL_TPB = 128;   // threads per block of the BL kernels (4 warps = 4 items x 32 elements)
+
+struct BLDev {
+  int D, N, E, P, n, nblk, Bp, B;
+  const int *perm, *iperm, *edges, *prior_vars;
+  const int* colptr;     // [N+1] blocks of permuted column k (diagonal block first, then rows ascending)
+  const int* blkrow;     // [nblk] row pose of each block
+  const int4* tsk;       // update tasks: (target block, con begin, con end, diagonal flag)
+  const int2* con;       // contributions: (block (p, s), block (k, s))
+  const int* fwdp;       // [N+1] per column: forward-substitution contributions
+  const int2* fwd;       // (block (k, s), s)
+  const int2* fac;       // factor items: (column k, block)
+  const int4* slotd;     // per slot: (off-diagonal block or -1, row pose is j, unique flag, 0)
+  const int *bc_ptr, *bc;   // per permuted pose: slot * 2 + side (fixed gather order)
+  const int *dup_ptr, *dup_blk, *dup_con;   // off-diagonal blocks shared by several edges: their slots
+  const int* fill;       // blocks no cost writes (fill-in), zeroed before assembly
+  int nfill, ndup;
+};
+
+// per-call device views of the BL workspace
+struct BLWs {
+  double* L;       // [nblk * DD][Bp]   assembled H blocks; below-diagonal blocks become L (diagonal blocks keep
+                   //                   the updated T_kk: the column's TRSM threads read it while L_kk is written)
+  double* Ld;      // [N * DD][Bp]     L_kk of every column (lower triangle) + inverse pivots (upper triangle)
+  double* x;       // [n][Bp]        rhs / solution (permuted order)
+  double* scr;     // [slots * SW][Bp] per-slot assembly contributions
+  double* cost;    // [slots][Bp]    per-slot objective (weight gradients in the backward)
+  double* S;       // [Bp]
+  double* Sprev;   // [Bp]
+  unsigned long long* maxd;   // [Bp] max diagonal (bits of a non-negative double: integer max == double max)
+  int* fail;       // [Bp] factorisation failure flag
+  int* st;         // [Bp] status
+  int* it;         // [Bp] iterations
+  int* stf;        // [Bp] final status (the iteration status is parked here during the final linearisation)
+};
+
+template <int D>
+struct BLC {
+  static constexpr int DD = D * D, NL = D * (D + 1) / 2;
+  // slot scratch fields (doubles): H_i (lower, NL), H_j (lower, NL), b_i (D), b_j (D), H_ij (DD)
+  static constexpr int H0 = 0, H1 = NL, B0 = 2 * NL, B1 = 2 * NL + D, HIJ = 2 * NL + 2 * D, SW = 2 * NL + 2 * D + DD;
+};
+
+__device__ __forceinline__ bool bl_item(const BLDev& g, long long nitems, int& b, long long& item) {
+  const long long t = (long long)blockIdx.x * BL_TPB + threadIdx.x;
+  b = (int)(t % g.Bp);
+  item = t / g.Bp;
+  return item < nitems;
+}
+__device__ __forceinline__ bool bl_frozen(const BLWs& w, int b) { return w.st[b] != DNLS_ST_OK; }
+
+// DevGraph with only the fields the per-cost device math (slot_jac / eval_slot / slot_cost) reads
+__device__ __forceinline__ DevGraph bl_cost_graph(const BLDev& g) {
+  DevGraph d{};
+  d.D = g.D;
+  d.N = g.N;
+  d.E = g.E;
+  d.P = g.P;
+  d.edges = g.edges;
+  d.prior_vars = g.prior_vars;
+  return d;
+}
+
+// ---------------------------------------------------------------------------- assembly (a1 + a2)
+__global__ void __launch_bounds__(BL_TPB) bl_zero_fill(BLDev g, BLWs w, int DD) {
+  int b;
+  long long it;
+  if (!bl_item(g, (long long)g.nfill * DD, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const int k = (int)(it / DD), e = (int)(it - (long long)k * DD);
+  w.L[((size_t)g.fill[k] * DD + e) * g.Bp + b] = 0.0;
+}
+
+// thread per (element, cost slot): compact Jacobian in registers, objective term, the slot's off-diagonal
+// block stored straight into the factor storage (single edge between its poses) or into the scratch,
+// the diagonal contributions and J^T r parts into the scratch (PAPER.md:64 J^T J, J^T r)
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_lin_slots(BLDev g, DevProb pr, BLWs w) {
+  using C = BLC<D>;
+  int b;
+  long long it;
+  const int slots = g.E + g.P;
+  if (!bl_item(g, slots, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const int slot = (int)it;
+  const DevGraph cg = bl_cost_graph(g);
+  const double* Tb = pr.poses + (size_t)b * g.N * GT<D>::PS;
+  SlotJ<D> J;
+  slot_jac<D>(cg, pr, Tb, b, slot, J);
+  double n2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < D; ++q) n2 = fma(J.c[q], J.c[q], n2);
+  double psi;
+  w.cost[(size_t)slot * g.Bp + b] = slot_cost(cg, pr, b, slot, J.ww * n2, psi);
+  J.ww *= psi;   // IRLS rescaling (reading W2)
+  const size_t Bp = g.Bp;
+  double* o = w.scr + (size_t)slot * C::SW * Bp + b;
+  const bool edge = slot < g.E;
+  // H_i / b_i: pose i (a prior's pose plays C_j's role: block 0 / rhs side 0, as in linearize_phase)
+  int e = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = q; a < D; ++a, ++e) {
+      o[(C::H0 + e) * Bp] = edge ? blk<D>(J, 1, a, q) : blk<D>(J, 0, a, q);
+      if (edge) o[(C::H1 + e) * Bp] = blk<D>(J, 0, a, q);
+    }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    o[(C::B0 + a) * Bp] = edge ? rhs<D>(J, 1, a) : rhs<D>(J, 0, a);
+    if (edge) o[(C::B1 + a) * Bp] = rhs<D>(J, 0, a);
+  }
+  if (edge) {
+    const int4 sd = g.slotd[slot];
+    double* T = sd.z ? w.L + (size_t)sd.x * C::DD * Bp + b : o + C::HIJ * Bp;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int a = 0; a < D; ++a) T[(q * D + a) * Bp] = sd.y ? blk<D>(J, 3, a, q) : blk<D>(J, 2, a, q);
+  }
+}
+
+// thread per (element, permuted pose): its diagonal block and b segment are the sums of its slots'
+// contributions in the fixed order of bc (deterministic, no atomics on values), damped, written once;
+// the element's max diagonal by an integer atomicMax on the bits of a non-negative double
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_lin_poses(BLDev g, BLWs w, double lam, int damping) {
+  using C = BLC<D>;
+  int b;
+  long long it;
+  if (!bl_item(g, g.N + g.ndup, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const size_t Bp = g.Bp;
+  if (it >= g.N) {   // an off-diagonal block shared by several (parallel) edges
+    const int k = (int)it - g.N;
+    double h[C::DD];
+#pragma unroll
+    for (int i = 0; i < C::DD; ++i) h[i] = 0.0;
+    for (int c = g.dup_ptr[k]; c < g.dup_ptr[k + 1]; ++c) {
+      const double* o = w.scr + ((size_t)g.dup_con[c] * C::SW + C::HIJ) * Bp + b;
+#pragma unroll
+      for (int i = 0; i < C::DD; ++i) h[i] += o[i * Bp];
+    }
+    double* T = w.L + (size_t)g.dup_blk[k] * C::DD * Bp + b;
+#pragma unroll
+    for (int i = 0; i < C::DD; ++i) T[i * Bp] = h[i];
+    return;
+  }
+  const int p = (int)it;
+  double h[C::NL], r[D];
+#pragma unroll
+  for (int i = 0; i < C::NL; ++i) h[i] = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) r[a] = 0.0;
+  for (int c = g.bc_ptr[p]; c < g.bc_ptr[p + 1]; ++c) {
+    const int code = g.bc[c];
+    const int side = code & 1;
+    const double* o = w.scr + (size_t)(code >> 1) * C::SW * Bp + b;
+    const double* oh = o + (side ? C::H1 : C::H0) * Bp;
+    const double* orr = o + (side ? C::B1 : C::B0) * Bp;
+#pragma unroll
+    for (int i = 0; i < C::NL; ++i) h[i] += oh[i * Bp];
+#pragma unroll
+    for (int a = 0; a < D; ++a) r[a] += orr[a * Bp];
+  }
+  double* T = w.L + (size_t)g.colptr[p] * C::DD * Bp + b;
+  double mymax = 0.0;
+  int e = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int a = q; a < D; ++a, ++e) {
+      double v = h[e];
+      if (a == q) {
+        if (lam > 0.0) v = (damping == 0) ? v * (1.0 + lam) : v + lam;
+        mymax = fmax(mymax, v);
+      }
+      T[(q * D + a) * Bp] = v;
+      if (a != q) T[(a * D + q) * Bp] = 0.0;   // upper triangle: the inverse pivots go there later
+    }
+#pragma unroll
+  for (int a = 0; a < D; ++a) w.x[((size_t)p * D + a) * Bp + b] = r[a];
+  if (mymax > 0.0) atomicMax(&w.maxd[b], (unsigned long long)__double_as_longlong(mymax));
+}
+
+// thread per element: S = sum of the slot terms in slot order; early stop (reading A14); resets the
+// failure flag and the max diagonal for the next assembly
+__global__ void __launch_bounds__(BL_TPB) bl_objective(BLDev g, BLWs w, int early_stop, double abs_tol,
+                                                       double rel_tol, int have_prev, int set_prev) {
+  const int b = blockIdx.x * BL_TPB + threadIdx.x;
+  if (b >= g.B) return;
+  double S = 0.0;
+  for (int s = 0; s < g.E + g.P; ++s) S += w.cost[(size_t)s * g.Bp + b];
+  if (w.st[b] != DNLS_ST_OK) return;
+  if (early_stop && have_prev && fabs(S - w.Sprev[b]) < abs_tol + rel_tol * w.Sprev[b]) w.st[b] = DNLS_ST_CONVERGED;
+  w.S[b] = S;
+  if (set_prev) w.Sprev[b] = S;
+}
+__global__ void __launch_bounds__(BL_TPB) bl_reset_iter(BLDev g, BLWs w) {
+  const int b = blockIdx.x * BL_TPB + threadIdx.x;
+  if (b >= g.Bp) return;
+  w.maxd[b] = 0ull;
+  w.fail[b] = 0;
+}
+
+// ---------------------------------------------------------------------------- factorisation (a3 + fused a4 forward)
+// Row-split items: one CTA = D warps x 32 consecutive elements works on one item; warp r owns row r of the
+// item's d x d block (or component r of a vector), so every thread issues all loads of one source block
+// before its FMAs (one memory round trip per contribution) and the d row threads share the column data
+// through L1.  blockIdx.x = item * (Bp / 32) + element group.
+__device__ __forceinline__ bool bl_row_item(const BLDev& g, long long nitems, int& b, long long& item, int& r) {
+  const int groups = g.Bp >> 5;
+  item = blockIdx.x / groups;
+  b = ((blockIdx.x - (int)(item * groups)) << 5) + (threadIdx.x & 31);
+  r = threadIdx.x >> 5;
+  return item < nitems;
+}
+inline unsigned bl_grid_rows(long long items, int Bp) { return (unsigned)(items * (Bp >> 5)); }
+// compiler fence between a batch of independent loads and their consumers: every load of the batch is
+// issued before the first FMA (one memory round trip per batch instead of one per few loads)
+__device__ __forceinline__ void bl_issue_fence() { asm volatile("" ::: "memory"); }
+
+// level l: update tasks T_pk -= sum_s L_ps L_ks^T (items [0, ntask)) and forward-substitution rows
+// x_k -= sum_s L_ks y_s of the level's columns (items [ntask, ntask + ncol)); warp r = row r
+template <int D>
+__global__ void __launch_bounds__(D * 32, 3) bl_update(BLDev g, BLWs w, int t0, int ntask, const int* cols, int ncol,
+                                                    int fused_fwd) {
+  using C = BLC<D>;
+  int b, r;
+  long long it;
+  if (!bl_row_item(g, (long long)ntask + (fused_fwd ? ncol : 0), b, it, r)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const size_t Bp = g.Bp;
+  if (it < ntask) {
+    const int4 tk = g.tsk[t0 + it];
+    double acc[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) acc[j] = 0.0;
+    for (int ci = tk.y; ci < tk.z; ++ci) {
+      const int2 cn = g.con[ci];
+      const double* Pp = w.L + ((size_t)cn.x * C::DD + r) * Bp + b;   // row r of L_ps: stride D entries
+      const double* Kp = w.L + (size_t)cn.y * C::DD * Bp + b;
+      double pv[D], kv[D][D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) pv[c] = Pp[(size_t)c * D * Bp];
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int j = 0; j < D; ++j) kv[c][j] = (!tk.w || j <= r) ? Kp[(c * D + j) * Bp] : 0.0;
+      bl_issue_fence();
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc[j] = fma(pv[c], kv[c][j], acc[j]);
+    }
+    double* T = w.L + ((size_t)tk.x * C::DD + r) * Bp + b;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      if (!tk.w || r >= j) T[(size_t)j * D * Bp] -= acc[j];
+    return;
+  }
+  const int k = cols[it - ntask];
+  double acc = 0.0;
+  for (int ci = g.fwdp[k]; ci < g.fwdp[k + 1]; ++ci) {
+    const int2 f = g.fwd[ci];
+    const double* Kp = w.L + ((size_t)f.x * C::DD + r) * Bp + b;
+    const double* y = w.x + (size_t)f.y * D * Bp + b;
+    double kv[D], yv[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      kv[c] = Kp[(size_t)c * D * Bp];
+      yv[c] = y[c * Bp];
+    }
+    bl_issue_fence();
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc = fma(kv[c], yv[c], acc);
+  }
+  w.x[((size_t)k * D + r) * Bp + b] -= acc;
+}
+
+// level l: item (column k, block): every thread factors L_kk in registers (redundantly; no barrier between
+// the diagonal Cholesky and the TRSM rows); the diagonal item stores L_kk, the inverse pivots (in the
+// block's unused upper triangle) and applies y_k = L_kk^-1 x_k; a below item solves L_pk = T_pk L_kk^-T
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_factor(BLDev g, BLWs w, int f0, int nfac, int fused_fwd) {
+  using C = BLC<D>;
+  int b;
+  long long it;
+  if (!bl_item(g, nfac, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const size_t Bp = g.Bp;
+  const int2 fi = g.fac[f0 + it];
+  const int k = fi.x;
+  const double* Kk = w.L + (size_t)g.colptr[k] * C::DD * Bp + b;
+  const double tol = 1e-13 * __longlong_as_double((long long)w.maxd[b]);
+  double a[D][D], iv[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = j; i < D; ++i) a[i][j] = Kk[(j * D + i) * Bp];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double piv = a[j][j];
+#pragma unroll
+    for (int q = 0; q < j; ++q) piv = fma(-a[j][q], a[j][q], piv);
+    if (!(piv > tol)) {
+      bad = true;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    iv[j] = inv;
+    a[j][j] = piv * inv;
+#pragma unroll
+    for (int i = j + 1; i < D; ++i) {
+      double s = a[i][j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) s = fma(-a[i][q], a[j][q], s);
+      a[i][j] = s * inv;
+    }
+  }
+  if (fi.y == g.colptr[k]) {
+    double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int i = j; i < D; ++i) Lk[(j * D + i) * Bp] = a[i][j];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Lk[ivpos<D>(0, j, D) * Bp] = iv[j];
+    if (bad) w.fail[b] = 1;
+    if (fused_fwd) {
+      double* xk = w.x + (size_t)k * D * Bp + b;
+      double y[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        double s = xk[q * Bp];
+#pragma unroll
+        for (int r = 0; r < q; ++r) s = fma(-a[q][r], y[r], s);
+        y[q] = s * iv[q];
+      }
+#pragma unroll
+      for (int q = 0; q < D; ++q) xk[q * Bp] = y[q];
+    }
+    return;
+  }
+  double* Pb = w.L + (size_t)fi.y * C::DD * Bp + b;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {   // row r of L_pk: x L_kk^T = t
+    double xr[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) xr[q] = Pb[(q * D + r) * Bp];
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      double s = xr[q];
+#pragma unroll
+      for (int j = 0; j < q; ++j) s = fma(-xr[j], a[q][j], s);
+      xr[q] = s * iv[q];
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) Pb[(q * D + r) * Bp] = xr[q];
+  }
+}
+
+// failed factorisation -> element frozen at its iterate (GN: status NOT_SPD), reading A15
+__global__ void __launch_bounds__(BL_TPB) bl_check_fail(BLDev g, BLWs w) {
+  const int b = blockIdx.x * BL_TPB + threadIdx.x;
+  if (b >= g.B) return;
+  if (w.fail[b] && w.st[b] == DNLS_ST_OK) w.st[b] = DNLS_ST_NOT_SPD;
+}
+
+// ---------------------------------------------------------------------------- triangular solves (a4 / a7)
+// standalone forward substitution of a level's columns: y_k = L_kk^-1 (x_k - sum_s L_ks y_s); warp r sums
+// component r, warp 0 applies L_kk^-1 (shared memory exchange)
+template <int D>
+__global__ void __launch_bounds__(D * 32, 3) bl_fsolve(BLDev g, BLWs w, const int* cols, int ncol, const int* skip) {
+  using C = BLC<D>;
+  __shared__ double sv[D][32];
+  int b, r;
+  long long it;
+  if (!bl_row_item(g, ncol, b, it, r)) return;   // uniform per CTA
+  const bool act = b < g.B && !(skip && skip[b]);
+  const size_t Bp = g.Bp;
+  const int k = cols[it];
+  const int lane = threadIdx.x & 31;
+  if (act) {
+    double acc = w.x[((size_t)k * D + r) * Bp + b];
+    for (int ci = g.fwdp[k]; ci < g.fwdp[k + 1]; ++ci) {
+      const int2 f = g.fwd[ci];
+      const double* Kp = w.L + ((size_t)f.x * C::DD + r) * Bp + b;
+      const double* y = w.x + (size_t)f.y * D * Bp + b;
+      double kv[D], yv[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        kv[c] = Kp[(size_t)c * D * Bp];
+        yv[c] = y[c * Bp];
+      }
+      bl_issue_fence();
+#pragma unroll
+      for (int c = 0; c < D; ++c) acc = fma(-kv[c], yv[c], acc);
+    }
+    sv[r][lane] = acc;
+  }
+  __syncthreads();
+  if (r != 0 || !act) return;
+  const double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+  double y[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    double s2 = sv[q][lane];
+#pragma unroll
+    for (int p = 0; p < q; ++p) s2 = fma(-Lk[(p * D + q) * Bp], y[p], s2);
+    y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) w.x[((size_t)k * D + q) * Bp + b] = y[q];
+}
+
+// backward substitution of a level's columns (levels root -> leaves): x_k = L_kk^-T (y_k - sum_p L_pk^T x_p);
+// warp c sums component c over the column's below blocks (two blocks per round trip), warp 0 applies L_kk^-T
+template <int D>
+__global__ void __launch_bounds__(D * 32, 3) bl_bsolve(BLDev g, BLWs w, const int* cols, int ncol, const int* skip) {
+  using C = BLC<D>;
+  __shared__ double sv[D][32];
+  int b, c;
+  long long it;
+  if (!bl_row_item(g, ncol, b, it, c)) return;
+  const bool act = b < g.B && !(skip && skip[b]);
+  const size_t Bp = g.Bp;
+  const int k = cols[it];
+  const int lane = threadIdx.x & 31;
+  if (act) {
+    double acc = w.x[((size_t)k * D + c) * Bp + b], acc2 = 0.0;
+    const int b0 = g.colptr[k] + 1, b1 = g.colptr[k + 1];
+    int bi = b0;
+    for (; bi + 1 < b1; bi += 2) {
+      const double* P0 = w.L + ((size_t)bi * C::DD + c * D) * Bp + b;   // column c of L_pk: D contiguous entries
+      const double* P1 = P0 + (size_t)C::DD * Bp;
+      const double* x0 = w.x + (size_t)g.blkrow[bi] * D * Bp + b;
+      const double* x1 = w.x + (size_t)g.blkrow[bi + 1] * D * Bp + b;
+      double l0[D], l1[D], v0[D], v1[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        l0[q] = P0[q * Bp];
+        l1[q] = P1[q * Bp];
+        v0[q] = x0[q * Bp];
+        v1[q] = x1[q * Bp];
+      }
+      bl_issue_fence();
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        acc = fma(-l0[q], v0[q], acc);
+        acc2 = fma(-l1[q], v1[q], acc2);
+      }
+    }
+    if (bi < b1) {
+      const double* P0 = w.L + ((size_t)bi * C::DD + c * D) * Bp + b;
+      const double* x0 = w.x + (size_t)g.blkrow[bi] * D * Bp + b;
+      double l0[D], v0[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        l0[q] = P0[q * Bp];
+        v0[q] = x0[q * Bp];
+      }
+#pragma unroll
+      for (int q = 0; q < D; ++q) acc = fma(-l0[q], v0[q], acc);
+    }
+    sv[c][lane] = acc + acc2;
+  }
+  __syncthreads();
+  if (c != 0 || !act) return;
+  const double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+  double y[D];
+#pragma unroll
+  for (int q = D - 1; q >= 0; --q) {
+    double s2 = sv[q][lane];
+#pragma unroll
+    for (int p = q + 1; p < D; ++p) s2 = fma(-Lk[(q * D + p) * Bp], y[p], s2);
+    y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) w.x[((size_t)k * D + q) * Bp + b] = y[q];
+}
+
+// ---------------------------------------------------------------------------- retraction (a5)
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_retract(BLDev g, DevProb pr, BLWs w, double alpha) {
+  constexpr int PS = GT<D>::PS;
+  int b;
+  long long it;
+  if (!bl_item(g, g.N, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const int o = (int)it;
+  const size_t Bp = g.Bp;
+  const double* dl = w.x + (size_t)g.iperm[o] * D * Bp + b;
+  double xi[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) xi[a] = -alpha * dl[a * Bp];
+  double* T = pr.poses + ((size_t)b * g.N + o) * PS;
+  if constexpr (D == 6) dev::se3_store(dev::se3_mul(dev::se3_load(T), dev::se3_exp(xi)), T);
+  else dev::se2_store(dev::se2_mul(dev::se2_load(T), dev::se2_exp(xi)), T);
+  if (o == 0) w.it[b] += 1;
+}
+
+__global__ void __launch_bounds__(BL_TPB) bl_init(BLDev g, BLWs w) {
+  const int b = blockIdx.x * BL_TPB + threadIdx.x;
+  if (b >= g.Bp) return;
+  w.st[b] = b < g.B ? DNLS_ST_OK : DNLS_ST_NOT_SPD;   // padding lanes stay frozen
+  w.it[b] = 0;
+  w.S[b] = 0.0;
+  w.Sprev[b] = 0.0;
+  w.maxd[b] = 0ull;
+  w.fail[b] = 0;
+}
+
+// before the final (implicit) linearisation: keep the iteration status in ws_st, re-activate every element
+__global__ void __launch_bounds__(BL_TPB) bl_pre_final(BLDev g, BLWs w) {
+  const int b = blockIdx.x * BL_TPB + threadIdx.x;
+  if (b >= g.B) return;
+  w.stf[b] = w.st[b];
+  w.st[b] = DNLS_ST_OK;
+}
+// final status: a failed final (implicit) factor takes precedence; not-converged warning bit; outputs
+__global__ void __launch_bounds__(BL_TPB) bl_finish(BLDev g, BLWs w, int implicit, double abs_tol, double rel_tol,
+                                                    double* objective, int* status, int* iterations) {
+  const int b = blockIdx.x * BL_TPB + threadIdx.x;
+  if (b >= g.B) return;
+  int s = implicit ? w.stf[b] : w.st[b];
+  if (implicit) {
+    if (w.fail[b]) s = DNLS_ST_NOT_SPD;
+    else if (w.it[b] > 0 && !(fabs(w.S[b] - w.Sprev[b]) < abs_tol + rel_tol * w.Sprev[b])) s |= DNLS_ST_WARN_NOT_CONVERGED;
+  }
+  if (objective) objective[b] = w.S[b];
+  if (status) status[b] = s;
+  if (iterations) iterations[b] = w.it[b];
+  w.stf[b] = s;
+  w.st[b] = s;
+}
+
+// objective at the final poses of an element without the implicit linearisation (S(theta_K))
+__global__ void __launch_bounds__(BL_TPB) bl_final_S(BLDev g, BLWs w) {
+  const int b = blockIdx.x * BL_TPB + threadIdx.x;
+  if (b >= g.B) return;
+  double S = 0.0;
+  for (int s = 0; s < g.E + g.P; ++s) S += w.cost[(size_t)s * g.Bp + b];
+  w.S[b] = S;
+}
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_cost_only(BLDev g, DevProb pr, BLWs w) {
+  int b;
+  long long it;
+  if (!bl_item(g, g.E + g.P, b, it)) return;
+  if (b >= g.B) return;
+  const int slot = (int)it;
+  const DevGraph cg = bl_cost_graph(g);
+  double c[D];
+  eval_slot<D>(cg, pr, pr.poses + (size_t)b * g.N * GT<D>::PS, b, slot, c, nullptr, nullptr, false);
+  const double wt = slot_weight<D>(cg, pr, b, slot);
+  double n2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < D; ++q) n2 += (wt * c[q]) * (wt * c[q]);
+  double psi;
+  w.cost[(size_t)slot * g.Bp + b] = slot_cost(cg, pr, b, slot, n2, psi);
+}
+
+// ---------------------------------------------------------------------------- implicit backward (a7 + a8)
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_bwd_rhs(BLDev g, DevProb pr, BLWs w, const double* gpose,
+                                                     int grad_kind) {
+  int b;
+  long long it;
+  if (!bl_item(g, g.N, b, it)) return;
+  if (b >= g.B) return;
+  const int o = (int)it;
+  double v[D];
+  tangent_grad<D>(pr.poses + (size_t)b * g.N * GT<D>::PS, gpose, grad_kind, b, g.N, o, v);
+  double* x = w.x + (size_t)g.iperm[o] * D * g.Bp + b;
+#pragma unroll
+  for (int a = 0; a < D; ++a) x[a * g.Bp] = v[a];
+}
+// per (element, slot): dL/dw = -2 w psi (1 - s/k^2) (C lambda).c (Prop. 1, readings A12 / W2); zero for
+// elements without a valid factor
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_bwd_slots(BLDev g, DevProb pr, BLWs w, double* out) {
+  int b;
+  long long it;
+  if (!bl_item(g, g.E + g.P, b, it)) return;
+  if (b >= g.B) return;
+  const int slot = (int)it;
+  const size_t Bp = g.Bp;
+  if ((w.stf[b] & DNLS_ST_CODE_MASK) == DNLS_ST_NOT_SPD) {
+    out[(size_t)slot * Bp + b] = 0.0;
+    return;
+  }
+  const DevGraph cg = bl_cost_graph(g);
+  const double* Tb = pr.poses + (size_t)b * g.N * GT<D>::PS;
+  double c[D], Ci[D * D], Cj[D * D];
+  eval_slot<D>(cg, pr, Tb, b, slot, c, Ci, Cj, true);
+  const double wt = slot_weight<D>(cg, pr, b, slot);
+  const bool edge = slot < g.E;
+  const int vi = edge ? g.edges[2 * slot] : g.prior_vars[slot - g.E];
+  const double* li = w.x + (size_t)g.iperm[vi] * D * Bp + b;
+  const double* lj = edge ? w.x + (size_t)g.iperm[g.edges[2 * slot + 1]] * D * Bp + b : li;
+  double lv[D], lw[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    lv[a] = li[a * Bp];
+    lw[a] = lj[a * Bp];
+  }
+  double dot = 0.0, n2 = 0.0;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    double cl = 0.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      cl = fma(Ci[r * D + q], lv[q], cl);
+      if (edge) cl = fma(Cj[r * D + q], lw[q], cl);
+    }
+    dot = fma(cl, c[r], dot);
+    n2 = fma(c[r], c[r], n2);
+  }
+  double psi;
+  const double sq = wt * wt * n2;
+  slot_cost(cg, pr, b, slot, sq, psi);
+  double fw = 1.0;
+  if (pr.radius != nullptr && edge) {
+    const double k = pr.radius[(size_t)b * pr.r_bstride];
+    fw = psi * (1.0 - sq / (k * k));
+  }
+  out[(size_t)slot * Bp + b] = -2.0 * wt * fw * dot;
+}
+// fixed-order batch reduction (or per-element copy) of the interleaved per-slot gradients
+__global__ void bl_reduce_wgrad(int B, int Bp, int E, int P, const double* src, double* ge, double* gp, long long bstride) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= E + P) return;
+  double* dst = slot < E ? ge : gp;
+  const int idx = slot < E ? slot : slot - E;
+  if (!dst) return;
+  const double* s = src + (size_t)slot * Bp;
+  if (bstride == 0) {
+    double acc = 0.0;
+    for (int b = 0; b < B; ++b) acc += s[b];
+    dst[idx] = acc;
+  } else {
+    for (int b = 0; b < B; ++b) dst[(size_t)b * bstride + idx] = s[b];
+  }
+}
+
+// ============================================================================ host plan
+struct BLPlan {
+  int D = 0, N = 0, E = 0, P = 0, nblk = 0, L = 0;
+  int* dbuf = nullptr;
+  BLDev dev{};
+  // host copies of the level schedule (launch sizes)
+  std::vector<int> lvl_ptr, tsk_lvl_ptr, fac_lvl_ptr;
+  const int* d_lvl_col = nullptr;
+  int64_t storage_doubles = 0;   // nblk * DD per element
+  ~BLPlan() {
+    if (dbuf) cudaFree(dbuf);
+  }
+};
+
+// symbolic data of the pose-level block factorisation from the graph's ordering (perm, column structures)
+inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
+  const int N = s.N, D = s.D;
+  pl.D = D;
+  pl.N = N;
+  pl.E = s.E;
+  pl.P = s.P;
+  std::vector<int32_t> colptr(N + 1, 0), blkrow;
+  for (int k = 0; k < N; ++k) {
+    colptr[k] = (int)blkrow.size();
+    blkrow.push_back(k);
+    for (int p : s.colstruct[k]) blkrow.push_back(p);
+  }
+  colptr[N] = (int)blkrow.size();
+  pl.nblk = colptr[N];
+  pl.storage_doubles = (int64_t)pl.nblk * D * D;
+  auto blk = [&](int p, int k) -> int {   // block (p, k), p >= k
+    if (p == k) return colptr[k];
+    const auto& R = s.colstruct[k];
+    auto it = std::lower_bound(R.begin(), R.end(), p);
+    if (it == R.end() || *it != p) return -1;
+    return colptr[k] + 1 + (int)(it - R.begin());
+  };
+  // levels: height in the pose-level elimination tree
+  std::vector<int> h(N, 0);
+  for (int k = 0; k < N; ++k)
+    if (s.parent[k] >= 0) h[s.parent[k]] = std::max(h[s.parent[k]], h[k] + 1);
+  int L = 0;
+  for (int k = 0; k < N; ++k) L = std::max(L, h[k] + 1);
+  pl.L = L;
+  pl.lvl_ptr.assign(L + 1, 0);
+  for (int k = 0; k < N; ++k) pl.lvl_ptr[h[k] + 1]++;
+  for (int l = 0; l < L; ++l) pl.lvl_ptr[l + 1] += pl.lvl_ptr[l];
+  std::vector<int32_t> lvl_col(N);
+  {
+    std::vector<int> fillp(pl.lvl_ptr.begin(), pl.lvl_ptr.end() - 1);
+    for (int k = 0; k < N; ++k) lvl_col[fillp[h[k]]++] = k;
+  }
+  // update tasks: target (p, k) for p in {k} U cs[k]; contributions from every s with k, p in cs[s]
+  std::vector<std::vector<int2>> tcon(pl.nblk);
+  std::vector<std::vector<int2>> fwdl(N);
+  for (int sc = 0; sc < N; ++sc) {
+    const auto& R = s.colstruct[sc];
+    for (size_t iq = 0; iq < R.size(); ++iq) {
+      const int k = R[iq];
+      fwdl[k].push_back(make_int2(blk(k, sc), sc));
+      for (size_t ip = iq; ip < R.size(); ++ip) {
+        const int p = R[ip];
+        tcon[blk(p, k)].push_back(make_int2(blk(p, sc), blk(k, sc)));
+      }
+    }
+  }
+  std::vector<int32_t> tsk, con, fwdp(N + 1, 0), fwd, fac;
+  pl.tsk_lvl_ptr.assign(L + 1, 0);
+  pl.fac_lvl_ptr.assign(L + 1, 0);
+  int ntask = 0, nfac = 0;
+  for (int l = 0; l < L; ++l) {
+    for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
+      const int k = lvl_col[i];
+      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) {
+        fac.push_back(k);
+        fac.push_back(bi);
+        ++nfac;
+        if (tcon[bi].empty()) continue;
+        tsk.push_back(bi);
+        tsk.push_back((int)con.size() / 2);
+        for (const int2& c : tcon[bi]) {
+          con.push_back(c.x);
+          con.push_back(c.y);
+        }
+        tsk.push_back((int)con.size() / 2);
+        tsk.push_back(bi == colptr[k] ? 1 : 0);
+        ++ntask;
+      }
+    }
+    pl.tsk_lvl_ptr[l + 1] = ntask;
+    pl.fac_lvl_ptr[l + 1] = nfac;
+  }
+  for (int k = 0; k < N; ++k) {
+    fwdp[k] = (int)fwd.size() / 2;
+    for (const int2& f : fwdl[k]) {
+      fwd.push_back(f.x);
+      fwd.push_back(f.y);
+    }
+  }
+  fwdp[N] = (int)fwd.size() / 2;
+  // assembly: per slot its off-diagonal block, orientation, unique flag; shared blocks; fill blocks
+  const int slots = s.E + s.P;
+  std::vector<int32_t> slotd(4 * (size_t)slots, 0);
+  std::map<int, std::vector<int>> shared;
+  std::vector<char> written(pl.nblk, 0);
+  for (int k = 0; k < N; ++k) written[colptr[k]] = 1;
+  std::map<std::pair<int, int>, int> pair_count;
+  for (int e = 0; e < s.E; ++e) {
+    const int pi = s.iperm[s.edges[2 * e]], pj = s.iperm[s.edges[2 * e + 1]];
+    pair_count[std::make_pair(std::min(pi, pj), std::max(pi, pj))]++;
+  }
+  for (int e = 0; e < s.E; ++e) {
+    const int pi = s.iperm[s.edges[2 * e]], pj = s.iperm[s.edges[2 * e + 1]];
+    const int Pp = std::max(pi, pj), Q = std::min(pi, pj);
+    const int bidx = blk(Pp, Q);
+    if (bidx < 0) return "bl_build: edge block missing from the factor pattern";
+    const bool uniq = pair_count[std::make_pair(Q, Pp)] == 1;
+    slotd[4 * e] = bidx;
+    slotd[4 * e + 1] = Pp == pj ? 1 : 0;
+    slotd[4 * e + 2] = uniq ? 1 : 0;
+    written[bidx] = 1;
+    if (!uniq) shared[bidx].push_back(e);
+  }
+  for (int k = 0; k < s.P; ++k) slotd[4 * (s.E + k)] = -1;
+  std::vector<int32_t> dup_ptr(1, 0), dup_blk, dup_con, fill;
+  for (auto& kv : shared) {
+    dup_blk.push_back(kv.first);
+    for (int e : kv.second) dup_con.push_back(e);
+    dup_ptr.push_back((int)dup_con.size());
+  }
+  for (int bi = 0; bi < pl.nblk; ++bi)
+    if (!written[bi]) fill.push_back(bi);
+  // upload (int32 arrays, 16-byte aligned)
+  std::vector<int32_t> buf;
+  std::vector<size_t> offs;
+  auto add = [&](const std::vector<int32_t>& v) {
+    while (buf.size() % 4) buf.push_back(0);
+    offs.push_back(buf.size());
+    buf.insert(buf.end(), v.begin(), v.end());
+    buf.push_back(0);
+  };
+  add(s.perm); add(s.iperm); add(s.edges); add(s.prior_vars);
+  add(colptr); add(blkrow); add(tsk); add(con); add(fwdp); add(fwd); add(fac); add(slotd);
+  add(s.bc_ptr); add(s.bc); add(dup_ptr); add(dup_blk); add(dup_con); add(fill); add(lvl_col);
+  while (buf.size() % 4) buf.push_back(0);
+  if (device >= 0) {
+    if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemcpy(pl.dbuf, buf.data(), buf.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      return "bl_build: device upload failed";
+    }
+  }
+  const int* d = pl.dbuf;
+  int k = 0;
+  BLDev& g = pl.dev;
+  g.D = D; g.N = N; g.E = s.E; g.P = s.P; g.n = N * D; g.nblk = pl.nblk;
+  auto ptr = [&](size_t o) { return d ? d + o : nullptr; };
+  g.perm = ptr(offs[k++]); g.iperm = ptr(offs[k++]); g.edges = ptr(offs[k++]); g.prior_vars = ptr(offs[k++]);
+  g.colptr = ptr(offs[k++]); g.blkrow = ptr(offs[k++]);
+  g.tsk = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  g.con = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  g.fwdp = ptr(offs[k++]);
+  g.fwd = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  g.fac = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  g.slotd = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  g.bc_ptr = ptr(offs[k++]); g.bc = ptr(offs[k++]);
+  g.dup_ptr = ptr(offs[k++]); g.dup_blk = ptr(offs[k++]); g.dup_con = ptr(offs[k++]);
+  g.fill = ptr(offs[k++]);
+  pl.d_lvl_col = ptr(offs[k++]);
+  g.nfill = (int)fill.size();
+  g.ndup = (int)dup_blk.size();
+  return std::string();
+}
+
+inline int bl_pad(int B) { return (B + 31) / 32 * 32; }
+
+struct BLLayout {
+  size_t L, Ld, x, scr, cost, S, Sprev, maxd, fail, st, it, stf, total;
+};
+inline BLLayout bl_layout_sizes(int D, int N, int E, int P, int64_t nblk, int B) {
+  const int Bp = bl_pad(B);
+  const size_t slots = (size_t)E + P, SW = D == 6 ? BLC<6>::SW : BLC<3>::SW;
+  const int64_t storage_doubles = nblk * D * D;
+  BLLayout l{};
+  size_t o = 0;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  l.L = o;     o = al(o + sizeof(double) * (size_t)storage_doubles * Bp);
+  l.Ld = o;    o = al(o + sizeof(double) * (size_t)N * D * D * Bp);
+  l.x = o;     o = al(o + sizeof(double) * (size_t)N * D * Bp);
+  l.scr = o;   o = al(o + sizeof(double) * slots * SW * Bp);
+  l.cost = o;  o = al(o + sizeof(double) * slots * Bp);
+  l.S = o;     o = al(o + sizeof(double) * Bp);
+  l.Sprev = o; o = al(o + sizeof(double) * Bp);
+  l.maxd = o;  o = al(o + sizeof(double) * Bp);
+  l.fail = o;  o = al(o + sizeof(int) * Bp);
+  l.st = o;    o = al(o + sizeof(int) * Bp);
+  l.it = o;    o = al(o + sizeof(int) * Bp);
+  l.stf = o;   o = al(o + sizeof(int) * Bp);
+  l.total = o;
+  return l;
+}
+inline BLLayout bl_layout(const BLPlan& pl, int B) { return bl_layout_sizes(pl.D, pl.N, pl.E, pl.P, pl.nblk, B); }
+inline BLWs bl_views(const BLLayout& l, void* base) {
+  char* p = (char*)base;
+  BLWs w;
+  w.L = (double*)(p + l.L);
+  w.Ld = (double*)(p + l.Ld);
+  w.x = (double*)(p + l.x);
+  w.scr = (double*)(p + l.scr);
+  w.cost = (double*)(p + l.cost);
+  w.S = (double*)(p + l.S);
+  w.Sprev = (double*)(p + l.Sprev);
+  w.maxd = (unsigned long long*)(p + l.maxd);
+  w.fail = (int*)(p + l.fail);
+  w.st = (int*)(p + l.st);
+  w.it = (int*)(p + l.it);
+  w.stf = (int*)(p + l.stf);
+  return w;
+}
+
+inline unsigned bl_grid(long long items, int Bp) { return (unsigned)((items * Bp + BL_TPB - 1) / BL_TPB); }
+inline unsigned bl_grid_b(int n) { return (unsigned)((n + BL_TPB - 1) / BL_TPB); }
+
+// phase timing for the factor-kernel roofline (bench): events around each factorisation when enabled
+struct BLPhaseTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  void begin(cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+    ev.push_back(std::make_pair(a, b));
+  }
+  void end(cudaStream_t s) {
+    if (on) cudaEventRecord(ev.back().second, s);
+  }
+};
+
+// linearise + assemble at the current poses (lam > 0: damping), objective into w.S
+template <int D>
+void bl_linearize(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, double lam, int damping, cudaStream_t s) {
+  BLDev g = pl.dev;
+  g.B = B;
+  g.Bp = bl_pad(B);
+  bl_reset_iter<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
+  if (g.nfill) bl_zero_fill<<<bl_grid((long long)g.nfill * D * D, g.Bp), BL_TPB, 0, s>>>(g, w, D * D);
+  bl_lin_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
+  bl_lin_poses<D><<<bl_grid(g.N + g.ndup, g.Bp), BL_TPB, 0, s>>>(g, w, lam, damping);
+}
+
+template <int D>
+void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaStream_t s) {
+  BLDev g = pl.dev;
+  g.B = B;
+  g.Bp = bl_pad(B);
+  for (int l = 0; l < pl.L; ++l) {
+    const int t0 = pl.tsk_lvl_ptr[l], nt = pl.tsk_lvl_ptr[l + 1] - t0;
+    const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
+    const long long nu = (long long)nt + (fused_fwd ? nc : 0);
+    if (nu > 0)
+      bl_update<D><<<bl_grid_rows(nu, g.Bp), D * 32, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
+    const int f0 = pl.fac_lvl_ptr[l], nf = pl.fac_lvl_ptr[l + 1] - f0;
+    bl_factor<D><<<bl_grid(nf, g.Bp), BL_TPB, 0, s>>>(g, w, f0, nf, fused_fwd ? 1 : 0);
+  }
+}
+
+template <int D>
+void bl_solve(const BLPlan& pl, int B, const BLWs& w, bool forward, const int* skip, cudaStream_t s) {
+  BLDev g = pl.dev;
+  g.B = B;
+  g.Bp = bl_pad(B);
+  if (forward)
+    for (int l = 0; l < pl.L; ++l) {
+      const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
+      bl_fsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+    }
+  for (int l = pl.L - 1; l >= 0; --l) {
+    const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
+    bl_bsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+  }
+}
+
+// K Gauss-Newton iterations (+ the undamped linearise + factor at theta_K in implicit mode)
+template <int D>
+void bl_forward(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, int K, double alpha, int early_stop,
+                double abs_tol, double rel_tol, bool implicit, double* objective, int* status, int* iterations,
+                BLPhaseTimer& tm, cudaStream_t s) {
+  BLDev g = pl.dev;
+  g.B = B;
+  g.Bp = bl_pad(B);
+  bl_init<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
+  for (int k = 0; k < K; ++k) {
+    bl_linearize<D>(pl, B, pr, w, -1.0, 0, s);
+    bl_objective<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, early_stop, abs_tol, rel_tol, k > 0 ? 1 : 0, 1);
+    tm.begin(s);
+    bl_factor_all<D>(pl, B, w, true, s);
+    tm.end(s);
+    bl_check_fail<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+    bl_solve<D>(pl, B, w, false, w.st, s);   // frozen / failed elements skip the solve and the retraction
+    bl_retract<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, alpha);
+  }
+  if (implicit) {
+    bl_pre_final<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+    bl_linearize<D>(pl, B, pr, w, -1.0, 0, s);
+    bl_objective<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, 0, abs_tol, rel_tol, 0, 0);
+    // the final factor is computed for every element that still has a defined iterate
+    tm.begin(s);
+    bl_factor_all<D>(pl, B, w, false, s);
+    tm.end(s);
+  } else {
+    bl_cost_only<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
+    bl_final_S<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+  }
+  bl_finish<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, implicit ? 1 : 0, abs_tol, rel_tol, objective, status, iterations);
+}
+
+// implicit backward on the BL factor of H(theta_K): lambda = H^-1 v, per-slot weight gradients, batch reduction
+template <int D>
+void bl_backward_implicit(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, const double* gpose,
+                          int grad_kind, double* ge, double* gp, long long bstride, cudaStream_t s) {
+  BLDev g = pl.dev;
+  g.B = B;
+  g.Bp = bl_pad(B);
+  bl_bwd_rhs<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, gpose, grad_kind);
+  bl_solve<D>(pl, B, w, true, nullptr, s);
+  bl_bwd_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w, w.cost);
+  const int slots = g.E + g.P;
+  if (slots > 0 && (ge || gp))
+    bl_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(B, g.Bp, g.E, g.P, w.cost, ge, gp, bstride);
+}

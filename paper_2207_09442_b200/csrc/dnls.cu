@@ -48,8 +48,18 @@ dnls_status cuda_check(const char* what) {
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 }  // namespace
 
+namespace {
+struct BLPlan;
+void bl_plan_delete(BLPlan* p);
+}  // namespace
+
 struct dnls_graph {
   Symbolic sym;
+  // batch-interleaved level-major plan (bl.cuh), built on first use
+  BLPlan* bl = nullptr;
+  std::string bl_err;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_ev;   // factorisation phases of the last BL forward
+  std::mutex bl_mu;
   int device = 0;
   int* dbuf = nullptr;
   size_t dbuf_bytes = 0;
@@ -65,6 +75,7 @@ struct dnls_graph {
     int kind;   // DNLS_BWD_* of the forward that wrote it
     int K;      // unroll: iterations whose factors are kept
     double alpha = 1.0;   // unroll: the GN step size of the recorded forward
+    int layout = 0;       // 0: per-element storage, 1: batch-interleaved (bl.cuh)
   };
   std::map<const void*, FactorRecord> cached;
   void drop(const void* ws) {
@@ -1181,6 +1192,8 @@ __global__ void k_export_rhs(DevGraph g, DevWs ws, double* out) {
   }
 }
 
+#include "bl.cuh"
+void bl_plan_delete(BLPlan* p) { delete p; }
 #endif  // !DNLS_CLUSTER_TU
 }  // namespace
 
@@ -1220,6 +1233,39 @@ cudaError_t launch_forward_cluster(int CL, int D, const DevGraph& g, DevProb pr,
 #else  // the main translation unit: host API
 
 namespace {
+// batch-interleaved level-major path (bl.cuh): Gauss-Newton with the
+// implicit (or no) backward and quadratic costs; chosen explicitly (batch_interleave == 32) or automatically
+bool bl_supported(const dnls_options* opt, const dnls_problem* prob) {
+  return opt->optimizer == DNLS_GN &&
+         (opt->backward_mode == DNLS_BWD_NONE || opt->backward_mode == DNLS_BWD_IMPLICIT) &&
+         (prob == nullptr || prob->radius == nullptr);
+}
+bool bl_choose(const dnls_graph* g, int batch, const dnls_options* opt, const dnls_problem* prob) {
+  if (!opt || opt->batch_interleave == 1 || !bl_supported(opt, prob)) return false;
+  if (opt->batch_interleave == 32) return true;
+  (void)g;
+  (void)batch;
+  return false;
+}
+size_t bl_ws_bytes(const dnls_graph* g, int batch) {
+  const Symbolic& s = g->sym;
+  return bl_layout_sizes(s.D, s.N, s.E, s.P, s.nnz_L_blocks, batch).total;
+}
+dnls_status bl_plan_for(dnls_graph* g, BLPlan** out) {
+  std::lock_guard<std::mutex> lk(g->bl_mu);
+  if (!g->bl) {
+    BLPlan* pl = new BLPlan();
+    DeviceGuard dguard(g->device);
+    const std::string e = bl_build(g->sym, g->device, *pl);
+    if (!e.empty()) {
+      delete pl;
+      return fail(DNLS_E_CUDA, e);
+    }
+    g->bl = pl;
+  }
+  *out = g->bl;
+  return DNLS_OK;
+}
 // CTAs per batch element for dnls_forward: a cluster when the
 // batch leaves most SMs idle and the graph has enough work per level to share
 int forward_cluster(const dnls_graph* g, int batch, int req) {
@@ -1259,6 +1305,25 @@ DNLS_API dnls_status dnls_debug_trace(int64_t* out, int32_t capacity, int32_t* c
   if (count) *count = 0;
   return fail(DNLS_E_UNSUPPORTED, "dnls_debug_trace: library built without -DDNLS_TRACE");
 #endif
+}
+
+DNLS_API dnls_status dnls_debug_phase_times(const dnls_graph* g, double* ms, int32_t capacity, int32_t* count) {
+  if (!g || !count) return fail(DNLS_E_INVALID, "dnls_debug_phase_times: NULL argument");
+  dnls_graph* gm = const_cast<dnls_graph*>(g);
+  std::lock_guard<std::mutex> lk(gm->bl_mu);
+  int n = 0;
+  for (auto& e : gm->phase_ev) {
+    float t = 0.f;
+    if (cudaEventSynchronize(e.second) == cudaSuccess && cudaEventElapsedTime(&t, e.first, e.second) == cudaSuccess &&
+        ms && n < capacity)
+      ms[n] = t;
+    ++n;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  gm->phase_ev.clear();
+  *count = std::min(n, (int)capacity);
+  return cuda_check("dnls_debug_phase_times");
 }
 
 #ifdef DNLS_LIN_PROBE
@@ -1419,6 +1484,7 @@ DNLS_API dnls_status dnls_graph_create(int32_t group, int32_t num_vars, int32_t 
 
 DNLS_API void dnls_graph_destroy(dnls_graph* g) {
   if (!g) return;
+  if (g->bl) bl_plan_delete(g->bl);
   if (g->dbuf) cudaFree(g->dbuf);
   delete g;
 }
@@ -1534,6 +1600,7 @@ DNLS_API dnls_status dnls_workspace_bytes(const dnls_graph* g, int32_t batch, co
   if (!g || !bytes) return fail(DNLS_E_INVALID, "dnls_workspace_bytes: NULL argument");
   if (batch < 0) return fail(DNLS_E_SHAPE, "dnls_workspace_bytes: batch < 0");
   *bytes = ws_layout(g->sym, batch, history_keep(opt)).total;
+  if (opt && opt->batch_interleave != 1 && bl_supported(opt, nullptr)) *bytes = std::max(*bytes, bl_ws_bytes(g, batch));
   return DNLS_OK;
 }
 
@@ -1633,6 +1700,30 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   fp.status = prob->status;
   fp.iterations = prob->iterations;
   cudaStream_t s = (cudaStream_t)stream;
+  if (bl_choose(g, batch, opt, prob)) {
+    if (ws_bytes < bl_ws_bytes(g, batch))
+      return fail(DNLS_E_WORKSPACE, "dnls_forward: workspace too small for the batch-interleaved path (" +
+                                        std::to_string(bl_ws_bytes(g, batch)) + " bytes)");
+    BLPlan* pl = nullptr;
+    if ((st = bl_plan_for(gm, &pl))) return st;
+    const BLWs bw = bl_views(bl_layout(*pl, batch), workspace);
+    BLPhaseTimer tm;
+    tm.on = std::getenv("DNLS_PHASE_TIMING") != nullptr;
+    DISPATCH_D(g->sym.D, bl_forward<DD>(*pl, batch, dev_prob(prob), bw, fp.K, fp.alpha, fp.early_stop, fp.abs_tol,
+                                        fp.rel_tol, fp.implicit != 0, prob->objective, prob->status, prob->iterations,
+                                        tm, s));
+    if ((st = cuda_check("dnls_forward: batch-interleaved launches"))) return st;
+    {
+      std::lock_guard<std::mutex> lk(gm->bl_mu);
+      for (auto& e : gm->phase_ev) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+      gm->phase_ev = tm.ev;
+    }
+    if (fp.implicit) gm->keep(workspace, dnls_graph::FactorRecord{batch, DNLS_BWD_IMPLICIT, 0, 1.0, 1});
+    return DNLS_OK;
+  }
   const int cl = (opt->optimizer == DNLS_DOGLEG || unroll) ? 1 : forward_cluster(g, batch, opt->cluster_ctas);
   if (cl == 1) {
     DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD, 1>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD, 1><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
@@ -1658,16 +1749,24 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
   if (grad_bstride < 0) return fail(DNLS_E_INVALID, "dnls_backward_implicit: grad_bstride < 0");
   if (grad_bstride > 0 && grad_bstride < std::max(g->sym.E, g->sym.P))
     return fail(DNLS_E_SHAPE, "dnls_backward_implicit: grad_bstride smaller than num_edges/num_priors");
-  {
-    dnls_graph::FactorRecord rec;
-    if (!const_cast<dnls_graph*>(g)->get(workspace, rec) || rec.batch != batch || rec.kind != DNLS_BWD_IMPLICIT)
-      return fail(DNLS_E_STATE,
-                  "dnls_backward_implicit: no implicit-mode dnls_forward on this workspace/batch "
-                  "(factor cache missing or overwritten)");
-  }
+  dnls_graph::FactorRecord rec{};
+  if (!const_cast<dnls_graph*>(g)->get(workspace, rec) || rec.batch != batch || rec.kind != DNLS_BWD_IMPLICIT)
+    return fail(DNLS_E_STATE,
+                "dnls_backward_implicit: no implicit-mode dnls_forward on this workspace/batch "
+                "(factor cache missing or overwritten)");
   if (batch == 0) return DNLS_OK;
   DeviceGuard dguard(g->device);
   if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_backward_implicit: cannot select the graph's device");
+  if (rec.layout == 1) {   // factor of the batch-interleaved path
+    if (grad_radius && prob->radius)
+      return fail(DNLS_E_UNSUPPORTED, "dnls_backward_implicit: no radius gradient on the batch-interleaved path");
+    BLPlan* pl = nullptr;
+    if ((st = bl_plan_for(const_cast<dnls_graph*>(g), &pl))) return st;
+    const BLWs bw = bl_views(bl_layout(*pl, batch), workspace);
+    DISPATCH_D(g->sym.D, bl_backward_implicit<DD>(*pl, batch, dev_prob(prob), bw, grad_poses, grad_kind, grad_w_edge,
+                                                  grad_w_prior, (long long)grad_bstride, (cudaStream_t)stream));
+    return cuda_check("dnls_backward_implicit: batch-interleaved launches");
+  }
   WsLayout l = ws_layout(g->sym, batch);
   DevWs ws = ws_views(l, workspace);
   cudaStream_t s = (cudaStream_t)stream;

@@ -1180,16 +1180,17 @@ __device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int*
     const int m = sa.y, ld = sa.z, w = sa.w;
     double* xs = x ? x + (size_t)D * P.snb[i].x : nullptr;
     if (w == D) {
-      // at most one warp factors redundantly and solves the TRSM rows (the fp64 pipe is shared);
-      // with a multi-warp team, lane 0 of the second warp stores L_jj and applies the forward
-      // substitution concurrently
-      const int Gr = G < 32 ? G : 32, sr = G >= 64 ? 32 : 0;
-      if (rank >= Gr && rank != sr) continue;
+      // at most one warp factors redundantly and solves the TRSM rows (the fp64 pipe is shared); its
+      // first lane stores L_jj and applies the forward substitution once every lane of the group has
+      // read the unfactored diagonal block (warp sync: the store overwrites what the others read --
+      // compute-sanitizer racecheck, profiles/r2_sanitizer.txt)
+      const int Gr = G < 32 ? G : 32;
+      if (rank >= Gr) continue;
       double a[D][D], iv[D];
       const bool bad = chol_regs<D>(Pn, ld, 0, tol, a, iv);
-      if (rank < Gr)
-        for (int r = D + rank; r < m; r += Gr) trsm_row_regs<D>(Pn, ld, 0, r, a, iv);
-      if (rank == sr) {
+      for (int r = D + rank; r < m; r += Gr) trsm_row_regs<D>(Pn, ld, 0, r, a, iv);
+      __syncwarp(ts.mask);
+      if (rank == 0) {
         store_diag<D>(Pn, ld, 0, a, iv);
         if (bad) *fail = 1;
         if (xs) {
@@ -1211,11 +1212,11 @@ __device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int*
       double a[D][D], iv[D];
       const bool bad = chol_regs<D>(Pn, ld, c0, tol, a, iv);
       for (int r = c0 + D + rank; r < m; r += G) trsm_row_regs<D>(Pn, ld, c0, r, a, iv);
-      if (rank == 0) {
+      ts.sync();   // every rank has read the unfactored diagonal block and written its TRSM rows
+      if (rank == 0) {   // the trailing update below reads rows >= c0 + D only
         store_diag<D>(Pn, ld, c0, a, iv);
         if (bad) *fail = 1;
       }
-      ts.sync();
       const int r0 = c0 + D;
       if (r0 < w) {
         const int nc = w - r0, nr = m - r0, nit = nc * nr;
@@ -1235,6 +1236,7 @@ __device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int*
       }
     }
     if (xs) {
+      ts.sync();   // the last diagonal block is stored
       if (G >= 32) {
         if (rank < 32) warp_trsv_lower_w<D>(Pn, ld, w, xs);
       } else if (rank == 0) {   // y = L_ss^-1 t, column-oriented, inverse pivots from ivpos

@@ -126,6 +126,15 @@ def dnls_status_summary(status: torch.Tensor, stream=None):
     return nf.value, nw.value
 
 
+def dnls_debug_phase_times(g: Graph, capacity: int = 4096) -> list:
+    """Factorisation-phase times (ms) of the last batch-interleaved forward (needs DNLS_PHASE_TIMING=1)."""
+    buf = np.zeros(capacity, dtype=np.float64)
+    n = ctypes.c_int32(0)
+    check(lib().dnls_debug_phase_times(g.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(capacity),
+                                       ctypes.byref(n)), "dnls_debug_phase_times")
+    return buf[:n.value].tolist()
+
+
 def dnls_graph_perm(g: Graph) -> np.ndarray:
     a, p = _i32(g.N)
     check(lib().dnls_graph_perm(g.handle, p), "dnls_graph_perm")

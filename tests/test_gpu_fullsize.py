@@ -12,10 +12,10 @@ from paper_2207_09442_b200.layer import PoseGraphSolver
 pytestmark = pytest.mark.gpu
 
 
-def run_full(N, B, K, opt="gn", mode="local", samples=(0, 1), **noise):
+def run_full(N, B, K, opt="gn", mode="local", samples=(0, 1), cluster=0, **noise):
     topo, data = make_case(N, dim=3, p=0.2, mode=mode, seed=0, B=B, **noise)
     solver = PoseGraphSolver(D.SE3, N, topo.edges, topo.prior_vars, device=0, max_iterations=K,
-                             optimizer=D.LM if opt == "lm" else D.GN)
+                             optimizer=D.LM if opt == "lm" else D.GN, cluster_ctas=cluster)
     t = to_dev(data)
     poses, obj, st, it = solver.forward(t["poses0"], t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
                                         implicit=True)
@@ -28,10 +28,13 @@ def run_full(N, B, K, opt="gn", mode="local", samples=(0, 1), **noise):
 
 
 def check_samples(topo, data, P, obj, ge, gp, v, samples, K, opt="gn"):
+    from test_gpu_parity import lm_has_tie
     sub = {k: (val[list(samples)] if k in ("poses0", "meas", "prior_meas") else val) for k, val in data.items()}
     res = oracle_results(topo, sub, max_iterations=K, implicit=True, optimizer=opt)
     for r, b in zip(res, samples):
-        assert pose_err(P[b], r.x) <= TOL_POSE, b
+        # LM: an accept decision at a rounding-level tie is compared on the converged iterate (reading A13)
+        tol = 1e-7 if opt == "lm" and lm_has_tie(r) else TOL_POSE
+        assert pose_err(P[b], r.x) <= tol, b
         assert abs(obj[b] - r.objective) <= TOL_OBJ * r.objective, b
         prob = oracle_problem(topo, sub, list(samples).index(b))
         a, c, _ = oimp.implicit_weight_grads(prob, r.x, v[b].reshape(-1), L_K=r.L_final)
@@ -43,7 +46,7 @@ def test_c2_full_size_sampled_parity():
     N, B, K = 256, 128, 10
     samples = (0, 1, 64, 127)
     topo, data, P, obj, st, ge, gp, v = run_full(N, B, K, samples=samples)
-    assert (st == 0).all()
+    assert ((st & 0xff) == 0).all()
     assert np.isfinite(P).all() and np.isfinite(ge).all()
     # properties on every element: rotations orthonormal, objective below the initial one
     R = P[..., :3]
@@ -56,8 +59,35 @@ def test_c4_full_size_sampled_parity():
     N, B, K = 1024, 256, 10
     samples = (0, 255)
     topo, data, P, obj, st, ge, gp, v = run_full(N, B, K, samples=samples)
-    assert (st == 0).all() and np.isfinite(P).all()
+    assert ((st & 0xff) == 0).all() and np.isfinite(P).all()
     check_samples(topo, data, P, obj, ge, gp, v, samples, K)
+
+
+def test_c4_graph_with_cluster_path_parity():
+    # N = 1024 with B <= 74: dnls_forward's automatic policy runs 2-CTA clusters per element (DESIGN.md
+    # "few large problems") -- the production cluster path at the size it runs at, vs the oracle
+    N, B, K = 1024, 8, 10
+    samples = (0, 7)
+    topo, data, P, obj, st, ge, gp, v = run_full(N, B, K, samples=samples)
+    assert ((st & 0xff) == 0).all() and np.isfinite(P).all()
+    check_samples(topo, data, P, obj, ge, gp, v, samples, K)
+    # the forced one-CTA kernel agrees on every element (the cluster splits the level work differently, so
+    # summation order -- not the result -- may differ at rounding level at this size)
+    _, _, P1, obj1, _, ge1, gp1, _ = run_full(N, B, K, samples=samples, cluster=1)
+    assert np.max(np.abs(P - P1)) <= 1e-11 * max(1.0, np.max(np.abs(P1)))
+    assert np.max(np.abs(obj - obj1) / obj1) <= 1e-11
+    assert np.max(np.abs(ge - ge1)) <= 1e-9 * np.max(np.abs(ge1))
+
+
+def test_c3_full_size_lm_parity_one_element():
+    # BASELINE.json configs[2]: SE3, 4096 poses, batch 16, LM K=10 + implicit backward, automatic 2-CTA
+    # clusters, x and the factor in global memory; the oracle (dense n = 24576, LAPACK branch of
+    # oracle.linalg.cholesky) on element 0 (SURVEY.md §8(d) "C3 ... use 1 element")
+    N, B, K = 4096, 16, 10
+    samples = (0,)
+    topo, data, P, obj, st, ge, gp, v = run_full(N, B, K, opt="lm", samples=samples)
+    assert ((st & 0xff) == 0).all() and np.isfinite(P).all()
+    check_samples(topo, data, P, obj, ge, gp, v, samples, K, opt="lm")
 
 
 def test_c3_lm_runs_and_decreases():
@@ -73,6 +103,6 @@ def test_c3_lm_runs_and_decreases():
     D.dnls_linearize(solver.graph, B, pr, None, 0, ws)
     poses, obj, st, it = solver.forward(t["poses0"], t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"])
     torch.cuda.synchronize()
-    assert (st.cpu().numpy() == 0).all() and (it.cpu().numpy() == K).all()
+    assert ((st.cpu().numpy() & 0xff) == 0).all() and (it.cpu().numpy() == K).all()
     assert (obj < obj0).all()
     assert torch.isfinite(poses).all()

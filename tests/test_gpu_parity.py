@@ -435,10 +435,11 @@ def test_welsch_forward_matches_oracle(dim, opt, radius):
     res = oracle_results(topo, data, max_iterations=8, optimizer=opt)
     P = poses.cpu().numpy()
     for b, r in enumerate(res):
-        if opt == "lm" and lm_has_tie(r):
-            continue
-        assert pose_err(P[b], r.x) <= TOL_POSE
         assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
+        if opt == "lm" and lm_has_tie(r):   # reading A13: compared on the converged iterate
+            assert pose_err(P[b], r.x) <= 1e-7
+        else:
+            assert pose_err(P[b], r.x) <= TOL_POSE
 
 
 @pytest.mark.parametrize("mode,per_el_radius", [("implicit", False), ("implicit", True), ("dlm", False)])
@@ -507,10 +508,11 @@ def test_forward_cluster_matches_oracle(cl, N, dim, opt, B):
                              torch.from_numpy(v).to(DEV), D.GRAD_TANGENT, per_element=True)
     torch.cuda.synchronize()
     for b, r in enumerate(res):
-        if opt == "lm" and lm_has_tie(r):
-            continue
-        assert pose_err(P[b], r.x) <= TOL_POSE
         assert abs(obj[b].item() - r.objective) <= TOL_OBJ * r.objective + 1e-20
+        if opt == "lm" and lm_has_tie(r):   # reading A13: compared on the converged iterate
+            assert pose_err(P[b], r.x) <= 1e-7
+        else:
+            assert pose_err(P[b], r.x) <= TOL_POSE
         assert (st[b].item() & 0xff) == r.status and it[b].item() == r.iterations
         a, c, _ = oimp.implicit_weight_grads(oracle_problem(topo, data, b), r.x, v[b].reshape(-1), L_K=r.L_final)
         assert rel_vec_err(np.concatenate([ge[b].cpu().numpy(), gp[b].cpu().numpy()]),
