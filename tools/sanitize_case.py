@@ -1,5 +1,5 @@
 """Small forward + backward runs for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
-  python tools/sanitize_case.py <case>   case in c1 | c2 | cluster | lm | unroll | dlm
+  python tools/sanitize_case.py <case>   case in c1 | c2 | cluster | lm | unroll | dlm | bl
 SURVEY.md §5 "race detection": the fused kernels rely on named barriers, mbarrier/TMA proxy ordering and
 cluster barriers; these cases exercise each path once."""
 import os
@@ -16,7 +16,8 @@ from paper_2207_09442_b200.layer import PoseGraphSolver  # noqa: E402
 
 case = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfg = {"c1": (16, 2, 4, {}), "c2": (256, 3, 4, {}), "cluster": (1024, 3, 2, {"cluster_ctas": 2}),
-       "lm": (64, 3, 3, {"optimizer": D.LM}), "unroll": (64, 3, 3, {}), "dlm": (64, 3, 3, {})}[case]
+       "lm": (64, 3, 3, {"optimizer": D.LM}), "unroll": (64, 3, 3, {}), "dlm": (64, 3, 3, {}),
+       "bl": (64, 3, 40, {"batch_interleave": 32})}[case]
 N, dim, B, opts = cfg
 topo = synth.cube_topology(N, dim=dim, p=0.3, seed=0)
 data = synth.cube_batch(topo, B, seed=0)
