@@ -389,6 +389,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(dev_index).start()
+    D.dnls_debug_launch_count(reset=True)
     ev_f, per_step = [], []
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -401,6 +402,7 @@ def main():
         e1.record(stream)
         per_step.append((e0, e1))
     t1.record(stream)
+    launches = D.dnls_debug_launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -568,8 +570,8 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # k_forward, k_backward / k_backward_dlm, k_reduce_wgrad (+ k_reduce_radius) per timed step
-            "gpu_launches": (3 + (0 if args.welsch is None else 1)) * args.steps,
+            # the library's own kernel launches inside the timed region (dnls_debug_launch_count)
+            "gpu_launches": launches,
             "clocks": clocks,
         }
         if world > 1:

@@ -341,6 +341,11 @@ DNLS_API dnls_status dnls_debug_trace(int64_t* out, int32_t capacity, int32_t* c
  * the factor-kernel roofline in bench.py).  Host-synchronous; clears the record.  count = phases written. */
 DNLS_API dnls_status dnls_debug_phase_times(const dnls_graph* g, double* ms, int32_t capacity, int32_t* count);
 
+/* Debug: number of kernels the library has enqueued in this process (every entry point counts its launches;
+ * bench.py reports the count of its timed region as gpu_launches).  reset != 0: the counter restarts at 0
+ * after being read.  Host-only, never fails for a non-NULL count (DNLS_E_INVALID otherwise). */
+DNLS_API dnls_status dnls_debug_launch_count(int64_t* count, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

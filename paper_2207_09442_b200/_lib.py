@@ -132,6 +132,7 @@ _SIGS = {
                                             ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
                                             ctypes.c_void_p]),
     "dnls_debug_phase_times": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_int32, c_int32_p]),
+    "dnls_debug_launch_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]),
     "dnls_block_offsets": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p]),
     "dnls_status_summary": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_int32_p, c_int32_p, ctypes.c_void_p]),
 }

@@ -83,13 +83,13 @@ __device__ __forceinline__ DevGraph bl_cost_graph(const BLDev& g) {
 }
 
 // ---------------------------------------------------------------------------- assembly (a1 + a2)
-__global__ void __launch_bounds__(BL_TPB) bl_zero_fill(BLDev g, BLWs w, int DD) {
+__global__ void __launch_bounds__(BL_TPB) bl_zero_fill(BLDev g, BLWs w, int DD, const int* fill, int nfill) {
   int b;
   long long it;
-  if (!bl_item(g, (long long)g.nfill * DD, b, it)) return;
+  if (!bl_item(g, (long long)nfill * DD, b, it)) return;
   if (b >= g.B || bl_frozen(w, b)) return;
   const int k = (int)(it / DD), e = (int)(it - (long long)k * DD);
-  w.L[((size_t)g.fill[k] * DD + e) * g.Bp + b] = 0.0;
+  w.L[((size_t)fill[k] * DD + e) * g.Bp + b] = 0.0;
 }
 
 // thread per (element, cost slot): compact Jacobian in registers, objective term, the slot's off-diagonal
@@ -204,14 +204,30 @@ __global__ void __launch_bounds__(BL_TPB) bl_lin_poses(BLDev g, BLWs w, double l
   if (mymax > 0.0) atomicMax(&w.maxd[b], (unsigned long long)__double_as_longlong(mymax));
 }
 
-// thread per element: S = sum of the slot terms in slot order; early stop (reading A14); resets the
-// failure flag and the max diagonal for the next assembly
-__global__ void __launch_bounds__(BL_TPB) bl_objective(BLDev g, BLWs w, int early_stop, double abs_tol,
-                                                       double rel_tol, int have_prev, int set_prev) {
-  const int b = blockIdx.x * BL_TPB + threadIdx.x;
-  if (b >= g.B) return;
+// S = sum of the slot terms (fixed order: BL_SW warps each sum a contiguous slot range for the same 32
+// elements, then the partials in warp order); final == 0: early stop (reading A14) and S_prev update,
+// final == 1: S(theta_K) only
+constexpr int BL_SW = 32;
+__global__ void __launch_bounds__(BL_SW * 32) bl_objective(BLDev g, BLWs w, int early_stop, double abs_tol,
+                                                          double rel_tol, int have_prev, int set_prev, int final) {
+  __shared__ double part[BL_SW][33];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int b = blockIdx.x * 32 + lane;
+  const int slots = g.E + g.P, chunk = (slots + BL_SW - 1) / BL_SW;
+  const int s0 = wp * chunk, s1 = min(slots, s0 + chunk);
+  double acc = 0.0;
+  if (b < g.B)
+    for (int sl = s0; sl < s1; ++sl) acc += w.cost[(size_t)sl * g.Bp + b];
+  part[wp][lane] = acc;
+  __syncthreads();
+  if (wp != 0 || b >= g.B) return;
   double S = 0.0;
-  for (int s = 0; s < g.E + g.P; ++s) S += w.cost[(size_t)s * g.Bp + b];
+#pragma unroll 8
+  for (int q = 0; q < BL_SW; ++q) S += part[q][lane];
+  if (final) {
+    w.S[b] = S;
+    return;
+  }
   if (w.st[b] != DNLS_ST_OK) return;
   if (early_stop && have_prev && fabs(S - w.Sprev[b]) < abs_tol + rel_tol * w.Sprev[b]) w.st[b] = DNLS_ST_CONVERGED;
   w.S[b] = S;
@@ -267,7 +283,7 @@ __global__ void __launch_bounds__(D * 32, 3) bl_update(BLDev g, BLWs w, int t0, 
 #pragma unroll
       for (int c = 0; c < D; ++c)
 #pragma unroll
-        for (int j = 0; j < D; ++j) kv[c][j] = (!tk.w || j <= r) ? Kp[(c * D + j) * Bp] : 0.0;
+        for (int j = 0; j < D; ++j) kv[c][j] = (!(tk.w & 1) || j <= r) ? Kp[(c * D + j) * Bp] : 0.0;
       bl_issue_fence();
 #pragma unroll
       for (int c = 0; c < D; ++c)
@@ -277,7 +293,7 @@ __global__ void __launch_bounds__(D * 32, 3) bl_update(BLDev g, BLWs w, int t0, 
     double* T = w.L + ((size_t)tk.x * C::DD + r) * Bp + b;
 #pragma unroll
     for (int j = 0; j < D; ++j)
-      if (!tk.w || r >= j) T[(size_t)j * D * Bp] -= acc[j];
+      if (!(tk.w & 1) || r >= j) T[(size_t)j * D * Bp] -= acc[j];
     return;
   }
   const int k = cols[it - ntask];
@@ -297,6 +313,737 @@ __global__ void __launch_bounds__(D * 32, 3) bl_update(BLDev g, BLWs w, int t0, 
     for (int c = 0; c < D; ++c) acc = fma(kv[c], yv[c], acc);
   }
   w.x[((size_t)k * D + r) * Bp + b] -= acc;
+}
+
+// level l, register-blocked: thread = (element, item); an update task accumulates the WHOLE d x d target
+// block in registers (acc[i][j] = sum_s sum_c L_ps[i][c] L_ks[j][c]), streaming the two source blocks
+// column by column (half a block pair per memory round trip): 2 d^2 loads per d^3 FMAs instead of the
+// row-split kernel's d (d + d^2).  A diagonal target (p == k) reads its single source block once and keeps
+// the lower triangle.  Fill targets (tk.w & 2: no cost writes them) are stored as -acc, so they need no
+// zeroing pass.  Warps enumerate (item, group of 32 elements) item-major.
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_update_rb(BLDev g, BLWs w, int t0, int ntask, const int* cols, int ncol,
+                                                       int fused_fwd) {
+  using C = BLC<D>;
+  constexpr int H = D / 2;   // source columns per round trip
+  int b;
+  long long it;
+  if (!bl_item(g, (long long)ntask + (fused_fwd ? ncol : 0), b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const size_t Bp = g.Bp;
+  if (it < ntask) {
+    const int4 tk = g.tsk[t0 + it];
+    double acc[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[i][j] = 0.0;
+    if (tk.w & 1) {   // diagonal target: T_kk -= sum_s L_ks L_ks^T (lower triangle)
+      for (int ci = tk.y; ci < tk.z; ++ci) {
+        const double* Kp = w.L + (size_t)g.con[ci].y * C::DD * Bp + b;
+#pragma unroll
+        for (int h = 0; h < D; h += H) {
+          double kv[H][D];
+#pragma unroll
+          for (int c = 0; c < H; ++c)
+#pragma unroll
+            for (int j = 0; j < D; ++j) kv[c][j] = Kp[((h + c) * D + j) * Bp];
+          bl_issue_fence();
+#pragma unroll
+          for (int c = 0; c < H; ++c)
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+              for (int j = 0; j <= i; ++j) acc[i][j] = fma(kv[c][i], kv[c][j], acc[i][j]);
+        }
+      }
+    } else {
+      for (int ci = tk.y; ci < tk.z; ++ci) {
+        const int2 cn = g.con[ci];
+        const double* Pp = w.L + (size_t)cn.x * C::DD * Bp + b;
+        const double* Kp = w.L + (size_t)cn.y * C::DD * Bp + b;
+#pragma unroll
+        for (int h = 0; h < D; h += H) {
+          double pv[H][D], kv[H][D];
+#pragma unroll
+          for (int c = 0; c < H; ++c)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              pv[c][j] = Pp[((h + c) * D + j) * Bp];
+              kv[c][j] = Kp[((h + c) * D + j) * Bp];
+            }
+          bl_issue_fence();
+#pragma unroll
+          for (int c = 0; c < H; ++c)
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+              for (int j = 0; j < D; ++j) acc[i][j] = fma(pv[c][i], kv[c][j], acc[i][j]);
+        }
+      }
+    }
+    double* T = w.L + (size_t)tk.x * C::DD * Bp + b;
+    const bool diag = tk.w & 1, fill = tk.w & 2;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        if (diag && i < j) continue;
+        double* t = T + (size_t)(j * D + i) * Bp;
+        *t = fill ? -acc[i][j] : *t - acc[i][j];
+      }
+    return;
+  }
+  // forward-substitution row of column k: x_k -= sum_s L_ks y_s
+  const int k = cols[it - ntask];
+  double acc[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) acc[i] = 0.0;
+  for (int ci = g.fwdp[k]; ci < g.fwdp[k + 1]; ++ci) {
+    const int2 f = g.fwd[ci];
+    const double* Kp = w.L + (size_t)f.x * C::DD * Bp + b;
+    const double* y = w.x + (size_t)f.y * D * Bp + b;
+    double kv[D][D], yv[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      yv[c] = y[c * Bp];
+#pragma unroll
+      for (int i = 0; i < D; ++i) kv[c][i] = Kp[(c * D + i) * Bp];
+    }
+    bl_issue_fence();
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int i = 0; i < D; ++i) acc[i] = fma(kv[c][i], yv[c], acc[i]);
+  }
+  double* xk = w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+  for (int i = 0; i < D; ++i) xk[i * Bp] -= acc[i];
+}
+
+// ---------------------------------------------------------------------------- persistent factorisation
+// One launch per factorisation.  One CTA = one group of GW consecutive elements for ALL levels; units of GW
+// threads (thread = element) take a level's work round robin and levels are separated by __syncthreads, so a
+// group's separator chain at the top of the elimination tree is worked by all units of its CTA instead of one
+// thread per (target, element) behind a per-level launch.
+//   * wide levels (>= coltask_min columns): a unit takes a whole column k -- the diagonal target's updates,
+//     L_kk in registers, the forward-substitution row and y_k = L_kk^-1 x_k, then every below target's updates
+//     solved straight from the accumulators (L_pk = (T_pk - acc) L_kk^-T): each block is read once and
+//     written once, T_kk is never stored.  Same arithmetic (and rounding) as bl_update_rb + bl_factor.
+//   * narrow levels: the contribution lists are split into chunks over all units (partial sums in the slot
+//     scratch, idle during the factorisation, subtracted in chunk order), then the level's blocks are factored
+//     unit by unit (bl_factor's arithmetic: redundant register Cholesky of L_kk per block).
+constexpr int BLP_NT = 256;
+
+struct BLPDev {
+  const int4* bcon;     // [nblk] per block: (contribution begin, end, flags (bit 0 diagonal, bit 1 fill), 0)
+  const int* it_lvl;    // [L+1] narrow levels: their work items
+  const int4* items;    // (target block or -1 = forward row, begin, end, flags | (partial slot + 1) << 8)
+  const int* rd_lvl;    // [L+1] narrow levels: their split reductions
+  const int4* red;      // (target block or -1, first slot, count, flags)
+  const int* lvl_ptr;   // [L+1] columns of each level in lvl_col
+  const int* lvl_col;
+  const int* fac_lvl;   // [L+1] factor items (g.fac) of each level
+  int L, coltask_min;
+};
+
+template <int D>
+__device__ __forceinline__ void bl_chol(double (&a)[D][D], double (&iv)[D], double tol, bool& bad) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double piv = a[j][j];
+#pragma unroll
+    for (int q = 0; q < j; ++q) piv = fma(-a[j][q], a[j][q], piv);
+    if (!(piv > tol)) {
+      bad = true;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    iv[j] = inv;
+    a[j][j] = piv * inv;
+#pragma unroll
+    for (int i = j + 1; i < D; ++i) {
+      double s = a[i][j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) s = fma(-a[i][q], a[j][q], s);
+      a[i][j] = s * inv;
+    }
+  }
+}
+
+// acc[i][j] = sum over the contributions [c0, c1) of (L_ps L_ks^T)(i, j) (diag: lower triangle, L_ks == L_ps),
+// register-blocked, half a block pair per memory round trip
+template <int D>
+__device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int b, int c0, int c1, bool diag,
+                                              double (&acc)[D][D]) {
+  using C = BLC<D>;
+  constexpr int H = D / 2;
+  const size_t Bp = g.Bp;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) acc[i][j] = 0.0;
+  if (diag) {
+    for (int ci = c0; ci < c1; ++ci) {
+      const double* Kp = w.L + (size_t)g.con[ci].y * C::DD * Bp + b;
+#pragma unroll
+      for (int h = 0; h < D; h += H) {
+        double kv[H][D];
+#pragma unroll
+        for (int c = 0; c < H; ++c)
+#pragma unroll
+          for (int j = 0; j < D; ++j) kv[c][j] = Kp[((h + c) * D + j) * Bp];
+        bl_issue_fence();
+#pragma unroll
+        for (int c = 0; c < H; ++c)
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j <= i; ++j) acc[i][j] = fma(kv[c][i], kv[c][j], acc[i][j]);
+      }
+    }
+  } else {
+    for (int ci = c0; ci < c1; ++ci) {
+      const int2 cn = g.con[ci];
+      const double* Pp = w.L + (size_t)cn.x * C::DD * Bp + b;
+      const double* Kp = w.L + (size_t)cn.y * C::DD * Bp + b;
+#pragma unroll
+      for (int h = 0; h < D; h += H) {
+        double pv[H][D], kv[H][D];
+#pragma unroll
+        for (int c = 0; c < H; ++c)
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            pv[c][j] = Pp[((h + c) * D + j) * Bp];
+            kv[c][j] = Kp[((h + c) * D + j) * Bp];
+          }
+        bl_issue_fence();
+#pragma unroll
+        for (int c = 0; c < H; ++c)
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) acc[i][j] = fma(pv[c][i], kv[c][j], acc[i][j]);
+      }
+    }
+  }
+}
+
+// forward-substitution sum of column k over [f0, f1): acc = sum_s L_ks y_s
+template <int D>
+__device__ __forceinline__ void bl_acc_fwd(const BLDev& g, const BLWs& w, int b, int f0, int f1, double (&acc)[D]) {
+  using C = BLC<D>;
+  const size_t Bp = g.Bp;
+#pragma unroll
+  for (int i = 0; i < D; ++i) acc[i] = 0.0;
+  for (int q = f0; q < f1; ++q) {
+    const int2 f = g.fwd[q];
+    const double* Kp = w.L + (size_t)f.x * C::DD * Bp + b;
+    const double* y = w.x + (size_t)f.y * D * Bp + b;
+    double kv[D][D], yv[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      yv[c] = y[c * Bp];
+#pragma unroll
+      for (int i = 0; i < D; ++i) kv[c][i] = Kp[(c * D + i) * Bp];
+    }
+    bl_issue_fence();
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int i = 0; i < D; ++i) acc[i] = fma(kv[c][i], yv[c], acc[i]);
+  }
+}
+
+// L_kk + inverse pivots -> Ld, failure flag, fused y_k = L_kk^-1 x_k
+template <int D>
+__device__ __forceinline__ void bl_store_diag(const BLDev& g, const BLWs& w, int b, int k, const double (&a)[D][D],
+                                              const double (&iv)[D], bool bad, bool fused_fwd) {
+  using C = BLC<D>;
+  const size_t Bp = g.Bp;
+  double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = j; i < D; ++i) Lk[(j * D + i) * Bp] = a[i][j];
+#pragma unroll
+  for (int j = 0; j < D; ++j) Lk[ivpos<D>(0, j, D) * Bp] = iv[j];
+  if (bad) w.fail[b] = 1;
+  if (fused_fwd) {
+    double* xk = w.x + (size_t)k * D * Bp + b;
+    double y[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      double s = xk[q * Bp];
+#pragma unroll
+      for (int r = 0; r < q; ++r) s = fma(-a[q][r], y[r], s);
+      y[q] = s * iv[q];
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) xk[q * Bp] = y[q];
+  }
+}
+
+// L_pk = t L_kk^-T row by row, t given column-major (t[q][r] = entry (r, q)); stored into the block
+template <int D>
+__device__ __forceinline__ void bl_trsm_store(double* Pb, size_t Bp, double (&t)[D][D], const double (&a)[D][D],
+                                              const double (&iv)[D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      double s = t[q][r];
+#pragma unroll
+      for (int j = 0; j < q; ++j) s = fma(-t[j][r], a[q][j], s);
+      t[q][r] = s * iv[q];
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) Pb[(q * D + r) * Bp] = t[q][r];
+  }
+}
+
+// next work index of a unit: dynamic scheduling through a shared counter (the result of an item does not depend
+// on the unit that computes it, so the schedule does not affect the arithmetic)
+template <int GW>
+__device__ __forceinline__ int bl_next(int* ctr, int base) {
+  const int lane = threadIdx.x & 31, lead = lane & ~(GW - 1);
+  const unsigned mask = (GW == 32) ? 0xffffffffu : (((1u << GW) - 1u) << lead);
+  int v = 0;
+  if (lane == lead) v = atomicAdd(ctr, 1);
+  return base + __shfl_sync(mask, v, lead);
+}
+
+template <int D, int GW>
+__global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev pd, int fused_fwd, int l_begin,
+                                                        int l_end) {
+  using C = BLC<D>;
+  __shared__ int ctr[4];
+  const int b = blockIdx.x * GW + (threadIdx.x % GW);
+  const bool act = b < g.B && !bl_frozen(w, b);
+  const size_t Bp = g.Bp;
+  const double tol = act ? 1e-13 * __longlong_as_double((long long)w.maxd[b]) : 0.0;
+  double* part = w.scr;   // partial sums of split items: [slot][DD][Bp]
+  if (threadIdx.x < 4) ctr[threadIdx.x] = 0;
+  __syncthreads();
+  int ph = 0;   // counters rotate over ctr[0..3]; a counter is reset two phases before its reuse
+  auto next = [&](int base) { return bl_next<GW>(&ctr[ph & 3], base); };
+  auto phase_end = [&]() {
+    if (threadIdx.x == 0) ctr[(ph + 2) & 3] = 0;
+    ++ph;
+    __syncthreads();
+  };
+  for (int l = l_begin; l < l_end; ++l) {
+    const int c0 = pd.lvl_ptr[l], c1 = pd.lvl_ptr[l + 1];
+    if (c1 - c0 >= pd.coltask_min) {
+      // ---- wide level: one column per unit
+      // every lane of a unit takes part in the scheduling (frozen elements skip the arithmetic)
+      for (int ci = next(c0); ci < c1; ci = next(c0)) {
+          if (!act) continue;
+          const int k = pd.lvl_col[ci];
+          const int kb0 = g.colptr[k], kb1 = g.colptr[k + 1];
+          double a[D][D], iv[D];
+          {
+            const int4 bc = pd.bcon[kb0];
+            double acc[D][D];
+            bl_acc_target<D>(g, w, b, bc.x, bc.y, true, acc);
+            const double* T = w.L + (size_t)kb0 * C::DD * Bp + b;
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+#pragma unroll
+              for (int i = j; i < D; ++i) a[i][j] = T[(j * D + i) * Bp] - acc[i][j];
+          }
+          bool bad = false;
+          bl_chol<D>(a, iv, tol, bad);
+          if (fused_fwd && g.fwdp[k + 1] > g.fwdp[k]) {
+            double acc[D];
+            bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], acc);
+            double* xk = w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+            for (int i = 0; i < D; ++i) xk[i * Bp] -= acc[i];
+          }
+          bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
+          for (int bi = kb0 + 1; bi < kb1; ++bi) {
+            const int4 bc = pd.bcon[bi];
+            double acc[D][D];
+            bl_acc_target<D>(g, w, b, bc.x, bc.y, false, acc);
+            double* Pb = w.L + (size_t)bi * C::DD * Bp + b;
+            double t[D][D];
+#pragma unroll
+            for (int q = 0; q < D; ++q)
+#pragma unroll
+              for (int r = 0; r < D; ++r) t[q][r] = ((bc.z & 2) ? 0.0 : Pb[(q * D + r) * Bp]) - acc[r][q];
+            bl_trsm_store<D>(Pb, Bp, t, a, iv);
+          }
+        }
+      phase_end();
+      continue;
+    }
+    // ---- narrow level, A: work items (targets / forward rows, long lists in chunks)
+    for (int ii = next(pd.it_lvl[l]); ii < pd.it_lvl[l + 1]; ii = next(pd.it_lvl[l])) {
+        if (!act) continue;
+        const int4 itm = pd.items[ii];
+        const int slot = (itm.w >> 8) - 1;
+        if (itm.x >= 0) {
+          const bool diag = itm.w & 1, fill = itm.w & 2;
+          double acc[D][D];
+          bl_acc_target<D>(g, w, b, itm.y, itm.z, diag, acc);
+          double* T = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.L + (size_t)itm.x * C::DD * Bp + b;
+#pragma unroll
+          for (int j = 0; j < D; ++j)
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              if (diag && i < j) continue;
+              double* t = T + (size_t)(j * D + i) * Bp;
+              *t = slot >= 0 ? acc[i][j] : (fill ? -acc[i][j] : *t - acc[i][j]);
+            }
+        } else if (fused_fwd) {
+          double acc[D];
+          bl_acc_fwd<D>(g, w, b, itm.y, itm.z, acc);
+          const int k = -2 - itm.x;
+          double* X = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+          for (int i = 0; i < D; ++i) X[i * Bp] = slot >= 0 ? acc[i] : X[i * Bp] - acc[i];
+        }
+      }
+    if (pd.rd_lvl[l + 1] > pd.rd_lvl[l]) {
+      phase_end();
+      // ---- R: split items, partials subtracted in chunk order
+      for (int ri = next(pd.rd_lvl[l]); ri < pd.rd_lvl[l + 1]; ri = next(pd.rd_lvl[l])) {
+          if (!act) continue;
+          const int4 rd = pd.red[ri];
+          if (rd.x >= 0) {
+            const bool diag = rd.w & 1, fill = rd.w & 2;
+            double* T = w.L + (size_t)rd.x * C::DD * Bp + b;
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+#pragma unroll
+              for (int i = 0; i < D; ++i) {
+                if (diag && i < j) continue;
+                double v = fill ? 0.0 : T[(j * D + i) * Bp];
+                for (int q = 0; q < rd.z; ++q) v -= part[((size_t)(rd.y + q) * C::DD + j * D + i) * Bp + b];
+                T[(j * D + i) * Bp] = v;
+              }
+          } else if (fused_fwd) {
+            double* xk = w.x + (size_t)(-2 - rd.x) * D * Bp + b;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              double v = xk[i * Bp];
+              for (int q = 0; q < rd.z; ++q) v -= part[((size_t)(rd.y + q) * C::DD + i) * Bp + b];
+              xk[i * Bp] = v;
+            }
+          }
+        }
+    }
+    phase_end();
+    // ---- F: the level's blocks (bl_factor's arithmetic)
+    for (int fi = next(pd.fac_lvl[l]); fi < pd.fac_lvl[l + 1]; fi = next(pd.fac_lvl[l])) {
+        if (!act) continue;
+        const int2 f = g.fac[fi];
+        const int k = f.x;
+        const int kb0 = g.colptr[k];
+        const double* Kk = w.L + (size_t)kb0 * C::DD * Bp + b;
+        double a[D][D], iv[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+#pragma unroll
+          for (int i = j; i < D; ++i) a[i][j] = Kk[(j * D + i) * Bp];
+        bool bad = false;
+        bl_chol<D>(a, iv, tol, bad);
+        if (f.y == kb0) {
+          bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
+        } else {
+          double* Pb = w.L + (size_t)f.y * C::DD * Bp + b;
+          double t[D][D];
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+#pragma unroll
+            for (int r = 0; r < D; ++r) t[q][r] = Pb[(q * D + r) * Bp];
+          bl_trsm_store<D>(Pb, Bp, t, a, iv);
+        }
+      }
+    phase_end();
+  }
+}
+
+// ---------------------------------------------------------------------------- TMA-fed persistent factorisation
+// bl_persist with the source blocks streamed through shared memory by the tensor-memory accelerator instead of
+// per-thread loads: the factor storage is viewed as a 2-D tensor [nblk * DD rows][Bp elements] and one
+// cp.async.bulk.tensor.2d copies the (DD x GW) tile of a block for a unit's GW elements (GW * 8 contiguous
+// bytes per row) into a stage of the unit's ring.  The unit's leader lane runs S contributions ahead of the
+// unit's arithmetic (per stage one mbarrier with the transaction count of its one or two tiles), so a unit
+// keeps S block pairs in flight without holding them in registers, and the arithmetic reads its element's
+// column of a tile from shared memory (lane = element: conflict-free).  Column tasks stream the column's whole
+// contribution range (its blocks' lists are contiguous in `con`, in block order); narrow-level items stream
+// their chunk.  The order of the arithmetic is that of bl_persist (identical results).
+constexpr int BLT_NU = 8;   // units per CTA
+
+struct BLTPipe {
+  double* buf;          // this unit's stages: [S][2][DD][GW]
+  uint64_t* bar;        // [S]
+  uint32_t par;         // parity bit per stage (consumer side)
+  int q_issue, q_use;   // contributions issued / consumed by this unit (stage = q % S)
+};
+
+__device__ __forceinline__ void blt_tile(const CUtensorMap* tm, uint32_t dst, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+// leader lane: issue contribution ci of the stream into stage q % S (diag: only the L_ks tile, into slot 1)
+template <int D, int GW, int S>
+__device__ __forceinline__ void blt_issue(const CUtensorMap* tm, const BLDev& g, BLTPipe& p, int ci, bool diag,
+                                          int x0) {
+  constexpr int TILE = D * D * GW;
+  const int st = p.q_issue % S;
+  const int2 cn = g.con[ci];
+  const uint32_t bar = smem_u32(&p.bar[st]);
+  const uint32_t bytes = (diag ? 1u : 2u) * (uint32_t)TILE * 8u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  double* s0 = p.buf + (size_t)st * 2 * TILE;
+  if (!diag) blt_tile(tm, smem_u32(s0), bar, x0, cn.x * D * D);
+  blt_tile(tm, smem_u32(s0 + TILE), bar, x0, cn.y * D * D);
+  ++p.q_issue;
+}
+
+// the contribution stream of a unit: con indices [c, c1), diagonal (single-tile) while c < cd
+struct BLTCursor {
+  int c, c1, cd;
+};
+
+template <int D, int GW, int S>
+__device__ __forceinline__ void blt_refill(const CUtensorMap* tm, const BLDev& g, BLTPipe& p, BLTCursor& cur,
+                                           bool leader, int x0) {
+  while (p.q_issue - p.q_use < S && cur.c < cur.c1) {
+    if (leader) blt_issue<D, GW, S>(tm, g, p, cur.c, cur.c < cur.cd, x0);
+    else ++p.q_issue;
+    ++cur.c;
+  }
+}
+
+// accumulate the next n contributions of the stream (acc as bl_acc_target), refilling the ring as stages free
+template <int D, int GW, int S>
+__device__ __forceinline__ void blt_acc(const CUtensorMap* tm, const BLDev& g, BLTPipe& p, BLTCursor& cur, int n,
+                                        bool diag, double (&acc)[D][D], int e, bool leader, unsigned umask, int x0) {
+  constexpr int TILE = D * D * GW;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) acc[i][j] = 0.0;
+  for (int q = 0; q < n; ++q) {
+    const int st = p.q_use % S;
+    mbar_wait(&p.bar[st], (p.par >> st) & 1u);
+    p.par ^= 1u << st;
+    const double* P = p.buf + (size_t)st * 2 * TILE + e;
+    const double* K = P + TILE;
+    if (diag) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        double kv[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) kv[j] = K[(c * D + j) * GW];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) acc[i][j] = fma(kv[i], kv[j], acc[i][j]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        double pv[D], kv[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          pv[j] = P[(c * D + j) * GW];
+          kv[j] = K[(c * D + j) * GW];
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) acc[i][j] = fma(pv[i], kv[j], acc[i][j]);
+      }
+    }
+    ++p.q_use;
+    __syncwarp(umask);   // every lane has read the stage before the leader refills it
+    if (leader) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    blt_refill<D, GW, S>(tm, g, p, cur, leader, x0);
+  }
+}
+
+template <int D, int GW, int S>
+__global__ void __launch_bounds__(BLT_NU * GW, 1) bl_persist_tma(const __grid_constant__ CUtensorMap tmL, BLDev g,
+                                                                 BLWs w, BLPDev pd, const int4* ccon, int fused_fwd,
+                                                                 int l_begin, int l_end) {
+  using C = BLC<D>;
+  constexpr int TILE = D * D * GW;
+  extern __shared__ __align__(128) double blt_smem[];
+  __shared__ uint64_t bars[BLT_NU * S];
+  __shared__ int ctr[4];
+  const int u = threadIdx.x / GW, e = threadIdx.x % GW;
+  const int lane = threadIdx.x & 31, lead = lane & ~(GW - 1);
+  const bool leader = lane == lead;
+  const unsigned umask = (GW == 32) ? 0xffffffffu : (((1u << GW) - 1u) << lead);
+  const int b = blockIdx.x * GW + e;
+  const int x0 = blockIdx.x * GW;
+  const bool act = b < g.B && !bl_frozen(w, b);
+  const size_t Bp = g.Bp;
+  const double tol = act ? 1e-13 * __longlong_as_double((long long)w.maxd[b]) : 0.0;
+  double* part = w.scr;
+  BLTPipe p;
+  p.buf = blt_smem + (size_t)u * S * 2 * TILE;
+  p.bar = bars + u * S;
+  p.par = 0;
+  p.q_issue = p.q_use = 0;
+  if (threadIdx.x < BLT_NU * S) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[threadIdx.x])) : "memory");
+  }
+  if (threadIdx.x < 4) ctr[threadIdx.x] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  int ph = 0;
+  auto next = [&](int base) { return bl_next<GW>(&ctr[ph & 3], base); };
+  auto phase_end = [&]() {
+    // the level's generic-proxy stores are read by the next levels' tensor copies
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (threadIdx.x == 0) ctr[(ph + 2) & 3] = 0;
+    ++ph;
+    __syncthreads();
+  };
+  for (int l = l_begin; l < l_end; ++l) {
+    const int c0 = pd.lvl_ptr[l], c1 = pd.lvl_ptr[l + 1];
+    if (c1 - c0 >= pd.coltask_min) {
+      for (int ci = next(c0); ci < c1; ci = next(c0)) {
+        // (the unit's lanes stay together: the scheduling and the pipeline are per unit; a frozen element's
+        // lane runs the pipeline and skips nothing but its stores)
+        const int k = pd.lvl_col[ci];
+        const int kb0 = g.colptr[k], kb1 = g.colptr[k + 1];
+        const int4 cc = ccon[k];
+        BLTCursor cur{cc.x, cc.y, cc.z};
+        blt_refill<D, GW, S>(&tmL, g, p, cur, leader, x0);
+        double a[D][D], iv[D];
+        {
+          const int4 bc = pd.bcon[kb0];
+          double acc[D][D];
+          blt_acc<D, GW, S>(&tmL, g, p, cur, bc.y - bc.x, true, acc, e, leader, umask, x0);
+          const double* T = w.L + (size_t)kb0 * C::DD * Bp + b;
+#pragma unroll
+          for (int j = 0; j < D; ++j)
+#pragma unroll
+            for (int i = j; i < D; ++i) a[i][j] = act ? T[(j * D + i) * Bp] - acc[i][j] : (i == j ? 1.0 : 0.0);
+        }
+        bool bad = false;
+        bl_chol<D>(a, iv, tol, bad);
+        if (act) {
+          if (fused_fwd && g.fwdp[k + 1] > g.fwdp[k]) {
+            double acc[D];
+            bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], acc);
+            double* xk = w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+            for (int i = 0; i < D; ++i) xk[i * Bp] -= acc[i];
+          }
+          bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
+        }
+        for (int bi = kb0 + 1; bi < kb1; ++bi) {
+          const int4 bc = pd.bcon[bi];
+          double acc[D][D];
+          blt_acc<D, GW, S>(&tmL, g, p, cur, bc.y - bc.x, false, acc, e, leader, umask, x0);
+          if (!act) continue;
+          double* Pb = w.L + (size_t)bi * C::DD * Bp + b;
+          double t[D][D];
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+#pragma unroll
+            for (int r = 0; r < D; ++r) t[q][r] = ((bc.z & 2) ? 0.0 : Pb[(q * D + r) * Bp]) - acc[r][q];
+          bl_trsm_store<D>(Pb, Bp, t, a, iv);
+        }
+      }
+      phase_end();
+      continue;
+    }
+    for (int ii = next(pd.it_lvl[l]); ii < pd.it_lvl[l + 1]; ii = next(pd.it_lvl[l])) {
+      const int4 itm = pd.items[ii];
+      const int slot = (itm.w >> 8) - 1;
+      if (itm.x >= 0) {
+        const bool diag = itm.w & 1, fill = itm.w & 2;
+        BLTCursor cur{itm.y, itm.z, diag ? itm.z : itm.y};
+        blt_refill<D, GW, S>(&tmL, g, p, cur, leader, x0);
+        double acc[D][D];
+        blt_acc<D, GW, S>(&tmL, g, p, cur, itm.z - itm.y, diag, acc, e, leader, umask, x0);
+        if (!act) continue;
+        double* T = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.L + (size_t)itm.x * C::DD * Bp + b;
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            if (diag && i < j) continue;
+            double* t = T + (size_t)(j * D + i) * Bp;
+            *t = slot >= 0 ? acc[i][j] : (fill ? -acc[i][j] : *t - acc[i][j]);
+          }
+      } else if (fused_fwd && act) {
+        double acc[D];
+        bl_acc_fwd<D>(g, w, b, itm.y, itm.z, acc);
+        const int k = -2 - itm.x;
+        double* X = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+        for (int i = 0; i < D; ++i) X[i * Bp] = slot >= 0 ? acc[i] : X[i * Bp] - acc[i];
+      }
+    }
+    if (pd.rd_lvl[l + 1] > pd.rd_lvl[l]) {
+      phase_end();
+      for (int ri = next(pd.rd_lvl[l]); ri < pd.rd_lvl[l + 1]; ri = next(pd.rd_lvl[l])) {
+        if (!act) continue;
+        const int4 rd = pd.red[ri];
+        if (rd.x >= 0) {
+          const bool diag = rd.w & 1, fill = rd.w & 2;
+          double* T = w.L + (size_t)rd.x * C::DD * Bp + b;
+#pragma unroll
+          for (int j = 0; j < D; ++j)
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              if (diag && i < j) continue;
+              double v = fill ? 0.0 : T[(j * D + i) * Bp];
+              for (int q = 0; q < rd.z; ++q) v -= part[((size_t)(rd.y + q) * C::DD + j * D + i) * Bp + b];
+              T[(j * D + i) * Bp] = v;
+            }
+        } else if (fused_fwd) {
+          double* xk = w.x + (size_t)(-2 - rd.x) * D * Bp + b;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            double v = xk[i * Bp];
+            for (int q = 0; q < rd.z; ++q) v -= part[((size_t)(rd.y + q) * C::DD + i) * Bp + b];
+            xk[i * Bp] = v;
+          }
+        }
+      }
+    }
+    phase_end();
+    for (int fi = next(pd.fac_lvl[l]); fi < pd.fac_lvl[l + 1]; fi = next(pd.fac_lvl[l])) {
+      if (!act) continue;
+      const int2 f = g.fac[fi];
+      const int k = f.x;
+      const int kb0 = g.colptr[k];
+      const double* Kk = w.L + (size_t)kb0 * C::DD * Bp + b;
+      double a[D][D], iv[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+#pragma unroll
+        for (int i = j; i < D; ++i) a[i][j] = Kk[(j * D + i) * Bp];
+      bool bad = false;
+      bl_chol<D>(a, iv, tol, bad);
+      if (f.y == kb0) {
+        bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
+      } else {
+        double* Pb = w.L + (size_t)f.y * C::DD * Bp + b;
+        double t[D][D];
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+#pragma unroll
+          for (int r = 0; r < D; ++r) t[q][r] = Pb[(q * D + r) * Bp];
+        bl_trsm_store<D>(Pb, Bp, t, a, iv);
+      }
+    }
+    phase_end();
+  }
 }
 
 // level l: item (column k, block): every thread factors L_kk in registers (redundantly; no barrier between
@@ -557,14 +1304,8 @@ __global__ void __launch_bounds__(BL_TPB) bl_finish(BLDev g, BLWs w, int implici
   w.st[b] = s;
 }
 
-// objective at the final poses of an element without the implicit linearisation (S(theta_K))
-__global__ void __launch_bounds__(BL_TPB) bl_final_S(BLDev g, BLWs w) {
-  const int b = blockIdx.x * BL_TPB + threadIdx.x;
-  if (b >= g.B) return;
-  double S = 0.0;
-  for (int s = 0; s < g.E + g.P; ++s) S += w.cost[(size_t)s * g.Bp + b];
-  w.S[b] = S;
-}
+// objective at the final poses of an element without the implicit linearisation (S(theta_K)): per-slot
+// costs, summed by bl_objective (final = 1)
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_cost_only(BLDev g, DevProb pr, BLWs w) {
   int b;
@@ -649,9 +1390,10 @@ __global__ void __launch_bounds__(BL_TPB) bl_bwd_slots(BLDev g, DevProb pr, BLWs
   }
   out[(size_t)slot * Bp + b] = -2.0 * wt * fw * dot;
 }
-// fixed-order batch reduction (or per-element copy) of the interleaved per-slot gradients
+// fixed-order batch reduction (or per-element copy) of the interleaved per-slot gradients: one warp per slot,
+// lane l sums elements l, l + 32, ... in order, then a fixed xor-shuffle tree (deterministic)
 __global__ void bl_reduce_wgrad(int B, int Bp, int E, int P, const double* src, double* ge, double* gp, long long bstride) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (slot >= E + P) return;
   double* dst = slot < E ? ge : gp;
   const int idx = slot < E ? slot : slot - E;
@@ -659,10 +1401,12 @@ __global__ void bl_reduce_wgrad(int B, int Bp, int E, int P, const double* src, 
   const double* s = src + (size_t)slot * Bp;
   if (bstride == 0) {
     double acc = 0.0;
-    for (int b = 0; b < B; ++b) acc += s[b];
-    dst[idx] = acc;
+    for (int b = lane; b < B; b += 32) acc += s[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) dst[idx] = acc;
   } else {
-    for (int b = 0; b < B; ++b) dst[(size_t)b * bstride + idx] = s[b];
+    for (int b = lane; b < B; b += 32) dst[(size_t)b * bstride + idx] = s[b];
   }
 }
 
@@ -674,6 +1418,14 @@ struct BLPlan {
   // host copies of the level schedule (launch sizes)
   std::vector<int> lvl_ptr, tsk_lvl_ptr, fac_lvl_ptr;
   const int* d_lvl_col = nullptr;
+  const int* d_fill0 = nullptr;   // fill blocks without an update task
+  int nfill0 = 0;
+  bool upd_rb = true;   // register-blocked update kernel (DNLS_BL_UPD=0: the row-split one)
+  int persist = -1;     // bl_persist group width (-1 automatic, 0: per-level bl_update* + bl_factor launches)
+  int persist_from = 0; // first level of the persistent launch (the levels below: per-level launches)
+  int tma = 1;          // the persistent launch streams its source blocks by TMA (bl_persist_tma)
+  const int4* d_ccon = nullptr;
+  BLPDev pd{};
   int64_t storage_doubles = 0;   // nblk * DD per element
   ~BLPlan() {
     if (dbuf) cudaFree(dbuf);
@@ -796,8 +1548,95 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     for (int e : kv.second) dup_con.push_back(e);
     dup_ptr.push_back((int)dup_con.size());
   }
+  // fill blocks (no cost writes them): targets of an update task are flagged (tk.w bit 1) -- the
+  // register-blocked update stores -acc there -- the others (none for a well-formed pattern) are zeroed
+  std::vector<char> tasked(pl.nblk, 0);
+  for (size_t t = 0; t < tsk.size(); t += 4) {
+    tasked[tsk[t]] = 1;
+    if (!written[tsk[t]]) tsk[t + 3] |= 2;
+  }
+  std::vector<int32_t> fill0;
   for (int bi = 0; bi < pl.nblk; ++bi)
-    if (!written[bi]) fill.push_back(bi);
+    if (!written[bi]) {
+      fill.push_back(bi);
+      if (!tasked[bi]) fill0.push_back(bi);
+    }
+  // persistent factorisation (bl_persist): per block its contribution range and flags; per narrow level its
+  // work items -- contribution lists longer than the level's chunk size split into chunks with a partial slot
+  // each (level-wide numbering; the partials live in the slot scratch, so the split is disabled where it would
+  // not fit) -- and the split reductions.  Chunk size: the level's contributions spread over ~2 items per unit
+  // of a CTA (16 units), at least 2 contributions per chunk.
+  std::vector<int32_t> bcon(4 * (size_t)pl.nblk, 0);
+  for (size_t t = 0; t < tsk.size(); t += 4) {
+    bcon[4 * (size_t)tsk[t]] = tsk[t + 1];
+    bcon[4 * (size_t)tsk[t] + 1] = tsk[t + 2];
+    bcon[4 * (size_t)tsk[t] + 2] = tsk[t + 3];
+  }
+  int ch_units = 32, ch_min = 2;
+  if (const char* env = std::getenv("DNLS_BL_CH")) sscanf(env, "%d,%d", &ch_units, &ch_min);
+  const size_t scr_doubles = (size_t)(s.E + s.P) * (D == 6 ? BLC<6>::SW : BLC<3>::SW);
+  std::vector<int32_t> it_lvl(L + 1, 0), items, rd_lvl(L + 1, 0), red;
+  for (int l = 0; l < L; ++l) {
+    int nc = 0;
+    for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
+      const int k = lvl_col[i];
+      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) nc += bcon[4 * (size_t)bi + 1] - bcon[4 * (size_t)bi];
+      nc += fwdp[k + 1] - fwdp[k];
+    }
+    int ch = std::max(ch_min, (nc + ch_units - 1) / ch_units);
+    for (int pass = 0; pass < 2; ++pass) {   // pass 1 without splitting if the partials do not fit
+      int nslot = 0;
+      std::vector<int32_t> it_l, rd_l;
+      auto add_item = [&](int tgt, int c0, int c1, int flags) {
+        const int n = c1 - c0, S = (n + ch - 1) / ch;
+        if (S <= 1) {
+          it_l.insert(it_l.end(), {tgt, c0, c1, flags});
+          return;
+        }
+        rd_l.insert(rd_l.end(), {tgt, nslot, S, flags});
+        for (int q = 0; q < S; ++q) {
+          const int a = c0 + (int)((int64_t)n * q / S), e = c0 + (int)((int64_t)n * (q + 1) / S);
+          it_l.insert(it_l.end(), {tgt, a, e, flags | ((nslot + 1) << 8)});
+          ++nslot;
+        }
+      };
+      for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
+        const int k = lvl_col[i];
+        for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi)
+          if (bcon[4 * (size_t)bi + 1] > bcon[4 * (size_t)bi])
+            add_item(bi, bcon[4 * (size_t)bi], bcon[4 * (size_t)bi + 1], bcon[4 * (size_t)bi + 2] & 3);
+        if (fwdp[k + 1] > fwdp[k]) add_item(-2 - k, fwdp[k], fwdp[k + 1], 0);
+      }
+      if (pass == 0 && (size_t)nslot * D * D > scr_doubles) {
+        ch = 1 << 30;
+        continue;
+      }
+      items.insert(items.end(), it_l.begin(), it_l.end());
+      red.insert(red.end(), rd_l.begin(), rd_l.end());
+      break;
+    }
+    it_lvl[l + 1] = (int)items.size() / 4;
+    rd_lvl[l + 1] = (int)red.size() / 4;
+  }
+  std::vector<int32_t> lvl_ptr32(pl.lvl_ptr.begin(), pl.lvl_ptr.end()), fac_lvl32(pl.fac_lvl_ptr.begin(),
+                                                                                   pl.fac_lvl_ptr.end());
+  // per column its whole contribution range (the blocks' lists are contiguous in con, in block order) and the
+  // end of the diagonal block's part: the TMA kernel streams [x, y), single tiles below z
+  std::vector<int32_t> ccon(4 * (size_t)N, 0);
+  for (int k = 0; k < N; ++k) {
+    int lo = -1, hi = -1;
+    for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) {
+      const int a = bcon[4 * (size_t)bi], e = bcon[4 * (size_t)bi + 1];
+      if (e <= a) continue;
+      if (lo < 0) lo = a;
+      else if (a != hi) return "bl_build: column contribution lists not contiguous";
+      hi = e;
+    }
+    if (lo >= 0 && bcon[4 * (size_t)colptr[k]] != lo) return "bl_build: diagonal block without contributions";
+    ccon[4 * (size_t)k] = lo < 0 ? 0 : lo;
+    ccon[4 * (size_t)k + 1] = lo < 0 ? 0 : hi;
+    ccon[4 * (size_t)k + 2] = lo < 0 ? 0 : bcon[4 * (size_t)colptr[k] + 1];
+  }
   // upload (int32 arrays, 16-byte aligned)
   std::vector<int32_t> buf;
   std::vector<size_t> offs;
@@ -809,7 +1648,8 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   };
   add(s.perm); add(s.iperm); add(s.edges); add(s.prior_vars);
   add(colptr); add(blkrow); add(tsk); add(con); add(fwdp); add(fwd); add(fac); add(slotd);
-  add(s.bc_ptr); add(s.bc); add(dup_ptr); add(dup_blk); add(dup_con); add(fill); add(lvl_col);
+  add(s.bc_ptr); add(s.bc); add(dup_ptr); add(dup_blk); add(dup_con); add(fill); add(lvl_col); add(fill0);
+  add(bcon); add(it_lvl); add(items); add(rd_lvl); add(red); add(lvl_ptr32); add(fac_lvl32); add(ccon);
   while (buf.size() % 4) buf.push_back(0);
   if (device >= 0) {
     if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
@@ -835,6 +1675,24 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   g.dup_ptr = ptr(offs[k++]); g.dup_blk = ptr(offs[k++]); g.dup_con = ptr(offs[k++]);
   g.fill = ptr(offs[k++]);
   pl.d_lvl_col = ptr(offs[k++]);
+  pl.d_fill0 = ptr(offs[k++]);
+  pl.nfill0 = (int)fill0.size();
+  pl.pd.bcon = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.pd.it_lvl = ptr(offs[k++]);
+  pl.pd.items = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.pd.rd_lvl = ptr(offs[k++]);
+  pl.pd.red = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.pd.lvl_ptr = ptr(offs[k++]);
+  pl.pd.fac_lvl = ptr(offs[k++]);
+  pl.d_ccon = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.pd.lvl_col = pl.d_lvl_col;
+  pl.pd.L = L;
+  pl.pd.coltask_min = 16;
+  if (const char* env = std::getenv("DNLS_BL_COLTASK")) pl.pd.coltask_min = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_PERSIST")) pl.persist = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_SPLIT")) pl.persist_from = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_TMA")) pl.tma = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_UPD")) pl.upd_rb = std::atoi(env) != 0;
   g.nfill = (int)fill.size();
   g.ndup = (int)dup_blk.size();
   return std::string();
@@ -912,10 +1770,39 @@ void bl_linearize(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, dou
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  bl_reset_iter<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
-  if (g.nfill) bl_zero_fill<<<bl_grid((long long)g.nfill * D * D, g.Bp), BL_TPB, 0, s>>>(g, w, D * D);
-  bl_lin_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
-  bl_lin_poses<D><<<bl_grid(g.N + g.ndup, g.Bp), BL_TPB, 0, s>>>(g, w, lam, damping);
+  DNLS_KL bl_reset_iter<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
+  // the register-blocked update stores its fill targets; the row-split one accumulates into zeroed blocks
+  const int* fl = (pl.upd_rb || pl.persist != 0) ? pl.d_fill0 : g.fill;
+  const int nf = (pl.upd_rb || pl.persist != 0) ? pl.nfill0 : g.nfill;
+  if (nf) DNLS_KL bl_zero_fill<<<bl_grid((long long)nf * D * D, g.Bp), BL_TPB, 0, s>>>(g, w, D * D, fl, nf);
+  DNLS_KL bl_lin_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
+  DNLS_KL bl_lin_poses<D><<<bl_grid(g.N + g.ndup, g.Bp), BL_TPB, 0, s>>>(g, w, lam, damping);
+}
+
+// tensor map of the factor storage viewed as [rows][Bp elements] doubles, box (gw elements x rows_box rows);
+// returns non-zero when the driver entry point is unavailable (the caller falls back to bl_persist)
+inline int blt_tensor_map(CUtensorMap* tm, const double* base, int Bp, size_t rows, int gw, int rows_box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static int tried = 0;
+  if (!tried) {
+    tried = 1;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  }
+  if (!encode) return 1;
+  const cuuint64_t dims[2] = {(cuuint64_t)Bp, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)Bp * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)gw, (cuuint32_t)rows_box};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 2;
 }
 
 template <int D>
@@ -923,14 +1810,46 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  for (int l = 0; l < pl.L; ++l) {
+  const int lsplit = pl.persist != 0 ? std::min(pl.L, std::max(0, pl.persist_from)) : pl.L;
+  for (int l = 0; l < lsplit; ++l) {
     const int t0 = pl.tsk_lvl_ptr[l], nt = pl.tsk_lvl_ptr[l + 1] - t0;
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
     const long long nu = (long long)nt + (fused_fwd ? nc : 0);
-    if (nu > 0)
-      bl_update<D><<<bl_grid_rows(nu, g.Bp), D * 32, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
+    if (nu > 0 && pl.upd_rb)
+      DNLS_KL bl_update_rb<D><<<bl_grid(nu, g.Bp), BL_TPB, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
+    else if (nu > 0)
+      DNLS_KL bl_update<D><<<bl_grid_rows(nu, g.Bp), D * 32, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
     const int f0 = pl.fac_lvl_ptr[l], nf = pl.fac_lvl_ptr[l + 1] - f0;
-    bl_factor<D><<<bl_grid(nf, g.Bp), BL_TPB, 0, s>>>(g, w, f0, nf, fused_fwd ? 1 : 0);
+    DNLS_KL bl_factor<D><<<bl_grid(nf, g.Bp), BL_TPB, 0, s>>>(g, w, f0, nf, fused_fwd ? 1 : 0);
+  }
+  if (lsplit < pl.L) {
+    // levels [lsplit, L) in one persistent launch; group width: the widest of 16 / 8 / 4 elements that still
+    // gives >= 128 CTAs (a sector is 4 doubles)
+    int gw = pl.persist;
+    if (gw < 0) gw = (B + 15) / 16 >= 128 ? 16 : (B + 7) / 8 >= 128 ? 8 : 4;
+    const int ff = fused_fwd ? 1 : 0;
+    if (pl.tma && gw <= 16) {
+      CUtensorMap tm;
+      if (!blt_tensor_map(&tm, w.L, g.Bp, (size_t)pl.nblk * D * D, gw, D * D)) {
+        constexpr int S = 2;
+        const size_t smem = (size_t)BLT_NU * S * 2 * D * D * gw * sizeof(double);
+#define BLT_LAUNCH(GWV)                                                                                      \
+  {                                                                                                          \
+    cudaFuncSetAttribute(bl_persist_tma<D, GWV, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    DNLS_KL bl_persist_tma<D, GWV, S><<<(B + GWV - 1) / GWV, BLT_NU * GWV, smem, s>>>(tm, g, w, pl.pd, pl.d_ccon, ff,   \
+                                                                            lsplit, pl.L);                  \
+  }
+        if (gw == 16) BLT_LAUNCH(16) else if (gw == 8) BLT_LAUNCH(8) else BLT_LAUNCH(4)
+#undef BLT_LAUNCH
+        return;
+      }
+    }
+    switch (gw) {
+      case 32: DNLS_KL bl_persist<D, 32><<<(B + 31) / 32, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
+      case 16: DNLS_KL bl_persist<D, 16><<<(B + 15) / 16, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
+      case 8: DNLS_KL bl_persist<D, 8><<<(B + 7) / 8, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
+      default: DNLS_KL bl_persist<D, 4><<<(B + 3) / 4, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
+    }
   }
 }
 
@@ -942,11 +1861,11 @@ void bl_solve(const BLPlan& pl, int B, const BLWs& w, bool forward, const int* s
   if (forward)
     for (int l = 0; l < pl.L; ++l) {
       const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
-      bl_fsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+      DNLS_KL bl_fsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
     }
   for (int l = pl.L - 1; l >= 0; --l) {
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
-    bl_bsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+    DNLS_KL bl_bsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
   }
 }
 
@@ -958,30 +1877,30 @@ void bl_forward(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, int K
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  bl_init<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
+  DNLS_KL bl_init<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
   for (int k = 0; k < K; ++k) {
     bl_linearize<D>(pl, B, pr, w, -1.0, 0, s);
-    bl_objective<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, early_stop, abs_tol, rel_tol, k > 0 ? 1 : 0, 1);
+    DNLS_KL bl_objective<<<g.Bp / 32, BL_SW * 32, 0, s>>>(g, w, early_stop, abs_tol, rel_tol, k > 0 ? 1 : 0, 1, 0);
     tm.begin(s);
     bl_factor_all<D>(pl, B, w, true, s);
     tm.end(s);
-    bl_check_fail<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+    DNLS_KL bl_check_fail<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
     bl_solve<D>(pl, B, w, false, w.st, s);   // frozen / failed elements skip the solve and the retraction
-    bl_retract<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, alpha);
+    DNLS_KL bl_retract<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, alpha);
   }
   if (implicit) {
-    bl_pre_final<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+    DNLS_KL bl_pre_final<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
     bl_linearize<D>(pl, B, pr, w, -1.0, 0, s);
-    bl_objective<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, 0, abs_tol, rel_tol, 0, 0);
+    DNLS_KL bl_objective<<<g.Bp / 32, BL_SW * 32, 0, s>>>(g, w, 0, abs_tol, rel_tol, 0, 0, 0);
     // the final factor is computed for every element that still has a defined iterate
     tm.begin(s);
     bl_factor_all<D>(pl, B, w, false, s);
     tm.end(s);
   } else {
-    bl_cost_only<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
-    bl_final_S<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+    DNLS_KL bl_cost_only<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
+    DNLS_KL bl_objective<<<g.Bp / 32, BL_SW * 32, 0, s>>>(g, w, 0, abs_tol, rel_tol, 0, 0, 1);
   }
-  bl_finish<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, implicit ? 1 : 0, abs_tol, rel_tol, objective, status, iterations);
+  DNLS_KL bl_finish<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, implicit ? 1 : 0, abs_tol, rel_tol, objective, status, iterations);
 }
 
 // implicit backward on the BL factor of H(theta_K): lambda = H^-1 v, per-slot weight gradients, batch reduction
@@ -991,10 +1910,10 @@ void bl_backward_implicit(const BLPlan& pl, int B, const DevProb& pr, const BLWs
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  bl_bwd_rhs<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, gpose, grad_kind);
+  DNLS_KL bl_bwd_rhs<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, gpose, grad_kind);
   bl_solve<D>(pl, B, w, true, nullptr, s);
-  bl_bwd_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w, w.cost);
+  DNLS_KL bl_bwd_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w, w.cost);
   const int slots = g.E + g.P;
   if (slots > 0 && (ge || gp))
-    bl_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(B, g.Bp, g.E, g.P, w.cost, ge, gp, bstride);
+    DNLS_KL bl_reduce_wgrad<<<(slots + 3) / 4, 128, 0, s>>>(B, g.Bp, g.E, g.P, w.cost, ge, gp, bstride);
 }

@@ -6,8 +6,10 @@
 // grid-wide synchronisation and no per-iteration launches exist.  The stage-level entry points
 // launch thin kernels around the same device phases.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -20,6 +22,12 @@
 #include "../../include/dnls.h"
 #include "phases.cuh"
 #include "symbolic.h"
+
+// every kernel launch of the library is counted (dnls_debug_launch_count; bench.py's gpu_launches)
+namespace dnls {
+extern std::atomic<long long> g_launches;
+}
+#define DNLS_KL ::dnls::g_launches.fetch_add(1, std::memory_order_relaxed),
 
 using namespace dnls;
 
@@ -1220,6 +1228,7 @@ cudaError_t launch_forward_cluster(int CL, int D, const DevGraph& g, DevProb pr,
     cudaError_t e = cudaFuncSetAttribute(k_forward<DD, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                          (int)smem);                                                 \
     if (e != cudaSuccess) return e;                                                                  \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                              \
     return cudaLaunchKernelEx(&cfg, k_forward<DD, CC>, g, pr, ws, fp);                               \
   }
   if (D == 6 && CL == 2) DNLS_LAUNCH_CL(6, 2)
@@ -1231,6 +1240,10 @@ cudaError_t launch_forward_cluster(int CL, int D, const DevGraph& g, DevProb pr,
 }
 }  // namespace dnls
 #else  // the main translation unit: host API
+
+namespace dnls {
+std::atomic<long long> g_launches{0};
+}
 
 namespace {
 // batch-interleaved level-major path (bl.cuh): Gauss-Newton with the
@@ -1305,6 +1318,12 @@ DNLS_API dnls_status dnls_debug_trace(int64_t* out, int32_t capacity, int32_t* c
   if (count) *count = 0;
   return fail(DNLS_E_UNSUPPORTED, "dnls_debug_trace: library built without -DDNLS_TRACE");
 #endif
+}
+
+DNLS_API dnls_status dnls_debug_launch_count(int64_t* count, int32_t reset) {
+  if (!count) return fail(DNLS_E_INVALID, "dnls_debug_launch_count: NULL argument");
+  *count = reset ? (int64_t)dnls::g_launches.exchange(0) : (int64_t)dnls::g_launches.load();
+  return DNLS_OK;
 }
 
 DNLS_API dnls_status dnls_debug_phase_times(const dnls_graph* g, double* ms, int32_t capacity, int32_t* count) {
@@ -1726,7 +1745,7 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
   }
   const int cl = (opt->optimizer == DNLS_DOGLEG || unroll) ? 1 : forward_cluster(g, batch, opt->cluster_ctas);
   if (cl == 1) {
-    DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD, 1>, smem_bytes(g->dg), "k_forward"))) return st; (k_forward<DD, 1><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
+    DISPATCH_D(g->sym.D, if ((st = set_smem(k_forward<DD, 1>, smem_bytes(g->dg), "k_forward"))) return st; (DNLS_KL k_forward<DD, 1><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, fp)));
   } else if (launch_forward_cluster(cl, g->sym.D, g->dg, dev_prob(prob), ws, fp, batch, s) != cudaSuccess) {
     return fail(DNLS_E_CUDA, std::string("dnls_forward: cluster launch: ") + cudaGetErrorString(cudaGetLastError()));
   }
@@ -1770,16 +1789,16 @@ DNLS_API dnls_status dnls_backward_implicit(const dnls_graph* g, int32_t batch, 
   WsLayout l = ws_layout(g->sym, batch);
   DevWs ws = ws_views(l, workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward<DD>, smem_bytes(g->dg), "k_backward"))) return st; (k_backward<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward<DD>, smem_bytes(g->dg), "k_backward"))) return st; (DNLS_KL k_backward<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind)));
   if ((st = cuda_check("dnls_backward_implicit: k_backward launch"))) return st;
   const int slots = g->sym.E + g->sym.P;
   if (slots > 0 && (grad_w_edge || grad_w_prior)) {
-    k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
+    DNLS_KL k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
                                                         grad_w_prior, (long long)grad_bstride);
     if ((st = cuda_check("dnls_backward_implicit: k_reduce_wgrad launch"))) return st;
   }
   if (grad_radius && prob->radius) {
-    k_reduce_radius<<<1, 32, 0, s>>>(batch, g->sym.E, slots, ws.rgrad, grad_radius, (long long)prob->radius_bstride);
+    DNLS_KL k_reduce_radius<<<1, 32, 0, s>>>(batch, g->sym.E, slots, ws.rgrad, grad_radius, (long long)prob->radius_bstride);
     if ((st = cuda_check("dnls_backward_implicit: k_reduce_radius launch"))) return st;
   }
   return DNLS_OK;
@@ -1808,16 +1827,16 @@ DNLS_API dnls_status dnls_backward_dlm(const dnls_graph* g, int32_t batch, const
   WsLayout l = ws_layout(g->sym, batch);
   DevWs ws = ws_views(l, workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward_dlm<DD>, smem_bytes(g->dg), "k_backward_dlm"))) return st; (k_backward_dlm<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind, epsilon)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward_dlm<DD>, smem_bytes(g->dg), "k_backward_dlm"))) return st; (DNLS_KL k_backward_dlm<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses, grad_kind, epsilon)));
   if ((st = cuda_check("dnls_backward_dlm: k_backward_dlm launch"))) return st;
   const int slots = g->sym.E + g->sym.P;
   if (slots > 0 && (grad_w_edge || grad_w_prior)) {
-    k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
+    DNLS_KL k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
                                                         grad_w_prior, (long long)grad_bstride);
     if ((st = cuda_check("dnls_backward_dlm: k_reduce_wgrad launch"))) return st;
   }
   if (grad_radius && prob->radius) {
-    k_reduce_radius<<<1, 32, 0, s>>>(batch, g->sym.E, slots, ws.rgrad, grad_radius, (long long)prob->radius_bstride);
+    DNLS_KL k_reduce_radius<<<1, 32, 0, s>>>(batch, g->sym.E, slots, ws.rgrad, grad_radius, (long long)prob->radius_bstride);
     if ((st = cuda_check("dnls_backward_dlm: k_reduce_radius launch"))) return st;
   }
   return DNLS_OK;
@@ -1850,12 +1869,12 @@ DNLS_API dnls_status dnls_backward_unroll(const dnls_graph* g, int32_t batch, co
   // UNROLL differentiates every recorded iteration; TRUNCATED the last rec.K (= min(T, K)) of them
   const int Tw = rec.K;
   DISPATCH_D(g->sym.D, if ((st = set_smem(k_backward_unroll<DD>, smem_bytes(g->dg), "k_backward_unroll"))) return st;
-             (k_backward_unroll<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses,
+             (DNLS_KL k_backward_unroll<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, grad_poses,
                                                                          grad_kind, Tw, rec.alpha, grad_poses0)));
   if ((st = cuda_check("dnls_backward_unroll: k_backward_unroll launch"))) return st;
   const int slots = g->sym.E + g->sym.P;
   if (slots > 0 && (grad_w_edge || grad_w_prior)) {
-    k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
+    DNLS_KL k_reduce_wgrad<<<(slots + 127) / 128, 128, 0, s>>>(batch, g->sym.E, g->sym.P, ws.cost, grad_w_edge,
                                                         grad_w_prior, (long long)grad_bstride);
     if ((st = cuda_check("dnls_backward_unroll: k_reduce_wgrad launch"))) return st;
   }
@@ -1877,7 +1896,7 @@ DNLS_API dnls_status dnls_linearize(const dnls_graph* g, int32_t batch, const dn
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
   DISPATCH_D(g->sym.D, if ((st = set_smem(k_linearize<DD>, smem_bytes(g->dg), "k_linearize"))) return st;
-             (k_linearize<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, lambda, damping, prob->objective)));
+             (DNLS_KL k_linearize<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, dev_prob(prob), ws, lambda, damping, prob->objective)));
   return cuda_check("dnls_linearize: launch");
 }
 
@@ -1891,7 +1910,7 @@ DNLS_API dnls_status dnls_factorize(const dnls_graph* g, int32_t batch, void* wo
   if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_factorize: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, if ((st = set_smem(k_factorize<DD>, smem_bytes(g->dg), "k_factorize"))) return st; (k_factorize<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, status)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_factorize<DD>, smem_bytes(g->dg), "k_factorize"))) return st; (DNLS_KL k_factorize<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, status)));
   return cuda_check("dnls_factorize: launch");
 }
 
@@ -1905,7 +1924,7 @@ DNLS_API dnls_status dnls_solve_factored(const dnls_graph* g, int32_t batch, voi
   if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_solve_factored: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, if ((st = set_smem(k_solve<DD>, smem_bytes(g->dg), "k_solve"))) return st; (k_solve<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, rhs, x)));
+  DISPATCH_D(g->sym.D, if ((st = set_smem(k_solve<DD>, smem_bytes(g->dg), "k_solve"))) return st; (DNLS_KL k_solve<DD><<<batch, NT, smem_bytes(g->dg), s>>>(g->dg, ws, rhs, x)));
   return cuda_check("dnls_solve_factored: launch");
 }
 
@@ -1919,7 +1938,7 @@ DNLS_API dnls_status dnls_export_factor(const dnls_graph* g, int32_t batch, cons
   if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_export_factor: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), const_cast<void*>(workspace));
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, (k_export_factor<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
+  DISPATCH_D(g->sym.D, (DNLS_KL k_export_factor<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
   return cuda_check("dnls_export_factor: launch");
 }
 
@@ -1934,7 +1953,7 @@ DNLS_API dnls_status dnls_import_matrix(const dnls_graph* g, int32_t batch, cons
   if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_import_matrix: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), workspace);
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, (k_import_matrix<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
+  DISPATCH_D(g->sym.D, (DNLS_KL k_import_matrix<DD><<<batch, NT, 0, s>>>(g->dg, ws, dense)));
   return cuda_check("dnls_import_matrix: launch");
 }
 
@@ -1948,7 +1967,7 @@ DNLS_API dnls_status dnls_export_rhs(const dnls_graph* g, int32_t batch, const v
   if (!dguard.ok) return fail(DNLS_E_CUDA, "dnls_export_rhs: cannot select the graph's device");
   DevWs ws = ws_views(ws_layout(g->sym, batch), const_cast<void*>(workspace));
   cudaStream_t s = (cudaStream_t)stream;
-  DISPATCH_D(g->sym.D, (k_export_rhs<DD><<<batch, NT, 0, s>>>(g->dg, ws, b)));
+  DISPATCH_D(g->sym.D, (DNLS_KL k_export_rhs<DD><<<batch, NT, 0, s>>>(g->dg, ws, b)));
   return cuda_check("dnls_export_rhs: launch");
 }
 

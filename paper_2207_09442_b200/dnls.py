@@ -135,6 +135,12 @@ def dnls_debug_phase_times(g: Graph, capacity: int = 4096) -> list:
     return buf[:n.value].tolist()
 
 
+def dnls_debug_launch_count(reset: bool = False) -> int:
+    n = ctypes.c_int64(0)
+    check(lib().dnls_debug_launch_count(ctypes.byref(n), 1 if reset else 0), "dnls_debug_launch_count")
+    return int(n.value)
+
+
 def dnls_graph_perm(g: Graph) -> np.ndarray:
     a, p = _i32(g.N)
     check(lib().dnls_graph_perm(g.handle, p), "dnls_graph_perm")

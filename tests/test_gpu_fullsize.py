@@ -12,10 +12,11 @@ from paper_2207_09442_b200.layer import PoseGraphSolver
 pytestmark = pytest.mark.gpu
 
 
-def run_full(N, B, K, opt="gn", mode="local", samples=(0, 1), cluster=0, **noise):
+def run_full(N, B, K, opt="gn", mode="local", samples=(0, 1), cluster=0, interleave=0, **noise):
     topo, data = make_case(N, dim=3, p=0.2, mode=mode, seed=0, B=B, **noise)
     solver = PoseGraphSolver(D.SE3, N, topo.edges, topo.prior_vars, device=0, max_iterations=K,
-                             optimizer=D.LM if opt == "lm" else D.GN, cluster_ctas=cluster)
+                             optimizer=D.LM if opt == "lm" else D.GN, cluster_ctas=cluster,
+                             batch_interleave=interleave)
     t = to_dev(data)
     poses, obj, st, it = solver.forward(t["poses0"], t["meas"], t["prior_meas"], t["w_edge"], t["w_prior"],
                                         implicit=True)
@@ -60,6 +61,19 @@ def test_c4_full_size_sampled_parity():
     samples = (0, 255)
     topo, data, P, obj, st, ge, gp, v = run_full(N, B, K, samples=samples)
     assert ((st & 0xff) == 0).all() and np.isfinite(P).all()
+    check_samples(topo, data, P, obj, ge, gp, v, samples, K)
+
+
+def test_c5_full_size_sampled_parity():
+    # BASELINE.json configs[4] at N=1: SE3, 1024 poses, batch 2048 on one GPU, GN K=10 + implicit backward, in
+    # the launch configuration bench.py times (automatic path choice: the batch-interleaved level-major path);
+    # oracle on the first, a middle and the last element
+    N, B, K = 1024, 2048, 10
+    samples = (0, 1031, 2047)
+    topo, data, P, obj, st, ge, gp, v = run_full(N, B, K, samples=samples)
+    assert ((st & 0xff) == 0).all() and np.isfinite(P).all() and np.isfinite(ge).all()
+    R = P[..., :3]
+    assert np.max(np.abs(np.einsum("bnij,bnkj->bnik", R, R) - np.eye(3))) < 1e-12
     check_samples(topo, data, P, obj, ge, gp, v, samples, K)
 
 
