@@ -63,6 +63,26 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def load_fp64_peak():
+    """Measured fp64 peak (profiles/r2_fp64_peak.json: cuBLAS DGEMM 8192^3, tools/fp64_peak.py), else the
+    B200 datasheet label."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_fp64_peak.json")) as f:
+            return float(json.load(f)["dgemm_tflops"]), "measured DGEMM (profiles/r2_fp64_peak.json)"
+    except Exception:
+        return 37.0, "datasheet label (37 TF/s)"
+
+
+def ncu_traffic(config, batch):
+    """ncu DRAM bytes per launch of the dominant kernel recorded for this config and batch (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            ent = json.load(f).get(config)
+        return ent if isinstance(ent, dict) and ent.get("batch") == batch else None
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """Samples SM clock / throttle reasons via NVML every 20 ms while running."""
 
@@ -424,29 +444,18 @@ def main():
         np.savez(f"{args.dump_shard}.rank{rank}.npz", poses=poses.cpu().numpy(), obj=obj.cpu().numpy(),
                  grads=torch.cat([r.reshape(-1) for r in reduced[0]]).cpu().numpy(), b0=b0, b1=b1)
 
-    # ---- roofline of the dominant kernel (k_forward): algorithmic bytes per launch / duration
+    # ---- roofline of the dominant kernel.  Algorithmic bytes per SURVEY.md 8(d): a GN iteration moves
+    # lin + factor + solve + update bytes per element (dnls_graph_stats), a factorisation 16 nnz(L) per element.
     per_iter = st["bytes_linearize"] + st["bytes_factor"] + st["bytes_solve"] + st["bytes_update"]
     alg_bytes = B * (K * per_iter + (0 if (dlm or unroll) else st["bytes_linearize"] + st["bytes_factor"]))
     peak, peak_src = load_peaks()
-    achieved = alg_bytes / Tf / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            tj = json.load(open(tp))
-            ent = tj.get(args.config) if isinstance(tj.get(args.config), dict) else None
-            if ent and ent.get("batch") == B:
-                traffic = ent.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_forward", "peak_source": peak_src,
-                "alg_bytes_per_launch": alg_bytes, "kernel_ms": Tf * 1e3,
-                "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)" + ("" if (dlm or unroll) else "+lin+factor") +
-                        ") per SURVEY.md 8(d); traffic = ncu dram read+write of one launch (profiles/ncu_traffic.json)"}
+    fp64_peak, fp64_src = load_fp64_peak()
+    tent = ncu_traffic(args.config, B)
+    fbytes = 16.0 * st["nnz_L"] * B
+    fflops = float(st["factor_flops"]) * B
 
-    # ---- batch-interleaved path: the factorisation phases of one forward (CUDA events around each of the
-    # K + 1 factorisations, DNLS_PHASE_TIMING) give the factor-kernel roofline of the configuration timed above
+    # the batch-interleaved path: CUDA events around each of the K + 1 factorisations of one forward
+    # (DNLS_PHASE_TIMING) -- the numeric-factorisation kernel of north_star, timed in the configuration above
     os.environ["DNLS_PHASE_TIMING"] = "1"
     poses.copy_(dv["poses0"])
     D.dnls_forward(g, B, opt, prob, ws)
@@ -454,42 +463,56 @@ def main():
     phases = D.dnls_debug_phase_times(g)
     path = "batch-interleaved level-major (bl.cuh)" if phases else "one CTA per element (k_forward)"
     if phases:
-        fbytes = 16.0 * st["nnz_L"] * B
         pm = statistics.median(phases)
-        roofline["kernel"] = "bl_update + bl_factor (one factorisation: all levels)"
-        roofline["kernel_ms"] = pm
-        roofline["alg_bytes_per_launch"] = fbytes
-        roofline["achieved"] = fbytes / (pm / 1e3) / 1e9
-        roofline["frac"] = roofline["achieved"] / peak
-        roofline["note"] = ("batch-interleaved path: the dominant phase is the factorisation (per-level update + "
-                            "factor launches); algorithmic bytes 16 nnz(L) B per factorisation (SURVEY.md 8(d) a3), "
-                            "median over the K+1 factorisations of one forward, CUDA events on the stream")
-        roofline["factorisations_ms"] = phases
-        roofline["forward_alg_bytes_per_launch"] = alg_bytes
-        roofline["forward_frac"] = alg_bytes / Tf / 1e9 / peak
-
-    # ---- factor-only roofline (north_star: "the numeric-factorisation kernel"): dnls_factorize on the
-    # assembled H(theta_0) of the same batch, 16 nnz(L) B algorithmic bytes per launch
-    if not args.no_factor_roofline:
-        fprob = D.make_problem(dv["poses0"], dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"])
-        fts = []
-        for r in range(args.warmup + args.steps):
-            D.dnls_linearize(g, B, fprob, None, D.DAMP_MARQUARDT, ws)
-            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            D.dnls_factorize(g, B, ws, sts)
-            b_.record(stream)
-            if r >= args.warmup:
-                fts.append((a, b_))
-        torch.cuda.synchronize()
-        fms = [a.elapsed_time(b) for a, b in fts]
-        tfac = statistics.median(fms) / 1e3
-        fbytes = 16.0 * st["nnz_L"] * B
-        roofline["factor"] = {"kernel": "k_factorize", "bound": "hbm", "achieved": fbytes / tfac / 1e9,
-                              "peak": peak, "unit": "GB/s", "frac": fbytes / tfac / 1e9 / peak,
-                              "alg_bytes_per_launch": fbytes, "kernel_ms_median": tfac * 1e3,
-                              "kernel_ms_min": min(fms), "flops_per_launch": st["factor_flops"] * B,
-                              "note": "16 nnz(L) B per launch (SURVEY.md 8(d) a3), standalone dnls_factorize"}
+        traffic = tent.get("dram_bytes_per_launch") if tent else None
+        roofline = {
+            "bound": "hbm", "achieved": fbytes / (pm / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": fbytes / (pm / 1e3) / 1e9 / peak, "traffic": traffic,
+            "traffic_over_algorithmic": None if traffic is None else traffic / fbytes,
+            "kernel": "numeric factorisation: per-level bl_update_rb/bl_update + bl_factor, tail levels in one "
+                      "bl_persist launch (one factorisation of the batch)",
+            "peak_source": peak_src, "alg_bytes_per_launch": fbytes, "kernel_ms": pm, "kernel_ms_min": min(phases),
+            "factorisations_ms": phases,
+            "fp64": {"flops_per_launch": fflops, "achieved_tflops": fflops / (pm / 1e3) / 1e12,
+                     "peak_tflops": fp64_peak, "frac": fflops / (pm / 1e3) / 1e12 / fp64_peak,
+                     "peak_source": fp64_src},
+            "forward": {"kernels": "whole dnls_forward (K GN iterations + final factorisation)",
+                        "alg_bytes": alg_bytes, "ms": Tf * 1e3, "frac": alg_bytes / Tf / 1e9 / peak},
+            "traffic_source": tent.get("source") if tent else None,
+            "note": "algorithmic bytes 16 nnz(L) B per factorisation (SURVEY.md 8(d) a3), median over the K+1 "
+                    "factorisations of one forward (CUDA events on the stream); traffic = ncu dram read+write per "
+                    "factorisation (cold-cache launch list, profiles/ncu_traffic.json): the left-looking updates "
+                    "re-read source blocks that do not stay in L2",
+        }
+    else:
+        traffic = tent.get("dram_bytes_per_launch") if tent else None
+        roofline = {"bound": "hbm", "achieved": alg_bytes / Tf / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": alg_bytes / Tf / 1e9 / peak, "traffic": traffic, "kernel": "k_forward",
+                    "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes, "kernel_ms": Tf * 1e3,
+                    "note": "algorithmic bytes = B*(K*(lin+factor+solve+update)" +
+                            ("" if (dlm or unroll) else "+lin+factor") +
+                            ") per SURVEY.md 8(d); traffic = ncu dram read+write of one launch (profiles/ncu_traffic.json)"}
+        # factor-only leg: dnls_factorize on the assembled H(theta_0) of the same batch
+        if not args.no_factor_roofline:
+            fprob = D.make_problem(dv["poses0"], dv["meas"], dv["prior_meas"], dv["w_edge"], dv["w_prior"])
+            fts = []
+            for r in range(args.warmup + args.steps):
+                D.dnls_linearize(g, B, fprob, None, D.DAMP_MARQUARDT, ws)
+                a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                D.dnls_factorize(g, B, ws, sts)
+                b_.record(stream)
+                if r >= args.warmup:
+                    fts.append((a, b_))
+            torch.cuda.synchronize()
+            fms = [a.elapsed_time(b) for a, b in fts]
+            tfac = statistics.median(fms) / 1e3
+            roofline["factor"] = {"kernel": "k_factorize", "bound": "hbm", "achieved": fbytes / tfac / 1e9,
+                                  "peak": peak, "unit": "GB/s", "frac": fbytes / tfac / 1e9 / peak,
+                                  "alg_bytes_per_launch": fbytes, "kernel_ms_median": tfac * 1e3,
+                                  "kernel_ms_min": min(fms), "flops_per_launch": fflops,
+                                  "fp64_frac": fflops / tfac / 1e12 / fp64_peak,
+                                  "note": "16 nnz(L) B per launch (SURVEY.md 8(d) a3), standalone dnls_factorize"}
 
     # ---- e2e through the public API (PoseGraphSolver) with pinned host buffers: H2D of the step's inputs,
     # D2H of theta_K, the objective and the (reduced) gradients

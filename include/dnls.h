@@ -111,8 +111,11 @@ typedef struct dnls_options {
   /* DNLS_BWD_TRUNCATED: number T >= 1 of final GN iterations the backward differentiates through
    * (TBPTT); the workspace keeps min(T, K) iterations.  Ignored by the other modes. */
   int32_t backward_steps;
-  /* Batch elements processed in lockstep by one CTA of dnls_forward (DESIGN.md "batch-interleaved
-   * path"): 0 = automatic, 1 = one element per CTA.  Larger values are chosen by the library only. */
+  /* Path of dnls_forward / dnls_backward_implicit (DESIGN.md §6 "throughput path"): 1 = one CTA per batch
+   * element (fused k_forward, any optimizer / backward mode); 32 = the batch-interleaved level-major path
+   * (element-interleaved factor storage, Gauss-Newton with the implicit or no backward, quadratic costs;
+   * other settings fall back to 1); 0 = automatic: 32 when supported and batch >= 512 (measured crossover,
+   * environment DNLS_BL_MIN_BATCH), else 1.  Results agree to rounding (summation order), tested. */
   int32_t batch_interleave;
 } dnls_options;
 

@@ -765,284 +765,101 @@ __global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev 
   }
 }
 
-// ---------------------------------------------------------------------------- TMA-fed persistent factorisation
-// bl_persist with the source blocks streamed through shared memory by the tensor-memory accelerator instead of
-// per-thread loads: the factor storage is viewed as a 2-D tensor [nblk * DD rows][Bp elements] and one
-// cp.async.bulk.tensor.2d copies the (DD x GW) tile of a block for a unit's GW elements (GW * 8 contiguous
-// bytes per row) into a stage of the unit's ring.  The unit's leader lane runs S contributions ahead of the
-// unit's arithmetic (per stage one mbarrier with the transaction count of its one or two tiles), so a unit
-// keeps S block pairs in flight without holding them in registers, and the arithmetic reads its element's
-// column of a tile from shared memory (lane = element: conflict-free).  Column tasks stream the column's whole
-// contribution range (its blocks' lists are contiguous in `con`, in block order); narrow-level items stream
-// their chunk.  The order of the arithmetic is that of bl_persist (identical results).
-constexpr int BLT_NU = 8;   // units per CTA
-
-struct BLTPipe {
-  double* buf;          // this unit's stages: [S][2][DD][GW]
-  uint64_t* bar;        // [S]
-  uint32_t par;         // parity bit per stage (consumer side)
-  int q_issue, q_use;   // contributions issued / consumed by this unit (stage = q % S)
-};
-
-__device__ __forceinline__ void blt_tile(const CUtensorMap* tm, uint32_t dst, uint32_t bar, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar)
-      : "memory");
-}
-
-// leader lane: issue contribution ci of the stream into stage q % S (diag: only the L_ks tile, into slot 1)
-template <int D, int GW, int S>
-__device__ __forceinline__ void blt_issue(const CUtensorMap* tm, const BLDev& g, BLTPipe& p, int ci, bool diag,
-                                          int x0) {
-  constexpr int TILE = D * D * GW;
-  const int st = p.q_issue % S;
-  const int2 cn = g.con[ci];
-  const uint32_t bar = smem_u32(&p.bar[st]);
-  const uint32_t bytes = (diag ? 1u : 2u) * (uint32_t)TILE * 8u;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  double* s0 = p.buf + (size_t)st * 2 * TILE;
-  if (!diag) blt_tile(tm, smem_u32(s0), bar, x0, cn.x * D * D);
-  blt_tile(tm, smem_u32(s0 + TILE), bar, x0, cn.y * D * D);
-  ++p.q_issue;
-}
-
-// the contribution stream of a unit: con indices [c, c1), diagonal (single-tile) while c < cd
-struct BLTCursor {
-  int c, c1, cd;
-};
-
-template <int D, int GW, int S>
-__device__ __forceinline__ void blt_refill(const CUtensorMap* tm, const BLDev& g, BLTPipe& p, BLTCursor& cur,
-                                           bool leader, int x0) {
-  while (p.q_issue - p.q_use < S && cur.c < cur.c1) {
-    if (leader) blt_issue<D, GW, S>(tm, g, p, cur.c, cur.c < cur.cd, x0);
-    else ++p.q_issue;
-    ++cur.c;
-  }
-}
-
-// accumulate the next n contributions of the stream (acc as bl_acc_target), refilling the ring as stages free
-template <int D, int GW, int S>
-__device__ __forceinline__ void blt_acc(const CUtensorMap* tm, const BLDev& g, BLTPipe& p, BLTCursor& cur, int n,
-                                        bool diag, double (&acc)[D][D], int e, bool leader, unsigned umask, int x0) {
-  constexpr int TILE = D * D * GW;
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) acc[i][j] = 0.0;
-  for (int q = 0; q < n; ++q) {
-    const int st = p.q_use % S;
-    mbar_wait(&p.bar[st], (p.par >> st) & 1u);
-    p.par ^= 1u << st;
-    const double* P = p.buf + (size_t)st * 2 * TILE + e;
-    const double* K = P + TILE;
-    if (diag) {
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        double kv[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) kv[j] = K[(c * D + j) * GW];
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-          for (int j = 0; j <= i; ++j) acc[i][j] = fma(kv[i], kv[j], acc[i][j]);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        double pv[D], kv[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          pv[j] = P[(c * D + j) * GW];
-          kv[j] = K[(c * D + j) * GW];
-        }
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-          for (int j = 0; j < D; ++j) acc[i][j] = fma(pv[i], kv[j], acc[i][j]);
-      }
-    }
-    ++p.q_use;
-    __syncwarp(umask);   // every lane has read the stage before the leader refills it
-    if (leader) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    blt_refill<D, GW, S>(tm, g, p, cur, leader, x0);
-  }
-}
-
-template <int D, int GW, int S>
-__global__ void __launch_bounds__(BLT_NU * GW, 1) bl_persist_tma(const __grid_constant__ CUtensorMap tmL, BLDev g,
-                                                                 BLWs w, BLPDev pd, const int4* ccon, int fused_fwd,
-                                                                 int l_begin, int l_end) {
+// persistent triangular solves over a level range (the single-column tail of the tree): one CTA per group of
+// GW elements; per column the units split the column's list (backward: its below blocks, forward: its
+// forward-substitution contributions), partial sums in shared memory added in unit order, unit 0 applies
+// L_kk^-T / L_kk^-1.  Backward runs the levels root -> l_begin, forward l_begin -> root.
+template <int D, int GW>
+__global__ void __launch_bounds__(BLP_NT) bl_persist_solve(BLDev g, BLWs w, BLPDev pd, const int* skip, int forward,
+                                                           int l_begin, int l_end) {
   using C = BLC<D>;
-  constexpr int TILE = D * D * GW;
-  extern __shared__ __align__(128) double blt_smem[];
-  __shared__ uint64_t bars[BLT_NU * S];
-  __shared__ int ctr[4];
+  constexpr int U = BLP_NT / GW;
+  __shared__ double part[U][D][GW];
   const int u = threadIdx.x / GW, e = threadIdx.x % GW;
-  const int lane = threadIdx.x & 31, lead = lane & ~(GW - 1);
-  const bool leader = lane == lead;
-  const unsigned umask = (GW == 32) ? 0xffffffffu : (((1u << GW) - 1u) << lead);
   const int b = blockIdx.x * GW + e;
-  const int x0 = blockIdx.x * GW;
-  const bool act = b < g.B && !bl_frozen(w, b);
+  const bool act = b < g.B && !(skip && skip[b]);
   const size_t Bp = g.Bp;
-  const double tol = act ? 1e-13 * __longlong_as_double((long long)w.maxd[b]) : 0.0;
-  double* part = w.scr;
-  BLTPipe p;
-  p.buf = blt_smem + (size_t)u * S * 2 * TILE;
-  p.bar = bars + u * S;
-  p.par = 0;
-  p.q_issue = p.q_use = 0;
-  if (threadIdx.x < BLT_NU * S) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[threadIdx.x])) : "memory");
-  }
-  if (threadIdx.x < 4) ctr[threadIdx.x] = 0;
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  int ph = 0;
-  auto next = [&](int base) { return bl_next<GW>(&ctr[ph & 3], base); };
-  auto phase_end = [&]() {
-    // the level's generic-proxy stores are read by the next levels' tensor copies
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    if (threadIdx.x == 0) ctr[(ph + 2) & 3] = 0;
-    ++ph;
-    __syncthreads();
-  };
-  for (int l = l_begin; l < l_end; ++l) {
-    const int c0 = pd.lvl_ptr[l], c1 = pd.lvl_ptr[l + 1];
-    if (c1 - c0 >= pd.coltask_min) {
-      for (int ci = next(c0); ci < c1; ci = next(c0)) {
-        // (the unit's lanes stay together: the scheduling and the pipeline are per unit; a frozen element's
-        // lane runs the pipeline and skips nothing but its stores)
-        const int k = pd.lvl_col[ci];
-        const int kb0 = g.colptr[k], kb1 = g.colptr[k + 1];
-        const int4 cc = ccon[k];
-        BLTCursor cur{cc.x, cc.y, cc.z};
-        blt_refill<D, GW, S>(&tmL, g, p, cur, leader, x0);
-        double a[D][D], iv[D];
-        {
-          const int4 bc = pd.bcon[kb0];
-          double acc[D][D];
-          blt_acc<D, GW, S>(&tmL, g, p, cur, bc.y - bc.x, true, acc, e, leader, umask, x0);
-          const double* T = w.L + (size_t)kb0 * C::DD * Bp + b;
+  const int nl = l_end - l_begin;
+  for (int li = 0; li < nl; ++li) {
+    const int l = forward ? l_begin + li : l_end - 1 - li;
+    for (int ci = pd.lvl_ptr[l]; ci < pd.lvl_ptr[l + 1]; ++ci) {
+      const int k = pd.lvl_col[ci];
+      double acc[D];
 #pragma unroll
-          for (int j = 0; j < D; ++j)
+      for (int i = 0; i < D; ++i) acc[i] = 0.0;
+      if (act) {
+        if (forward) {
+          for (int q = g.fwdp[k] + u; q < g.fwdp[k + 1]; q += U) {
+            const int2 f = g.fwd[q];
+            const double* Kp = w.L + (size_t)f.x * C::DD * Bp + b;
+            const double* y = w.x + (size_t)f.y * D * Bp + b;
+            double kv[D][D], yv[D];
 #pragma unroll
-            for (int i = j; i < D; ++i) a[i][j] = act ? T[(j * D + i) * Bp] - acc[i][j] : (i == j ? 1.0 : 0.0);
-        }
-        bool bad = false;
-        bl_chol<D>(a, iv, tol, bad);
-        if (act) {
-          if (fused_fwd && g.fwdp[k + 1] > g.fwdp[k]) {
-            double acc[D];
-            bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], acc);
-            double* xk = w.x + (size_t)k * D * Bp + b;
+            for (int c = 0; c < D; ++c) {
+              yv[c] = y[c * Bp];
 #pragma unroll
-            for (int i = 0; i < D; ++i) xk[i * Bp] -= acc[i];
-          }
-          bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
-        }
-        for (int bi = kb0 + 1; bi < kb1; ++bi) {
-          const int4 bc = pd.bcon[bi];
-          double acc[D][D];
-          blt_acc<D, GW, S>(&tmL, g, p, cur, bc.y - bc.x, false, acc, e, leader, umask, x0);
-          if (!act) continue;
-          double* Pb = w.L + (size_t)bi * C::DD * Bp + b;
-          double t[D][D];
-#pragma unroll
-          for (int q = 0; q < D; ++q)
-#pragma unroll
-            for (int r = 0; r < D; ++r) t[q][r] = ((bc.z & 2) ? 0.0 : Pb[(q * D + r) * Bp]) - acc[r][q];
-          bl_trsm_store<D>(Pb, Bp, t, a, iv);
-        }
-      }
-      phase_end();
-      continue;
-    }
-    for (int ii = next(pd.it_lvl[l]); ii < pd.it_lvl[l + 1]; ii = next(pd.it_lvl[l])) {
-      const int4 itm = pd.items[ii];
-      const int slot = (itm.w >> 8) - 1;
-      if (itm.x >= 0) {
-        const bool diag = itm.w & 1, fill = itm.w & 2;
-        BLTCursor cur{itm.y, itm.z, diag ? itm.z : itm.y};
-        blt_refill<D, GW, S>(&tmL, g, p, cur, leader, x0);
-        double acc[D][D];
-        blt_acc<D, GW, S>(&tmL, g, p, cur, itm.z - itm.y, diag, acc, e, leader, umask, x0);
-        if (!act) continue;
-        double* T = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.L + (size_t)itm.x * C::DD * Bp + b;
-#pragma unroll
-        for (int j = 0; j < D; ++j)
-#pragma unroll
-          for (int i = 0; i < D; ++i) {
-            if (diag && i < j) continue;
-            double* t = T + (size_t)(j * D + i) * Bp;
-            *t = slot >= 0 ? acc[i][j] : (fill ? -acc[i][j] : *t - acc[i][j]);
-          }
-      } else if (fused_fwd && act) {
-        double acc[D];
-        bl_acc_fwd<D>(g, w, b, itm.y, itm.z, acc);
-        const int k = -2 - itm.x;
-        double* X = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.x + (size_t)k * D * Bp + b;
-#pragma unroll
-        for (int i = 0; i < D; ++i) X[i * Bp] = slot >= 0 ? acc[i] : X[i * Bp] - acc[i];
-      }
-    }
-    if (pd.rd_lvl[l + 1] > pd.rd_lvl[l]) {
-      phase_end();
-      for (int ri = next(pd.rd_lvl[l]); ri < pd.rd_lvl[l + 1]; ri = next(pd.rd_lvl[l])) {
-        if (!act) continue;
-        const int4 rd = pd.red[ri];
-        if (rd.x >= 0) {
-          const bool diag = rd.w & 1, fill = rd.w & 2;
-          double* T = w.L + (size_t)rd.x * C::DD * Bp + b;
-#pragma unroll
-          for (int j = 0; j < D; ++j)
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-              if (diag && i < j) continue;
-              double v = fill ? 0.0 : T[(j * D + i) * Bp];
-              for (int q = 0; q < rd.z; ++q) v -= part[((size_t)(rd.y + q) * C::DD + j * D + i) * Bp + b];
-              T[(j * D + i) * Bp] = v;
+              for (int i = 0; i < D; ++i) kv[c][i] = Kp[(c * D + i) * Bp];
             }
-        } else if (fused_fwd) {
-          double* xk = w.x + (size_t)(-2 - rd.x) * D * Bp + b;
+            bl_issue_fence();
 #pragma unroll
-          for (int i = 0; i < D; ++i) {
-            double v = xk[i * Bp];
-            for (int q = 0; q < rd.z; ++q) v -= part[((size_t)(rd.y + q) * C::DD + i) * Bp + b];
-            xk[i * Bp] = v;
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+              for (int i = 0; i < D; ++i) acc[i] = fma(kv[c][i], yv[c], acc[i]);
+          }
+        } else {
+          for (int bi = g.colptr[k] + 1 + u; bi < g.colptr[k + 1]; bi += U) {
+            const double* P0 = w.L + (size_t)bi * C::DD * Bp + b;
+            const double* x0 = w.x + (size_t)g.blkrow[bi] * D * Bp + b;
+            double lv[D][D], xv[D];
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+              xv[q] = x0[q * Bp];
+#pragma unroll
+              for (int c = 0; c < D; ++c) lv[c][q] = P0[(c * D + q) * Bp];
+            }
+            bl_issue_fence();
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+              for (int q = 0; q < D; ++q) acc[c] = fma(lv[c][q], xv[q], acc[c]);
           }
         }
       }
-    }
-    phase_end();
-    for (int fi = next(pd.fac_lvl[l]); fi < pd.fac_lvl[l + 1]; fi = next(pd.fac_lvl[l])) {
-      if (!act) continue;
-      const int2 f = g.fac[fi];
-      const int k = f.x;
-      const int kb0 = g.colptr[k];
-      const double* Kk = w.L + (size_t)kb0 * C::DD * Bp + b;
-      double a[D][D], iv[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j)
+      for (int i = 0; i < D; ++i) part[u][i][e] = acc[i];
+      __syncthreads();
+      if (u == 0 && act) {
+        double* xk = w.x + (size_t)k * D * Bp + b;
+        const double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+        double t[D], y[D];
 #pragma unroll
-        for (int i = j; i < D; ++i) a[i][j] = Kk[(j * D + i) * Bp];
-      bool bad = false;
-      bl_chol<D>(a, iv, tol, bad);
-      if (f.y == kb0) {
-        bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
-      } else {
-        double* Pb = w.L + (size_t)f.y * C::DD * Bp + b;
-        double t[D][D];
+        for (int i = 0; i < D; ++i) {
+          double s = 0.0;
+          for (int v = 0; v < U; ++v) s += part[v][i][e];
+          t[i] = xk[i * Bp] - s;
+        }
+        if (forward) {
 #pragma unroll
-        for (int q = 0; q < D; ++q)
+          for (int q = 0; q < D; ++q) {
+            double s2 = t[q];
 #pragma unroll
-          for (int r = 0; r < D; ++r) t[q][r] = Pb[(q * D + r) * Bp];
-        bl_trsm_store<D>(Pb, Bp, t, a, iv);
+            for (int r = 0; r < q; ++r) s2 = fma(-Lk[(r * D + q) * Bp], y[r], s2);
+            y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+          }
+        } else {
+#pragma unroll
+          for (int q = D - 1; q >= 0; --q) {
+            double s2 = t[q];
+#pragma unroll
+            for (int p = q + 1; p < D; ++p) s2 = fma(-Lk[(q * D + p) * Bp], y[p], s2);
+            y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) xk[i * Bp] = y[i];
       }
+      __syncthreads();
     }
-    phase_end();
   }
 }
 
@@ -1420,11 +1237,11 @@ struct BLPlan {
   const int* d_lvl_col = nullptr;
   const int* d_fill0 = nullptr;   // fill blocks without an update task
   int nfill0 = 0;
-  bool upd_rb = true;   // register-blocked update kernel (DNLS_BL_UPD=0: the row-split one)
+  int upd = -1;         // update kernel below the persistent levels: -1 automatic, 0 row-split, 1 register-blocked
   int persist = -1;     // bl_persist group width (-1 automatic, 0: per-level bl_update* + bl_factor launches)
-  int persist_from = 0; // first level of the persistent launch (the levels below: per-level launches)
-  int tma = 1;          // the persistent launch streams its source blocks by TMA (bl_persist_tma)
-  const int4* d_ccon = nullptr;
+  int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
+  int tail_from = 0;      // first level of the single-column tail
+
   BLPDev pd{};
   int64_t storage_doubles = 0;   // nblk * DD per element
   ~BLPlan() {
@@ -1620,23 +1437,6 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   }
   std::vector<int32_t> lvl_ptr32(pl.lvl_ptr.begin(), pl.lvl_ptr.end()), fac_lvl32(pl.fac_lvl_ptr.begin(),
                                                                                    pl.fac_lvl_ptr.end());
-  // per column its whole contribution range (the blocks' lists are contiguous in con, in block order) and the
-  // end of the diagonal block's part: the TMA kernel streams [x, y), single tiles below z
-  std::vector<int32_t> ccon(4 * (size_t)N, 0);
-  for (int k = 0; k < N; ++k) {
-    int lo = -1, hi = -1;
-    for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) {
-      const int a = bcon[4 * (size_t)bi], e = bcon[4 * (size_t)bi + 1];
-      if (e <= a) continue;
-      if (lo < 0) lo = a;
-      else if (a != hi) return "bl_build: column contribution lists not contiguous";
-      hi = e;
-    }
-    if (lo >= 0 && bcon[4 * (size_t)colptr[k]] != lo) return "bl_build: diagonal block without contributions";
-    ccon[4 * (size_t)k] = lo < 0 ? 0 : lo;
-    ccon[4 * (size_t)k + 1] = lo < 0 ? 0 : hi;
-    ccon[4 * (size_t)k + 2] = lo < 0 ? 0 : bcon[4 * (size_t)colptr[k] + 1];
-  }
   // upload (int32 arrays, 16-byte aligned)
   std::vector<int32_t> buf;
   std::vector<size_t> offs;
@@ -1649,7 +1449,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   add(s.perm); add(s.iperm); add(s.edges); add(s.prior_vars);
   add(colptr); add(blkrow); add(tsk); add(con); add(fwdp); add(fwd); add(fac); add(slotd);
   add(s.bc_ptr); add(s.bc); add(dup_ptr); add(dup_blk); add(dup_con); add(fill); add(lvl_col); add(fill0);
-  add(bcon); add(it_lvl); add(items); add(rd_lvl); add(red); add(lvl_ptr32); add(fac_lvl32); add(ccon);
+  add(bcon); add(it_lvl); add(items); add(rd_lvl); add(red); add(lvl_ptr32); add(fac_lvl32);
   while (buf.size() % 4) buf.push_back(0);
   if (device >= 0) {
     if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
@@ -1684,15 +1484,16 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.pd.red = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.pd.lvl_ptr = ptr(offs[k++]);
   pl.pd.fac_lvl = ptr(offs[k++]);
-  pl.d_ccon = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.pd.lvl_col = pl.d_lvl_col;
   pl.pd.L = L;
   pl.pd.coltask_min = 16;
   if (const char* env = std::getenv("DNLS_BL_COLTASK")) pl.pd.coltask_min = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_PERSIST")) pl.persist = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_SPLIT")) pl.persist_from = std::atoi(env);
-  if (const char* env = std::getenv("DNLS_BL_TMA")) pl.tma = std::atoi(env);
-  if (const char* env = std::getenv("DNLS_BL_UPD")) pl.upd_rb = std::atoi(env) != 0;
+
+  if (const char* env = std::getenv("DNLS_BL_UPD")) pl.upd = std::atoi(env);
+  pl.tail_from = L;
+  while (pl.tail_from > 0 && pl.lvl_ptr[pl.tail_from] - pl.lvl_ptr[pl.tail_from - 1] == 1) --pl.tail_from;
   g.nfill = (int)fill.size();
   g.ndup = (int)dup_blk.size();
   return std::string();
@@ -1765,6 +1566,25 @@ struct BLPhaseTimer {
 };
 
 // linearise + assemble at the current poses (lam > 0: damping), objective into w.S
+// launch schedule of a factorisation for a batch (measured, profiles/r2_factor_experiments): with >= 1024
+// elements (32 warp groups) every (target, element) thread of the register-blocked update has enough company
+// to cover the memory latency and the single-column tail of the tree runs in one persistent launch (group
+// width: the widest of 16 / 8 / 4 elements giving >= 128 CTAs); smaller batches use the row-split update
+// (6 warps per target) for every level.  Environment overrides: DNLS_BL_UPD, DNLS_BL_PERSIST, DNLS_BL_SPLIT.
+struct BLSched {
+  bool rb;
+  int lsplit, gw;
+};
+inline BLSched bl_schedule(const BLPlan& pl, int B) {
+  const bool large = bl_pad(B) / 32 >= 32;
+  BLSched sc;
+  sc.rb = pl.upd >= 0 ? pl.upd != 0 : large;
+  const bool persist = pl.persist == 0 ? false : (pl.persist > 0 || large);
+  sc.lsplit = !persist ? pl.L : (pl.persist_from >= 0 ? std::min(pl.L, pl.persist_from) : pl.tail_from);
+  sc.gw = pl.persist > 0 ? pl.persist : ((B + 15) / 16 >= 128 ? 16 : (B + 7) / 8 >= 128 ? 8 : 4);
+  return sc;
+}
+
 template <int D>
 void bl_linearize(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, double lam, int damping, cudaStream_t s) {
   BLDev g = pl.dev;
@@ -1772,37 +1592,13 @@ void bl_linearize(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, dou
   g.Bp = bl_pad(B);
   DNLS_KL bl_reset_iter<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
   // the register-blocked update stores its fill targets; the row-split one accumulates into zeroed blocks
-  const int* fl = (pl.upd_rb || pl.persist != 0) ? pl.d_fill0 : g.fill;
-  const int nf = (pl.upd_rb || pl.persist != 0) ? pl.nfill0 : g.nfill;
+  const BLSched sc = bl_schedule(pl, B);
+  const bool zero_all = !sc.rb && sc.lsplit > 0;
+  const int* fl = zero_all ? g.fill : pl.d_fill0;
+  const int nf = zero_all ? g.nfill : pl.nfill0;
   if (nf) DNLS_KL bl_zero_fill<<<bl_grid((long long)nf * D * D, g.Bp), BL_TPB, 0, s>>>(g, w, D * D, fl, nf);
   DNLS_KL bl_lin_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
   DNLS_KL bl_lin_poses<D><<<bl_grid(g.N + g.ndup, g.Bp), BL_TPB, 0, s>>>(g, w, lam, damping);
-}
-
-// tensor map of the factor storage viewed as [rows][Bp elements] doubles, box (gw elements x rows_box rows);
-// returns non-zero when the driver entry point is unavailable (the caller falls back to bl_persist)
-inline int blt_tensor_map(CUtensorMap* tm, const double* base, int Bp, size_t rows, int gw, int rows_box) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  static int tried = 0;
-  if (!tried) {
-    tried = 1;
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    else
-      cudaGetLastError();
-  }
-  if (!encode) return 1;
-  const cuuint64_t dims[2] = {(cuuint64_t)Bp, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)Bp * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)gw, (cuuint32_t)rows_box};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : 2;
 }
 
 template <int D>
@@ -1810,12 +1606,13 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  const int lsplit = pl.persist != 0 ? std::min(pl.L, std::max(0, pl.persist_from)) : pl.L;
+  const BLSched sc = bl_schedule(pl, B);
+  const int lsplit = sc.lsplit;
   for (int l = 0; l < lsplit; ++l) {
     const int t0 = pl.tsk_lvl_ptr[l], nt = pl.tsk_lvl_ptr[l + 1] - t0;
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
     const long long nu = (long long)nt + (fused_fwd ? nc : 0);
-    if (nu > 0 && pl.upd_rb)
+    if (nu > 0 && sc.rb)
       DNLS_KL bl_update_rb<D><<<bl_grid(nu, g.Bp), BL_TPB, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
     else if (nu > 0)
       DNLS_KL bl_update<D><<<bl_grid_rows(nu, g.Bp), D * 32, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
@@ -1825,25 +1622,8 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   if (lsplit < pl.L) {
     // levels [lsplit, L) in one persistent launch; group width: the widest of 16 / 8 / 4 elements that still
     // gives >= 128 CTAs (a sector is 4 doubles)
-    int gw = pl.persist;
-    if (gw < 0) gw = (B + 15) / 16 >= 128 ? 16 : (B + 7) / 8 >= 128 ? 8 : 4;
+    const int gw = sc.gw;
     const int ff = fused_fwd ? 1 : 0;
-    if (pl.tma && gw <= 16) {
-      CUtensorMap tm;
-      if (!blt_tensor_map(&tm, w.L, g.Bp, (size_t)pl.nblk * D * D, gw, D * D)) {
-        constexpr int S = 2;
-        const size_t smem = (size_t)BLT_NU * S * 2 * D * D * gw * sizeof(double);
-#define BLT_LAUNCH(GWV)                                                                                      \
-  {                                                                                                          \
-    cudaFuncSetAttribute(bl_persist_tma<D, GWV, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    DNLS_KL bl_persist_tma<D, GWV, S><<<(B + GWV - 1) / GWV, BLT_NU * GWV, smem, s>>>(tm, g, w, pl.pd, pl.d_ccon, ff,   \
-                                                                            lsplit, pl.L);                  \
-  }
-        if (gw == 16) BLT_LAUNCH(16) else if (gw == 8) BLT_LAUNCH(8) else BLT_LAUNCH(4)
-#undef BLT_LAUNCH
-        return;
-      }
-    }
     switch (gw) {
       case 32: DNLS_KL bl_persist<D, 32><<<(B + 31) / 32, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
       case 16: DNLS_KL bl_persist<D, 16><<<(B + 15) / 16, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
@@ -1858,12 +1638,25 @@ void bl_solve(const BLPlan& pl, int B, const BLWs& w, bool forward, const int* s
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  if (forward)
-    for (int l = 0; l < pl.L; ++l) {
+  const BLSched sc = bl_schedule(pl, B);
+  auto tail = [&](int fwd) {
+    if (sc.lsplit >= pl.L) return;
+    switch (sc.gw) {
+      case 32: DNLS_KL bl_persist_solve<D, 32><<<(B + 31) / 32, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      case 16: DNLS_KL bl_persist_solve<D, 16><<<(B + 15) / 16, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      case 8: DNLS_KL bl_persist_solve<D, 8><<<(B + 7) / 8, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      default: DNLS_KL bl_persist_solve<D, 4><<<(B + 3) / 4, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+    }
+  };
+  if (forward) {
+    for (int l = 0; l < sc.lsplit; ++l) {
       const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
       DNLS_KL bl_fsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
     }
-  for (int l = pl.L - 1; l >= 0; --l) {
+    tail(1);
+  }
+  tail(0);
+  for (int l = sc.lsplit - 1; l >= 0; --l) {
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
     DNLS_KL bl_bsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
   }

@@ -6,7 +6,6 @@
 // grid-wide synchronisation and no per-iteration launches exist.  The stage-level entry points
 // launch thin kernels around the same device phases.
 #include <cuda_runtime.h>
-#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1256,9 +1255,11 @@ bool bl_supported(const dnls_options* opt, const dnls_problem* prob) {
 bool bl_choose(const dnls_graph* g, int batch, const dnls_options* opt, const dnls_problem* prob) {
   if (!opt || opt->batch_interleave == 1 || !bl_supported(opt, prob)) return false;
   if (opt->batch_interleave == 32) return true;
+  // automatic: many problems per GPU (measured crossover); below it one CTA
+  // per element (k_forward) keeps each problem's factor on chip
   (void)g;
-  (void)batch;
-  return false;
+  static const int min_batch = std::getenv("DNLS_BL_MIN_BATCH") ? std::atoi(std::getenv("DNLS_BL_MIN_BATCH")) : 512;
+  return batch >= min_batch;
 }
 size_t bl_ws_bytes(const dnls_graph* g, int batch) {
   const Symbolic& s = g->sym;
