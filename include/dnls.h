@@ -308,7 +308,10 @@ DNLS_API dnls_status dnls_solve_factored(const dnls_graph* g, int32_t batch, voi
  *   export_factor: [B][n][n] permuted order, lower triangle of the storage (H after
  *     dnls_linearize/import, L after dnls_factorize), zeros elsewhere;
  *   import_matrix: [B][n][n] ORIGINAL order symmetric matrix -> storage (pattern entries only);
- *   export_rhs:    [B][N][d] ORIGINAL order b = J^T r from the last dnls_linearize. */
+ *   export_rhs:    [B][N][d] ORIGINAL order b = J^T r from the last dnls_linearize.
+ * dnls_solve_factored and the two exports read the per-element storage: on a workspace whose last
+ * dnls_forward ran the batch-interleaved path (its factor is element-interleaved) they return
+ * DNLS_E_UNSUPPORTED. */
 DNLS_API dnls_status dnls_export_factor(const dnls_graph* g, int32_t batch, const void* workspace,
                                         size_t ws_bytes, double* dense, void* stream);
 DNLS_API dnls_status dnls_import_matrix(const dnls_graph* g, int32_t batch, const double* dense,

@@ -23,6 +23,7 @@ constexpr int BL_TPB = 128;   // threads per block of the BL kernels (4 warps = 
 
 struct BLDev {
   int D, N, E, P, n, nblk, Bp, B;
+  int gmajor;            // bl_update_rb: group-major warp order (DNLS_BL_GMAJOR)
   const int *perm, *iperm, *edges, *prior_vars;
   const int* colptr;     // [N+1] blocks of permuted column k (diagonal block first, then rows ascending)
   const int* blkrow;     // [nblk] row pose of each block
@@ -69,6 +70,16 @@ __device__ __forceinline__ bool bl_item(const BLDev& g, long long nitems, int& b
   return item < nitems;
 }
 __device__ __forceinline__ bool bl_frozen(const BLWs& w, int b) { return w.st[b] != DNLS_ST_OK; }
+// group-major variant: consecutive warps take the items of one group of 32 elements, so the CTAs resident at
+// a time work on few groups and share their source blocks through L2 (g.gmajor)
+__device__ __forceinline__ bool bl_item_gm(const BLDev& g, long long nitems, int& b, long long& item) {
+  const long long t = (long long)blockIdx.x * BL_TPB + threadIdx.x;
+  const long long wp = t >> 5;
+  const long long grp = wp / nitems;
+  item = wp - grp * nitems;
+  b = (int)(grp * 32 + (t & 31));
+  return grp < (g.Bp >> 5);
+}
 
 // DevGraph with only the fields the per-cost device math (slot_jac / eval_slot / slot_cost) reads
 __device__ __forceinline__ DevGraph bl_cost_graph(const BLDev& g) {
@@ -328,7 +339,8 @@ __global__ void __launch_bounds__(BL_TPB) bl_update_rb(BLDev g, BLWs w, int t0, 
   constexpr int H = D / 2;   // source columns per round trip
   int b;
   long long it;
-  if (!bl_item(g, (long long)ntask + (fused_fwd ? ncol : 0), b, it)) return;
+  const long long nit = (long long)ntask + (fused_fwd ? ncol : 0);
+  if (!(g.gmajor ? bl_item_gm(g, nit, b, it) : bl_item(g, nit, b, it))) return;
   if (b >= g.B || bl_frozen(w, b)) return;
   const size_t Bp = g.Bp;
   if (it < ntask) {
@@ -871,7 +883,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_factor(BLDev g, BLWs w, int f0, int
   using C = BLC<D>;
   int b;
   long long it;
-  if (!bl_item(g, nfac, b, it)) return;
+  if (!(g.gmajor ? bl_item_gm(g, nfac, b, it) : bl_item(g, nfac, b, it))) return;
   if (b >= g.B || bl_frozen(w, b)) return;
   const size_t Bp = g.Bp;
   const int2 fi = g.fac[f0 + it];
@@ -1489,6 +1501,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.pd.coltask_min = 16;
   if (const char* env = std::getenv("DNLS_BL_COLTASK")) pl.pd.coltask_min = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_PERSIST")) pl.persist = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_GMAJOR")) g.gmajor = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_SPLIT")) pl.persist_from = std::atoi(env);
 
   if (const char* env = std::getenv("DNLS_BL_UPD")) pl.upd = std::atoi(env);

@@ -103,6 +103,15 @@ struct dnls_graph {
 };
 
 namespace {
+// the stage-level views read the per-element storage: a workspace whose last forward ran the batch-interleaved
+// path holds its factor element-interleaved -- refused instead of read as garbage
+dnls_status per_element_storage(const char* what, const dnls_graph* g, const void* ws) {
+  dnls_graph::FactorRecord rec;
+  if (const_cast<dnls_graph*>(g)->get(ws, rec) && rec.layout == 1)
+    return fail(DNLS_E_UNSUPPORTED, std::string(what) + ": the workspace holds the batch-interleaved factor of the "
+                                    "last dnls_forward (batch_interleave = 1 keeps the per-element layout)");
+  return DNLS_OK;
+}
 // Runs the calling thread's CUDA calls on the graph's device and restores the previous one
 // (the graph's index arrays and the caller's buffers live on that device).
 struct DeviceGuard {
@@ -1919,6 +1928,7 @@ DNLS_API dnls_status dnls_solve_factored(const dnls_graph* g, int32_t batch, voi
                                          const double* rhs, double* x, void* stream) {
   dnls_status st = check_common("dnls_solve_factored", g, batch, workspace, ws_bytes);
   if (st) return st;
+  if ((st = per_element_storage("dnls_solve_factored", g, workspace))) return st;
   if (batch > 0 && (!rhs || !x)) return fail(DNLS_E_INVALID, "dnls_solve_factored: rhs/x is NULL");
   if (batch == 0) return DNLS_OK;
   DeviceGuard dguard(g->device);
@@ -1933,6 +1943,7 @@ DNLS_API dnls_status dnls_export_factor(const dnls_graph* g, int32_t batch, cons
                                         double* dense, void* stream) {
   dnls_status st = check_common("dnls_export_factor", g, batch, workspace, ws_bytes);
   if (st) return st;
+  if ((st = per_element_storage("dnls_export_factor", g, workspace))) return st;
   if (batch > 0 && !dense) return fail(DNLS_E_INVALID, "dnls_export_factor: dense is NULL");
   if (batch == 0) return DNLS_OK;
   DeviceGuard dguard(g->device);
@@ -1962,6 +1973,7 @@ DNLS_API dnls_status dnls_export_rhs(const dnls_graph* g, int32_t batch, const v
                                      double* b, void* stream) {
   dnls_status st = check_common("dnls_export_rhs", g, batch, workspace, ws_bytes);
   if (st) return st;
+  if ((st = per_element_storage("dnls_export_rhs", g, workspace))) return st;
   if (batch > 0 && !b) return fail(DNLS_E_INVALID, "dnls_export_rhs: b is NULL");
   if (batch == 0) return DNLS_OK;
   DeviceGuard dguard(g->device);
