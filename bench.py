@@ -286,7 +286,7 @@ def main():
     ap.add_argument("--epsilon", type=float, default=1e-3, help="DLM epsilon")
     ap.add_argument("--optimizer", default=None, choices=["gn", "lm", "dogleg"],
                     help="override the config's inner optimizer (dogleg: PAPER.md:153 trust region)")
-    ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 8],
+    ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 4, 8],
                     help="CTAs per batch element in the forward (0 = automatic)")
     ap.add_argument("--welsch", type=float, default=None,
                     help="Welsch radius of the Between edges (PAPER.md:168 robust PGO); default: quadratic costs")

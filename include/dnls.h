@@ -98,8 +98,8 @@ typedef struct dnls_options {
   double rel_tol;
   int32_t backward_mode;    /* dnls_backward: IMPLICIT keeps the undamped factor of H(theta_K) */
   int32_t cluster_ctas;     /* CTAs sharing one batch element in dnls_forward: 0 = automatic (a cluster
-                               of 2 CTAs when the batch leaves half the SMs idle and N >= 1024,
-                               DESIGN.md "few large problems"), else 1, 2 or 8 */
+                               of 4 / 2 CTAs when 4B / 2B <= #SMs and N >= 1024,
+                               DESIGN.md "few large problems"), else 1, 2, 4 or 8 */
   /* Dogleg trust region (reading DL1): initial, maximum and
    * minimum radius of the tangent step, defaults 1, 1e4, 1e-10.  Step: the GN point if it lies in
    * the radius, else the scaled gradient (Cauchy point outside) or the dogleg interpolation;

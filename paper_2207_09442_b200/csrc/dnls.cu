@@ -1240,8 +1240,10 @@ cudaError_t launch_forward_cluster(int CL, int D, const DevGraph& g, DevProb pr,
     return cudaLaunchKernelEx(&cfg, k_forward<DD, CC>, g, pr, ws, fp);                               \
   }
   if (D == 6 && CL == 2) DNLS_LAUNCH_CL(6, 2)
+  if (D == 6 && CL == 4) DNLS_LAUNCH_CL(6, 4)
   if (D == 6 && CL == 8) DNLS_LAUNCH_CL(6, 8)
   if (D == 3 && CL == 2) DNLS_LAUNCH_CL(3, 2)
+  if (D == 3 && CL == 4) DNLS_LAUNCH_CL(3, 4)
   if (D == 3 && CL == 8) DNLS_LAUNCH_CL(3, 8)
 #undef DNLS_LAUNCH_CL
   return cudaErrorInvalidValue;
@@ -1292,12 +1294,14 @@ dnls_status bl_plan_for(dnls_graph* g, BLPlan** out) {
 // CTAs per batch element for dnls_forward: a cluster when the
 // batch leaves most SMs idle and the graph has enough work per level to share
 int forward_cluster(const dnls_graph* g, int batch, int req) {
-  if (req == 1 || req == 2 || req == 8) return req;
+  if (req == 1 || req == 2 || req == 4 || req == 8) return req;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // measured on C3 (4096 poses, B = 16): 1 CTA 2.18k, 2 CTAs 2.53k, 8 CTAs 1.62k problem-iter/s --
-  // the cluster barriers and the all-global working set outweigh the wider levels beyond 2
+  // measured on C3 (4096 poses, B = 16; profiles/r2u_c3_cl*.json): 1 CTA 2.40k, 2 CTAs 2.67k, 4 CTAs 2.99k,
+  // 8 CTAs 1.60k problem-iter/s -- beyond 4 the cluster barriers and the all-global working set outweigh the
+  // wider levels
   if (g->sym.N < 1024) return 1;
+  if (batch * 4 <= sms) return 4;
   if (batch * 2 <= sms) return 2;
   return 1;
 }
@@ -1698,8 +1702,9 @@ DNLS_API dnls_status dnls_forward(const dnls_graph* g, int32_t batch, const dnls
     return fail(DNLS_E_INVALID, "dnls_forward: invalid Dogleg trust radii");
   if (opt->damping != DNLS_DAMP_MARQUARDT && opt->damping != DNLS_DAMP_IDENTITY)
     return fail(DNLS_E_INVALID, "dnls_forward: unknown damping");
-  if (opt->cluster_ctas != 0 && opt->cluster_ctas != 1 && opt->cluster_ctas != 2 && opt->cluster_ctas != 8)
-    return fail(DNLS_E_INVALID, "dnls_forward: cluster_ctas must be 0 (automatic), 1, 2 or 8");
+  if (opt->cluster_ctas != 0 && opt->cluster_ctas != 1 && opt->cluster_ctas != 2 && opt->cluster_ctas != 4 &&
+      opt->cluster_ctas != 8)
+    return fail(DNLS_E_INVALID, "dnls_forward: cluster_ctas must be 0 (automatic), 1, 2, 4 or 8");
   dnls_graph* gm = const_cast<dnls_graph*>(g);
   gm->drop(workspace);
   if (batch == 0) return DNLS_OK;
