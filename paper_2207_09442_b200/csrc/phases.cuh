@@ -1152,6 +1152,60 @@ __device__ void level_factor_teams(const Pk& P, const LView& V, double tol, int*
   constexpr int NW = NT / 32;
   const int nsn = P.nsn;
   if (nsn <= 0) return;
+  if constexpr (CL > 1) {
+    // wide panels of a sparse level (the separator supernodes of large problems; C3r's reach ~1554 columns):
+    // a team of at most one CTA would leave the group's other CTAs waiting at the level barrier, so every
+    // thread of the group works on one panel at a time -- per D-column block the redundant diagonal
+    // Cholesky, the TRSM rows and the trailing update split over CL * NT threads, two group barriers.  The
+    // same arithmetic per entry as the team path (identical factor).
+    bool coop = nsn <= 2;
+    if (coop) {
+      bool wide = false;
+      for (int i = 0; i < nsn; ++i) wide |= P.sna[i].w >= 8 * D;
+      coop = wide;
+    }
+    if (coop) {
+      const int gt = crank<CL>() * NT + threadIdx.x, GT = CL * NT;
+      for (int i = 0; i < nsn; ++i) {
+        const int4 sa = P.sna[i];
+        double* Pn = V.at(sa.x);
+        const int m = sa.y, ld = sa.z, w = sa.w;
+        double* xs = x ? x + (size_t)D * P.snb[i].x : nullptr;
+        for (int c0 = 0; c0 < w; c0 += D) {
+          double a[D][D], iv[D];
+          const bool bad = chol_regs<D>(Pn, ld, c0, tol, a, iv);
+          for (int r = c0 + D + gt; r < m; r += GT) trsm_row_regs<D>(Pn, ld, c0, r, a, iv);
+          gsync<CL>();   // every thread has read the unfactored diagonal block, the TRSM rows are written
+          if (gt == 0) {
+            store_diag<D>(Pn, ld, c0, a, iv);
+            if (bad) *fail = 1;
+          }
+          const int r0 = c0 + D;
+          if (r0 < w) {
+            const int nc = w - r0, nr = m - r0, nit = nc * nr;
+            for (int t = gt; t < nit; t += GT) {
+              const int ci = t / nr, ri = t - ci * nr;
+              if (ri < ci) continue;
+              const int c = r0 + ci, r = r0 + ri;
+              double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+              for (int k = 0; k < D; k += 2) {
+                s0 = fma(Pn[(size_t)(c0 + k) * ld + r], Pn[(size_t)(c0 + k) * ld + c], s0);
+                if (k + 1 < D) s1 = fma(Pn[(size_t)(c0 + k + 1) * ld + r], Pn[(size_t)(c0 + k + 1) * ld + c], s1);
+              }
+              Pn[(size_t)c * ld + r] -= s0 + s1;
+            }
+          }
+          gsync<CL>();
+        }
+        if (xs) {
+          if (gt < 32) warp_trsv_lower_w<D>(Pn, ld, w, xs);
+          gsync<CL>();
+        }
+      }
+      return;
+    }
+  }
   const int nsc = (nsn + CL - 1) / CL;   // panels per CTA of the group
   int G;
   if (nsc >= NT) {
