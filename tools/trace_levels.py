@@ -28,8 +28,9 @@ data = synth.cube_batch(topo, cfg["B"], seed=0)
 dev = torch.device("cuda", 0)
 t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in data.items() if k != "gt"}
 opt = {"lm": D.LM, "gn": D.GN}[cfg["opt"]]
+# one CTA per element: the trace buffer lives in the main translation unit (the clustered kernel has its own)
 solver = PoseGraphSolver(D.SE3, topo.num_poses, topo.edges, topo.prior_vars, device=0, max_iterations=K,
-                         optimizer=opt)
+                         optimizer=opt, cluster_ctas=1)
 buf = (ctypes.c_int64 * (2 * 8192))()
 n = ctypes.c_int32()
 _lib.lib().dnls_debug_trace(buf, 8192, ctypes.byref(n))
