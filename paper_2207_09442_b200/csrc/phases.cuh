@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include "lie.cuh"
+#include "symbolic.h"
 
 namespace dnls {
 
@@ -932,21 +933,22 @@ __device__ __forceinline__ void warp_trsv_upper_w(const double* P, int ld, int w
 // prefetched into a double buffer in shared memory by TMA bulk copies one level ahead, so all
 // index reads of the numeric phases hit shared memory.
 struct Pk {
-  int ntasks, ncons, nrows, nfcons, nsn, nsnr, nul, nfl, maxb, level, first, last;
+  int ntasks, ncons, nrows, nfcons, nsn, nsnr, nul, nfl, maxb, level, first, last, nul3;
   const int4 *task4, *con4, *row4, *fcon4, *sna, *snb;
-  const int *snr, *ulane, *flane, *snm, *snw;
+  const int *snr, *ulane, *flane, *ulane3, *snm, *snw;   // ulane: 1-row update items, ulane3: UPD_ROWS-row items
 };
 __device__ __forceinline__ Pk pk_view(const int* b) {
   Pk p;
   const int4 h0 = reinterpret_cast<const int4*>(b)[0], h1 = reinterpret_cast<const int4*>(b)[1];
-  const int4 h2 = reinterpret_cast<const int4*>(b)[2];
+  const int4 h2 = reinterpret_cast<const int4*>(b)[2], h3 = reinterpret_cast<const int4*>(b)[3];
   p.ntasks = h0.x; p.ncons = h0.y; p.nrows = h0.z; p.nfcons = h0.w;
   p.nsn = h1.x; p.nsnr = h1.y; p.nul = h1.z; p.nfl = h1.w;
   p.maxb = h2.x;
+  p.nul3 = h3.x;
   p.level = h2.y;
   p.first = h2.z;
   p.last = h2.w;
-  p.task4 = reinterpret_cast<const int4*>(b) + 3;
+  p.task4 = reinterpret_cast<const int4*>(b) + 4;
   p.con4 = p.task4 + p.ntasks;
   p.row4 = p.con4 + p.ncons;
   p.fcon4 = p.row4 + p.nrows;
@@ -955,7 +957,8 @@ __device__ __forceinline__ Pk pk_view(const int* b) {
   p.snr = reinterpret_cast<const int*>(p.snb + p.nsn);
   p.ulane = p.snr + p.nsnr;
   p.flane = p.ulane + p.nul;
-  p.snm = p.flane + p.nfl;
+  p.ulane3 = p.flane + p.nfl;
+  p.snm = p.ulane3 + p.nul3;
   p.snw = p.snm + p.nsn + 1;
   return p;
 }
@@ -1353,53 +1356,49 @@ __device__ void level_bwd_gather(const Pk& P, const LView& V, double* x) {
   }
 }
 
-// partial row a of update task tk over the contributions ci = lane (mod G) of the task: the G
-// lanes of a group take whole source panels, so their (independent) loads overlap.
-template <int D>
-__device__ __forceinline__ void pk_task_row_partial(const Pk& P, const LView& V, const int4 tk, int a, int lane,
-                                                    int G, double (&acc)[D]) {
+// partial rows a0 .. a0 + R - 1 of update task tk over the contributions ci = lane (mod G) of the task: the G
+// lanes of a group take whole source panels, so their (independent) loads overlap; R rows per item share the
+// loads of the target's column block (R + D loads per R * D FMAs).  Per accumulator the FMAs run over the
+// source columns in order (the same sequence for any R).
+template <int D, int R>
+__device__ __forceinline__ void pk_task_rows_partial(const Pk& P, const LView& V, const int4 tk, int a0, int lane,
+                                                     int G, double (&acc)[R * D]) {
   for (int ci = tk.z + lane; ci < tk.w; ci += G) {
     const int4 c = P.con4[ci];
-    const double* A = V.at(c.x) + a;
+    const double* A = V.at(c.x) + a0;
     const double* Bm = V.at(c.y);
     const size_t ld = c.z;
     int k = 0;
-    for (; k + 6 <= c.w; k += 6) {   // 6 columns (one pose block) of loads in flight: one round trip
-      double av[6], bv[6][D];
-#pragma unroll
-      for (int u = 0; u < 6; ++u) {
-        av[u] = A[(k + u) * ld];
-#pragma unroll
-        for (int q = 0; q < D; ++q) bv[u][q] = Bm[(k + u) * ld + q];
-      }
-#pragma unroll
-      for (int u = 0; u < 6; ++u)
-#pragma unroll
-        for (int q = 0; q < D; ++q) acc[q] = fma(av[u], bv[u][q], acc[q]);
-    }
-    for (; k + 3 <= c.w; k += 3) {
-      double av[3], bv[3][D];
+    for (; k + 3 <= c.w; k += 3) {   // 3 source columns of loads in flight
+      double av[3][R], bv[3][D];
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
-        av[u] = A[(k + u) * ld];
+#pragma unroll
+        for (int r = 0; r < R; ++r) av[u][r] = A[(k + u) * ld + r];
 #pragma unroll
         for (int q = 0; q < D; ++q) bv[u][q] = Bm[(k + u) * ld + q];
       }
 #pragma unroll
       for (int u = 0; u < 3; ++u)
 #pragma unroll
-        for (int q = 0; q < D; ++q) acc[q] = fma(av[u], bv[u][q], acc[q]);
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int q = 0; q < D; ++q) acc[r * D + q] = fma(av[u][r], bv[u][q], acc[r * D + q]);
     }
     for (; k < c.w; ++k) {
-      const double av = A[k * ld];
+      double av[R], bv[D];
 #pragma unroll
-      for (int q = 0; q < D; ++q) acc[q] = fma(av, Bm[k * ld + q], acc[q]);
+      for (int r = 0; r < R; ++r) av[r] = A[k * ld + r];
+#pragma unroll
+      for (int q = 0; q < D; ++q) bv[q] = Bm[k * ld + q];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[r * D + q] = fma(av[r], bv[q], acc[r * D + q]);
     }
   }
 }
 
-// partial forward-substitution sum of scalar row a of pose row rw.x over the contributions
-// ci = lane (mod G)
 template <int D>
 __device__ __forceinline__ double pk_fwd_row_partial(const Pk& P, const LView& V, const double* x, int4 rw, int a,
                                                      int lane, int G) {
@@ -1472,25 +1471,30 @@ __device__ void factor_phase(const DevGraph& g, const LView& L, double* stage, d
 #endif
     const LView V = L.level(stage, lo, hi);
     {   // (U) gather-form updates: item = (task, row a) owns an aligned group of G lanes (lane map)
-      for (int base = crank<CL>() * NT; base < P.nul; base += CL * NT) {
+      constexpr int R = CL == 1 ? UPD_ROWS : 1, IPT = D / R;   // rows per item, items per task
+      const int nul = CL == 1 ? P.nul3 : P.nul;
+      const int* ulane = CL == 1 ? P.ulane3 : P.ulane;
+      for (int base = crank<CL>() * NT; base < nul; base += CL * NT) {
         const int Ln = base + threadIdx.x;
-        const int e = Ln < P.nul ? P.ulane[Ln] : -1;
+        const int e = Ln < nul ? ulane[Ln] : -1;
         const bool valid = e >= 0;
         const int G = valid ? 1 << ((e >> 5) & 7) : 1, lane = valid ? (e & 31) : 0;
         const int item = valid ? e >> 8 : 0;
-        const int t = item / D, a = item - t * D;
-        double acc[D];
-#pragma unroll
-        for (int q = 0; q < D; ++q) acc[q] = 0.0;
+        const int t = item / IPT, a0 = (item - t * IPT) * R;
         const int4 tk = P.ntasks > 0 ? P.task4[t] : make_int4(0, 0, 0, 0);
-#ifndef DNLS_SKIP_U
-        if (valid) pk_task_row_partial<D>(P, V, tk, a, lane, G, acc);
-#endif
-        group_reduce_var<D>(acc, G);
-        if (valid && lane == 0) {
-          double* T = V.at(tk.x) + a;
+        double acc[R * D];
 #pragma unroll
-          for (int q = 0; q < D; ++q) T[(size_t)q * tk.y] -= acc[q];
+        for (int q = 0; q < R * D; ++q) acc[q] = 0.0;
+#ifndef DNLS_SKIP_U
+        if (valid) pk_task_rows_partial<D, R>(P, V, tk, a0, lane, G, acc);
+#endif
+        group_reduce_var<R * D>(acc, G);
+        if (valid && lane == 0) {
+          double* T = V.at(tk.x) + a0;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int q = 0; q < D; ++q) T[(size_t)q * tk.y + r] -= acc[r * D + q];
         }
       }
     }

@@ -582,10 +582,12 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
     };
     auto chunk_ints = [&](const Chunk& c) {
       // header + descriptors + lane maps (upper bound: one lane per work unit, capped at 32) + prefixes
-      int64_t n = 12 + 4LL * ((int64_t)c.tasks.size() + c.ncons + (int64_t)c.rows.size() + c.nfcons +
+      int64_t n = 16 + 4LL * ((int64_t)c.tasks.size() + c.ncons + (int64_t)c.rows.size() + c.nfcons +
                               2LL * (int64_t)c.sns.size()) + c.nsnr;
       const int64_t ui = (int64_t)D * c.tasks.size(), fi = (int64_t)D * c.rows.size();
+      const int64_t u3 = (int64_t)(D / UPD_ROWS) * c.tasks.size();
       n += std::max<int64_t>(ui, std::min<int64_t>(opt.cta_threads, 32 * ui));
+      n += std::max<int64_t>(u3, std::min<int64_t>(opt.cta_threads, 32 * u3));
       n += std::max<int64_t>(fi, std::min<int64_t>(opt.cta_threads, 32 * fi));
       n += 2LL * (c.sns.size() + 1) + 4;
       return n;
@@ -595,17 +597,23 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
       auto push4 = [&](int x0, int x1, int x2, int x3) {
         S.pk.push_back(x0); S.pk.push_back(x1); S.pk.push_back(x2); S.pk.push_back(x3);
       };
-      std::vector<int> uwork, fwork;
-      for (int t : c.tasks)
+      // two lane maps of the update items: one row of a target block per item (the clustered kernels: more
+      // items to spread over the cluster) and UPD_ROWS rows per item (the one-CTA kernel: the rows share the
+      // loads of the target's column block)
+      std::vector<int> uwork, uwork3, fwork;
+      for (int t : c.tasks) {
         for (int a = 0; a < D; ++a) uwork.push_back(S.ut_cptr[t + 1] - S.ut_cptr[t]);
+        for (int a = 0; a < D / UPD_ROWS; ++a) uwork3.push_back(S.ut_cptr[t + 1] - S.ut_cptr[t]);
+      }
       for (int p : c.rows)
         for (int a = 0; a < D; ++a) fwork.push_back(S.fc_ptr[p + 1] - S.fc_ptr[p]);
-      const std::vector<int> ulanes = lane_map(uwork), flanes = lane_map(fwork);
+      const std::vector<int> ulanes = lane_map(uwork), ulanes3 = lane_map(uwork3), flanes = lane_map(fwork);
       int maxb = 0;
       for (int sn : c.sns) maxb = std::max(maxb, S.sn_ncols[sn]);
       push4((int)c.tasks.size(), c.ncons, (int)c.rows.size(), c.nfcons);
       push4((int)c.sns.size(), c.nsnr, (int)ulanes.size(), (int)flanes.size());
       push4(maxb, lv, first ? 1 : 0, last ? 1 : 0);
+      push4((int)ulanes3.size(), 0, 0, 0);
       int ccur = 0;
       for (int t : c.tasks) {
         const int n = S.ut_cptr[t + 1] - S.ut_cptr[t];
@@ -633,6 +641,7 @@ std::string analyze(int D, int N, int E, const int32_t* edges, int P, const int3
         for (int p : S.sn_rows[sn]) S.pk.push_back(p);
       for (int v : ulanes) S.pk.push_back(v);
       for (int v : flanes) S.pk.push_back(v);
+      for (int v : ulanes3) S.pk.push_back(v);
       int pm = 0, pw = 0;
       S.pk.push_back(0);
       for (int sn : c.sns) S.pk.push_back(pm += S.sn_m[sn]);

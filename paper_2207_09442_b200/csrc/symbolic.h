@@ -7,6 +7,10 @@
 #include <string>
 #include <vector>
 
+// rows of a D x D target block per update item of the per-element factorisation (lane map of the level
+// packets; the kernel's gather accumulates UPD_ROWS x D entries per item): 3 -> 2 items per SE3 block
+constexpr int UPD_ROWS = 3;
+
 namespace dnls {
 
 struct SymbolicOptions {

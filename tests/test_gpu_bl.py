@@ -82,3 +82,25 @@ def test_bl_parallel_edges_early_stop_and_failures():
     assert np.all((st & 0xff) == D.ST_NOT_SPD) and np.all(it == 0)
     assert np.array_equal(P, data["poses0"])
     assert np.all(ge == 0) and np.all(gp == 0)
+
+
+@pytest.mark.parametrize("dim,N,B,split,gw", [(3, 64, 37, "4", "4"), (2, 100, 33, "6", "8"), (3, 125, 40, "0", "16")])
+def test_bl_large_batch_schedule_on_small_cases(monkeypatch, dim, N, B, split, gw):
+    # the schedule bench.py's C5 run uses (register-blocked update + persistent tail with chunked update lists
+    # and dynamic unit scheduling + persistent tail solves) forced on small ragged batches, SE2 and SE3,
+    # against the oracle; the plan reads the environment when the graph's batch-interleaved plan is built
+    monkeypatch.setenv("DNLS_BL_UPD", "1")
+    monkeypatch.setenv("DNLS_BL_PERSIST", gw)
+    monkeypatch.setenv("DNLS_BL_SPLIT", split)
+    topo, data = make_case(N, dim=dim, p=0.3, mode="local", seed=N + B, B=B)
+    v = np.random.default_rng(N).standard_normal((B, N, 6 if dim == 3 else 3))
+    P, obj, st, it, ge, gp = solve(topo, data, 6, True, v=v)
+    samples = sorted({0, B // 2, B - 1})
+    sub = {k: (val[samples] if k in ("poses0", "meas", "prior_meas") else val) for k, val in data.items()}
+    res = oracle_results(topo, sub, max_iterations=6, implicit=True)
+    for r, b in zip(res, samples):
+        assert pose_err(P[b], r.x) <= TOL_POSE, b
+        assert abs(obj[b] - r.objective) <= TOL_OBJ * r.objective + 1e-20
+        prob = oracle_problem(topo, sub, samples.index(b))
+        a, c, _ = oimp.implicit_weight_grads(prob, r.x, v[b].reshape(-1), L_K=r.L_final)
+        assert rel_vec_err(np.concatenate([ge[b], gp[b]]), np.concatenate([a, c])) <= TOL_GRAD, b
