@@ -333,10 +333,16 @@ __global__ void __launch_bounds__(D * 32, 3) bl_update(BLDev g, BLWs w, int t0, 
 // the lower triangle.  Fill targets (tk.w & 2: no cost writes them) are stored as -acc, so they need no
 // zeroing pass.  Warps enumerate (item, group of 32 elements) item-major.
 template <int D>
-__global__ void __launch_bounds__(BL_TPB) bl_update_rb(BLDev g, BLWs w, int t0, int ntask, const int* cols, int ncol,
+#ifndef DNLS_RB_MINB
+#define DNLS_RB_MINB 1
+#endif
+__global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_rb(BLDev g, BLWs w, int t0, int ntask, const int* cols, int ncol,
                                                        int fused_fwd) {
   using C = BLC<D>;
-  constexpr int H = D / 2;   // source columns per round trip
+#ifndef DNLS_RB_HD
+#define DNLS_RB_HD 2
+#endif
+  constexpr int H = D / DNLS_RB_HD;   // source columns per round trip
   int b;
   long long it;
   const long long nit = (long long)ntask + (fused_fwd ? ncol : 0);
@@ -1078,6 +1084,62 @@ __global__ void __launch_bounds__(D * 32, 3) bl_bsolve(BLDev g, BLWs w, const in
   for (int q = 0; q < D; ++q) w.x[((size_t)k * D + q) * Bp + b] = y[q];
 }
 
+// backward substitution, column task (large batches): thread per (element, column k of the level), one below
+// block per round trip (D^2 + D loads per D^2 FMAs), the same two interleaved accumulators and order as
+// bl_bsolve (identical results), L_kk^-T applied in registers
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_bsolve_ct(BLDev g, BLWs w, const int* cols, int ncol, const int* skip) {
+  using C = BLC<D>;
+  int b;
+  long long it;
+  if (!bl_item(g, ncol, b, it)) return;
+  if (b >= g.B || (skip && skip[b])) return;
+  const size_t Bp = g.Bp;
+  const int k = cols[it];
+  double acc[2][D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    acc[0][c] = w.x[((size_t)k * D + c) * Bp + b];
+    acc[1][c] = 0.0;
+  }
+  const int b0 = g.colptr[k] + 1, b1 = g.colptr[k + 1];
+  for (int bi = b0; bi < b1; ++bi) {
+    const int h = (bi - b0) & 1;
+    const double* P0 = w.L + (size_t)bi * C::DD * Bp + b;
+    const double* x0 = w.x + (size_t)g.blkrow[bi] * D * Bp + b;
+    double l0[D][D], v0[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      v0[q] = x0[q * Bp];
+#pragma unroll
+      for (int c = 0; c < D; ++c) l0[c][q] = P0[(c * D + q) * Bp];
+    }
+    bl_issue_fence();
+    if (h == 0) {
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[0][c] = fma(-l0[c][q], v0[q], acc[0][c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[1][c] = fma(-l0[c][q], v0[q], acc[1][c]);
+    }
+  }
+  const double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+  double y[D];
+#pragma unroll
+  for (int q = D - 1; q >= 0; --q) {
+    double s2 = acc[0][q] + acc[1][q];
+#pragma unroll
+    for (int p = q + 1; p < D; ++p) s2 = fma(-Lk[(q * D + p) * Bp], y[p], s2);
+    y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) w.x[((size_t)k * D + q) * Bp + b] = y[q];
+}
+
 // ---------------------------------------------------------------------------- retraction (a5)
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_retract(BLDev g, DevProb pr, BLWs w, double alpha) {
@@ -1253,6 +1315,7 @@ struct BLPlan {
   int persist = -1;     // bl_persist group width (-1 automatic, 0: per-level bl_update* + bl_factor launches)
   int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
   int tail_from = 0;      // first level of the single-column tail
+  int bsolve_ct = 0;      // experiment: column-task backward solve on levels with >= this many columns (0: off)
 
   BLPDev pd{};
   int64_t storage_doubles = 0;   // nblk * DD per element
@@ -1505,6 +1568,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   if (const char* env = std::getenv("DNLS_BL_SPLIT")) pl.persist_from = std::atoi(env);
 
   if (const char* env = std::getenv("DNLS_BL_UPD")) pl.upd = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_BSCT")) pl.bsolve_ct = std::atoi(env);
   pl.tail_from = L;
   while (pl.tail_from > 0 && pl.lvl_ptr[pl.tail_from] - pl.lvl_ptr[pl.tail_from - 1] == 1) --pl.tail_from;
   g.nfill = (int)fill.size();
@@ -1671,7 +1735,10 @@ void bl_solve(const BLPlan& pl, int B, const BLWs& w, bool forward, const int* s
   tail(0);
   for (int l = sc.lsplit - 1; l >= 0; --l) {
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
-    DNLS_KL bl_bsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+    if (sc.rb && pl.bsolve_ct && nc >= pl.bsolve_ct)
+      DNLS_KL bl_bsolve_ct<D><<<bl_grid(nc, g.Bp), BL_TPB, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+    else
+      DNLS_KL bl_bsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
   }
 }
 

@@ -159,3 +159,11 @@ def test_workspace_bytes_host_only():
     n8 = D.dnls_workspace_bytes(g, 8)
     st = D.dnls_graph_stats(g)
     assert n8 >= 8 * 8 * st["storage_doubles"] and n8 > n1 > 0
+
+
+def test_launch_counter_host_only():
+    # dnls_debug_launch_count (bench.py's gpu_launches): host-only, read / reset, NULL rejected; no kernel
+    # launches without a GPU, so a reset counter stays 0
+    D.dnls_debug_launch_count(reset=True)
+    assert D.dnls_debug_launch_count() == 0
+    assert _lib.lib().dnls_debug_launch_count(None, 0) == 1   # DNLS_E_INVALID
