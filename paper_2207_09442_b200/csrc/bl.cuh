@@ -334,13 +334,13 @@ __global__ void __launch_bounds__(D * 32, 3) bl_update(BLDev g, BLWs w, int t0, 
 // zeroing pass.  Warps enumerate (item, group of 32 elements) item-major.
 template <int D>
 #ifndef DNLS_RB_MINB
-#define DNLS_RB_MINB 1
+#define DNLS_RB_MINB 3
 #endif
 __global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_rb(BLDev g, BLWs w, int t0, int ntask, const int* cols, int ncol,
                                                        int fused_fwd) {
   using C = BLC<D>;
 #ifndef DNLS_RB_HD
-#define DNLS_RB_HD 2
+#define DNLS_RB_HD 1
 #endif
   constexpr int H = D / DNLS_RB_HD;   // source columns per round trip
   int b;
@@ -452,6 +452,9 @@ __global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_rb(BLDev g, BL
 //     scratch, idle during the factorisation, subtracted in chunk order), then the level's blocks are factored
 //     unit by unit (bl_factor's arithmetic: redundant register Cholesky of L_kk per block).
 constexpr int BLP_NT = 256;
+#ifndef DNLS_PT_HD
+#define DNLS_PT_HD 1   // bl_acc_target: source columns per round trip = D / DNLS_PT_HD
+#endif
 
 struct BLPDev {
   const int4* bcon;     // [nblk] per block: (contribution begin, end, flags (bit 0 diagonal, bit 1 fill), 0)
@@ -495,7 +498,7 @@ template <int D>
 __device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int b, int c0, int c1, bool diag,
                                               double (&acc)[D][D]) {
   using C = BLC<D>;
-  constexpr int H = D / 2;
+  constexpr int H = D / DNLS_PT_HD;
   const size_t Bp = g.Bp;
 #pragma unroll
   for (int i = 0; i < D; ++i)
@@ -894,74 +897,29 @@ __global__ void __launch_bounds__(BL_TPB) bl_factor(BLDev g, BLWs w, int f0, int
   const size_t Bp = g.Bp;
   const int2 fi = g.fac[f0 + it];
   const int k = fi.x;
+  const bool diag = fi.y == g.colptr[k];
   const double* Kk = w.L + (size_t)g.colptr[k] * C::DD * Bp + b;
+  double* Pb = w.L + (size_t)fi.y * C::DD * Bp + b;
   const double tol = 1e-13 * __longlong_as_double((long long)w.maxd[b]);
-  double a[D][D], iv[D];
+  // T_kk and (a below item) the whole T_pk in one memory round trip, before any store
+  double a[D][D], iv[D], t[D][D];
 #pragma unroll
   for (int j = 0; j < D; ++j)
 #pragma unroll
     for (int i = j; i < D; ++i) a[i][j] = Kk[(j * D + i) * Bp];
-  bool bad = false;
+  if (!diag) {
 #pragma unroll
-  for (int j = 0; j < D; ++j) {
-    double piv = a[j][j];
+    for (int q = 0; q < D; ++q)
 #pragma unroll
-    for (int q = 0; q < j; ++q) piv = fma(-a[j][q], a[j][q], piv);
-    if (!(piv > tol)) {
-      bad = true;
-      piv = 1.0;
-    }
-    const double inv = rsqrt(piv);
-    iv[j] = inv;
-    a[j][j] = piv * inv;
-#pragma unroll
-    for (int i = j + 1; i < D; ++i) {
-      double s = a[i][j];
-#pragma unroll
-      for (int q = 0; q < j; ++q) s = fma(-a[i][q], a[j][q], s);
-      a[i][j] = s * inv;
-    }
+      for (int r = 0; r < D; ++r) t[q][r] = Pb[(q * D + r) * Bp];
   }
-  if (fi.y == g.colptr[k]) {
-    double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
-#pragma unroll
-    for (int j = 0; j < D; ++j)
-#pragma unroll
-      for (int i = j; i < D; ++i) Lk[(j * D + i) * Bp] = a[i][j];
-#pragma unroll
-    for (int j = 0; j < D; ++j) Lk[ivpos<D>(0, j, D) * Bp] = iv[j];
-    if (bad) w.fail[b] = 1;
-    if (fused_fwd) {
-      double* xk = w.x + (size_t)k * D * Bp + b;
-      double y[D];
-#pragma unroll
-      for (int q = 0; q < D; ++q) {
-        double s = xk[q * Bp];
-#pragma unroll
-        for (int r = 0; r < q; ++r) s = fma(-a[q][r], y[r], s);
-        y[q] = s * iv[q];
-      }
-#pragma unroll
-      for (int q = 0; q < D; ++q) xk[q * Bp] = y[q];
-    }
+  bool bad = false;
+  bl_chol<D>(a, iv, tol, bad);
+  if (diag) {
+    bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
     return;
   }
-  double* Pb = w.L + (size_t)fi.y * C::DD * Bp + b;
-#pragma unroll
-  for (int r = 0; r < D; ++r) {   // row r of L_pk: x L_kk^T = t
-    double xr[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q) xr[q] = Pb[(q * D + r) * Bp];
-#pragma unroll
-    for (int q = 0; q < D; ++q) {
-      double s = xr[q];
-#pragma unroll
-      for (int j = 0; j < q; ++j) s = fma(-xr[j], a[q][j], s);
-      xr[q] = s * iv[q];
-    }
-#pragma unroll
-    for (int q = 0; q < D; ++q) Pb[(q * D + r) * Bp] = xr[q];
-  }
+  bl_trsm_store<D>(Pb, Bp, t, a, iv);   // row r of L_pk: x L_kk^T = t
 }
 
 // failed factorisation -> element frozen at its iterate (GN: status NOT_SPD), reading A15
@@ -1315,7 +1273,7 @@ struct BLPlan {
   int persist = -1;     // bl_persist group width (-1 automatic, 0: per-level bl_update* + bl_factor launches)
   int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
   int tail_from = 0;      // first level of the single-column tail
-  int bsolve_ct = 0;      // experiment: column-task backward solve on levels with >= this many columns (0: off)
+  int bsolve_ct = 16;     // column-task backward solve on levels with >= this many columns (0: off)
 
   BLPDev pd{};
   int64_t storage_doubles = 0;   // nblk * DD per element
@@ -1464,7 +1422,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     bcon[4 * (size_t)tsk[t] + 1] = tsk[t + 2];
     bcon[4 * (size_t)tsk[t] + 2] = tsk[t + 3];
   }
-  int ch_units = 32, ch_min = 2;
+  int ch_units = 16, ch_min = 2;
   if (const char* env = std::getenv("DNLS_BL_CH")) sscanf(env, "%d,%d", &ch_units, &ch_min);
   const size_t scr_doubles = (size_t)(s.E + s.P) * (D == 6 ? BLC<6>::SW : BLC<3>::SW);
   std::vector<int32_t> it_lvl(L + 1, 0), items, rd_lvl(L + 1, 0), red;
