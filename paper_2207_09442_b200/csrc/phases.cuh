@@ -1369,17 +1369,21 @@ __device__ __forceinline__ void pk_task_rows_partial(const Pk& P, const LView& V
     const double* Bm = V.at(c.y);
     const size_t ld = c.z;
     int k = 0;
-    for (; k + 3 <= c.w; k += 3) {   // 3 source columns of loads in flight
-      double av[3][R], bv[3][D];
+#ifndef DNLS_UK
+#define DNLS_UK 3
+#endif
+    constexpr int UK = DNLS_UK;
+    for (; k + UK <= c.w; k += UK) {   // UK source columns of loads in flight
+      double av[UK][R], bv[UK][D];
 #pragma unroll
-      for (int u = 0; u < 3; ++u) {
+      for (int u = 0; u < UK; ++u) {
 #pragma unroll
         for (int r = 0; r < R; ++r) av[u][r] = A[(k + u) * ld + r];
 #pragma unroll
         for (int q = 0; q < D; ++q) bv[u][q] = Bm[(k + u) * ld + q];
       }
 #pragma unroll
-      for (int u = 0; u < 3; ++u)
+      for (int u = 0; u < UK; ++u)
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
