@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", "dnls.cu"), os.path.join(HERE, "csrc", "dnls_cluster.cu"),
        os.path.join(HERE, "csrc", "symbolic.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("phases.cuh", "lie.cuh", "symbolic.h")] + [
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("phases.cuh", "bl.cuh", "lie.cuh", "symbolic.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "dnls.h")]
 OUT = os.path.join(HERE, "lib", "libdnls.so")
 OUT_TRACE = os.path.join(HERE, "lib", "libdnls_trace.so")

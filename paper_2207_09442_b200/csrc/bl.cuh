@@ -623,6 +623,181 @@ __device__ __forceinline__ void bl_trsm_store(double* Pb, size_t Bp, double (&t)
   }
 }
 
+// column task: the whole column k for element b -- the diagonal target's updates, L_kk in registers, the
+// forward-substitution row and y_k = L_kk^-1 x_k, then every below target's updates solved straight from the
+// accumulators (L_pk = (T_pk - acc) L_kk^-T): each block is read once and written once, T_kk is never stored.
+// Same arithmetic (and rounding) as bl_update_rb + bl_factor (same contribution order per target).
+template <int D>
+__device__ __forceinline__ void bl_column_task(const BLDev& g, const BLWs& w, const int4* bcon, int b, int k,
+                                               double tol, bool fused_fwd) {
+  using C = BLC<D>;
+  const size_t Bp = g.Bp;
+  const int kb0 = g.colptr[k], kb1 = g.colptr[k + 1];
+  double a[D][D], iv[D];
+  {
+    const int4 bc = bcon[kb0];
+    double acc[D][D];
+    bl_acc_target<D>(g, w, b, bc.x, bc.y, true, acc);
+    const double* T = w.L + (size_t)kb0 * C::DD * Bp + b;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int i = j; i < D; ++i) a[i][j] = T[(j * D + i) * Bp] - acc[i][j];
+  }
+  bool bad = false;
+  bl_chol<D>(a, iv, tol, bad);
+  if (fused_fwd && g.fwdp[k + 1] > g.fwdp[k]) {
+    double acc[D];
+    bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], acc);
+    double* xk = w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+    for (int i = 0; i < D; ++i) xk[i * Bp] -= acc[i];
+  }
+  bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd);
+  for (int bi = kb0 + 1; bi < kb1; ++bi) {
+    const int4 bc = bcon[bi];
+    double acc[D][D];
+    bl_acc_target<D>(g, w, b, bc.x, bc.y, false, acc);
+    double* Pb = w.L + (size_t)bi * C::DD * Bp + b;
+    double t[D][D];
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int r = 0; r < D; ++r) t[q][r] = ((bc.z & 2) ? 0.0 : Pb[(q * D + r) * Bp]) - acc[r][q];
+    bl_trsm_store<D>(Pb, Bp, t, a, iv);
+  }
+}
+
+// work item (target block, or forward row -2 - k; contribution range [y, z); flags | (partial slot + 1) << 8):
+// a whole list is applied in place (T -= acc; a fill target stores -acc; x_k -= acc), a chunk of a split list
+// stores its partial sum in the slot scratch (idle during the factorisation) for the reduction
+template <int D>
+__device__ __forceinline__ void bl_work_item(const BLDev& g, const BLWs& w, double* part, const int4 itm, int b,
+                                             bool fused_fwd) {
+  using C = BLC<D>;
+  const size_t Bp = g.Bp;
+  const int slot = (itm.w >> 8) - 1;
+  if (itm.x >= 0) {
+    const bool diag = itm.w & 1, fill = itm.w & 2;
+    double acc[D][D];
+    bl_acc_target<D>(g, w, b, itm.y, itm.z, diag, acc);
+    double* T = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.L + (size_t)itm.x * C::DD * Bp + b;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        if (diag && i < j) continue;
+        double* t = T + (size_t)(j * D + i) * Bp;
+        *t = slot >= 0 ? acc[i][j] : (fill ? -acc[i][j] : *t - acc[i][j]);
+      }
+  } else if (fused_fwd) {
+    double acc[D];
+    bl_acc_fwd<D>(g, w, b, itm.y, itm.z, acc);
+    const int k = -2 - itm.x;
+    double* X = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+    for (int i = 0; i < D; ++i) X[i * Bp] = slot >= 0 ? acc[i] : X[i * Bp] - acc[i];
+  }
+}
+
+// level l of the large-batch schedule: thread = (element, work item) over the level's items, where
+// contribution lists longer than the plan's chunk size are split (a level's time is set by its longest
+// update chain: one memory round trip per contribution); the partials are reduced by bl_factor_red
+template <int D>
+__global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_items(BLDev g, BLWs w, const int4* items, int i0,
+                                                                       int nit, int fused_fwd) {
+  int b;
+  long long it;
+  if (!bl_item(g, nit, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  bl_work_item<D>(g, w, w.scr, items[i0 + it], b, fused_fwd != 0);
+}
+
+// bl_factor with the level's split reductions folded in: T_kk and T_pk minus their chunk partials (in chunk
+// order), x_k minus the forward row's partials, then bl_factor's arithmetic.  pr = (first slot, count) per
+// block (bred) and per column's forward row (cred).
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0, int nfac, int fused_fwd,
+                                                       const int2* bred, const int2* cred) {
+  using C = BLC<D>;
+  int b;
+  long long it;
+  if (!bl_item(g, nfac, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const size_t Bp = g.Bp;
+  const int2 fi = g.fac[f0 + it];
+  const int k = fi.x, kb0 = g.colptr[k];
+  const bool diag = fi.y == kb0;
+  const double* Kk = w.L + (size_t)kb0 * C::DD * Bp + b;
+  double* Pb = w.L + (size_t)fi.y * C::DD * Bp + b;
+  const double* part = w.scr + b;
+  const double tol = 1e-13 * __longlong_as_double((long long)w.maxd[b]);
+  double a[D][D], iv[D], t[D][D];
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = j; i < D; ++i) a[i][j] = Kk[(j * D + i) * Bp];
+  if (!diag) {
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+      for (int r = 0; r < D; ++r) t[q][r] = Pb[(q * D + r) * Bp];
+  }
+  const int2 rk = bred[kb0];
+  for (int q = 0; q < rk.y; ++q) {
+    const double* pp = part + (size_t)(rk.x + q) * C::DD * Bp;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int i = j; i < D; ++i) a[i][j] -= pp[(j * D + i) * Bp];
+  }
+  if (!diag) {
+    const int2 rp = bred[fi.y];
+    for (int q = 0; q < rp.y; ++q) {
+      const double* pp = part + (size_t)(rp.x + q) * C::DD * Bp;
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int r = 0; r < D; ++r) t[c][r] -= pp[(c * D + r) * Bp];
+    }
+  }
+  bool bad = false;
+  bl_chol<D>(a, iv, tol, bad);
+  if (diag) {
+    if (fused_fwd) {
+      const int2 rc = cred[k];
+      if (rc.y > 0) {
+        double* xk = w.x + (size_t)k * D * Bp + b;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double v = xk[i * Bp];
+          for (int q = 0; q < rc.y; ++q) v -= part[((size_t)(rc.x + q) * C::DD + i) * Bp];
+          xk[i * Bp] = v;
+        }
+      }
+    }
+    bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
+    return;
+  }
+  bl_trsm_store<D>(Pb, Bp, t, a, iv);
+}
+
+// bottom of the elimination tree in ONE launch: every maximal subtree of columns of height <= the plan's
+// sub_top is an item; thread = (element, subtree) walks the subtree's columns in increasing index (children
+// before parents: parent[k] > k) as column tasks.  A subtree's factor blocks are written and re-read by the
+// same thread within a few microseconds, so the left-looking source re-reads hit L1 / L2 instead of DRAM and
+// the bottom levels cost no per-level launches.  Items are ordered by decreasing size (largest first).
+template <int D>
+__global__ void __launch_bounds__(BL_TPB, 2) bl_subtree(BLDev g, BLWs w, const int4* bcon, const int* sub_ptr,
+                                                       const int* sub_col, int nsub, int fused_fwd) {
+  int b;
+  long long it;
+  if (!bl_item(g, nsub, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  const double tol = 1e-13 * __longlong_as_double((long long)w.maxd[b]);
+  for (int q = sub_ptr[it]; q < sub_ptr[it + 1]; ++q) bl_column_task<D>(g, w, bcon, b, sub_col[q], tol, fused_fwd != 0);
+}
+
 // next work index of a unit: dynamic scheduling through a shared counter (the result of an item does not depend
 // on the unit that computes it, so the schedule does not affect the arithmetic)
 template <int GW>
@@ -660,41 +835,7 @@ __global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev 
       // every lane of a unit takes part in the scheduling (frozen elements skip the arithmetic)
       for (int ci = next(c0); ci < c1; ci = next(c0)) {
           if (!act) continue;
-          const int k = pd.lvl_col[ci];
-          const int kb0 = g.colptr[k], kb1 = g.colptr[k + 1];
-          double a[D][D], iv[D];
-          {
-            const int4 bc = pd.bcon[kb0];
-            double acc[D][D];
-            bl_acc_target<D>(g, w, b, bc.x, bc.y, true, acc);
-            const double* T = w.L + (size_t)kb0 * C::DD * Bp + b;
-#pragma unroll
-            for (int j = 0; j < D; ++j)
-#pragma unroll
-              for (int i = j; i < D; ++i) a[i][j] = T[(j * D + i) * Bp] - acc[i][j];
-          }
-          bool bad = false;
-          bl_chol<D>(a, iv, tol, bad);
-          if (fused_fwd && g.fwdp[k + 1] > g.fwdp[k]) {
-            double acc[D];
-            bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], acc);
-            double* xk = w.x + (size_t)k * D * Bp + b;
-#pragma unroll
-            for (int i = 0; i < D; ++i) xk[i * Bp] -= acc[i];
-          }
-          bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd != 0);
-          for (int bi = kb0 + 1; bi < kb1; ++bi) {
-            const int4 bc = pd.bcon[bi];
-            double acc[D][D];
-            bl_acc_target<D>(g, w, b, bc.x, bc.y, false, acc);
-            double* Pb = w.L + (size_t)bi * C::DD * Bp + b;
-            double t[D][D];
-#pragma unroll
-            for (int q = 0; q < D; ++q)
-#pragma unroll
-              for (int r = 0; r < D; ++r) t[q][r] = ((bc.z & 2) ? 0.0 : Pb[(q * D + r) * Bp]) - acc[r][q];
-            bl_trsm_store<D>(Pb, Bp, t, a, iv);
-          }
+          bl_column_task<D>(g, w, pd.bcon, b, pd.lvl_col[ci], tol, fused_fwd != 0);
         }
       phase_end();
       continue;
@@ -702,29 +843,7 @@ __global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev 
     // ---- narrow level, A: work items (targets / forward rows, long lists in chunks)
     for (int ii = next(pd.it_lvl[l]); ii < pd.it_lvl[l + 1]; ii = next(pd.it_lvl[l])) {
         if (!act) continue;
-        const int4 itm = pd.items[ii];
-        const int slot = (itm.w >> 8) - 1;
-        if (itm.x >= 0) {
-          const bool diag = itm.w & 1, fill = itm.w & 2;
-          double acc[D][D];
-          bl_acc_target<D>(g, w, b, itm.y, itm.z, diag, acc);
-          double* T = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.L + (size_t)itm.x * C::DD * Bp + b;
-#pragma unroll
-          for (int j = 0; j < D; ++j)
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-              if (diag && i < j) continue;
-              double* t = T + (size_t)(j * D + i) * Bp;
-              *t = slot >= 0 ? acc[i][j] : (fill ? -acc[i][j] : *t - acc[i][j]);
-            }
-        } else if (fused_fwd) {
-          double acc[D];
-          bl_acc_fwd<D>(g, w, b, itm.y, itm.z, acc);
-          const int k = -2 - itm.x;
-          double* X = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.x + (size_t)k * D * Bp + b;
-#pragma unroll
-          for (int i = 0; i < D; ++i) X[i * Bp] = slot >= 0 ? acc[i] : X[i * Bp] - acc[i];
-        }
+        bl_work_item<D>(g, w, part, pd.items[ii], b, fused_fwd != 0);
       }
     if (pd.rd_lvl[l + 1] > pd.rd_lvl[l]) {
       phase_end();
@@ -1274,6 +1393,14 @@ struct BLPlan {
   int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
   int tail_from = 0;      // first level of the single-column tail
   int bsolve_ct = 16;     // column-task backward solve on levels with >= this many columns (0: off)
+  int lch = 0;            // per-level chunked update (bl_update_items + bl_factor_red): chunk size (0: off)
+  std::vector<int> lit_lvl_ptr;   // per level: its chunked work items
+  const int4* d_litems = nullptr;
+  const int2 *d_bred = nullptr, *d_cred = nullptr;
+  int sub_top = -1;       // bl_subtree covers the columns of height <= sub_top (-1: off)
+  bool sub_any = false;   // bl_subtree for any batch size (default: the large-batch schedule only)
+  int nsub = 0;           // its items: maximal subtrees of those columns, largest first
+  const int *d_sub_ptr = nullptr, *d_sub_col = nullptr;
 
   BLPDev pd{};
   int64_t storage_doubles = 0;   // nblk * DD per element
@@ -1468,6 +1595,74 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     it_lvl[l + 1] = (int)items.size() / 4;
     rd_lvl[l + 1] = (int)red.size() / 4;
   }
+  // per-level chunked update (large-batch schedule): every level's target lists and forward rows as work items,
+  // lists longer than lch contributions split into ceil(n / lch) nearly equal chunks; the first chunk is applied
+  // in place, the others store partials (level-local slots in the slot scratch) that bl_factor_red subtracts in
+  // chunk order.  bred / cred: per block / column (first slot, count) of its partials.
+  int lch = 8;
+  if (const char* env = std::getenv("DNLS_BL_LCH")) lch = std::atoi(env);
+  std::vector<int32_t> litems, bred(2 * (size_t)pl.nblk, 0), cred(2 * (size_t)N, 0);
+  pl.lit_lvl_ptr.assign(L + 1, 0);
+  if (lch > 0) {
+    const size_t cap = scr_doubles / ((size_t)D * D);
+    for (int l = 0; l < L; ++l) {
+      int nslot = 0;
+      auto add = [&](int tgt, int c0, int c1, int flags, int32_t* red2) {
+        const int n = c1 - c0;
+        int S = (n + lch - 1) / lch;
+        if ((size_t)(nslot + S - 1) > cap) S = 1;   // partials would not fit: whole list in place
+        if (S <= 1) {
+          litems.insert(litems.end(), {tgt, c0, c1, flags});
+          return;
+        }
+        red2[0] = nslot;
+        red2[1] = S - 1;
+        for (int q = 0; q < S; ++q) {
+          const int a = c0 + (int)((int64_t)n * q / S), e = c0 + (int)((int64_t)n * (q + 1) / S);
+          litems.insert(litems.end(), {tgt, a, e, flags | (q == 0 ? 0 : ((nslot + 1) << 8))});
+          if (q > 0) ++nslot;
+        }
+      };
+      for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
+        const int k = lvl_col[i];
+        for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi)
+          if (bcon[4 * (size_t)bi + 1] > bcon[4 * (size_t)bi])
+            add(bi, bcon[4 * (size_t)bi], bcon[4 * (size_t)bi + 1], bcon[4 * (size_t)bi + 2] & 3, &bred[2 * (size_t)bi]);
+        if (fwdp[k + 1] > fwdp[k]) add(-2 - k, fwdp[k], fwdp[k + 1], 0, &cred[2 * (size_t)k]);
+      }
+      pl.lit_lvl_ptr[l + 1] = (int)litems.size() / 4;
+    }
+  }
+  pl.lch = lch;
+  // bottom subtrees (bl_subtree): every column of height <= sub_top belongs to the subtree of its highest
+  // ancestor of height <= sub_top; a subtree's columns in increasing index (children first), subtrees by
+  // decreasing block count (the longest items start first)
+  int sub_top = 10;
+  if (const char* env = std::getenv("DNLS_BL_SUB")) sub_top = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_SUBANY")) pl.sub_any = std::atoi(env) != 0;
+  sub_top = std::min(sub_top, L - 1);
+  std::vector<int32_t> sub_ptr(1, 0), sub_col;
+  if (sub_top >= 0) {
+    std::vector<int> root(N, -1);
+    for (int k = N - 1; k >= 0; --k)
+      if (h[k] <= sub_top) root[k] = (s.parent[k] >= 0 && h[s.parent[k]] <= sub_top) ? root[s.parent[k]] : k;
+    std::map<int, std::vector<int>> subs;
+    for (int k = 0; k < N; ++k)
+      if (root[k] >= 0) subs[root[k]].push_back(k);
+    std::vector<std::pair<int, int>> order;   // (-blocks, root)
+    for (auto& kv : subs) {
+      int nb = 0;
+      for (int k : kv.second) nb += colptr[k + 1] - colptr[k];
+      order.push_back(std::make_pair(-nb, kv.first));
+    }
+    std::sort(order.begin(), order.end());
+    for (auto& o : order) {
+      for (int k : subs[o.second]) sub_col.push_back(k);
+      sub_ptr.push_back((int)sub_col.size());
+    }
+  }
+  pl.sub_top = sub_top;
+  pl.nsub = (int)sub_ptr.size() - 1;
   std::vector<int32_t> lvl_ptr32(pl.lvl_ptr.begin(), pl.lvl_ptr.end()), fac_lvl32(pl.fac_lvl_ptr.begin(),
                                                                                    pl.fac_lvl_ptr.end());
   // upload (int32 arrays, 16-byte aligned)
@@ -1483,6 +1678,8 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   add(colptr); add(blkrow); add(tsk); add(con); add(fwdp); add(fwd); add(fac); add(slotd);
   add(s.bc_ptr); add(s.bc); add(dup_ptr); add(dup_blk); add(dup_con); add(fill); add(lvl_col); add(fill0);
   add(bcon); add(it_lvl); add(items); add(rd_lvl); add(red); add(lvl_ptr32); add(fac_lvl32);
+  add(sub_ptr); add(sub_col);
+  add(litems); add(bred); add(cred);
   while (buf.size() % 4) buf.push_back(0);
   if (device >= 0) {
     if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
@@ -1517,6 +1714,11 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.pd.red = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.pd.lvl_ptr = ptr(offs[k++]);
   pl.pd.fac_lvl = ptr(offs[k++]);
+  pl.d_sub_ptr = ptr(offs[k++]);
+  pl.d_sub_col = ptr(offs[k++]);
+  pl.d_litems = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.d_bred = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.d_cred = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.pd.lvl_col = pl.d_lvl_col;
   pl.pd.L = L;
   pl.pd.coltask_min = 16;
@@ -1609,6 +1811,7 @@ struct BLPhaseTimer {
 struct BLSched {
   bool rb;
   int lsplit, gw;
+  int lfirst;   // first level of the per-level launches (levels below: bl_subtree)
 };
 inline BLSched bl_schedule(const BLPlan& pl, int B) {
   const bool large = bl_pad(B) / 32 >= 32;
@@ -1617,6 +1820,7 @@ inline BLSched bl_schedule(const BLPlan& pl, int B) {
   const bool persist = pl.persist == 0 ? false : (pl.persist > 0 || large);
   sc.lsplit = !persist ? pl.L : (pl.persist_from >= 0 ? std::min(pl.L, pl.persist_from) : pl.tail_from);
   sc.gw = pl.persist > 0 ? pl.persist : ((B + 15) / 16 >= 128 ? 16 : (B + 7) / 8 >= 128 ? 8 : 4);
+  sc.lfirst = (pl.sub_top >= 0 && pl.nsub > 0 && (large || pl.sub_any)) ? pl.sub_top + 1 : 0;
   return sc;
 }
 
@@ -1642,11 +1846,24 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   g.B = B;
   g.Bp = bl_pad(B);
   const BLSched sc = bl_schedule(pl, B);
-  const int lsplit = sc.lsplit;
-  for (int l = 0; l < lsplit; ++l) {
+  const int lsplit = std::max(sc.lsplit, sc.lfirst);
+  if (sc.lfirst > 0)
+    DNLS_KL bl_subtree<D><<<bl_grid(pl.nsub, g.Bp), BL_TPB, 0, s>>>(g, w, pl.pd.bcon, pl.d_sub_ptr, pl.d_sub_col,
+                                                                    pl.nsub, fused_fwd ? 1 : 0);
+  for (int l = sc.lfirst; l < lsplit; ++l) {
     const int t0 = pl.tsk_lvl_ptr[l], nt = pl.tsk_lvl_ptr[l + 1] - t0;
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
     const long long nu = (long long)nt + (fused_fwd ? nc : 0);
+    if (sc.rb && pl.lch > 0) {
+      // chunked work items of the level (forward rows skipped in the final factorisation: they have no
+      // effect there), then the factor launch with the split reductions folded in
+      const int i0 = pl.lit_lvl_ptr[l], ni = pl.lit_lvl_ptr[l + 1] - i0;
+      if (ni > 0)
+        DNLS_KL bl_update_items<D><<<bl_grid(ni, g.Bp), BL_TPB, 0, s>>>(g, w, pl.d_litems, i0, ni, fused_fwd ? 1 : 0);
+      const int f0 = pl.fac_lvl_ptr[l], nf = pl.fac_lvl_ptr[l + 1] - f0;
+      DNLS_KL bl_factor_red<D><<<bl_grid(nf, g.Bp), BL_TPB, 0, s>>>(g, w, f0, nf, fused_fwd ? 1 : 0, pl.d_bred, pl.d_cred);
+      continue;
+    }
     if (nu > 0 && sc.rb)
       DNLS_KL bl_update_rb<D><<<bl_grid(nu, g.Bp), BL_TPB, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
     else if (nu > 0)
