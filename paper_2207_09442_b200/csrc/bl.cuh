@@ -19,7 +19,39 @@
 // Gauss-Newton (and the implicit backward) with quadratic or Welsch costs; LM / Dogleg / DLM / unroll
 // use the per-element path.
 
-constexpr int BL_TPB = 128;   // threads per block of the BL kernels (4 warps = 4 items x 32 elements)
+constexpr int BL_TPB = 128;
+
+// Programmatic dependent launch (PDL): every BL kernel is launched with programmatic stream serialisation, so
+// the next kernel on the stream is scheduled while this one drains; it waits (griddepcontrol.wait: the previous
+// grid has completed and its memory is visible) before touching any data, then lets its own dependent launch.
+// g_bl_pdl = 0 (DNLS_PDL=0) launches without the attribute (the wait is then a no-op).
+__device__ __forceinline__ void bl_pdl() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline int bl_pdl_on() {
+  static const int on = [] {
+    const char* e = std::getenv("DNLS_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void bl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  ::dnls::g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = bl_pdl_on() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+   // threads per block of the BL kernels (4 warps = 4 items x 32 elements)
 
 struct BLDev {
   int D, N, E, P, n, nblk, Bp, B;
@@ -95,6 +127,7 @@ __device__ __forceinline__ DevGraph bl_cost_graph(const BLDev& g) {
 
 // ---------------------------------------------------------------------------- assembly (a1 + a2)
 __global__ void __launch_bounds__(BL_TPB) bl_zero_fill(BLDev g, BLWs w, int DD, const int* fill, int nfill) {
+  bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, (long long)nfill * DD, b, it)) return;
@@ -108,6 +141,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_zero_fill(BLDev g, BLWs w, int DD, 
 // the diagonal contributions and J^T r parts into the scratch (PAPER.md:64 J^T J, J^T r)
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_lin_slots(BLDev g, DevProb pr, BLWs w) {
+  bl_pdl();
   using C = BLC<D>;
   int b;
   long long it;
@@ -157,6 +191,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_lin_slots(BLDev g, DevProb pr, BLWs
 // the element's max diagonal by an integer atomicMax on the bits of a non-negative double
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_lin_poses(BLDev g, BLWs w, double lam, int damping) {
+  bl_pdl();
   using C = BLC<D>;
   int b;
   long long it;
@@ -221,6 +256,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_lin_poses(BLDev g, BLWs w, double l
 constexpr int BL_SW = 32;
 __global__ void __launch_bounds__(BL_SW * 32) bl_objective(BLDev g, BLWs w, int early_stop, double abs_tol,
                                                           double rel_tol, int have_prev, int set_prev, int final) {
+  bl_pdl();
   __shared__ double part[BL_SW][33];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int b = blockIdx.x * 32 + lane;
@@ -245,6 +281,7 @@ __global__ void __launch_bounds__(BL_SW * 32) bl_objective(BLDev g, BLWs w, int 
   if (set_prev) w.Sprev[b] = S;
 }
 __global__ void __launch_bounds__(BL_TPB) bl_reset_iter(BLDev g, BLWs w) {
+  bl_pdl();
   const int b = blockIdx.x * BL_TPB + threadIdx.x;
   if (b >= g.Bp) return;
   w.maxd[b] = 0ull;
@@ -273,6 +310,7 @@ __device__ __forceinline__ void bl_issue_fence() { asm volatile("" ::: "memory")
 template <int D>
 __global__ void __launch_bounds__(D * 32, 3) bl_update(BLDev g, BLWs w, int t0, int ntask, const int* cols, int ncol,
                                                     int fused_fwd) {
+  bl_pdl();
   using C = BLC<D>;
   int b, r;
   long long it;
@@ -338,6 +376,7 @@ template <int D>
 #endif
 __global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_rb(BLDev g, BLWs w, int t0, int ntask, const int* cols, int ncol,
                                                        int fused_fwd) {
+  bl_pdl();
   using C = BLC<D>;
 #ifndef DNLS_RB_HD
 #define DNLS_RB_HD 1
@@ -706,6 +745,7 @@ __device__ __forceinline__ void bl_work_item(const BLDev& g, const BLWs& w, doub
 template <int D>
 __global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_items(BLDev g, BLWs w, const int4* items, int i0,
                                                                        int nit, int fused_fwd) {
+  bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, nit, b, it)) return;
@@ -719,6 +759,7 @@ __global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_items(BLDev g,
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0, int nfac, int fused_fwd,
                                                        const int2* bred, const int2* cred) {
+  bl_pdl();
   using C = BLC<D>;
   int b;
   long long it;
@@ -788,8 +829,12 @@ __global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0,
 // same thread within a few microseconds, so the left-looking source re-reads hit L1 / L2 instead of DRAM and
 // the bottom levels cost no per-level launches.  Items are ordered by decreasing size (largest first).
 template <int D>
-__global__ void __launch_bounds__(BL_TPB, 2) bl_subtree(BLDev g, BLWs w, const int4* bcon, const int* sub_ptr,
+#ifndef DNLS_SUB_MINB
+#define DNLS_SUB_MINB 2
+#endif
+__global__ void __launch_bounds__(BL_TPB, DNLS_SUB_MINB) bl_subtree(BLDev g, BLWs w, const int4* bcon, const int* sub_ptr,
                                                        const int* sub_col, int nsub, int fused_fwd) {
+  bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, nsub, b, it)) return;
@@ -812,6 +857,7 @@ __device__ __forceinline__ int bl_next(int* ctr, int base) {
 template <int D, int GW>
 __global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev pd, int fused_fwd, int l_begin,
                                                         int l_end) {
+  bl_pdl();
   using C = BLC<D>;
   __shared__ int ctr[4];
   const int b = blockIdx.x * GW + (threadIdx.x % GW);
@@ -912,6 +958,7 @@ __global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev 
 template <int D, int GW>
 __global__ void __launch_bounds__(BLP_NT) bl_persist_solve(BLDev g, BLWs w, BLPDev pd, const int* skip, int forward,
                                                            int l_begin, int l_end) {
+  bl_pdl();
   using C = BLC<D>;
   constexpr int U = BLP_NT / GW;
   __shared__ double part[U][D][GW];
@@ -1008,6 +1055,7 @@ __global__ void __launch_bounds__(BLP_NT) bl_persist_solve(BLDev g, BLWs w, BLPD
 // block's unused upper triangle) and applies y_k = L_kk^-1 x_k; a below item solves L_pk = T_pk L_kk^-T
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_factor(BLDev g, BLWs w, int f0, int nfac, int fused_fwd) {
+  bl_pdl();
   using C = BLC<D>;
   int b;
   long long it;
@@ -1043,6 +1091,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_factor(BLDev g, BLWs w, int f0, int
 
 // failed factorisation -> element frozen at its iterate (GN: status NOT_SPD), reading A15
 __global__ void __launch_bounds__(BL_TPB) bl_check_fail(BLDev g, BLWs w) {
+  bl_pdl();
   const int b = blockIdx.x * BL_TPB + threadIdx.x;
   if (b >= g.B) return;
   if (w.fail[b] && w.st[b] == DNLS_ST_OK) w.st[b] = DNLS_ST_NOT_SPD;
@@ -1053,6 +1102,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_check_fail(BLDev g, BLWs w) {
 // component r, warp 0 applies L_kk^-1 (shared memory exchange)
 template <int D>
 __global__ void __launch_bounds__(D * 32, 3) bl_fsolve(BLDev g, BLWs w, const int* cols, int ncol, const int* skip) {
+  bl_pdl();
   using C = BLC<D>;
   __shared__ double sv[D][32];
   int b, r;
@@ -1099,6 +1149,7 @@ __global__ void __launch_bounds__(D * 32, 3) bl_fsolve(BLDev g, BLWs w, const in
 // warp c sums component c over the column's below blocks (two blocks per round trip), warp 0 applies L_kk^-T
 template <int D>
 __global__ void __launch_bounds__(D * 32, 3) bl_bsolve(BLDev g, BLWs w, const int* cols, int ncol, const int* skip) {
+  bl_pdl();
   using C = BLC<D>;
   __shared__ double sv[D][32];
   int b, c;
@@ -1166,6 +1217,7 @@ __global__ void __launch_bounds__(D * 32, 3) bl_bsolve(BLDev g, BLWs w, const in
 // bl_bsolve (identical results), L_kk^-T applied in registers
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_bsolve_ct(BLDev g, BLWs w, const int* cols, int ncol, const int* skip) {
+  bl_pdl();
   using C = BLC<D>;
   int b;
   long long it;
@@ -1220,6 +1272,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_bsolve_ct(BLDev g, BLWs w, const in
 // ---------------------------------------------------------------------------- retraction (a5)
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_retract(BLDev g, DevProb pr, BLWs w, double alpha) {
+  bl_pdl();
   constexpr int PS = GT<D>::PS;
   int b;
   long long it;
@@ -1238,6 +1291,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_retract(BLDev g, DevProb pr, BLWs w
 }
 
 __global__ void __launch_bounds__(BL_TPB) bl_init(BLDev g, BLWs w) {
+  bl_pdl();
   const int b = blockIdx.x * BL_TPB + threadIdx.x;
   if (b >= g.Bp) return;
   w.st[b] = b < g.B ? DNLS_ST_OK : DNLS_ST_NOT_SPD;   // padding lanes stay frozen
@@ -1250,6 +1304,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_init(BLDev g, BLWs w) {
 
 // before the final (implicit) linearisation: keep the iteration status in ws_st, re-activate every element
 __global__ void __launch_bounds__(BL_TPB) bl_pre_final(BLDev g, BLWs w) {
+  bl_pdl();
   const int b = blockIdx.x * BL_TPB + threadIdx.x;
   if (b >= g.B) return;
   w.stf[b] = w.st[b];
@@ -1258,6 +1313,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_pre_final(BLDev g, BLWs w) {
 // final status: a failed final (implicit) factor takes precedence; not-converged warning bit; outputs
 __global__ void __launch_bounds__(BL_TPB) bl_finish(BLDev g, BLWs w, int implicit, double abs_tol, double rel_tol,
                                                     double* objective, int* status, int* iterations) {
+  bl_pdl();
   const int b = blockIdx.x * BL_TPB + threadIdx.x;
   if (b >= g.B) return;
   int s = implicit ? w.stf[b] : w.st[b];
@@ -1276,6 +1332,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_finish(BLDev g, BLWs w, int implici
 // costs, summed by bl_objective (final = 1)
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_cost_only(BLDev g, DevProb pr, BLWs w) {
+  bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, g.E + g.P, b, it)) return;
@@ -1296,6 +1353,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_cost_only(BLDev g, DevProb pr, BLWs
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_bwd_rhs(BLDev g, DevProb pr, BLWs w, const double* gpose,
                                                      int grad_kind) {
+  bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, g.N, b, it)) return;
@@ -1311,6 +1369,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_bwd_rhs(BLDev g, DevProb pr, BLWs w
 // elements without a valid factor
 template <int D>
 __global__ void __launch_bounds__(BL_TPB) bl_bwd_slots(BLDev g, DevProb pr, BLWs w, double* out) {
+  bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, g.E + g.P, b, it)) return;
@@ -1361,6 +1420,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_bwd_slots(BLDev g, DevProb pr, BLWs
 // fixed-order batch reduction (or per-element copy) of the interleaved per-slot gradients: one warp per slot,
 // lane l sums elements l, l + 32, ... in order, then a fixed xor-shuffle tree (deterministic)
 __global__ void bl_reduce_wgrad(int B, int Bp, int E, int P, const double* src, double* ge, double* gp, long long bstride) {
+  bl_pdl();
   const int slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (slot >= E + P) return;
   double* dst = slot < E ? ge : gp;
@@ -1603,13 +1663,21 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   if (const char* env = std::getenv("DNLS_BL_LCH")) lch = std::atoi(env);
   std::vector<int32_t> litems, bred(2 * (size_t)pl.nblk, 0), cred(2 * (size_t)N, 0);
   pl.lit_lvl_ptr.assign(L + 1, 0);
+  int litems_want = 0, lch_min = 2;   // narrow levels: chunks small enough for ~litems_want items (0: off)
+  if (const char* env = std::getenv("DNLS_BL_LITEMS")) sscanf(env, "%d,%d", &litems_want, &lch_min);
   if (lch > 0) {
     const size_t cap = scr_doubles / ((size_t)D * D);
     for (int l = 0; l < L; ++l) {
-      int nslot = 0;
+      int nslot = 0, ncl = 0;
+      for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
+        const int k = lvl_col[i];
+        for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) ncl += bcon[4 * (size_t)bi + 1] - bcon[4 * (size_t)bi];
+        ncl += fwdp[k + 1] - fwdp[k];
+      }
+      const int lchl = litems_want > 0 ? std::max(lch_min, std::min(lch, (ncl + litems_want - 1) / litems_want)) : lch;
       auto add = [&](int tgt, int c0, int c1, int flags, int32_t* red2) {
         const int n = c1 - c0;
-        int S = (n + lch - 1) / lch;
+        int S = (n + lchl - 1) / lchl;
         if ((size_t)(nslot + S - 1) > cap) S = 1;   // partials would not fit: whole list in place
         if (S <= 1) {
           litems.insert(litems.end(), {tgt, c0, c1, flags});
@@ -1812,6 +1880,7 @@ struct BLSched {
   bool rb;
   int lsplit, gw;
   int lfirst;   // first level of the per-level launches (levels below: bl_subtree)
+  int fsplit;   // first level of the factorisation's persistent launch (chunked per-level items: none)
 };
 inline BLSched bl_schedule(const BLPlan& pl, int B) {
   const bool large = bl_pad(B) / 32 >= 32;
@@ -1820,6 +1889,7 @@ inline BLSched bl_schedule(const BLPlan& pl, int B) {
   const bool persist = pl.persist == 0 ? false : (pl.persist > 0 || large);
   sc.lsplit = !persist ? pl.L : (pl.persist_from >= 0 ? std::min(pl.L, pl.persist_from) : pl.tail_from);
   sc.gw = pl.persist > 0 ? pl.persist : ((B + 15) / 16 >= 128 ? 16 : (B + 7) / 8 >= 128 ? 8 : 4);
+  sc.fsplit = (sc.rb && pl.lch > 0 && pl.persist_from < 0) ? pl.L : sc.lsplit;
   sc.lfirst = (pl.sub_top >= 0 && pl.nsub > 0 && (large || pl.sub_any)) ? pl.sub_top + 1 : 0;
   return sc;
 }
@@ -1829,15 +1899,15 @@ void bl_linearize(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, dou
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  DNLS_KL bl_reset_iter<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
+  bl_launch(bl_reset_iter, bl_grid_b(g.Bp), BL_TPB, s, g, w);
   // the register-blocked update stores its fill targets; the row-split one accumulates into zeroed blocks
   const BLSched sc = bl_schedule(pl, B);
   const bool zero_all = !sc.rb && sc.lsplit > 0;
   const int* fl = zero_all ? g.fill : pl.d_fill0;
   const int nf = zero_all ? g.nfill : pl.nfill0;
-  if (nf) DNLS_KL bl_zero_fill<<<bl_grid((long long)nf * D * D, g.Bp), BL_TPB, 0, s>>>(g, w, D * D, fl, nf);
-  DNLS_KL bl_lin_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
-  DNLS_KL bl_lin_poses<D><<<bl_grid(g.N + g.ndup, g.Bp), BL_TPB, 0, s>>>(g, w, lam, damping);
+  if (nf) bl_launch(bl_zero_fill, bl_grid((long long)nf * D * D, g.Bp), BL_TPB, s, g, w, D * D, fl, nf);
+  bl_launch(bl_lin_slots<D>, bl_grid(g.E + g.P, g.Bp), BL_TPB, s, g, pr, w);
+  bl_launch(bl_lin_poses<D>, bl_grid(g.N + g.ndup, g.Bp), BL_TPB, s, g, w, lam, damping);
 }
 
 template <int D>
@@ -1846,9 +1916,9 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   g.B = B;
   g.Bp = bl_pad(B);
   const BLSched sc = bl_schedule(pl, B);
-  const int lsplit = std::max(sc.lsplit, sc.lfirst);
+  const int lsplit = std::max(sc.fsplit, sc.lfirst);
   if (sc.lfirst > 0)
-    DNLS_KL bl_subtree<D><<<bl_grid(pl.nsub, g.Bp), BL_TPB, 0, s>>>(g, w, pl.pd.bcon, pl.d_sub_ptr, pl.d_sub_col,
+    bl_launch(bl_subtree<D>, bl_grid(pl.nsub, g.Bp), BL_TPB, s, g, w, pl.pd.bcon, pl.d_sub_ptr, pl.d_sub_col,
                                                                     pl.nsub, fused_fwd ? 1 : 0);
   for (int l = sc.lfirst; l < lsplit; ++l) {
     const int t0 = pl.tsk_lvl_ptr[l], nt = pl.tsk_lvl_ptr[l + 1] - t0;
@@ -1859,17 +1929,17 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
       // effect there), then the factor launch with the split reductions folded in
       const int i0 = pl.lit_lvl_ptr[l], ni = pl.lit_lvl_ptr[l + 1] - i0;
       if (ni > 0)
-        DNLS_KL bl_update_items<D><<<bl_grid(ni, g.Bp), BL_TPB, 0, s>>>(g, w, pl.d_litems, i0, ni, fused_fwd ? 1 : 0);
+        bl_launch(bl_update_items<D>, bl_grid(ni, g.Bp), BL_TPB, s, g, w, pl.d_litems, i0, ni, fused_fwd ? 1 : 0);
       const int f0 = pl.fac_lvl_ptr[l], nf = pl.fac_lvl_ptr[l + 1] - f0;
-      DNLS_KL bl_factor_red<D><<<bl_grid(nf, g.Bp), BL_TPB, 0, s>>>(g, w, f0, nf, fused_fwd ? 1 : 0, pl.d_bred, pl.d_cred);
+      bl_launch(bl_factor_red<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, f0, nf, fused_fwd ? 1 : 0, pl.d_bred, pl.d_cred);
       continue;
     }
     if (nu > 0 && sc.rb)
-      DNLS_KL bl_update_rb<D><<<bl_grid(nu, g.Bp), BL_TPB, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
+      bl_launch(bl_update_rb<D>, bl_grid(nu, g.Bp), BL_TPB, s, g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
     else if (nu > 0)
-      DNLS_KL bl_update<D><<<bl_grid_rows(nu, g.Bp), D * 32, 0, s>>>(g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
+      bl_launch(bl_update<D>, bl_grid_rows(nu, g.Bp), D * 32, s, g, w, t0, nt, pl.d_lvl_col + c0, nc, fused_fwd ? 1 : 0);
     const int f0 = pl.fac_lvl_ptr[l], nf = pl.fac_lvl_ptr[l + 1] - f0;
-    DNLS_KL bl_factor<D><<<bl_grid(nf, g.Bp), BL_TPB, 0, s>>>(g, w, f0, nf, fused_fwd ? 1 : 0);
+    bl_launch(bl_factor<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, f0, nf, fused_fwd ? 1 : 0);
   }
   if (lsplit < pl.L) {
     // levels [lsplit, L) in one persistent launch; group width: the widest of 16 / 8 / 4 elements that still
@@ -1877,10 +1947,10 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
     const int gw = sc.gw;
     const int ff = fused_fwd ? 1 : 0;
     switch (gw) {
-      case 32: DNLS_KL bl_persist<D, 32><<<(B + 31) / 32, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
-      case 16: DNLS_KL bl_persist<D, 16><<<(B + 15) / 16, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
-      case 8: DNLS_KL bl_persist<D, 8><<<(B + 7) / 8, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
-      default: DNLS_KL bl_persist<D, 4><<<(B + 3) / 4, BLP_NT, 0, s>>>(g, w, pl.pd, ff, lsplit, pl.L); break;
+      case 32: bl_launch(bl_persist<D, 32>, (B + 31) / 32, BLP_NT, s, g, w, pl.pd, ff, lsplit, pl.L); break;
+      case 16: bl_launch(bl_persist<D, 16>, (B + 15) / 16, BLP_NT, s, g, w, pl.pd, ff, lsplit, pl.L); break;
+      case 8: bl_launch(bl_persist<D, 8>, (B + 7) / 8, BLP_NT, s, g, w, pl.pd, ff, lsplit, pl.L); break;
+      default: bl_launch(bl_persist<D, 4>, (B + 3) / 4, BLP_NT, s, g, w, pl.pd, ff, lsplit, pl.L); break;
     }
   }
 }
@@ -1894,16 +1964,16 @@ void bl_solve(const BLPlan& pl, int B, const BLWs& w, bool forward, const int* s
   auto tail = [&](int fwd) {
     if (sc.lsplit >= pl.L) return;
     switch (sc.gw) {
-      case 32: DNLS_KL bl_persist_solve<D, 32><<<(B + 31) / 32, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
-      case 16: DNLS_KL bl_persist_solve<D, 16><<<(B + 15) / 16, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
-      case 8: DNLS_KL bl_persist_solve<D, 8><<<(B + 7) / 8, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
-      default: DNLS_KL bl_persist_solve<D, 4><<<(B + 3) / 4, BLP_NT, 0, s>>>(g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      case 32: bl_launch(bl_persist_solve<D, 32>, (B + 31) / 32, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      case 16: bl_launch(bl_persist_solve<D, 16>, (B + 15) / 16, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      case 8: bl_launch(bl_persist_solve<D, 8>, (B + 7) / 8, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      default: bl_launch(bl_persist_solve<D, 4>, (B + 3) / 4, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
     }
   };
   if (forward) {
     for (int l = 0; l < sc.lsplit; ++l) {
       const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
-      DNLS_KL bl_fsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+      bl_launch(bl_fsolve<D>, bl_grid_rows(nc, g.Bp), D * 32, s, g, w, pl.d_lvl_col + c0, nc, skip);
     }
     tail(1);
   }
@@ -1911,9 +1981,9 @@ void bl_solve(const BLPlan& pl, int B, const BLWs& w, bool forward, const int* s
   for (int l = sc.lsplit - 1; l >= 0; --l) {
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
     if (sc.rb && pl.bsolve_ct && nc >= pl.bsolve_ct)
-      DNLS_KL bl_bsolve_ct<D><<<bl_grid(nc, g.Bp), BL_TPB, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+      bl_launch(bl_bsolve_ct<D>, bl_grid(nc, g.Bp), BL_TPB, s, g, w, pl.d_lvl_col + c0, nc, skip);
     else
-      DNLS_KL bl_bsolve<D><<<bl_grid_rows(nc, g.Bp), D * 32, 0, s>>>(g, w, pl.d_lvl_col + c0, nc, skip);
+      bl_launch(bl_bsolve<D>, bl_grid_rows(nc, g.Bp), D * 32, s, g, w, pl.d_lvl_col + c0, nc, skip);
   }
 }
 
@@ -1925,30 +1995,30 @@ void bl_forward(const BLPlan& pl, int B, const DevProb& pr, const BLWs& w, int K
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  DNLS_KL bl_init<<<bl_grid_b(g.Bp), BL_TPB, 0, s>>>(g, w);
+  bl_launch(bl_init, bl_grid_b(g.Bp), BL_TPB, s, g, w);
   for (int k = 0; k < K; ++k) {
     bl_linearize<D>(pl, B, pr, w, -1.0, 0, s);
-    DNLS_KL bl_objective<<<g.Bp / 32, BL_SW * 32, 0, s>>>(g, w, early_stop, abs_tol, rel_tol, k > 0 ? 1 : 0, 1, 0);
+    bl_launch(bl_objective, g.Bp / 32, BL_SW * 32, s, g, w, early_stop, abs_tol, rel_tol, k > 0 ? 1 : 0, 1, 0);
     tm.begin(s);
     bl_factor_all<D>(pl, B, w, true, s);
     tm.end(s);
-    DNLS_KL bl_check_fail<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+    bl_launch(bl_check_fail, bl_grid_b(B), BL_TPB, s, g, w);
     bl_solve<D>(pl, B, w, false, w.st, s);   // frozen / failed elements skip the solve and the retraction
-    DNLS_KL bl_retract<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, alpha);
+    bl_launch(bl_retract<D>, bl_grid(g.N, g.Bp), BL_TPB, s, g, pr, w, alpha);
   }
   if (implicit) {
-    DNLS_KL bl_pre_final<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w);
+    bl_launch(bl_pre_final, bl_grid_b(B), BL_TPB, s, g, w);
     bl_linearize<D>(pl, B, pr, w, -1.0, 0, s);
-    DNLS_KL bl_objective<<<g.Bp / 32, BL_SW * 32, 0, s>>>(g, w, 0, abs_tol, rel_tol, 0, 0, 0);
+    bl_launch(bl_objective, g.Bp / 32, BL_SW * 32, s, g, w, 0, abs_tol, rel_tol, 0, 0, 0);
     // the final factor is computed for every element that still has a defined iterate
     tm.begin(s);
     bl_factor_all<D>(pl, B, w, false, s);
     tm.end(s);
   } else {
-    DNLS_KL bl_cost_only<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w);
-    DNLS_KL bl_objective<<<g.Bp / 32, BL_SW * 32, 0, s>>>(g, w, 0, abs_tol, rel_tol, 0, 0, 1);
+    bl_launch(bl_cost_only<D>, bl_grid(g.E + g.P, g.Bp), BL_TPB, s, g, pr, w);
+    bl_launch(bl_objective, g.Bp / 32, BL_SW * 32, s, g, w, 0, abs_tol, rel_tol, 0, 0, 1);
   }
-  DNLS_KL bl_finish<<<bl_grid_b(B), BL_TPB, 0, s>>>(g, w, implicit ? 1 : 0, abs_tol, rel_tol, objective, status, iterations);
+  bl_launch(bl_finish, bl_grid_b(B), BL_TPB, s, g, w, implicit ? 1 : 0, abs_tol, rel_tol, objective, status, iterations);
 }
 
 // implicit backward on the BL factor of H(theta_K): lambda = H^-1 v, per-slot weight gradients, batch reduction
@@ -1958,10 +2028,10 @@ void bl_backward_implicit(const BLPlan& pl, int B, const DevProb& pr, const BLWs
   BLDev g = pl.dev;
   g.B = B;
   g.Bp = bl_pad(B);
-  DNLS_KL bl_bwd_rhs<D><<<bl_grid(g.N, g.Bp), BL_TPB, 0, s>>>(g, pr, w, gpose, grad_kind);
+  bl_launch(bl_bwd_rhs<D>, bl_grid(g.N, g.Bp), BL_TPB, s, g, pr, w, gpose, grad_kind);
   bl_solve<D>(pl, B, w, true, nullptr, s);
-  DNLS_KL bl_bwd_slots<D><<<bl_grid(g.E + g.P, g.Bp), BL_TPB, 0, s>>>(g, pr, w, w.cost);
+  bl_launch(bl_bwd_slots<D>, bl_grid(g.E + g.P, g.Bp), BL_TPB, s, g, pr, w, w.cost);
   const int slots = g.E + g.P;
   if (slots > 0 && (ge || gp))
-    DNLS_KL bl_reduce_wgrad<<<(slots + 3) / 4, 128, 0, s>>>(B, g.Bp, g.E, g.P, w.cost, ge, gp, bstride);
+    bl_launch(bl_reduce_wgrad, (slots + 3) / 4, 128, s, B, g.Bp, g.E, g.P, w.cost, ge, gp, bstride);
 }
