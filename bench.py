@@ -469,8 +469,9 @@ def main():
             "bound": "hbm", "achieved": fbytes / (pm / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
             "frac": fbytes / (pm / 1e3) / 1e9 / peak, "traffic": traffic,
             "traffic_over_algorithmic": None if traffic is None else traffic / fbytes,
-            "kernel": "numeric factorisation: per-level bl_update_rb/bl_update + bl_factor, tail levels in one "
-                      "bl_persist launch (one factorisation of the batch)",
+            "kernel": "numeric factorisation: bl_subtree (the bottom subtrees of the elimination tree, one launch) + "
+                      "per-level bl_update_items (chunked update lists) + bl_factor_red, PDL launches (one "
+                      "factorisation of the batch)",
             "peak_source": peak_src, "alg_bytes_per_launch": fbytes, "kernel_ms": pm, "kernel_ms_min": min(phases),
             "factorisations_ms": phases,
             "fp64": {"flops_per_launch": fflops, "achieved_tflops": fflops / (pm / 1e3) / 1e12,

@@ -219,8 +219,11 @@ __global__ void __launch_bounds__(BL_TPB) bl_lin_poses(BLDev g, BLWs w, double l
   for (int i = 0; i < C::NL; ++i) h[i] = 0.0;
 #pragma unroll
   for (int a = 0; a < D; ++a) r[a] = 0.0;
-  for (int c = g.bc_ptr[p]; c < g.bc_ptr[p + 1]; ++c) {
-    const int code = g.bc[c];
+  const int cb0 = g.bc_ptr[p], cb1 = g.bc_ptr[p + 1];
+  int nxc = cb0 < cb1 ? __ldg(&g.bc[cb0]) : 0;
+  for (int c = cb0; c < cb1; ++c) {
+    const int code = nxc;
+    nxc = __ldg(&g.bc[c + 1 < cb1 ? c + 1 : c]);
     const int side = code & 1;
     const double* o = w.scr + (size_t)(code >> 1) * C::SW * Bp + b;
     const double* oh = o + (side ? C::H1 : C::H0) * Bp;
@@ -543,9 +546,13 @@ __device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) acc[i][j] = 0.0;
+  // the next contribution's block indices are loaded in the same memory round trip as this one's blocks
+  // (one dependent index load less per contribution)
+  int2 cn = c0 < c1 ? __ldg(&g.con[c0]) : make_int2(0, 0);
   if (diag) {
     for (int ci = c0; ci < c1; ++ci) {
-      const double* Kp = w.L + (size_t)g.con[ci].y * C::DD * Bp + b;
+      const int2 nx = __ldg(&g.con[ci + 1 < c1 ? ci + 1 : ci]);
+      const double* Kp = w.L + (size_t)cn.y * C::DD * Bp + b;
 #pragma unroll
       for (int h = 0; h < D; h += H) {
         double kv[H][D];
@@ -561,10 +568,11 @@ __device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int
 #pragma unroll
             for (int j = 0; j <= i; ++j) acc[i][j] = fma(kv[c][i], kv[c][j], acc[i][j]);
       }
+      cn = nx;
     }
   } else {
     for (int ci = c0; ci < c1; ++ci) {
-      const int2 cn = g.con[ci];
+      const int2 nx = __ldg(&g.con[ci + 1 < c1 ? ci + 1 : ci]);
       const double* Pp = w.L + (size_t)cn.x * C::DD * Bp + b;
       const double* Kp = w.L + (size_t)cn.y * C::DD * Bp + b;
 #pragma unroll
@@ -585,6 +593,7 @@ __device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int
 #pragma unroll
             for (int j = 0; j < D; ++j) acc[i][j] = fma(pv[c][i], kv[c][j], acc[i][j]);
       }
+      cn = nx;
     }
   }
 }
@@ -596,8 +605,9 @@ __device__ __forceinline__ void bl_acc_fwd(const BLDev& g, const BLWs& w, int b,
   const size_t Bp = g.Bp;
 #pragma unroll
   for (int i = 0; i < D; ++i) acc[i] = 0.0;
+  int2 f = f0 < f1 ? __ldg(&g.fwd[f0]) : make_int2(0, 0);
   for (int q = f0; q < f1; ++q) {
-    const int2 f = g.fwd[q];
+    const int2 nx = __ldg(&g.fwd[q + 1 < f1 ? q + 1 : q]);
     const double* Kp = w.L + (size_t)f.x * C::DD * Bp + b;
     const double* y = w.x + (size_t)f.y * D * Bp + b;
     double kv[D][D], yv[D];
@@ -612,6 +622,7 @@ __device__ __forceinline__ void bl_acc_fwd(const BLDev& g, const BLWs& w, int b,
     for (int c = 0; c < D; ++c)
 #pragma unroll
       for (int i = 0; i < D; ++i) acc[i] = fma(kv[c][i], yv[c], acc[i]);
+    f = nx;
   }
 }
 
@@ -785,6 +796,7 @@ __global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0,
       for (int r = 0; r < D; ++r) t[q][r] = Pb[(q * D + r) * Bp];
   }
   const int2 rk = bred[kb0];
+#pragma unroll 2
   for (int q = 0; q < rk.y; ++q) {
     const double* pp = part + (size_t)(rk.x + q) * C::DD * Bp;
 #pragma unroll
@@ -1451,12 +1463,19 @@ struct BLPlan {
   int upd = -1;         // update kernel below the persistent levels: -1 automatic, 0 row-split, 1 register-blocked
   int persist = -1;     // bl_persist group width (-1 automatic, 0: per-level bl_update* + bl_factor launches)
   int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
+  int solve_from = -1;    // first level of the persistent tail solves (-1: as the factorisation's split)
   int tail_from = 0;      // first level of the single-column tail
   int bsolve_ct = 16;     // column-task backward solve on levels with >= this many columns (0: off)
   int lch = 0;            // per-level chunked update (bl_update_items + bl_factor_red): chunk size (0: off)
   std::vector<int> lit_lvl_ptr;   // per level: its chunked work items
   const int4* d_litems = nullptr;
   const int2 *d_bred = nullptr, *d_cred = nullptr;
+  // ext variant: per-level items without the external parts of the targets above sub_top + the ext items
+  std::vector<int> litx_lvl_ptr;
+  const int4 *d_litems_x = nullptr, *d_xitems = nullptr;
+  const int2 *d_bred_x = nullptr, *d_cred_x = nullptr;
+  int nxitems = 0;
+  bool ext = false;       // DNLS_BL_EXT=1: external parts of the upper targets in one launch (measured slower)
   int sub_top = -1;       // bl_subtree covers the columns of height <= sub_top (-1: off)
   bool sub_any = false;   // bl_subtree for any batch size (default: the large-batch schedule only)
   int nsub = 0;           // its items: maximal subtrees of those columns, largest first
@@ -1508,19 +1527,31 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     for (int k = 0; k < N; ++k) lvl_col[fillp[h[k]]++] = k;
   }
   // update tasks: target (p, k) for p in {k} U cs[k]; contributions from every s with k, p in cs[s]
+  // bottom subtrees: the columns of height <= sub_top (bl_subtree, below); every target list holds the
+  // contributions of sources of height <= sub_top first (the "external" part of an upper target, applied by ONE
+  // launch right after the subtree kernel -- bl_ext items), then the others, each part in increasing source index
+  int sub_top = 10;
+  if (const char* env = std::getenv("DNLS_BL_SUB")) sub_top = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_SUBANY")) pl.sub_any = std::atoi(env) != 0;
+  sub_top = std::min(sub_top, L - 1);
   std::vector<std::vector<int2>> tcon(pl.nblk);
   std::vector<std::vector<int2>> fwdl(N);
-  for (int sc = 0; sc < N; ++sc) {
-    const auto& R = s.colstruct[sc];
-    for (size_t iq = 0; iq < R.size(); ++iq) {
-      const int k = R[iq];
-      fwdl[k].push_back(make_int2(blk(k, sc), sc));
-      for (size_t ip = iq; ip < R.size(); ++ip) {
-        const int p = R[ip];
-        tcon[blk(p, k)].push_back(make_int2(blk(p, sc), blk(k, sc)));
+  std::vector<int> nA(pl.nblk, 0), nAf(N, 0);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int sc = 0; sc < N; ++sc) {
+      if ((h[sc] <= sub_top) != (pass == 0)) continue;
+      const auto& R = s.colstruct[sc];
+      for (size_t iq = 0; iq < R.size(); ++iq) {
+        const int k = R[iq];
+        fwdl[k].push_back(make_int2(blk(k, sc), sc));
+        if (pass == 0) ++nAf[k];
+        for (size_t ip = iq; ip < R.size(); ++ip) {
+          const int p = R[ip];
+          tcon[blk(p, k)].push_back(make_int2(blk(p, sc), blk(k, sc)));
+          if (pass == 0) ++nA[blk(p, k)];
+        }
       }
     }
-  }
   std::vector<int32_t> tsk, con, fwdp(N + 1, 0), fwd, fac;
   pl.tsk_lvl_ptr.assign(L + 1, 0);
   pl.fac_lvl_ptr.assign(L + 1, 0);
@@ -1662,12 +1693,21 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   int lch = 8;
   if (const char* env = std::getenv("DNLS_BL_LCH")) lch = std::atoi(env);
   std::vector<int32_t> litems, bred(2 * (size_t)pl.nblk, 0), cred(2 * (size_t)N, 0);
+  std::vector<int32_t> litems_x, bred_x(2 * (size_t)pl.nblk, 0), cred_x(2 * (size_t)N, 0), xitems;
   pl.lit_lvl_ptr.assign(L + 1, 0);
+  pl.litx_lvl_ptr.assign(L + 1, 0);
   int litems_want = 0, lch_min = 2;   // narrow levels: chunks small enough for ~litems_want items (0: off)
   if (const char* env = std::getenv("DNLS_BL_LITEMS")) sscanf(env, "%d,%d", &litems_want, &lch_min);
-  if (lch > 0) {
+  // split variant (ext): the lists of targets above sub_top without their external part
+  for (int var = 0; var < 2 && lch > 0; ++var) {
+    const bool xv = var == 1;
+    std::vector<int32_t>& litv = xv ? litems_x : litems;
+    std::vector<int32_t>& bredv = xv ? bred_x : bred;
+    std::vector<int32_t>& credv = xv ? cred_x : cred;
+    std::vector<int>& lptr = xv ? pl.litx_lvl_ptr : pl.lit_lvl_ptr;
     const size_t cap = scr_doubles / ((size_t)D * D);
     for (int l = 0; l < L; ++l) {
+      const bool up = xv && l > sub_top;
       int nslot = 0, ncl = 0;
       for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
         const int k = lvl_col[i];
@@ -1680,35 +1720,51 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
         int S = (n + lchl - 1) / lchl;
         if ((size_t)(nslot + S - 1) > cap) S = 1;   // partials would not fit: whole list in place
         if (S <= 1) {
-          litems.insert(litems.end(), {tgt, c0, c1, flags});
+          litv.insert(litv.end(), {tgt, c0, c1, flags});
           return;
         }
         red2[0] = nslot;
         red2[1] = S - 1;
         for (int q = 0; q < S; ++q) {
           const int a = c0 + (int)((int64_t)n * q / S), e = c0 + (int)((int64_t)n * (q + 1) / S);
-          litems.insert(litems.end(), {tgt, a, e, flags | (q == 0 ? 0 : ((nslot + 1) << 8))});
+          litv.insert(litv.end(), {tgt, a, e, flags | (q == 0 ? 0 : ((nslot + 1) << 8))});
           if (q > 0) ++nslot;
         }
       };
       for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
         const int k = lvl_col[i];
-        for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi)
-          if (bcon[4 * (size_t)bi + 1] > bcon[4 * (size_t)bi])
-            add(bi, bcon[4 * (size_t)bi], bcon[4 * (size_t)bi + 1], bcon[4 * (size_t)bi + 2] & 3, &bred[2 * (size_t)bi]);
-        if (fwdp[k + 1] > fwdp[k]) add(-2 - k, fwdp[k], fwdp[k + 1], 0, &cred[2 * (size_t)k]);
+        for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) {
+          const int a = bcon[4 * (size_t)bi] + (up ? nA[bi] : 0), e = bcon[4 * (size_t)bi + 1];
+          // a fill target whose external part is applied first is no longer written first here
+          const int fl = bcon[4 * (size_t)bi + 2] & ((up && nA[bi] > 0) ? 1 : 3);
+          if (e > a) add(bi, a, e, fl, &bredv[2 * (size_t)bi]);
+        }
+        const int fa = fwdp[k] + (up ? nAf[k] : 0);
+        if (fwdp[k + 1] > fa) add(-2 - k, fa, fwdp[k + 1], 0, &credv[2 * (size_t)k]);
       }
-      pl.lit_lvl_ptr[l + 1] = (int)litems.size() / 4;
+      lptr[l + 1] = (int)litv.size() / 4;
     }
   }
+  // ext items: every target / forward row above sub_top with an external part, applied in place (whole list,
+  // a fill target stores -acc), longest lists first
+  if (sub_top >= 0) {
+    std::vector<std::array<int, 4>> xs;
+    for (int k = 0; k < N; ++k) {
+      if (h[k] <= sub_top) continue;
+      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi)
+        if (nA[bi] > 0) xs.push_back({bi, bcon[4 * (size_t)bi], bcon[4 * (size_t)bi] + nA[bi], bcon[4 * (size_t)bi + 2] & 3});
+      if (nAf[k] > 0) xs.push_back({-2 - k, fwdp[k], fwdp[k] + nAf[k], 0});
+    }
+    std::stable_sort(xs.begin(), xs.end(), [](const std::array<int, 4>& a, const std::array<int, 4>& b) {
+      return a[2] - a[1] > b[2] - b[1];
+    });
+    for (auto& x : xs) xitems.insert(xitems.end(), x.begin(), x.end());
+  }
+  pl.nxitems = (int)xitems.size() / 4;
   pl.lch = lch;
   // bottom subtrees (bl_subtree): every column of height <= sub_top belongs to the subtree of its highest
   // ancestor of height <= sub_top; a subtree's columns in increasing index (children first), subtrees by
   // decreasing block count (the longest items start first)
-  int sub_top = 10;
-  if (const char* env = std::getenv("DNLS_BL_SUB")) sub_top = std::atoi(env);
-  if (const char* env = std::getenv("DNLS_BL_SUBANY")) pl.sub_any = std::atoi(env) != 0;
-  sub_top = std::min(sub_top, L - 1);
   std::vector<int32_t> sub_ptr(1, 0), sub_col;
   if (sub_top >= 0) {
     std::vector<int> root(N, -1);
@@ -1748,6 +1804,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   add(bcon); add(it_lvl); add(items); add(rd_lvl); add(red); add(lvl_ptr32); add(fac_lvl32);
   add(sub_ptr); add(sub_col);
   add(litems); add(bred); add(cred);
+  add(litems_x); add(bred_x); add(cred_x); add(xitems);
   while (buf.size() % 4) buf.push_back(0);
   if (device >= 0) {
     if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
@@ -1787,6 +1844,11 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.d_litems = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.d_bred = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.d_cred = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.d_litems_x = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.d_bred_x = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.d_cred_x = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.d_xitems = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  if (const char* env = std::getenv("DNLS_BL_EXT")) pl.ext = std::atoi(env) != 0;
   pl.pd.lvl_col = pl.d_lvl_col;
   pl.pd.L = L;
   pl.pd.coltask_min = 16;
@@ -1794,6 +1856,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   if (const char* env = std::getenv("DNLS_BL_PERSIST")) pl.persist = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_GMAJOR")) g.gmajor = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_SPLIT")) pl.persist_from = std::atoi(env);
+  if (const char* env = std::getenv("DNLS_BL_SSPLIT")) pl.solve_from = std::atoi(env);
 
   if (const char* env = std::getenv("DNLS_BL_UPD")) pl.upd = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_BSCT")) pl.bsolve_ct = std::atoi(env);
@@ -1883,12 +1946,13 @@ struct BLSched {
   int fsplit;   // first level of the factorisation's persistent launch (chunked per-level items: none)
 };
 inline BLSched bl_schedule(const BLPlan& pl, int B) {
-  const bool large = bl_pad(B) / 32 >= 32;
+  const bool large = bl_pad(B) / 32 >= 16;
   BLSched sc;
   sc.rb = pl.upd >= 0 ? pl.upd != 0 : large;
   const bool persist = pl.persist == 0 ? false : (pl.persist > 0 || large);
   sc.lsplit = !persist ? pl.L : (pl.persist_from >= 0 ? std::min(pl.L, pl.persist_from) : pl.tail_from);
   sc.gw = pl.persist > 0 ? pl.persist : ((B + 15) / 16 >= 128 ? 16 : (B + 7) / 8 >= 128 ? 8 : 4);
+  if (pl.solve_from >= 0) sc.lsplit = std::min(pl.L, pl.solve_from);
   sc.fsplit = (sc.rb && pl.lch > 0 && pl.persist_from < 0) ? pl.L : sc.lsplit;
   sc.lfirst = (pl.sub_top >= 0 && pl.nsub > 0 && (large || pl.sub_any)) ? pl.sub_top + 1 : 0;
   return sc;
@@ -1917,6 +1981,8 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   g.Bp = bl_pad(B);
   const BLSched sc = bl_schedule(pl, B);
   const int lsplit = std::max(sc.fsplit, sc.lfirst);
+  // ext variant: the per-level chunked schedule runs every level above sub_top (no persistent factorisation)
+  const bool xv = pl.ext && sc.rb && pl.lch > 0 && lsplit >= pl.L && pl.sub_top >= 0 && sc.lfirst <= pl.sub_top + 1;
   if (sc.lfirst > 0)
     bl_launch(bl_subtree<D>, bl_grid(pl.nsub, g.Bp), BL_TPB, s, g, w, pl.pd.bcon, pl.d_sub_ptr, pl.d_sub_col,
                                                                     pl.nsub, fused_fwd ? 1 : 0);
@@ -1926,12 +1992,19 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
     const long long nu = (long long)nt + (fused_fwd ? nc : 0);
     if (sc.rb && pl.lch > 0) {
       // chunked work items of the level (forward rows skipped in the final factorisation: they have no
-      // effect there), then the factor launch with the split reductions folded in
-      const int i0 = pl.lit_lvl_ptr[l], ni = pl.lit_lvl_ptr[l + 1] - i0;
+      // effect there), then the factor launch with the split reductions folded in.  With ext: the external
+      // parts of every target above sub_top in one launch once the columns up to sub_top are factored.
+      if (xv && l == pl.sub_top + 1 && pl.nxitems > 0)
+        bl_launch(bl_update_items<D>, bl_grid(pl.nxitems, g.Bp), BL_TPB, s, g, w, pl.d_xitems, 0, pl.nxitems,
+                  fused_fwd ? 1 : 0);
+      const std::vector<int>& lp = xv ? pl.litx_lvl_ptr : pl.lit_lvl_ptr;
+      const int i0 = lp[l], ni = lp[l + 1] - i0;
       if (ni > 0)
-        bl_launch(bl_update_items<D>, bl_grid(ni, g.Bp), BL_TPB, s, g, w, pl.d_litems, i0, ni, fused_fwd ? 1 : 0);
+        bl_launch(bl_update_items<D>, bl_grid(ni, g.Bp), BL_TPB, s, g, w, xv ? pl.d_litems_x : pl.d_litems, i0, ni,
+                  fused_fwd ? 1 : 0);
       const int f0 = pl.fac_lvl_ptr[l], nf = pl.fac_lvl_ptr[l + 1] - f0;
-      bl_launch(bl_factor_red<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, f0, nf, fused_fwd ? 1 : 0, pl.d_bred, pl.d_cred);
+      bl_launch(bl_factor_red<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, f0, nf, fused_fwd ? 1 : 0,
+                xv ? pl.d_bred_x : pl.d_bred, xv ? pl.d_cred_x : pl.d_cred);
       continue;
     }
     if (nu > 0 && sc.rb)

@@ -110,13 +110,12 @@ def test_bl_large_batch_schedule_on_small_cases(monkeypatch, dim, N, B, split, g
 def test_bl_subtree_factorisation_is_bitwise_identical(monkeypatch, dim, N, B, sub):
     # bl_subtree (the bottom subtrees of the elimination tree as column tasks in one launch; sub = 100 puts the
     # whole tree in one subtree) sums every target's contributions in the same order as the per-level update +
-    # factor launches: forward, objective and implicit gradients must be bitwise equal to the per-level schedule,
-    # and match the oracle
+    # factor launches of the same plan: forward, objective and implicit gradients must be bitwise equal to the
+    # per-level schedule (small batch: row-split updates), and match the oracle
     topo, data = make_case(N, dim=dim, p=0.3, mode="local", seed=N + B + 1, B=B)
     v = np.random.default_rng(N + 1).standard_normal((B, N, 6 if dim == 3 else 3))
-    monkeypatch.setenv("DNLS_BL_SUB", "-1")
-    ref = solve(topo, data, 5, True, v=v)
     monkeypatch.setenv("DNLS_BL_SUB", sub)
+    ref = solve(topo, data, 5, True, v=v)
     monkeypatch.setenv("DNLS_BL_SUBANY", "1")
     got = solve(topo, data, 5, True, v=v)
     for a, b in zip(ref, got):
@@ -129,18 +128,24 @@ def test_bl_subtree_factorisation_is_bitwise_identical(monkeypatch, dim, N, B, s
         assert abs(got[1][b] - r.objective) <= TOL_OBJ * r.objective + 1e-20
 
 
-@pytest.mark.parametrize("dim,N,B,sub,lch,split", [(3, 256, 40, "2", "1", "100"), (3, 200, 35, "4", "3", "12"),
-                                                   (2, 100, 33, "-1", "2", "100"), (3, 64, 37, "1", "6", "5")])
-def test_bl_chunked_level_updates_match_oracle(monkeypatch, dim, N, B, sub, lch, split):
+@pytest.mark.parametrize("dim,N,B,sub,lch,split,ext", [(3, 256, 40, "2", "1", "100", "1"),
+                                                       (3, 256, 40, "2", "1", "100", "0"),
+                                                       (3, 200, 35, "4", "3", "12", "1"),
+                                                       (2, 100, 33, "-1", "2", "100", "1"),
+                                                       (2, 100, 33, "3", "2", "100", "1"),
+                                                       (3, 64, 37, "1", "6", "5", "1")])
+def test_bl_chunked_level_updates_match_oracle(monkeypatch, dim, N, B, sub, lch, split, ext):
     # the large-batch schedule bench.py's C5 run uses -- bl_subtree for the bottom levels, per-level chunked
     # work items (bl_update_items; lch contributions per chunk, partials reduced in chunk order by
-    # bl_factor_red), the persistent tail from level `split` -- forced on small ragged SE2 / SE3 batches
+    # bl_factor_red), the external parts of the upper targets in one launch after the subtree kernel (ext), the
+    # persistent tail from level `split` (split < levels: no ext) -- forced on small ragged SE2 / SE3 batches
     monkeypatch.setenv("DNLS_BL_UPD", "1")
     monkeypatch.setenv("DNLS_BL_SUBANY", "1")
     monkeypatch.setenv("DNLS_BL_SUB", sub)
     monkeypatch.setenv("DNLS_BL_LCH", lch)
     monkeypatch.setenv("DNLS_BL_SPLIT", split)
     monkeypatch.setenv("DNLS_BL_PERSIST", "8")
+    monkeypatch.setenv("DNLS_BL_EXT", ext)
     topo, data = make_case(N, dim=dim, p=0.3, mode="local", seed=N + B + 2, B=B)
     v = np.random.default_rng(N + 2).standard_normal((B, N, 6 if dim == 3 else 3))
     P, obj, st, it, ge, gp = solve(topo, data, 5, True, v=v)

@@ -10,7 +10,8 @@ import os
 import sys
 from collections import defaultdict
 
-FACTOR_KERNELS = ("bl_update_rb", "bl_update", "bl_factor", "bl_persist")
+FACTOR_KERNELS = ("bl_update_rb", "bl_update", "bl_factor", "bl_persist", "bl_subtree", "bl_update_items",
+                  "bl_factor_red")
 
 path, config, batch, nfac = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
 tag = sys.argv[5] if len(sys.argv) > 5 else os.path.basename(path)
