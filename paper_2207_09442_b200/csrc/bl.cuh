@@ -37,12 +37,12 @@ inline int bl_pdl_on() {
   return on;
 }
 template <typename... KArgs, typename... Args>
-inline void bl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+inline void bl_launch_smem(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   ::dnls::g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -50,6 +50,10 @@ inline void bl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s
   cfg.attrs = at;
   cfg.numAttrs = bl_pdl_on() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline void bl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  bl_launch_smem(k, grid, block, 0, s, args...);
 }
    // threads per block of the BL kernels (4 warps = 4 items x 32 elements)
 
@@ -535,19 +539,21 @@ __device__ __forceinline__ void bl_chol(double (&a)[D][D], double (&iv)[D], doub
 }
 
 // acc[i][j] = sum over the contributions [c0, c1) of (L_ps L_ks^T)(i, j) (diag: lower triangle, L_ks == L_ps),
-// register-blocked, half a block pair per memory round trip
+// register-blocked, a whole block pair per memory round trip.  init != nullptr (the in-place form): acc starts from
+// the target block T (entry (i, j) at init[(j D + i) Bp]) and the products are subtracted, acc = T - sum -- the
+// target's loads then share the first contribution's round trip instead of costing one after the loop.
 template <int D>
 __device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int b, int c0, int c1, bool diag,
-                                              double (&acc)[D][D]) {
+                                              double (&acc)[D][D], const double* init = nullptr) {
   using C = BLC<D>;
   constexpr int H = D / DNLS_PT_HD;
   const size_t Bp = g.Bp;
+  const double sg = init ? -1.0 : 1.0;
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
-    for (int j = 0; j < D; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < D; ++j) acc[i][j] = (init && (!diag || j <= i)) ? init[(j * D + i) * Bp] : 0.0;
   // the next contribution's block indices are loaded in the same memory round trip as this one's blocks
-  // (one dependent index load less per contribution)
   int2 cn = c0 < c1 ? __ldg(&g.con[c0]) : make_int2(0, 0);
   if (diag) {
     for (int ci = c0; ci < c1; ++ci) {
@@ -566,7 +572,7 @@ __device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int
 #pragma unroll
           for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j <= i; ++j) acc[i][j] = fma(kv[c][i], kv[c][j], acc[i][j]);
+            for (int j = 0; j <= i; ++j) acc[i][j] = fma(sg * kv[c][i], kv[c][j], acc[i][j]);
       }
       cn = nx;
     }
@@ -591,20 +597,22 @@ __device__ __forceinline__ void bl_acc_target(const BLDev& g, const BLWs& w, int
 #pragma unroll
           for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j < D; ++j) acc[i][j] = fma(pv[c][i], kv[c][j], acc[i][j]);
+            for (int j = 0; j < D; ++j) acc[i][j] = fma(sg * pv[c][i], kv[c][j], acc[i][j]);
       }
       cn = nx;
     }
   }
 }
 
-// forward-substitution sum of column k over [f0, f1): acc = sum_s L_ks y_s
+// forward-substitution sum of column k over [f0, f1): acc = sum_s L_ks y_s; init != nullptr: acc = x_k - sum
 template <int D>
-__device__ __forceinline__ void bl_acc_fwd(const BLDev& g, const BLWs& w, int b, int f0, int f1, double (&acc)[D]) {
+__device__ __forceinline__ void bl_acc_fwd(const BLDev& g, const BLWs& w, int b, int f0, int f1, double (&acc)[D],
+                                           const double* init = nullptr) {
   using C = BLC<D>;
   const size_t Bp = g.Bp;
+  const double sg = init ? -1.0 : 1.0;
 #pragma unroll
-  for (int i = 0; i < D; ++i) acc[i] = 0.0;
+  for (int i = 0; i < D; ++i) acc[i] = init ? init[i * Bp] : 0.0;
   int2 f = f0 < f1 ? __ldg(&g.fwd[f0]) : make_int2(0, 0);
   for (int q = f0; q < f1; ++q) {
     const int2 nx = __ldg(&g.fwd[q + 1 < f1 ? q + 1 : q]);
@@ -621,7 +629,7 @@ __device__ __forceinline__ void bl_acc_fwd(const BLDev& g, const BLWs& w, int b,
 #pragma unroll
     for (int c = 0; c < D; ++c)
 #pragma unroll
-      for (int i = 0; i < D; ++i) acc[i] = fma(kv[c][i], yv[c], acc[i]);
+      for (int i = 0; i < D; ++i) acc[i] = fma(sg * kv[c][i], yv[c], acc[i]);
     f = nx;
   }
 }
@@ -686,34 +694,35 @@ __device__ __forceinline__ void bl_column_task(const BLDev& g, const BLWs& w, co
   double a[D][D], iv[D];
   {
     const int4 bc = bcon[kb0];
-    double acc[D][D];
-    bl_acc_target<D>(g, w, b, bc.x, bc.y, true, acc);
-    const double* T = w.L + (size_t)kb0 * C::DD * Bp + b;
-#pragma unroll
-    for (int j = 0; j < D; ++j)
-#pragma unroll
-      for (int i = j; i < D; ++i) a[i][j] = T[(j * D + i) * Bp] - acc[i][j];
+    bl_acc_target<D>(g, w, b, bc.x, bc.y, true, a, w.L + (size_t)kb0 * C::DD * Bp + b);   // a = T_kk - sum
   }
   bool bad = false;
   bl_chol<D>(a, iv, tol, bad);
-  if (fused_fwd && g.fwdp[k + 1] > g.fwdp[k]) {
-    double acc[D];
-    bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], acc);
+  bl_store_diag<D>(g, w, b, k, a, iv, bad, false);
+  if (fused_fwd) {   // y_k = L_kk^-1 (x_k - sum_s L_ks y_s), x_k read in the first contribution's round trip
     double* xk = w.x + (size_t)k * D * Bp + b;
+    double t[D], y[D];
+    bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], t, xk);
 #pragma unroll
-    for (int i = 0; i < D; ++i) xk[i * Bp] -= acc[i];
+    for (int q = 0; q < D; ++q) {
+      double s2 = t[q];
+#pragma unroll
+      for (int r = 0; r < q; ++r) s2 = fma(-a[q][r], y[r], s2);
+      y[q] = s2 * iv[q];
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) xk[q * Bp] = y[q];
   }
-  bl_store_diag<D>(g, w, b, k, a, iv, bad, fused_fwd);
   for (int bi = kb0 + 1; bi < kb1; ++bi) {
     const int4 bc = bcon[bi];
-    double acc[D][D];
-    bl_acc_target<D>(g, w, b, bc.x, bc.y, false, acc);
     double* Pb = w.L + (size_t)bi * C::DD * Bp + b;
+    double acc[D][D];
+    bl_acc_target<D>(g, w, b, bc.x, bc.y, false, acc, (bc.z & 2) ? nullptr : Pb);   // T_pk - sum (fill: -sum)
     double t[D][D];
 #pragma unroll
     for (int q = 0; q < D; ++q)
 #pragma unroll
-      for (int r = 0; r < D; ++r) t[q][r] = ((bc.z & 2) ? 0.0 : Pb[(q * D + r) * Bp]) - acc[r][q];
+      for (int r = 0; r < D; ++r) t[q][r] = (bc.z & 2) ? -acc[r][q] : acc[r][q];
     bl_trsm_store<D>(Pb, Bp, t, a, iv);
   }
 }
@@ -729,24 +738,25 @@ __device__ __forceinline__ void bl_work_item(const BLDev& g, const BLWs& w, doub
   const int slot = (itm.w >> 8) - 1;
   if (itm.x >= 0) {
     const bool diag = itm.w & 1, fill = itm.w & 2;
-    double acc[D][D];
-    bl_acc_target<D>(g, w, b, itm.y, itm.z, diag, acc);
     double* T = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.L + (size_t)itm.x * C::DD * Bp + b;
+    double acc[D][D];
+    // in place: acc = T - sum (a fill target: -sum); a chunk partial: acc = sum
+    bl_acc_target<D>(g, w, b, itm.y, itm.z, diag, acc, (slot >= 0 || fill) ? nullptr : T);
+    const double sg = (slot < 0 && fill) ? -1.0 : 1.0;
 #pragma unroll
     for (int j = 0; j < D; ++j)
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         if (diag && i < j) continue;
-        double* t = T + (size_t)(j * D + i) * Bp;
-        *t = slot >= 0 ? acc[i][j] : (fill ? -acc[i][j] : *t - acc[i][j]);
+        T[(size_t)(j * D + i) * Bp] = sg * acc[i][j];
       }
   } else if (fused_fwd) {
-    double acc[D];
-    bl_acc_fwd<D>(g, w, b, itm.y, itm.z, acc);
     const int k = -2 - itm.x;
     double* X = slot >= 0 ? part + (size_t)slot * C::DD * Bp + b : w.x + (size_t)k * D * Bp + b;
+    double acc[D];
+    bl_acc_fwd<D>(g, w, b, itm.y, itm.z, acc, slot >= 0 ? nullptr : X);
 #pragma unroll
-    for (int i = 0; i < D; ++i) X[i * Bp] = slot >= 0 ? acc[i] : X[i * Bp] - acc[i];
+    for (int i = 0; i < D; ++i) X[i * Bp] = acc[i];
   }
 }
 
@@ -960,6 +970,119 @@ __global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev 
         }
       }
     phase_end();
+  }
+}
+
+// level-parallel persistent triangular solves over the levels [l_begin, L) (backward: root -> l_begin, forward:
+// l_begin -> root): one CTA per group of GW elements, U = BLP_NT / GW units.  Per level, the level's items --
+// (column, below block) pairs for the backward substitution, (column, forward contribution) pairs for the forward
+// one, contiguous per column -- go round robin over the units, each storing its d-vector product in shared
+// memory; after one barrier the units take the level's columns: x_k minus the column's item vectors in item order
+// (independent of which unit computed them), then L_kk^-T (backward) / L_kk^-1 (forward).  Two barriers per level
+// instead of a launch per level (or two barriers per column in bl_persist_solve).
+struct BLSDev {
+  const int2* bit;      // backward items (column position in lvl_col, block)
+  const int* bit_lvl;   // [L+1]
+  const int2* bcol;     // per column position: (first backward item, count)
+  const int2* fit;      // forward items (column position, forward contribution index)
+  const int* fit_lvl;   // [L+1]
+  const int2* fcol;     // per column position: (first forward item, count)
+};
+
+template <int D, int GW>
+__global__ void __launch_bounds__(BLP_NT) bl_lsolve(BLDev g, BLWs w, BLPDev pd, BLSDev sd, const int* skip,
+                                                    int forward, int l_begin, int l_end) {
+  bl_pdl();
+  using C = BLC<D>;
+  constexpr int U = BLP_NT / GW;
+  extern __shared__ double spart[];   // [level items][D][GW]
+  const int u = threadIdx.x / GW, e = threadIdx.x % GW;
+  const int b = blockIdx.x * GW + e;
+  const bool act = b < g.B && !(skip && skip[b]);
+  const size_t Bp = g.Bp;
+  const int2* items = forward ? sd.fit : sd.bit;
+  const int* ilvl = forward ? sd.fit_lvl : sd.bit_lvl;
+  const int2* icol = forward ? sd.fcol : sd.bcol;
+  const int nl = l_end - l_begin;
+  for (int li = 0; li < nl; ++li) {
+    const int l = forward ? l_begin + li : l_end - 1 - li;
+    const int i0 = ilvl[l], i1 = ilvl[l + 1];
+    for (int ii = i0 + u; ii < i1; ii += U) {
+      double acc[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) acc[i] = 0.0;
+      if (act) {
+        const int2 it = items[ii];
+        if (forward) {   // acc = L_ks y_s
+          const int2 f = g.fwd[it.y];
+          const double* Kp = w.L + (size_t)f.x * C::DD * Bp + b;
+          const double* y = w.x + (size_t)f.y * D * Bp + b;
+          double kv[D][D], yv[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            yv[c] = y[c * Bp];
+#pragma unroll
+            for (int i = 0; i < D; ++i) kv[c][i] = Kp[(c * D + i) * Bp];
+          }
+          bl_issue_fence();
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+#pragma unroll
+            for (int i = 0; i < D; ++i) acc[i] = fma(kv[c][i], yv[c], acc[i]);
+        } else {   // acc = L_pk^T x_p
+          const double* P0 = w.L + (size_t)it.y * C::DD * Bp + b;
+          const double* x0 = w.x + (size_t)g.blkrow[it.y] * D * Bp + b;
+          double lv[D][D], xv[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            xv[q] = x0[q * Bp];
+#pragma unroll
+            for (int c = 0; c < D; ++c) lv[c][q] = P0[(c * D + q) * Bp];
+          }
+          bl_issue_fence();
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+#pragma unroll
+            for (int q = 0; q < D; ++q) acc[c] = fma(lv[c][q], xv[q], acc[c]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) spart[((size_t)(ii - i0) * D + i) * GW + e] = acc[i];
+    }
+    __syncthreads();
+    for (int ci = pd.lvl_ptr[l] + u; ci < pd.lvl_ptr[l + 1]; ci += U) {
+      if (!act) continue;
+      const int k = pd.lvl_col[ci];
+      const int2 rg = icol[ci];
+      double* xk = w.x + (size_t)k * D * Bp + b;
+      const double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+      double t[D], y[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) t[i] = xk[i * Bp];
+      for (int q = 0; q < rg.y; ++q)
+#pragma unroll
+        for (int i = 0; i < D; ++i) t[i] -= spart[((size_t)(rg.x - i0 + q) * D + i) * GW + e];
+      if (forward) {
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          double s2 = t[q];
+#pragma unroll
+          for (int r = 0; r < q; ++r) s2 = fma(-Lk[(r * D + q) * Bp], y[r], s2);
+          y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+        }
+      } else {
+#pragma unroll
+        for (int q = D - 1; q >= 0; --q) {
+          double s2 = t[q];
+#pragma unroll
+          for (int p = q + 1; p < D; ++p) s2 = fma(-Lk[(q * D + p) * Bp], y[p], s2);
+          y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) xk[i * Bp] = y[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -1464,7 +1587,11 @@ struct BLPlan {
   int persist = -1;     // bl_persist group width (-1 automatic, 0: per-level bl_update* + bl_factor launches)
   int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
   int solve_from = -1;    // first level of the persistent tail solves (-1: as the factorisation's split)
+  int lsolve = 1;         // persistent tail solves: 1 level-parallel bl_lsolve, 0 bl_persist_solve (DNLS_BL_LSOLVE)
+  BLSDev sd{};
+  std::vector<int> bit_lvl_h, fit_lvl_h;   // host copies: items per level of bl_lsolve
   int tail_from = 0;      // first level of the single-column tail
+  int narrow_from = 0;    // first level of the narrow top (every level above has <= 6 columns)
   int bsolve_ct = 16;     // column-task backward solve on levels with >= this many columns (0: off)
   int lch = 0;            // per-level chunked update (bl_update_items + bl_factor_red): chunk size (0: off)
   std::vector<int> lit_lvl_ptr;   // per level: its chunked work items
@@ -1761,6 +1888,25 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     for (auto& x : xs) xitems.insert(xitems.end(), x.begin(), x.end());
   }
   pl.nxitems = (int)xitems.size() / 4;
+  // bl_lsolve items: per level, per column (in lvl_col order) its below blocks (backward) / forward contributions
+  std::vector<int32_t> bit, fit, bcolv(2 * (size_t)N, 0), fcolv(2 * (size_t)N, 0);
+  pl.bit_lvl_h.assign(L + 1, 0);
+  pl.fit_lvl_h.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) {
+    for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
+      const int k = lvl_col[i];
+      bcolv[2 * (size_t)i] = (int)bit.size() / 2;
+      bcolv[2 * (size_t)i + 1] = colptr[k + 1] - colptr[k] - 1;
+      for (int bi = colptr[k] + 1; bi < colptr[k + 1]; ++bi) bit.insert(bit.end(), {i, bi});
+      fcolv[2 * (size_t)i] = (int)fit.size() / 2;
+      fcolv[2 * (size_t)i + 1] = fwdp[k + 1] - fwdp[k];
+      for (int q = fwdp[k]; q < fwdp[k + 1]; ++q) fit.insert(fit.end(), {i, q});
+    }
+    pl.bit_lvl_h[l + 1] = (int)bit.size() / 2;
+    pl.fit_lvl_h[l + 1] = (int)fit.size() / 2;
+  }
+  std::vector<int32_t> bit_lvl32(pl.bit_lvl_h.begin(), pl.bit_lvl_h.end()), fit_lvl32(pl.fit_lvl_h.begin(),
+                                                                                       pl.fit_lvl_h.end());
   pl.lch = lch;
   // bottom subtrees (bl_subtree): every column of height <= sub_top belongs to the subtree of its highest
   // ancestor of height <= sub_top; a subtree's columns in increasing index (children first), subtrees by
@@ -1805,6 +1951,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   add(sub_ptr); add(sub_col);
   add(litems); add(bred); add(cred);
   add(litems_x); add(bred_x); add(cred_x); add(xitems);
+  add(bit); add(bit_lvl32); add(bcolv); add(fit); add(fit_lvl32); add(fcolv);
   while (buf.size() % 4) buf.push_back(0);
   if (device >= 0) {
     if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
@@ -1848,6 +1995,13 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.d_bred_x = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.d_cred_x = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.d_xitems = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.sd.bit = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.sd.bit_lvl = ptr(offs[k++]);
+  pl.sd.bcol = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.sd.fit = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.sd.fit_lvl = ptr(offs[k++]);
+  pl.sd.fcol = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  if (const char* env = std::getenv("DNLS_BL_LSOLVE")) pl.lsolve = std::atoi(env);
   if (const char* env = std::getenv("DNLS_BL_EXT")) pl.ext = std::atoi(env) != 0;
   pl.pd.lvl_col = pl.d_lvl_col;
   pl.pd.L = L;
@@ -1862,6 +2016,9 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   if (const char* env = std::getenv("DNLS_BL_BSCT")) pl.bsolve_ct = std::atoi(env);
   pl.tail_from = L;
   while (pl.tail_from > 0 && pl.lvl_ptr[pl.tail_from] - pl.lvl_ptr[pl.tail_from - 1] == 1) --pl.tail_from;
+  // level-parallel tail solves (bl_lsolve) from the first level above which every level has <= 6 columns
+  pl.narrow_from = L;
+  while (pl.narrow_from > 0 && pl.lvl_ptr[pl.narrow_from] - pl.lvl_ptr[pl.narrow_from - 1] <= 6) --pl.narrow_from;
   g.nfill = (int)fill.size();
   g.ndup = (int)dup_blk.size();
   return std::string();
@@ -1944,6 +2101,7 @@ struct BLSched {
   int lsplit, gw;
   int lfirst;   // first level of the per-level launches (levels below: bl_subtree)
   int fsplit;   // first level of the factorisation's persistent launch (chunked per-level items: none)
+  int sgw;      // bl_lsolve group width
 };
 inline BLSched bl_schedule(const BLPlan& pl, int B) {
   const bool large = bl_pad(B) / 32 >= 16;
@@ -1952,7 +2110,12 @@ inline BLSched bl_schedule(const BLPlan& pl, int B) {
   const bool persist = pl.persist == 0 ? false : (pl.persist > 0 || large);
   sc.lsplit = !persist ? pl.L : (pl.persist_from >= 0 ? std::min(pl.L, pl.persist_from) : pl.tail_from);
   sc.gw = pl.persist > 0 ? pl.persist : ((B + 15) / 16 >= 128 ? 16 : (B + 7) / 8 >= 128 ? 8 : 4);
-  if (pl.solve_from >= 0) sc.lsplit = std::min(pl.L, pl.solve_from);
+  // bl_lsolve group width: 8 elements per CTA when that still gives >= 148 CTAs (C5: 256 CTAs), else 4
+  sc.sgw = pl.persist > 0 ? pl.persist : ((B + 7) / 8 >= 148 ? 8 : 4);
+  if (pl.solve_from >= 0)
+    sc.lsplit = std::min(pl.L, pl.solve_from);
+  else if (persist && pl.lsolve && pl.persist_from < 0)
+    sc.lsplit = pl.narrow_from;   // bl_lsolve: the narrow top of the tree (measured: C5 ss20 / gw 8 best)
   sc.fsplit = (sc.rb && pl.lch > 0 && pl.persist_from < 0) ? pl.L : sc.lsplit;
   sc.lfirst = (pl.sub_top >= 0 && pl.nsub > 0 && (large || pl.sub_any)) ? pl.sub_top + 1 : 0;
   return sc;
@@ -2034,24 +2197,51 @@ void bl_solve(const BLPlan& pl, int B, const BLWs& w, bool forward, const int* s
   g.B = B;
   g.Bp = bl_pad(B);
   const BLSched sc = bl_schedule(pl, B);
+  // bl_lsolve: the first level from which every level's items fit the shared-memory budget
+  int ls = sc.lsplit;
+  size_t smem = 0;
+  if (pl.lsolve && ls < pl.L) {
+    constexpr size_t budget = 200 * 1024;
+    auto need = [&](int l) {
+      const int ni = std::max(pl.bit_lvl_h[l + 1] - pl.bit_lvl_h[l], pl.fit_lvl_h[l + 1] - pl.fit_lvl_h[l]);
+      return (size_t)ni * D * sc.sgw * sizeof(double);
+    };
+    int lo = pl.L;
+    while (lo > ls && need(lo - 1) <= budget) --lo;
+    ls = lo;
+    for (int l = ls; l < pl.L; ++l) smem = std::max(smem, need(l));
+  }
   auto tail = [&](int fwd) {
-    if (sc.lsplit >= pl.L) return;
+    if (ls >= pl.L) return;
+    if (pl.lsolve) {
+      auto go = [&](auto kern, int gw) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        bl_launch_smem(kern, (B + gw - 1) / gw, BLP_NT, smem, s, g, w, pl.pd, pl.sd, skip, fwd, ls, pl.L);
+      };
+      switch (sc.sgw) {
+        case 32: go(bl_lsolve<D, 32>, 32); break;
+        case 16: go(bl_lsolve<D, 16>, 16); break;
+        case 8: go(bl_lsolve<D, 8>, 8); break;
+        default: go(bl_lsolve<D, 4>, 4); break;
+      }
+      return;
+    }
     switch (sc.gw) {
-      case 32: bl_launch(bl_persist_solve<D, 32>, (B + 31) / 32, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
-      case 16: bl_launch(bl_persist_solve<D, 16>, (B + 15) / 16, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
-      case 8: bl_launch(bl_persist_solve<D, 8>, (B + 7) / 8, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
-      default: bl_launch(bl_persist_solve<D, 4>, (B + 3) / 4, BLP_NT, s, g, w, pl.pd, skip, fwd, sc.lsplit, pl.L); break;
+      case 32: bl_launch(bl_persist_solve<D, 32>, (B + 31) / 32, BLP_NT, s, g, w, pl.pd, skip, fwd, ls, pl.L); break;
+      case 16: bl_launch(bl_persist_solve<D, 16>, (B + 15) / 16, BLP_NT, s, g, w, pl.pd, skip, fwd, ls, pl.L); break;
+      case 8: bl_launch(bl_persist_solve<D, 8>, (B + 7) / 8, BLP_NT, s, g, w, pl.pd, skip, fwd, ls, pl.L); break;
+      default: bl_launch(bl_persist_solve<D, 4>, (B + 3) / 4, BLP_NT, s, g, w, pl.pd, skip, fwd, ls, pl.L); break;
     }
   };
   if (forward) {
-    for (int l = 0; l < sc.lsplit; ++l) {
+    for (int l = 0; l < ls; ++l) {
       const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
       bl_launch(bl_fsolve<D>, bl_grid_rows(nc, g.Bp), D * 32, s, g, w, pl.d_lvl_col + c0, nc, skip);
     }
     tail(1);
   }
   tail(0);
-  for (int l = sc.lsplit - 1; l >= 0; --l) {
+  for (int l = ls - 1; l >= 0; --l) {
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
     if (sc.rb && pl.bsolve_ct && nc >= pl.bsolve_ct)
       bl_launch(bl_bsolve_ct<D>, bl_grid(nc, g.Bp), BL_TPB, s, g, w, pl.d_lvl_col + c0, nc, skip);

@@ -84,14 +84,16 @@ def test_bl_parallel_edges_early_stop_and_failures():
     assert np.all(ge == 0) and np.all(gp == 0)
 
 
-@pytest.mark.parametrize("dim,N,B,split,gw", [(3, 64, 37, "4", "4"), (2, 100, 33, "6", "8"), (3, 125, 40, "0", "16")])
-def test_bl_large_batch_schedule_on_small_cases(monkeypatch, dim, N, B, split, gw):
+@pytest.mark.parametrize("dim,N,B,split,gw,lsolve", [(3, 64, 37, "4", "4", "1"), (2, 100, 33, "6", "8", "1"),
+                                                    (3, 125, 40, "0", "16", "1"), (3, 64, 37, "4", "4", "0")])
+def test_bl_large_batch_schedule_on_small_cases(monkeypatch, dim, N, B, split, gw, lsolve):
     # the schedule bench.py's C5 run uses (register-blocked update + persistent tail with chunked update lists
     # and dynamic unit scheduling + persistent tail solves) forced on small ragged batches, SE2 and SE3,
     # against the oracle; the plan reads the environment when the graph's batch-interleaved plan is built
     monkeypatch.setenv("DNLS_BL_UPD", "1")
     monkeypatch.setenv("DNLS_BL_PERSIST", gw)
     monkeypatch.setenv("DNLS_BL_SPLIT", split)
+    monkeypatch.setenv("DNLS_BL_LSOLVE", lsolve)   # tail solves: level-parallel bl_lsolve / bl_persist_solve
     topo, data = make_case(N, dim=dim, p=0.3, mode="local", seed=N + B, B=B)
     v = np.random.default_rng(N).standard_normal((B, N, 6 if dim == 3 else 3))
     P, obj, st, it, ge, gp = solve(topo, data, 6, True, v=v)
@@ -107,19 +109,26 @@ def test_bl_large_batch_schedule_on_small_cases(monkeypatch, dim, N, B, split, g
 
 
 @pytest.mark.parametrize("dim,N,B,sub", [(3, 256, 40, "4"), (3, 256, 33, "8"), (2, 100, 35, "100"), (3, 64, 37, "0")])
-def test_bl_subtree_factorisation_is_bitwise_identical(monkeypatch, dim, N, B, sub):
+def test_bl_subtree_factorisation_matches_per_level_schedule(monkeypatch, dim, N, B, sub):
     # bl_subtree (the bottom subtrees of the elimination tree as column tasks in one launch; sub = 100 puts the
     # whole tree in one subtree) sums every target's contributions in the same order as the per-level update +
-    # factor launches of the same plan: forward, objective and implicit gradients must be bitwise equal to the
-    # per-level schedule (small batch: row-split updates), and match the oracle
+    # factor launches of the same plan, starting from T (T - p1 - p2 ...) where the row-split kernel forms
+    # T - (p1 + p2 ...): forward, objective and implicit gradients agree with the per-level schedule (small
+    # batch: row-split updates) to rounding, and match the oracle
     topo, data = make_case(N, dim=dim, p=0.3, mode="local", seed=N + B + 1, B=B)
     v = np.random.default_rng(N + 1).standard_normal((B, N, 6 if dim == 3 else 3))
     monkeypatch.setenv("DNLS_BL_SUB", sub)
     ref = solve(topo, data, 5, True, v=v)
     monkeypatch.setenv("DNLS_BL_SUBANY", "1")
     got = solve(topo, data, 5, True, v=v)
-    for a, b in zip(ref, got):
-        assert np.array_equal(a, b)
+    assert np.max(np.abs(got[0] - ref[0])) <= 1e-11 * max(1.0, np.max(np.abs(ref[0])))
+    assert np.max(np.abs(got[1] - ref[1]) / ref[1]) <= 1e-11
+    assert np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
+    # weight gradients as one vector per element (the prior weight's gradient is rounding noise at the optimum)
+    gr = np.concatenate([ref[4], ref[5]], axis=1)
+    gg = np.concatenate([got[4], got[5]], axis=1)
+    for b in range(B):
+        assert rel_vec_err(gg[b], gr[b]) <= 1e-9, b
     samples = [0, B - 1]
     subd = {k: (val[samples] if k in ("poses0", "meas", "prior_meas") else val) for k, val in data.items()}
     res = oracle_results(topo, subd, max_iterations=5, implicit=True)
