@@ -114,8 +114,8 @@ typedef struct dnls_options {
   /* Path of dnls_forward / dnls_backward_implicit (DESIGN.md §6 "throughput path"): 1 = one CTA per batch
    * element (fused k_forward, any optimizer / backward mode); 32 = the batch-interleaved level-major path
    * (element-interleaved factor storage, Gauss-Newton with the implicit or no backward, quadratic costs;
-   * other settings fall back to 1); 0 = automatic: 32 when supported and batch >= 512 (measured crossover,
-   * environment DNLS_BL_MIN_BATCH), else 1.  Results agree to rounding (summation order), tested. */
+   * other settings fall back to 1); 0 = automatic: 32 when supported, batch >= 256 and batch x num_vars >=
+   * 262144 (measured crossover, environment DNLS_BL_MIN_BATCH for the batch bound), else 1.  Results agree to rounding (summation order), tested. */
   int32_t batch_interleave;
 } dnls_options;
 

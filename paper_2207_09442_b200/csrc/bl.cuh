@@ -778,16 +778,10 @@ __global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_items(BLDev g,
 // order), x_k minus the forward row's partials, then bl_factor's arithmetic.  pr = (first slot, count) per
 // block (bred) and per column's forward row (cred).
 template <int D>
-__global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0, int nfac, int fused_fwd,
-                                                       const int2* bred, const int2* cred) {
-  bl_pdl();
+__device__ __forceinline__ void bl_factor_item(const BLDev& g, const BLWs& w, const int2 fi, int b, bool fused_fwd,
+                                               const int2* bred, const int2* cred) {
   using C = BLC<D>;
-  int b;
-  long long it;
-  if (!bl_item(g, nfac, b, it)) return;
-  if (b >= g.B || bl_frozen(w, b)) return;
   const size_t Bp = g.Bp;
-  const int2 fi = g.fac[f0 + it];
   const int k = fi.x, kb0 = g.colptr[k];
   const bool diag = fi.y == kb0;
   const double* Kk = w.L + (size_t)kb0 * C::DD * Bp + b;
@@ -843,6 +837,17 @@ __global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0,
     return;
   }
   bl_trsm_store<D>(Pb, Bp, t, a, iv);
+}
+
+template <int D>
+__global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0, int nfac, int fused_fwd,
+                                                       const int2* bred, const int2* cred) {
+  bl_pdl();
+  int b;
+  long long it;
+  if (!bl_item(g, nfac, b, it)) return;
+  if (b >= g.B || bl_frozen(w, b)) return;
+  bl_factor_item<D>(g, w, g.fac[f0 + it], b, fused_fwd != 0, bred, cred);
 }
 
 // bottom of the elimination tree in ONE launch: every maximal subtree of columns of height <= the plan's
@@ -2104,7 +2109,7 @@ struct BLSched {
   int sgw;      // bl_lsolve group width
 };
 inline BLSched bl_schedule(const BLPlan& pl, int B) {
-  const bool large = bl_pad(B) / 32 >= 16;
+  const bool large = bl_pad(B) / 32 >= 8;
   BLSched sc;
   sc.rb = pl.upd >= 0 ? pl.upd != 0 : large;
   const bool persist = pl.persist == 0 ? false : (pl.persist > 0 || large);

@@ -1269,9 +1269,10 @@ bool bl_choose(const dnls_graph* g, int batch, const dnls_options* opt, const dn
   if (opt->batch_interleave == 32) return true;
   // automatic: many problems per GPU (measured crossover); below it one CTA
   // per element (k_forward) keeps each problem's factor on chip
-  (void)g;
-  static const int min_batch = std::getenv("DNLS_BL_MIN_BATCH") ? std::atoi(std::getenv("DNLS_BL_MIN_BATCH")) : 512;
-  return batch >= min_batch;
+  // (profiles/r3q: C4 graph, 1024 poses: B = 256 132k vs 112k problem-iter/s, B = 128 73k vs 112k; C2 graph, 256
+  // poses: B = 256 317k vs 555k, B = 512 568k vs 550k): batch >= 256 and batch x poses >= 256 x 1024
+  static const int min_batch = std::getenv("DNLS_BL_MIN_BATCH") ? std::atoi(std::getenv("DNLS_BL_MIN_BATCH")) : 256;
+  return batch >= min_batch && (long long)batch * g->sym.N >= 262144LL;
 }
 size_t bl_ws_bytes(const dnls_graph* g, int batch) {
   const Symbolic& s = g->sym;
