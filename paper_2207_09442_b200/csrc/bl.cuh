@@ -840,14 +840,14 @@ __device__ __forceinline__ void bl_factor_item(const BLDev& g, const BLWs& w, co
 }
 
 template <int D>
-__global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, int f0, int nfac, int fused_fwd,
-                                                       const int2* bred, const int2* cred) {
+__global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, const int2* fac, int f0, int nfac,
+                                                       int fused_fwd, const int2* bred, const int2* cred) {
   bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, nfac, b, it)) return;
   if (b >= g.B || bl_frozen(w, b)) return;
-  bl_factor_item<D>(g, w, g.fac[f0 + it], b, fused_fwd != 0, bred, cred);
+  bl_factor_item<D>(g, w, fac[f0 + it], b, fused_fwd != 0, bred, cred);
 }
 
 // bottom of the elimination tree in ONE launch: every maximal subtree of columns of height <= the plan's
@@ -1592,6 +1592,8 @@ struct BLPlan {
   int persist = -1;     // bl_persist group width (-1 automatic, 0: per-level bl_update* + bl_factor launches)
   int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
   int solve_from = -1;    // first level of the persistent tail solves (-1: as the factorisation's split)
+  std::vector<int> facf_lvl_ptr;   // per level: factor items of the columns outside the subtrees
+  const int2* d_facf = nullptr;
   int lsolve = 1;         // persistent tail solves: 1 level-parallel bl_lsolve, 0 bl_persist_solve (DNLS_BL_LSOLVE)
   BLSDev sd{};
   std::vector<int> bit_lvl_h, fit_lvl_h;   // host copies: items per level of bl_lsolve
@@ -1602,14 +1604,11 @@ struct BLPlan {
   std::vector<int> lit_lvl_ptr;   // per level: its chunked work items
   const int4* d_litems = nullptr;
   const int2 *d_bred = nullptr, *d_cred = nullptr;
-  // ext variant: per-level items without the external parts of the targets above sub_top + the ext items
-  std::vector<int> litx_lvl_ptr;
-  const int4 *d_litems_x = nullptr, *d_xitems = nullptr;
-  const int2 *d_bred_x = nullptr, *d_cred_x = nullptr;
-  int nxitems = 0;
-  bool ext = false;       // DNLS_BL_EXT=1: external parts of the upper targets in one launch (measured slower)
+  // filtered variant (with bl_subtree): per-level items / reductions of the columns outside the subtrees
+  std::vector<int> litf_lvl_ptr;
+  const int4* d_litems_f = nullptr;
+  const int2 *d_bred_f = nullptr, *d_cred_f = nullptr;
   int sub_top = -1;       // bl_subtree covers the columns of height <= sub_top (-1: off)
-  bool sub_any = false;   // bl_subtree for any batch size (default: the large-batch schedule only)
   int nsub = 0;           // its items: maximal subtrees of those columns, largest first
   const int *d_sub_ptr = nullptr, *d_sub_col = nullptr;
 
@@ -1659,31 +1658,24 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     for (int k = 0; k < N; ++k) lvl_col[fillp[h[k]]++] = k;
   }
   // update tasks: target (p, k) for p in {k} U cs[k]; contributions from every s with k, p in cs[s]
-  // bottom subtrees: the columns of height <= sub_top (bl_subtree, below); every target list holds the
-  // contributions of sources of height <= sub_top first (the "external" part of an upper target, applied by ONE
-  // launch right after the subtree kernel -- bl_ext items), then the others, each part in increasing source index
-  int sub_top = 10;
+  // bottom subtrees: the columns of height <= sub_top (no height bound by default) whose subtree work is bounded
+  // are factored by bl_subtree, below
+  int sub_top = 1 << 20;
   if (const char* env = std::getenv("DNLS_BL_SUB")) sub_top = std::atoi(env);
-  if (const char* env = std::getenv("DNLS_BL_SUBANY")) pl.sub_any = std::atoi(env) != 0;
   sub_top = std::min(sub_top, L - 1);
   std::vector<std::vector<int2>> tcon(pl.nblk);
   std::vector<std::vector<int2>> fwdl(N);
-  std::vector<int> nA(pl.nblk, 0), nAf(N, 0);
-  for (int pass = 0; pass < 2; ++pass)
-    for (int sc = 0; sc < N; ++sc) {
-      if ((h[sc] <= sub_top) != (pass == 0)) continue;
-      const auto& R = s.colstruct[sc];
-      for (size_t iq = 0; iq < R.size(); ++iq) {
-        const int k = R[iq];
-        fwdl[k].push_back(make_int2(blk(k, sc), sc));
-        if (pass == 0) ++nAf[k];
-        for (size_t ip = iq; ip < R.size(); ++ip) {
-          const int p = R[ip];
-          tcon[blk(p, k)].push_back(make_int2(blk(p, sc), blk(k, sc)));
-          if (pass == 0) ++nA[blk(p, k)];
-        }
+  for (int sc = 0; sc < N; ++sc) {
+    const auto& R = s.colstruct[sc];
+    for (size_t iq = 0; iq < R.size(); ++iq) {
+      const int k = R[iq];
+      fwdl[k].push_back(make_int2(blk(k, sc), sc));
+      for (size_t ip = iq; ip < R.size(); ++ip) {
+        const int p = R[ip];
+        tcon[blk(p, k)].push_back(make_int2(blk(p, sc), blk(k, sc)));
       }
     }
+  }
   std::vector<int32_t> tsk, con, fwdp(N + 1, 0), fwd, fac;
   pl.tsk_lvl_ptr.assign(L + 1, 0);
   pl.fac_lvl_ptr.assign(L + 1, 0);
@@ -1818,6 +1810,42 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     it_lvl[l + 1] = (int)items.size() / 4;
     rd_lvl[l + 1] = (int)red.size() / 4;
   }
+  // bottom subtrees (bl_subtree): a column is in a subtree when its height is <= sub_top and the work of the
+  // subtree rooted at it -- memory round trips of its column tasks: contributions + forward contributions + blocks --
+  // is <= subw (the longest thread chain of the kernel bounds it: uncapped, C5's largest subtree is 539 round
+  // trips against a mean of 91).  Eligibility is closed under descendants; a subtree is rooted at an eligible
+  // column whose parent is not eligible.  Its columns in increasing index (children first), subtrees by decreasing
+  // work.  The other columns (in_sub = 0) are factored by the per-level launches.
+  int subw = 400;   // measured at C5 (profiles/r3/): uncapped 2.34 ms, 80: 2.29, 160: 2.26, 240-400: 2.22-2.23, 600: 2.25
+  if (const char* env = std::getenv("DNLS_BL_SUBW")) subw = std::atoi(env);
+  std::vector<int32_t> sub_ptr(1, 0), sub_col;
+  std::vector<char> in_sub(N, 0);
+  if (sub_top >= 0) {
+    std::vector<long long> W(N, 0);
+    for (int k = 0; k < N; ++k) {
+      long long wk = (colptr[k + 1] - colptr[k]) + (fwdp[k + 1] - fwdp[k]);
+      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) wk += bcon[4 * (size_t)bi + 1] - bcon[4 * (size_t)bi];
+      W[k] += wk;
+      if (s.parent[k] >= 0) W[s.parent[k]] += W[k];
+    }
+    auto elig = [&](int k) { return h[k] <= sub_top && (subw <= 0 || W[k] <= subw); };
+    std::vector<int> root(N, -1);
+    for (int k = N - 1; k >= 0; --k)
+      if (elig(k)) root[k] = (s.parent[k] >= 0 && elig(s.parent[k])) ? root[s.parent[k]] : k;
+    std::map<int, std::vector<int>> subs;
+    for (int k = 0; k < N; ++k)
+      if (root[k] >= 0) {
+        subs[root[k]].push_back(k);
+        in_sub[k] = 1;
+      }
+    std::vector<std::pair<long long, int>> order;   // (-work, root)
+    for (auto& kv : subs) order.push_back(std::make_pair(-W[kv.first], kv.first));
+    std::sort(order.begin(), order.end());
+    for (auto& o : order) {
+      for (int k : subs[o.second]) sub_col.push_back(k);
+      sub_ptr.push_back((int)sub_col.size());
+    }
+  }
   // per-level chunked update (large-batch schedule): every level's target lists and forward rows as work items,
   // lists longer than lch contributions split into ceil(n / lch) nearly equal chunks; the first chunk is applied
   // in place, the others store partials (level-local slots in the slot scratch) that bl_factor_red subtracts in
@@ -1825,21 +1853,20 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   int lch = 8;
   if (const char* env = std::getenv("DNLS_BL_LCH")) lch = std::atoi(env);
   std::vector<int32_t> litems, bred(2 * (size_t)pl.nblk, 0), cred(2 * (size_t)N, 0);
-  std::vector<int32_t> litems_x, bred_x(2 * (size_t)pl.nblk, 0), cred_x(2 * (size_t)N, 0), xitems;
+  std::vector<int32_t> litems_f, bred_f(2 * (size_t)pl.nblk, 0), cred_f(2 * (size_t)N, 0);
   pl.lit_lvl_ptr.assign(L + 1, 0);
-  pl.litx_lvl_ptr.assign(L + 1, 0);
+  pl.litf_lvl_ptr.assign(L + 1, 0);
   int litems_want = 0, lch_min = 2;   // narrow levels: chunks small enough for ~litems_want items (0: off)
   if (const char* env = std::getenv("DNLS_BL_LITEMS")) sscanf(env, "%d,%d", &litems_want, &lch_min);
-  // split variant (ext): the lists of targets above sub_top without their external part
+  // filtered variant: without the columns of the bottom subtrees (factored by bl_subtree)
   for (int var = 0; var < 2 && lch > 0; ++var) {
-    const bool xv = var == 1;
-    std::vector<int32_t>& litv = xv ? litems_x : litems;
-    std::vector<int32_t>& bredv = xv ? bred_x : bred;
-    std::vector<int32_t>& credv = xv ? cred_x : cred;
-    std::vector<int>& lptr = xv ? pl.litx_lvl_ptr : pl.lit_lvl_ptr;
+    const bool fv = var == 1;
+    std::vector<int32_t>& litv = fv ? litems_f : litems;
+    std::vector<int32_t>& bredv = fv ? bred_f : bred;
+    std::vector<int32_t>& credv = fv ? cred_f : cred;
+    std::vector<int>& lptr = fv ? pl.litf_lvl_ptr : pl.lit_lvl_ptr;
     const size_t cap = scr_doubles / ((size_t)D * D);
     for (int l = 0; l < L; ++l) {
-      const bool up = xv && l > sub_top;
       int nslot = 0, ncl = 0;
       for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
         const int k = lvl_col[i];
@@ -1865,34 +1892,27 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
       };
       for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
         const int k = lvl_col[i];
+        if (fv && in_sub[k]) continue;   // factored by bl_subtree
         for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) {
-          const int a = bcon[4 * (size_t)bi] + (up ? nA[bi] : 0), e = bcon[4 * (size_t)bi + 1];
-          // a fill target whose external part is applied first is no longer written first here
-          const int fl = bcon[4 * (size_t)bi + 2] & ((up && nA[bi] > 0) ? 1 : 3);
-          if (e > a) add(bi, a, e, fl, &bredv[2 * (size_t)bi]);
+          const int a = bcon[4 * (size_t)bi], e = bcon[4 * (size_t)bi + 1];
+          if (e > a) add(bi, a, e, bcon[4 * (size_t)bi + 2] & 3, &bredv[2 * (size_t)bi]);
         }
-        const int fa = fwdp[k] + (up ? nAf[k] : 0);
-        if (fwdp[k + 1] > fa) add(-2 - k, fa, fwdp[k + 1], 0, &credv[2 * (size_t)k]);
+        if (fwdp[k + 1] > fwdp[k]) add(-2 - k, fwdp[k], fwdp[k + 1], 0, &credv[2 * (size_t)k]);
       }
       lptr[l + 1] = (int)litv.size() / 4;
     }
   }
-  // ext items: every target / forward row above sub_top with an external part, applied in place (whole list,
-  // a fill target stores -acc), longest lists first
-  if (sub_top >= 0) {
-    std::vector<std::array<int, 4>> xs;
-    for (int k = 0; k < N; ++k) {
-      if (h[k] <= sub_top) continue;
-      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi)
-        if (nA[bi] > 0) xs.push_back({bi, bcon[4 * (size_t)bi], bcon[4 * (size_t)bi] + nA[bi], bcon[4 * (size_t)bi + 2] & 3});
-      if (nAf[k] > 0) xs.push_back({-2 - k, fwdp[k], fwdp[k] + nAf[k], 0});
+  // the per-level factor items of the columns outside the subtrees (chunked schedule)
+  std::vector<int32_t> facf;
+  pl.facf_lvl_ptr.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) {
+    for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
+      const int k = lvl_col[i];
+      if (in_sub[k]) continue;
+      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) facf.insert(facf.end(), {k, bi});
     }
-    std::stable_sort(xs.begin(), xs.end(), [](const std::array<int, 4>& a, const std::array<int, 4>& b) {
-      return a[2] - a[1] > b[2] - b[1];
-    });
-    for (auto& x : xs) xitems.insert(xitems.end(), x.begin(), x.end());
+    pl.facf_lvl_ptr[l + 1] = (int)facf.size() / 2;
   }
-  pl.nxitems = (int)xitems.size() / 4;
   // bl_lsolve items: per level, per column (in lvl_col order) its below blocks (backward) / forward contributions
   std::vector<int32_t> bit, fit, bcolv(2 * (size_t)N, 0), fcolv(2 * (size_t)N, 0);
   pl.bit_lvl_h.assign(L + 1, 0);
@@ -1913,29 +1933,6 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   std::vector<int32_t> bit_lvl32(pl.bit_lvl_h.begin(), pl.bit_lvl_h.end()), fit_lvl32(pl.fit_lvl_h.begin(),
                                                                                        pl.fit_lvl_h.end());
   pl.lch = lch;
-  // bottom subtrees (bl_subtree): every column of height <= sub_top belongs to the subtree of its highest
-  // ancestor of height <= sub_top; a subtree's columns in increasing index (children first), subtrees by
-  // decreasing block count (the longest items start first)
-  std::vector<int32_t> sub_ptr(1, 0), sub_col;
-  if (sub_top >= 0) {
-    std::vector<int> root(N, -1);
-    for (int k = N - 1; k >= 0; --k)
-      if (h[k] <= sub_top) root[k] = (s.parent[k] >= 0 && h[s.parent[k]] <= sub_top) ? root[s.parent[k]] : k;
-    std::map<int, std::vector<int>> subs;
-    for (int k = 0; k < N; ++k)
-      if (root[k] >= 0) subs[root[k]].push_back(k);
-    std::vector<std::pair<int, int>> order;   // (-blocks, root)
-    for (auto& kv : subs) {
-      int nb = 0;
-      for (int k : kv.second) nb += colptr[k + 1] - colptr[k];
-      order.push_back(std::make_pair(-nb, kv.first));
-    }
-    std::sort(order.begin(), order.end());
-    for (auto& o : order) {
-      for (int k : subs[o.second]) sub_col.push_back(k);
-      sub_ptr.push_back((int)sub_col.size());
-    }
-  }
   pl.sub_top = sub_top;
   pl.nsub = (int)sub_ptr.size() - 1;
   std::vector<int32_t> lvl_ptr32(pl.lvl_ptr.begin(), pl.lvl_ptr.end()), fac_lvl32(pl.fac_lvl_ptr.begin(),
@@ -1955,8 +1952,9 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   add(bcon); add(it_lvl); add(items); add(rd_lvl); add(red); add(lvl_ptr32); add(fac_lvl32);
   add(sub_ptr); add(sub_col);
   add(litems); add(bred); add(cred);
-  add(litems_x); add(bred_x); add(cred_x); add(xitems);
+  add(litems_f); add(bred_f); add(cred_f);
   add(bit); add(bit_lvl32); add(bcolv); add(fit); add(fit_lvl32); add(fcolv);
+  add(facf);
   while (buf.size() % 4) buf.push_back(0);
   if (device >= 0) {
     if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
@@ -1996,10 +1994,9 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.d_litems = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.d_bred = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.d_cred = reinterpret_cast<const int2*>(ptr(offs[k++]));
-  pl.d_litems_x = reinterpret_cast<const int4*>(ptr(offs[k++]));
-  pl.d_bred_x = reinterpret_cast<const int2*>(ptr(offs[k++]));
-  pl.d_cred_x = reinterpret_cast<const int2*>(ptr(offs[k++]));
-  pl.d_xitems = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.d_litems_f = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.d_bred_f = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.d_cred_f = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.sd.bit = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.sd.bit_lvl = ptr(offs[k++]);
   pl.sd.bcol = reinterpret_cast<const int2*>(ptr(offs[k++]));
@@ -2007,7 +2004,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.sd.fit_lvl = ptr(offs[k++]);
   pl.sd.fcol = reinterpret_cast<const int2*>(ptr(offs[k++]));
   if (const char* env = std::getenv("DNLS_BL_LSOLVE")) pl.lsolve = std::atoi(env);
-  if (const char* env = std::getenv("DNLS_BL_EXT")) pl.ext = std::atoi(env) != 0;
+  pl.d_facf = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.pd.lvl_col = pl.d_lvl_col;
   pl.pd.L = L;
   pl.pd.coltask_min = 16;
@@ -2104,7 +2101,7 @@ struct BLPhaseTimer {
 struct BLSched {
   bool rb;
   int lsplit, gw;
-  int lfirst;   // first level of the per-level launches (levels below: bl_subtree)
+  bool sub;     // bl_subtree for the bottom subtrees (with the chunked per-level schedule)
   int fsplit;   // first level of the factorisation's persistent launch (chunked per-level items: none)
   int sgw;      // bl_lsolve group width
 };
@@ -2122,7 +2119,7 @@ inline BLSched bl_schedule(const BLPlan& pl, int B) {
   else if (persist && pl.lsolve && pl.persist_from < 0)
     sc.lsplit = pl.narrow_from;   // bl_lsolve: the narrow top of the tree (measured: C5 ss20 / gw 8 best)
   sc.fsplit = (sc.rb && pl.lch > 0 && pl.persist_from < 0) ? pl.L : sc.lsplit;
-  sc.lfirst = (pl.sub_top >= 0 && pl.nsub > 0 && (large || pl.sub_any)) ? pl.sub_top + 1 : 0;
+  sc.sub = pl.sub_top >= 0 && pl.nsub > 0 && sc.rb && pl.lch > 0;
   return sc;
 }
 
@@ -2148,31 +2145,30 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   g.B = B;
   g.Bp = bl_pad(B);
   const BLSched sc = bl_schedule(pl, B);
-  const int lsplit = std::max(sc.fsplit, sc.lfirst);
-  // ext variant: the per-level chunked schedule runs every level above sub_top (no persistent factorisation)
-  const bool xv = pl.ext && sc.rb && pl.lch > 0 && lsplit >= pl.L && pl.sub_top >= 0 && sc.lfirst <= pl.sub_top + 1;
-  if (sc.lfirst > 0)
+  const int lsplit = sc.fsplit;
+  // chunked schedule: the bottom subtrees in one launch, then per level the items / factor items of the other
+  // columns (levels whose columns are all in subtrees launch nothing)
+  const bool sub = sc.sub && lsplit > pl.sub_top;
+  if (sub)
     bl_launch(bl_subtree<D>, bl_grid(pl.nsub, g.Bp), BL_TPB, s, g, w, pl.pd.bcon, pl.d_sub_ptr, pl.d_sub_col,
-                                                                    pl.nsub, fused_fwd ? 1 : 0);
-  for (int l = sc.lfirst; l < lsplit; ++l) {
+              pl.nsub, fused_fwd ? 1 : 0);
+  for (int l = 0; l < lsplit; ++l) {
     const int t0 = pl.tsk_lvl_ptr[l], nt = pl.tsk_lvl_ptr[l + 1] - t0;
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;
     const long long nu = (long long)nt + (fused_fwd ? nc : 0);
     if (sc.rb && pl.lch > 0) {
       // chunked work items of the level (forward rows skipped in the final factorisation: they have no
-      // effect there), then the factor launch with the split reductions folded in.  With ext: the external
-      // parts of every target above sub_top in one launch once the columns up to sub_top are factored.
-      if (xv && l == pl.sub_top + 1 && pl.nxitems > 0)
-        bl_launch(bl_update_items<D>, bl_grid(pl.nxitems, g.Bp), BL_TPB, s, g, w, pl.d_xitems, 0, pl.nxitems,
-                  fused_fwd ? 1 : 0);
-      const std::vector<int>& lp = xv ? pl.litx_lvl_ptr : pl.lit_lvl_ptr;
+      // effect there), then the factor launch with the split reductions folded in
+      const std::vector<int>& lp = sub ? pl.litf_lvl_ptr : pl.lit_lvl_ptr;
       const int i0 = lp[l], ni = lp[l + 1] - i0;
       if (ni > 0)
-        bl_launch(bl_update_items<D>, bl_grid(ni, g.Bp), BL_TPB, s, g, w, xv ? pl.d_litems_x : pl.d_litems, i0, ni,
+        bl_launch(bl_update_items<D>, bl_grid(ni, g.Bp), BL_TPB, s, g, w, sub ? pl.d_litems_f : pl.d_litems, i0, ni,
                   fused_fwd ? 1 : 0);
-      const int f0 = pl.fac_lvl_ptr[l], nf = pl.fac_lvl_ptr[l + 1] - f0;
-      bl_launch(bl_factor_red<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, f0, nf, fused_fwd ? 1 : 0,
-                xv ? pl.d_bred_x : pl.d_bred, xv ? pl.d_cred_x : pl.d_cred);
+      const std::vector<int>& fp = sub ? pl.facf_lvl_ptr : pl.fac_lvl_ptr;
+      const int f0 = fp[l], nf = fp[l + 1] - f0;
+      if (nf > 0)
+        bl_launch(bl_factor_red<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, sub ? pl.d_facf : pl.dev.fac, f0, nf,
+                  fused_fwd ? 1 : 0, sub ? pl.d_bred_f : pl.d_bred, sub ? pl.d_cred_f : pl.d_cred);
       continue;
     }
     if (nu > 0 && sc.rb)

@@ -108,18 +108,20 @@ def test_bl_large_batch_schedule_on_small_cases(monkeypatch, dim, N, B, split, g
         assert rel_vec_err(np.concatenate([ge[b], gp[b]]), np.concatenate([a, c])) <= TOL_GRAD, b
 
 
-@pytest.mark.parametrize("dim,N,B,sub", [(3, 256, 40, "4"), (3, 256, 33, "8"), (2, 100, 35, "100"), (3, 64, 37, "0")])
-def test_bl_subtree_factorisation_matches_per_level_schedule(monkeypatch, dim, N, B, sub):
+@pytest.mark.parametrize("dim,N,B,sub,subw", [(3, 256, 40, "4", "0"), (3, 256, 33, "8", "30"), (2, 100, 35, "100", "0"),
+                                              (3, 64, 37, "0", "0"), (3, 256, 40, "10", "12")])
+def test_bl_subtree_factorisation_matches_per_level_schedule(monkeypatch, dim, N, B, sub, subw):
     # bl_subtree (the bottom subtrees of the elimination tree as column tasks in one launch; sub = 100 puts the
-    # whole tree in one subtree) sums every target's contributions in the same order as the per-level update +
-    # factor launches of the same plan, starting from T (T - p1 - p2 ...) where the row-split kernel forms
-    # T - (p1 + p2 ...): forward, objective and implicit gradients agree with the per-level schedule (small
-    # batch: row-split updates) to rounding, and match the oracle
+    # whole tree in one subtree; subw caps the work of a subtree, the other low columns go through the filtered
+    # per-level launches) against the chunked per-level schedule without subtrees: same contributions per target
+    # in the same order up to the chunk split -- agreement to rounding, and with the oracle
     topo, data = make_case(N, dim=dim, p=0.3, mode="local", seed=N + B + 1, B=B)
     v = np.random.default_rng(N + 1).standard_normal((B, N, 6 if dim == 3 else 3))
-    monkeypatch.setenv("DNLS_BL_SUB", sub)
+    monkeypatch.setenv("DNLS_BL_UPD", "1")
+    monkeypatch.setenv("DNLS_BL_SUB", "-1")
     ref = solve(topo, data, 5, True, v=v)
-    monkeypatch.setenv("DNLS_BL_SUBANY", "1")
+    monkeypatch.setenv("DNLS_BL_SUB", sub)
+    monkeypatch.setenv("DNLS_BL_SUBW", subw)
     got = solve(topo, data, 5, True, v=v)
     assert np.max(np.abs(got[0] - ref[0])) <= 1e-11 * max(1.0, np.max(np.abs(ref[0])))
     assert np.max(np.abs(got[1] - ref[1]) / ref[1]) <= 1e-11
@@ -137,24 +139,23 @@ def test_bl_subtree_factorisation_matches_per_level_schedule(monkeypatch, dim, N
         assert abs(got[1][b] - r.objective) <= TOL_OBJ * r.objective + 1e-20
 
 
-@pytest.mark.parametrize("dim,N,B,sub,lch,split,ext", [(3, 256, 40, "2", "1", "100", "1"),
-                                                       (3, 256, 40, "2", "1", "100", "0"),
-                                                       (3, 200, 35, "4", "3", "12", "1"),
-                                                       (2, 100, 33, "-1", "2", "100", "1"),
-                                                       (2, 100, 33, "3", "2", "100", "1"),
-                                                       (3, 64, 37, "1", "6", "5", "1")])
-def test_bl_chunked_level_updates_match_oracle(monkeypatch, dim, N, B, sub, lch, split, ext):
+@pytest.mark.parametrize("dim,N,B,sub,lch,split,subw", [(3, 256, 40, "2", "1", "100", "0"),
+                                                        (3, 256, 40, "6", "1", "100", "20"),
+                                                        (3, 200, 35, "4", "3", "12", "0"),
+                                                        (2, 100, 33, "-1", "2", "100", "0"),
+                                                        (2, 100, 33, "3", "2", "100", "10"),
+                                                        (3, 64, 37, "1", "6", "5", "0")])
+def test_bl_chunked_level_updates_match_oracle(monkeypatch, dim, N, B, sub, lch, split, subw):
     # the large-batch schedule bench.py's C5 run uses -- bl_subtree for the bottom levels, per-level chunked
     # work items (bl_update_items; lch contributions per chunk, partials reduced in chunk order by
-    # bl_factor_red), the external parts of the upper targets in one launch after the subtree kernel (ext), the
-    # persistent tail from level `split` (split < levels: no ext) -- forced on small ragged SE2 / SE3 batches
+    # bl_factor_red), work-capped subtrees (subw; the other low columns in the filtered per-level launches), the
+    # persistent tail from level `split` -- forced on small ragged SE2 / SE3 batches
     monkeypatch.setenv("DNLS_BL_UPD", "1")
-    monkeypatch.setenv("DNLS_BL_SUBANY", "1")
     monkeypatch.setenv("DNLS_BL_SUB", sub)
+    monkeypatch.setenv("DNLS_BL_SUBW", subw)
     monkeypatch.setenv("DNLS_BL_LCH", lch)
     monkeypatch.setenv("DNLS_BL_SPLIT", split)
     monkeypatch.setenv("DNLS_BL_PERSIST", "8")
-    monkeypatch.setenv("DNLS_BL_EXT", ext)
     topo, data = make_case(N, dim=dim, p=0.3, mode="local", seed=N + B + 2, B=B)
     v = np.random.default_rng(N + 2).standard_normal((B, N, 6 if dim == 3 else 3))
     P, obj, st, it, ge, gp = solve(topo, data, 5, True, v=v)
