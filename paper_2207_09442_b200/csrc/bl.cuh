@@ -799,9 +799,27 @@ __device__ __forceinline__ void bl_factor_item(const BLDev& g, const BLWs& w, co
 #pragma unroll
       for (int r = 0; r < D; ++r) t[q][r] = Pb[(q * D + r) * Bp];
   }
+  // T_kk's chunk partials, two per memory round trip (subtracted in chunk order)
   const int2 rk = bred[kb0];
-#pragma unroll 2
-  for (int q = 0; q < rk.y; ++q) {
+  int q = 0;
+  for (; q + 1 < rk.y; q += 2) {
+    const double* p0 = part + (size_t)(rk.x + q) * C::DD * Bp;
+    const double* p1 = p0 + (size_t)C::DD * Bp;
+    double v0[D][D], v1[D][D];
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int i = j; i < D; ++i) {
+        v0[i][j] = p0[(j * D + i) * Bp];
+        v1[i][j] = p1[(j * D + i) * Bp];
+      }
+    bl_issue_fence();
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int i = j; i < D; ++i) a[i][j] = (a[i][j] - v0[i][j]) - v1[i][j];
+  }
+  if (q < rk.y) {
     const double* pp = part + (size_t)(rk.x + q) * C::DD * Bp;
 #pragma unroll
     for (int j = 0; j < D; ++j)

@@ -1,0 +1,11 @@
+#!/bin/bash
+# factor_red: T_kk partials two per round trip; chunk-size sweep after in-place accumulation
+mkdir -p gpurun_out/r3u
+O=gpurun_out/r3u
+timeout 900 python -m pytest tests/test_gpu_bl.py -x -q 2>&1 | tail -2
+run() { # tag, env...
+  local tag=$1; shift
+  env "$@" timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $ARGS > $O/$tag.json 2>$O/$tag.err
+  python -c "import json; d=json.load(open('$O/$tag.json')); r=d['roofline']; print('$tag', round(d['value']), round(d['ms_per_step'],2), round(r['kernel_ms'],3), round(r['frac'],4))" || tail -3 $O/$tag.err
+}
+for C in 8 6 10 12 16; do run lch$C DNLS_BL_LCH=$C; done
