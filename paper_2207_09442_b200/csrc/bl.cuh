@@ -1627,6 +1627,7 @@ struct BLPlan {
   const int4* d_litems_f = nullptr;
   const int2 *d_bred_f = nullptr, *d_cred_f = nullptr;
   int sub_top = -1;       // bl_subtree covers the columns of height <= sub_top (-1: off)
+  std::vector<int> sub_pass;   // subtrees of pass p: [sub_pass[p], sub_pass[p+1])
   int nsub = 0;           // its items: maximal subtrees of those columns, largest first
   const int *d_sub_ptr = nullptr, *d_sub_col = nullptr;
 
@@ -1834,34 +1835,52 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   // trips against a mean of 91).  Eligibility is closed under descendants; a subtree is rooted at an eligible
   // column whose parent is not eligible.  Its columns in increasing index (children first), subtrees by decreasing
   // work.  The other columns (in_sub = 0) are factored by the per-level launches.
-  int subw = 400;   // measured at C5 (profiles/r3/): uncapped 2.34 ms, 80: 2.29, 160: 2.26, 240-400: 2.22-2.23, 600: 2.25
-  if (const char* env = std::getenv("DNLS_BL_SUBW")) subw = std::atoi(env);
+  // passes: pass p groups the columns not taken by earlier passes whose residual subtree work (their own column
+  // task plus that of their untaken descendants) is <= cap p; one bl_subtree launch per pass, in pass order (a
+  // pass's subtree contains every untaken descendant of its root, so earlier passes hold the rest)
+  std::vector<int> subw = {400};   // measured at C5 (profiles/r3/): uncapped 2.34 ms, 80: 2.29, 160: 2.26,
+                                   // 240-400: 2.22-2.23, 600: 2.25
+  if (const char* env = std::getenv("DNLS_BL_SUBW")) {
+    subw.clear();
+    for (const char* c = env; *c;) {
+      subw.push_back(std::atoi(c));
+      while (*c && *c != ',') ++c;
+      if (*c == ',') ++c;
+    }
+  }
   std::vector<int32_t> sub_ptr(1, 0), sub_col;
+  pl.sub_pass.assign(1, 0);
   std::vector<char> in_sub(N, 0);
   if (sub_top >= 0) {
-    std::vector<long long> W(N, 0);
+    std::vector<long long> wk(N, 0);
     for (int k = 0; k < N; ++k) {
-      long long wk = (colptr[k + 1] - colptr[k]) + (fwdp[k + 1] - fwdp[k]);
-      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) wk += bcon[4 * (size_t)bi + 1] - bcon[4 * (size_t)bi];
-      W[k] += wk;
-      if (s.parent[k] >= 0) W[s.parent[k]] += W[k];
+      wk[k] = (colptr[k + 1] - colptr[k]) + (fwdp[k + 1] - fwdp[k]);
+      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) wk[k] += bcon[4 * (size_t)bi + 1] - bcon[4 * (size_t)bi];
     }
-    auto elig = [&](int k) { return h[k] <= sub_top && (subw <= 0 || W[k] <= subw); };
-    std::vector<int> root(N, -1);
-    for (int k = N - 1; k >= 0; --k)
-      if (elig(k)) root[k] = (s.parent[k] >= 0 && elig(s.parent[k])) ? root[s.parent[k]] : k;
-    std::map<int, std::vector<int>> subs;
-    for (int k = 0; k < N; ++k)
-      if (root[k] >= 0) {
-        subs[root[k]].push_back(k);
-        in_sub[k] = 1;
+    for (int cap : subw) {
+      std::vector<long long> W(N, 0);
+      for (int k = 0; k < N; ++k) {
+        if (in_sub[k]) continue;
+        W[k] += wk[k];
+        if (s.parent[k] >= 0) W[s.parent[k]] += W[k];
       }
-    std::vector<std::pair<long long, int>> order;   // (-work, root)
-    for (auto& kv : subs) order.push_back(std::make_pair(-W[kv.first], kv.first));
-    std::sort(order.begin(), order.end());
-    for (auto& o : order) {
-      for (int k : subs[o.second]) sub_col.push_back(k);
-      sub_ptr.push_back((int)sub_col.size());
+      auto elig = [&](int k) { return !in_sub[k] && h[k] <= sub_top && (cap <= 0 || W[k] <= cap); };
+      std::vector<int> root(N, -1);
+      for (int k = N - 1; k >= 0; --k)
+        if (elig(k)) root[k] = (s.parent[k] >= 0 && elig(s.parent[k])) ? root[s.parent[k]] : k;
+      std::map<int, std::vector<int>> subs;
+      for (int k = 0; k < N; ++k)
+        if (root[k] >= 0) subs[root[k]].push_back(k);
+      for (auto& kv : subs)
+        for (int k : kv.second) in_sub[k] = 1;
+      std::vector<std::pair<long long, int>> order;   // (-work, root)
+      for (auto& kv : subs) order.push_back(std::make_pair(-W[kv.first], kv.first));
+      std::sort(order.begin(), order.end());
+      for (auto& o : order) {
+        for (int k : subs[o.second]) sub_col.push_back(k);
+        sub_ptr.push_back((int)sub_col.size());
+      }
+      pl.sub_pass.push_back((int)sub_ptr.size() - 1);
     }
   }
   // per-level chunked update (large-batch schedule): every level's target lists and forward rows as work items,
@@ -2168,8 +2187,12 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
   // columns (levels whose columns are all in subtrees launch nothing)
   const bool sub = sc.sub && lsplit > pl.sub_top;
   if (sub)
-    bl_launch(bl_subtree<D>, bl_grid(pl.nsub, g.Bp), BL_TPB, s, g, w, pl.pd.bcon, pl.d_sub_ptr, pl.d_sub_col,
-              pl.nsub, fused_fwd ? 1 : 0);
+    for (size_t p = 0; p + 1 < pl.sub_pass.size(); ++p) {
+      const int a = pl.sub_pass[p], n = pl.sub_pass[p + 1] - a;
+      if (n > 0)
+        bl_launch(bl_subtree<D>, bl_grid(n, g.Bp), BL_TPB, s, g, w, pl.pd.bcon, pl.d_sub_ptr + a, pl.d_sub_col, n,
+                  fused_fwd ? 1 : 0);
+    }
   for (int l = 0; l < lsplit; ++l) {
     const int t0 = pl.tsk_lvl_ptr[l], nt = pl.tsk_lvl_ptr[l + 1] - t0;
     const int c0 = pl.lvl_ptr[l], nc = pl.lvl_ptr[l + 1] - c0;

@@ -1,5 +1,7 @@
 """Small forward + backward runs for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
-  python tools/sanitize_case.py <case>   case in c1 | c2 | cluster | lm | unroll | dlm | bl
+  python tools/sanitize_case.py <case>   case in c1 | c2 | cluster | lm | unroll | dlm | bl | bll
+(bll: the batch-interleaved large-batch schedule forced on a small batch -- bl_subtree with a tight work cap, the
+filtered chunked per-level items + bl_factor_red, the bl_lsolve tail solves in shared memory, PDL launches)
 SURVEY.md §5 "race detection": the fused kernels rely on named barriers, mbarrier/TMA proxy ordering and
 cluster barriers; these cases exercise each path once."""
 import os
@@ -17,7 +19,9 @@ from paper_2207_09442_b200.layer import PoseGraphSolver  # noqa: E402
 case = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfg = {"c1": (16, 2, 4, {}), "c2": (256, 3, 4, {}), "cluster": (1024, 3, 2, {"cluster_ctas": 2}),
        "lm": (64, 3, 3, {"optimizer": D.LM}), "unroll": (64, 3, 3, {}), "dlm": (64, 3, 3, {}),
-       "bl": (64, 3, 40, {"batch_interleave": 32})}[case]
+       "bl": (64, 3, 40, {"batch_interleave": 32}), "bll": (256, 3, 40, {"batch_interleave": 32})}[case]
+if case == "bll":
+    os.environ.update(DNLS_BL_UPD="1", DNLS_BL_PERSIST="4", DNLS_BL_SUBW="20", DNLS_BL_LCH="2")
 N, dim, B, opts = cfg
 topo = synth.cube_topology(N, dim=dim, p=0.3, seed=0)
 data = synth.cube_batch(topo, B, seed=0)
