@@ -769,20 +769,22 @@ __global__ void __launch_bounds__(BL_TPB, DNLS_RB_MINB) bl_update_items(BLDev g,
   bl_pdl();
   int b;
   long long it;
-  if (!bl_item(g, nit, b, it)) return;
-  if (b >= g.B || bl_frozen(w, b)) return;
-  bl_work_item<D>(g, w, w.scr, items[i0 + it], b, fused_fwd != 0);
+  if (!bl_item(g, nit, b, it) || b >= g.B) return;
+  const int4 itm = items[i0 + it];   // loaded with the status: one round trip before the item's data
+  if (w.st[b] != DNLS_ST_OK) return;
+  bl_work_item<D>(g, w, w.scr, itm, b, fused_fwd != 0);
 }
 
 // bl_factor with the level's split reductions folded in: T_kk and T_pk minus their chunk partials (in chunk
 // order), x_k minus the forward row's partials, then bl_factor's arithmetic.  pr = (first slot, count) per
 // block (bred) and per column's forward row (cred).
 template <int D>
-__device__ __forceinline__ void bl_factor_item(const BLDev& g, const BLWs& w, const int2 fi, int b, bool fused_fwd,
+__device__ __forceinline__ void bl_factor_item(const BLDev& g, const BLWs& w, const int4 fr, int b, bool fused_fwd,
                                                const int2* bred, const int2* cred) {
   using C = BLC<D>;
   const size_t Bp = g.Bp;
-  const int k = fi.x, kb0 = g.colptr[k];
+  const int k = fr.x, kb0 = fr.z;   // record: (column, block, the column's diagonal block, 0)
+  const int2 fi = make_int2(fr.x, fr.y);
   const bool diag = fi.y == kb0;
   const double* Kk = w.L + (size_t)kb0 * C::DD * Bp + b;
   double* Pb = w.L + (size_t)fi.y * C::DD * Bp + b;
@@ -858,14 +860,15 @@ __device__ __forceinline__ void bl_factor_item(const BLDev& g, const BLWs& w, co
 }
 
 template <int D>
-__global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, const int2* fac, int f0, int nfac,
+__global__ void __launch_bounds__(BL_TPB) bl_factor_red(BLDev g, BLWs w, const int4* facr, int f0, int nfac,
                                                        int fused_fwd, const int2* bred, const int2* cred) {
   bl_pdl();
   int b;
   long long it;
-  if (!bl_item(g, nfac, b, it)) return;
-  if (b >= g.B || bl_frozen(w, b)) return;
-  bl_factor_item<D>(g, w, fac[f0 + it], b, fused_fwd != 0, bred, cred);
+  if (!bl_item(g, nfac, b, it) || b >= g.B) return;
+  const int4 fr = facr[f0 + it];   // loaded with the status: one round trip before the item's data
+  if (w.st[b] != DNLS_ST_OK) return;
+  bl_factor_item<D>(g, w, fr, b, fused_fwd != 0, bred, cred);
 }
 
 // bottom of the elimination tree in ONE launch: every maximal subtree of columns of height <= the plan's
@@ -1611,7 +1614,7 @@ struct BLPlan {
   int persist_from = -1; // first level of the persistent launch (-1: the single-column tail of the tree)
   int solve_from = -1;    // first level of the persistent tail solves (-1: as the factorisation's split)
   std::vector<int> facf_lvl_ptr;   // per level: factor items of the columns outside the subtrees
-  const int2* d_facf = nullptr;
+  const int4 *d_facf = nullptr, *d_facr = nullptr;
   int lsolve = 1;         // persistent tail solves: 1 level-parallel bl_lsolve, 0 bl_persist_solve (DNLS_BL_LSOLVE)
   BLSDev sd{};
   std::vector<int> bit_lvl_h, fit_lvl_h;   // host copies: items per level of bl_lsolve
@@ -1940,15 +1943,19 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
     }
   }
   // the per-level factor items of the columns outside the subtrees (chunked schedule)
-  std::vector<int32_t> facf;
+  // (records (column, block, diagonal block of the column, 0) for bl_factor_red; facr: every column, same order
+  // as fac / fac_lvl_ptr)
+  std::vector<int32_t> facf, facr;
   pl.facf_lvl_ptr.assign(L + 1, 0);
   for (int l = 0; l < L; ++l) {
     for (int i = pl.lvl_ptr[l]; i < pl.lvl_ptr[l + 1]; ++i) {
       const int k = lvl_col[i];
-      if (in_sub[k]) continue;
-      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) facf.insert(facf.end(), {k, bi});
+      for (int bi = colptr[k]; bi < colptr[k + 1]; ++bi) {
+        facr.insert(facr.end(), {k, bi, colptr[k], 0});
+        if (!in_sub[k]) facf.insert(facf.end(), {k, bi, colptr[k], 0});
+      }
     }
-    pl.facf_lvl_ptr[l + 1] = (int)facf.size() / 2;
+    pl.facf_lvl_ptr[l + 1] = (int)facf.size() / 4;
   }
   // bl_lsolve items: per level, per column (in lvl_col order) its below blocks (backward) / forward contributions
   std::vector<int32_t> bit, fit, bcolv(2 * (size_t)N, 0), fcolv(2 * (size_t)N, 0);
@@ -1991,7 +1998,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   add(litems); add(bred); add(cred);
   add(litems_f); add(bred_f); add(cred_f);
   add(bit); add(bit_lvl32); add(bcolv); add(fit); add(fit_lvl32); add(fcolv);
-  add(facf);
+  add(facf); add(facr);
   while (buf.size() % 4) buf.push_back(0);
   if (device >= 0) {
     if (cudaMalloc(&pl.dbuf, buf.size() * sizeof(int32_t)) != cudaSuccess ||
@@ -2041,7 +2048,8 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.sd.fit_lvl = ptr(offs[k++]);
   pl.sd.fcol = reinterpret_cast<const int2*>(ptr(offs[k++]));
   if (const char* env = std::getenv("DNLS_BL_LSOLVE")) pl.lsolve = std::atoi(env);
-  pl.d_facf = reinterpret_cast<const int2*>(ptr(offs[k++]));
+  pl.d_facf = reinterpret_cast<const int4*>(ptr(offs[k++]));
+  pl.d_facr = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.pd.lvl_col = pl.d_lvl_col;
   pl.pd.L = L;
   pl.pd.coltask_min = 16;
@@ -2208,7 +2216,7 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
       const std::vector<int>& fp = sub ? pl.facf_lvl_ptr : pl.fac_lvl_ptr;
       const int f0 = fp[l], nf = fp[l + 1] - f0;
       if (nf > 0)
-        bl_launch(bl_factor_red<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, sub ? pl.d_facf : pl.dev.fac, f0, nf,
+        bl_launch(bl_factor_red<D>, bl_grid(nf, g.Bp), BL_TPB, s, g, w, sub ? pl.d_facf : pl.d_facr, f0, nf,
                   fused_fwd ? 1 : 0, sub ? pl.d_bred_f : pl.d_bred, sub ? pl.d_cred_f : pl.d_cred);
       continue;
     }
