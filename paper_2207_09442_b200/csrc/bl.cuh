@@ -685,24 +685,31 @@ __device__ __forceinline__ void bl_trsm_store(double* Pb, size_t Bp, double (&t)
 // forward-substitution row and y_k = L_kk^-1 x_k, then every below target's updates solved straight from the
 // accumulators (L_pk = (T_pk - acc) L_kk^-T): each block is read once and written once, T_kk is never stored.
 // Same arithmetic (and rounding) as bl_update_rb + bl_factor (same contribution order per target).
+// column record: r0 = (k, first block, end block, forward begin), r1 = (forward end, diagonal contributions
+// begin, end, 0) -- one load instead of a chain colptr -> bcon
+__device__ __forceinline__ void bl_column_record(const BLDev& g, const int4* bcon, int k, int4& r0, int4& r1) {
+  const int kb0 = g.colptr[k];
+  const int4 bc = bcon[kb0];
+  r0 = make_int4(k, kb0, g.colptr[k + 1], g.fwdp[k]);
+  r1 = make_int4(g.fwdp[k + 1], bc.x, bc.y, 0);
+}
+
 template <int D>
-__device__ __forceinline__ void bl_column_task(const BLDev& g, const BLWs& w, const int4* bcon, int b, int k,
-                                               double tol, bool fused_fwd) {
+__device__ __forceinline__ void bl_column_task(const BLDev& g, const BLWs& w, const int4* bcon, int b, const int4 r0,
+                                               const int4 r1, double tol, bool fused_fwd) {
   using C = BLC<D>;
   const size_t Bp = g.Bp;
-  const int kb0 = g.colptr[k], kb1 = g.colptr[k + 1];
+  const int k = r0.x, kb0 = r0.y, kb1 = r0.z;
   double a[D][D], iv[D];
-  {
-    const int4 bc = bcon[kb0];
-    bl_acc_target<D>(g, w, b, bc.x, bc.y, true, a, w.L + (size_t)kb0 * C::DD * Bp + b);   // a = T_kk - sum
-  }
+  int4 bcn = kb0 + 1 < kb1 ? bcon[kb0 + 1] : make_int4(0, 0, 0, 0);   // the first below block's range, early
+  bl_acc_target<D>(g, w, b, r1.y, r1.z, true, a, w.L + (size_t)kb0 * C::DD * Bp + b);   // a = T_kk - sum
   bool bad = false;
   bl_chol<D>(a, iv, tol, bad);
   bl_store_diag<D>(g, w, b, k, a, iv, bad, false);
   if (fused_fwd) {   // y_k = L_kk^-1 (x_k - sum_s L_ks y_s), x_k read in the first contribution's round trip
     double* xk = w.x + (size_t)k * D * Bp + b;
     double t[D], y[D];
-    bl_acc_fwd<D>(g, w, b, g.fwdp[k], g.fwdp[k + 1], t, xk);
+    bl_acc_fwd<D>(g, w, b, r0.w, r1.x, t, xk);
 #pragma unroll
     for (int q = 0; q < D; ++q) {
       double s2 = t[q];
@@ -714,7 +721,8 @@ __device__ __forceinline__ void bl_column_task(const BLDev& g, const BLWs& w, co
     for (int q = 0; q < D; ++q) xk[q * Bp] = y[q];
   }
   for (int bi = kb0 + 1; bi < kb1; ++bi) {
-    const int4 bc = bcon[bi];
+    const int4 bc = bcn;
+    if (bi + 1 < kb1) bcn = bcon[bi + 1];   // the next block's range, with this block's loads
     double* Pb = w.L + (size_t)bi * C::DD * Bp + b;
     double acc[D][D];
     bl_acc_target<D>(g, w, b, bc.x, bc.y, false, acc, (bc.z & 2) ? nullptr : Pb);   // T_pk - sum (fill: -sum)
@@ -881,14 +889,23 @@ template <int D>
 #define DNLS_SUB_MINB 2
 #endif
 __global__ void __launch_bounds__(BL_TPB, DNLS_SUB_MINB) bl_subtree(BLDev g, BLWs w, const int4* bcon, const int* sub_ptr,
-                                                       const int* sub_col, int nsub, int fused_fwd) {
+                                                       const int4* sub_rec, int nsub, int fused_fwd) {
   bl_pdl();
   int b;
   long long it;
   if (!bl_item(g, nsub, b, it)) return;
   if (b >= g.B || bl_frozen(w, b)) return;
   const double tol = 1e-13 * __longlong_as_double((long long)w.maxd[b]);
-  for (int q = sub_ptr[it]; q < sub_ptr[it + 1]; ++q) bl_column_task<D>(g, w, bcon, b, sub_col[q], tol, fused_fwd != 0);
+  const int q0 = sub_ptr[it], q1 = sub_ptr[it + 1];
+  int4 r0 = sub_rec[2 * q0], r1 = sub_rec[2 * q0 + 1];
+  for (int q = q0; q < q1; ++q) {
+    const int4 c0 = r0, c1 = r1;
+    if (q + 1 < q1) {   // the next column's record, with this column's first loads
+      r0 = sub_rec[2 * q + 2];
+      r1 = sub_rec[2 * q + 3];
+    }
+    bl_column_task<D>(g, w, bcon, b, c0, c1, tol, fused_fwd != 0);
+  }
 }
 
 // next work index of a unit: dynamic scheduling through a shared counter (the result of an item does not depend
@@ -929,7 +946,9 @@ __global__ void __launch_bounds__(BLP_NT, 1) bl_persist(BLDev g, BLWs w, BLPDev 
       // every lane of a unit takes part in the scheduling (frozen elements skip the arithmetic)
       for (int ci = next(c0); ci < c1; ci = next(c0)) {
           if (!act) continue;
-          bl_column_task<D>(g, w, pd.bcon, b, pd.lvl_col[ci], tol, fused_fwd != 0);
+          int4 r0, r1;
+          bl_column_record(g, pd.bcon, pd.lvl_col[ci], r0, r1);
+          bl_column_task<D>(g, w, pd.bcon, b, r0, r1, tol, fused_fwd != 0);
         }
       phase_end();
       continue;
@@ -1632,7 +1651,8 @@ struct BLPlan {
   int sub_top = -1;       // bl_subtree covers the columns of height <= sub_top (-1: off)
   std::vector<int> sub_pass;   // subtrees of pass p: [sub_pass[p], sub_pass[p+1])
   int nsub = 0;           // its items: maximal subtrees of those columns, largest first
-  const int *d_sub_ptr = nullptr, *d_sub_col = nullptr;
+  const int* d_sub_ptr = nullptr;
+  const int4* d_sub_rec = nullptr;
 
   BLPDev pd{};
   int64_t storage_doubles = 0;   // nblk * DD per element
@@ -1977,6 +1997,11 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   std::vector<int32_t> bit_lvl32(pl.bit_lvl_h.begin(), pl.bit_lvl_h.end()), fit_lvl32(pl.fit_lvl_h.begin(),
                                                                                        pl.fit_lvl_h.end());
   pl.lch = lch;
+  std::vector<int32_t> sub_rec;   // per subtree column: (k, first block, end block, forward begin), (forward end,
+                                  // diagonal contributions begin, end, 0)
+  for (int k : sub_col)
+    sub_rec.insert(sub_rec.end(), {k, colptr[k], colptr[k + 1], fwdp[k], fwdp[k + 1], bcon[4 * (size_t)colptr[k]],
+                                   bcon[4 * (size_t)colptr[k] + 1], 0});
   pl.sub_top = sub_top;
   pl.nsub = (int)sub_ptr.size() - 1;
   std::vector<int32_t> lvl_ptr32(pl.lvl_ptr.begin(), pl.lvl_ptr.end()), fac_lvl32(pl.fac_lvl_ptr.begin(),
@@ -1994,7 +2019,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   add(colptr); add(blkrow); add(tsk); add(con); add(fwdp); add(fwd); add(fac); add(slotd);
   add(s.bc_ptr); add(s.bc); add(dup_ptr); add(dup_blk); add(dup_con); add(fill); add(lvl_col); add(fill0);
   add(bcon); add(it_lvl); add(items); add(rd_lvl); add(red); add(lvl_ptr32); add(fac_lvl32);
-  add(sub_ptr); add(sub_col);
+  add(sub_ptr); add(sub_rec);
   add(litems); add(bred); add(cred);
   add(litems_f); add(bred_f); add(cred_f);
   add(bit); add(bit_lvl32); add(bcolv); add(fit); add(fit_lvl32); add(fcolv);
@@ -2034,7 +2059,7 @@ inline std::string bl_build(const Symbolic& s, int device, BLPlan& pl) {
   pl.pd.lvl_ptr = ptr(offs[k++]);
   pl.pd.fac_lvl = ptr(offs[k++]);
   pl.d_sub_ptr = ptr(offs[k++]);
-  pl.d_sub_col = ptr(offs[k++]);
+  pl.d_sub_rec = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.d_litems = reinterpret_cast<const int4*>(ptr(offs[k++]));
   pl.d_bred = reinterpret_cast<const int2*>(ptr(offs[k++]));
   pl.d_cred = reinterpret_cast<const int2*>(ptr(offs[k++]));
@@ -2198,7 +2223,7 @@ void bl_factor_all(const BLPlan& pl, int B, const BLWs& w, bool fused_fwd, cudaS
     for (size_t p = 0; p + 1 < pl.sub_pass.size(); ++p) {
       const int a = pl.sub_pass[p], n = pl.sub_pass[p + 1] - a;
       if (n > 0)
-        bl_launch(bl_subtree<D>, bl_grid(n, g.Bp), BL_TPB, s, g, w, pl.pd.bcon, pl.d_sub_ptr + a, pl.d_sub_col, n,
+        bl_launch(bl_subtree<D>, bl_grid(n, g.Bp), BL_TPB, s, g, w, pl.pd.bcon, pl.d_sub_ptr + a, pl.d_sub_rec, n,
                   fused_fwd ? 1 : 0);
     }
   for (int l = 0; l < lsplit; ++l) {
