@@ -1035,7 +1035,7 @@ struct BLSDev {
 };
 
 template <int D, int GW>
-__global__ void __launch_bounds__(BLP_NT) bl_lsolve(BLDev g, BLWs w, BLPDev pd, BLSDev sd, const int* skip,
+__global__ void __launch_bounds__(BLP_NT, 2) bl_lsolve(BLDev g, BLWs w, BLPDev pd, BLSDev sd, const int* skip,
                                                     int forward, int l_begin, int l_end) {
   bl_pdl();
   using C = BLC<D>;
@@ -1049,9 +1049,29 @@ __global__ void __launch_bounds__(BLP_NT) bl_lsolve(BLDev g, BLWs w, BLPDev pd, 
   const int* ilvl = forward ? sd.fit_lvl : sd.bit_lvl;
   const int2* icol = forward ? sd.fcol : sd.bcol;
   const int nl = l_end - l_begin;
+  // a column's x_k, strictly lower L_kk entries and inverse pivots: the unit's first column of the level is
+  // loaded before the level's items (in their memory round trip), the others after the barrier
+  auto load_col = [&](int ci, int& k, int2& rg, double (&xv)[D], double (&lo)[D][D], double (&iv)[D]) {
+    k = pd.lvl_col[ci];
+    rg = icol[ci];
+    const double* xk = w.x + (size_t)k * D * Bp + b;
+    const double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      xv[q] = xk[q * Bp];
+      iv[q] = Lk[ivpos<D>(0, q, D) * Bp];
+#pragma unroll
+      for (int r = 0; r < q; ++r) lo[q][r] = Lk[(r * D + q) * Bp];   // entry (q, r), q > r
+    }
+  };
   for (int li = 0; li < nl; ++li) {
     const int l = forward ? l_begin + li : l_end - 1 - li;
     const int i0 = ilvl[l], i1 = ilvl[l + 1];
+    const int ci0 = pd.lvl_ptr[l] + u;
+    int k0 = 0;
+    int2 rg0 = make_int2(0, 0);
+    double xp[D], lp[D][D], ivp[D];
+    if (act && ci0 < pd.lvl_ptr[l + 1]) load_col(ci0, k0, rg0, xp, lp, ivp);
     for (int ii = i0 + u; ii < i1; ii += U) {
       double acc[D];
 #pragma unroll
@@ -1095,15 +1115,24 @@ __global__ void __launch_bounds__(BLP_NT) bl_lsolve(BLDev g, BLWs w, BLPDev pd, 
       for (int i = 0; i < D; ++i) spart[((size_t)(ii - i0) * D + i) * GW + e] = acc[i];
     }
     __syncthreads();
-    for (int ci = pd.lvl_ptr[l] + u; ci < pd.lvl_ptr[l + 1]; ci += U) {
+    for (int ci = ci0; ci < pd.lvl_ptr[l + 1]; ci += U) {
       if (!act) continue;
-      const int k = pd.lvl_col[ci];
-      const int2 rg = icol[ci];
-      double* xk = w.x + (size_t)k * D * Bp + b;
-      const double* Lk = w.Ld + (size_t)k * C::DD * Bp + b;
-      double t[D], y[D];
+      int k;
+      int2 rg;
+      double t[D], lo[D][D], iv[D], y[D];
+      if (ci == ci0) {
+        k = k0;
+        rg = rg0;
 #pragma unroll
-      for (int i = 0; i < D; ++i) t[i] = xk[i * Bp];
+        for (int q = 0; q < D; ++q) {
+          t[q] = xp[q];
+          iv[q] = ivp[q];
+#pragma unroll
+          for (int r = 0; r < q; ++r) lo[q][r] = lp[q][r];
+        }
+      } else {
+        load_col(ci, k, rg, t, lo, iv);
+      }
       for (int q = 0; q < rg.y; ++q)
 #pragma unroll
         for (int i = 0; i < D; ++i) t[i] -= spart[((size_t)(rg.x - i0 + q) * D + i) * GW + e];
@@ -1112,18 +1141,19 @@ __global__ void __launch_bounds__(BLP_NT) bl_lsolve(BLDev g, BLWs w, BLPDev pd, 
         for (int q = 0; q < D; ++q) {
           double s2 = t[q];
 #pragma unroll
-          for (int r = 0; r < q; ++r) s2 = fma(-Lk[(r * D + q) * Bp], y[r], s2);
-          y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+          for (int r = 0; r < q; ++r) s2 = fma(-lo[q][r], y[r], s2);
+          y[q] = s2 * iv[q];
         }
       } else {
 #pragma unroll
         for (int q = D - 1; q >= 0; --q) {
           double s2 = t[q];
 #pragma unroll
-          for (int p = q + 1; p < D; ++p) s2 = fma(-Lk[(q * D + p) * Bp], y[p], s2);
-          y[q] = s2 * Lk[ivpos<D>(0, q, D) * Bp];
+          for (int p = q + 1; p < D; ++p) s2 = fma(-lo[p][q], y[p], s2);
+          y[q] = s2 * iv[q];
         }
       }
+      double* xk = w.x + (size_t)k * D * Bp + b;
 #pragma unroll
       for (int i = 0; i < D; ++i) xk[i * Bp] = y[i];
     }
